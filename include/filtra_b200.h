@@ -1,0 +1,205 @@
+/*
+ * filtra_b200 -- C-ABI of the B200-native filtered int8 top-k hot path.
+ *
+ * Plain pointers and sizes only (no torch types). Device pointers are
+ * caller-owned; every call is asynchronous on the given cudaStream_t (passed as
+ * void*) unless documented otherwise. Return codes: 0 = ok, otherwise one of
+ * FB_ERR_*; fb_last_error() returns the thread-local message of the last
+ * failure. Codes map 1:1 onto the reference's Python exceptions (see
+ * paper_2511_14881_b200/_native.py).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/filtra):
+ *   fb_hash_leaves        <- bloom.hash_seed / positions_from_seed / hash_positions  (bloom.py:65-88)
+ *   fb_bloom_build        <- bloom.build_bloom                                       (bloom.py:114-144)
+ *   fb_filter_eval        <- filter_query.eval_compiled + bloom.bloom_eval_leaf      (filter_query.py:314-356, bloom.py:160-181)
+ *   fb_quantize           <- quantize.quantize_vector / quantize_matrix              (quantize.py:64-76)
+ *   fb_topk_plan_create /
+ *   fb_topk_execute       <- ivf.search_clusters + ivf._select_topk, batched; with a
+ *                            filter program this is retrieval.codesigned_search      (ivf.py:272-334, retrieval.py:110-144)
+ *   fb_merge_topk         <- serve._reduce_topk over the per-shard results           (serve.py:98-121)
+ *   fb_dequant_scores     <- quantize.dequantize applied to both operands of the dot (quantize.py:79-81)
+ */
+#ifndef FILTRA_B200_H
+#define FILTRA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FB_ABI_VERSION 1
+
+enum fb_status {
+  FB_OK = 0,
+  FB_ERR_INVALID = 1,          /* ValueError: bad params, unaligned slot range, unbalanced program */
+  FB_ERR_DIM_MISMATCH = 2,     /* errors.DimMismatch */
+  FB_ERR_LENGTH_MISMATCH = 3,  /* errors.LengthMismatch */
+  FB_ERR_DEGENERATE = 4,       /* errors.DegenerateRange */
+  FB_ERR_CUDA = 5,             /* CUDA runtime failure */
+  FB_ERR_UNSUPPORTED = 6,      /* outside this build's limits (documented per call) */
+  FB_ERR_NO_DEVICE = 7         /* no sm_100 device */
+};
+
+/* Opcodes of the postfix filter program (filter_query.OpCode, filter_query.py:253-257). */
+enum fb_opcode { FB_OP_PUSH_LEAF = 0, FB_OP_AND = 1, FB_OP_OR = 2, FB_OP_NOT = 3 };
+
+#define FB_MAX_K_HASHES 32     /* K per leaf (reference: unbounded; 5 by default) */
+#define FB_MAX_STACK 64        /* filter program stack depth */
+#define FB_MAX_LEAVES 16384    /* distinct leaves per batch (14-bit op argument) */
+
+/*
+ * Device-resident index over one shard's slot space (ivf.IvfIndex + bloom.BloomIndex).
+ *   items     int8  [n_slots, dim_pad]  quantized rows in slot order; padding rows/columns are 0
+ *   planes    u64   [m_bits, n_words]   transposed Bloom planes (bloom.py:91-111 layout)
+ *   valid     u64   [n_words]           validity words (padding slots cleared)
+ *   id_rank   u32   [n_slots]           rank of the slot's item_id among the shard's valid
+ *                                       items (ascending u64); equal scores break by it
+ *   item_ids  u64   [n_slots]           item id per slot
+ *   row_sum   i32   [n_slots]           sum of the row's codes (dequantised-score term); may be NULL
+ */
+typedef struct fb_index {
+  const int8_t* items;
+  const uint64_t* planes;
+  const uint64_t* valid;
+  const uint32_t* id_rank;
+  const uint64_t* item_ids;
+  const int32_t* row_sum;
+  int64_t n_slots;   /* multiple of 64 */
+  int64_t n_words;   /* n_slots / 64 */
+  int32_t dim;       /* logical embedding dimension */
+  int32_t dim_pad;   /* row stride in bytes: dim rounded up to 32 */
+  int32_t m_bits;
+  int32_t k_hashes;
+} fb_index_t;
+
+/*
+ * A batch of compiled filters (filter_query.CompiledFilter, one per query), with the
+ * leaves de-duplicated across the batch. All arrays are device pointers.
+ *   leaf_pos   i16 [n_leaves * k_max]  plane indices per leaf, ascending, -1 padded
+ *   op_offset  i32 [n_queries + 1]     query q's ops are ops[op_offset[q] .. op_offset[q+1])
+ *   ops        u16 [...]               (opcode << 14) | leaf index
+ * A query with zero ops is unfiltered (mask = validity).
+ */
+typedef struct fb_filter_prog {
+  int32_t n_queries;
+  int32_t n_leaves;
+  int32_t k_max;
+  int32_t max_stack;
+  const int16_t* leaf_pos;
+  const int32_t* op_offset;
+  const uint16_t* ops;
+} fb_filter_prog_t;
+
+/* Work counters (ivf.ScanStats + bloom.FilterStats), filled analytically by the plan. */
+typedef struct fb_stats {
+  int64_t slots_scanned;
+  int64_t tiles;
+  int64_t max_tile_rows;
+  int64_t slots_evaluated;
+  int64_t fallback_queries;   /* queries that needed the exact-threshold fallback on the last execute */
+} fb_stats_t;
+
+int fb_abi_version(void);
+const char* fb_last_error(void);
+/* 1 when device 0 is sm_100 and the sm_100a cubin loads; else 0 (message in fb_last_error). */
+int fb_device_ok(void);
+
+/* Host: positions of n (fid, value) leaves; pos_out[n*k_hashes] ascending, -1 padded;
+ * n_pos_out[n] (nullable) = number of distinct positions. */
+int fb_hash_leaves(const uint64_t* fid, const uint64_t* value, int64_t n, int32_t m_bits,
+                   int32_t k_hashes, int32_t* pos_out, int32_t* n_pos_out);
+
+/* Device: zero `planes` then set bit (p, slot) for every pair and hash position p. */
+int fb_bloom_build(const uint64_t* fid, const uint64_t* value, const int64_t* slot,
+                   int64_t n_pairs, int64_t n_slots, int32_t m_bits, int32_t k_hashes,
+                   uint64_t* planes, void* stream);
+
+/* Device: masks_out[q][w - w0] for words [w0, w1) of every query's program.
+ * apply_valid = 1 gives eval_compiled semantics; 0 gives the raw program value
+ * (bloom_eval_leaf for single-leaf programs). */
+int fb_filter_eval(const fb_index_t* idx, const fb_filter_prog_t* prog, int64_t w0, int64_t w1,
+                   int32_t apply_valid, uint64_t* masks_out, void* stream);
+
+/* Device: int8 out[rows, out_stride] = clip(rint((x - gmin) * (255 / (gmax - gmin))) - 128)
+ * in float64; columns [cols, out_stride) are zeroed. */
+int fb_quantize(const float* x, int64_t rows, int32_t cols, double gmin, double gmax,
+                int8_t* out, int32_t out_stride, void* stream);
+
+/* Same as fb_quantize for float64 inputs (quantize_matrix / quantize_vector cast to float64). */
+int fb_quantize_f64(const double* x, int64_t rows, int32_t cols, double gmin, double gmax,
+                    int8_t* out, int32_t out_stride, void* stream);
+
+/* Device: out[r] = sum of int8 row r over cols (row_sum for fb_index_t). */
+int fb_row_sums(const int8_t* x, int64_t rows, int32_t cols, int32_t stride, int32_t* out,
+                void* stream);
+
+/* ---- batched filtered top-k ------------------------------------------------------ */
+typedef struct fb_topk_plan fb_topk_plan_t;
+
+enum fb_plan_flags {
+  FB_PLAN_FORCE_FALLBACK = 1,  /* testing: take the exact-threshold fallback for every query */
+  FB_PLAN_SIMT = 2,            /* use the SIMT scan kernel instead of the tcgen05 one */
+  FB_PLAN_NO_SAMPLE = 4        /* skip the sampling pass (threshold 0 for every query) */
+};
+
+/* Plan for `n_queries` queries against `idx` over the slot ranges ranges[2*i], ranges[2*i+1]
+ * (host array; starts must be 64-aligned). Allocates all device scratch once. */
+int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k,
+                        const int64_t* ranges, int32_t n_ranges, int32_t flags,
+                        fb_topk_plan_t** plan_out);
+int fb_topk_plan_destroy(fb_topk_plan_t* plan);
+/* Fills stats analytically for one execute of this plan (host). */
+int fb_topk_plan_stats(const fb_topk_plan_t* plan, fb_stats_t* stats);
+
+/* Hot path: queries_q int8 [n_queries, dim_pad]; prog may be NULL (unfiltered);
+ * masks u64 [n_queries, n_words] (nullable) is an explicit per-query slot mask ANDed
+ * into eligibility (search_clusters' `mask` argument, ivf.py:285-312).
+ * Outputs (device, [n_queries, k], rows sorted by (score desc, item_id asc)):
+ *   out_ids u64, out_scores i32, out_count i32 [n_queries] = min(k, eligible);
+ *   out_keys u64 (nullable): ((score ^ 2^31) << 32) | (~id_rank) -- the merge key;
+ *   out_fscores f64 (nullable): dequantised scores (needs idx->row_sum and gmin/gmax).
+ * No host synchronisation; capturable in a CUDA graph. */
+int fb_topk_execute(fb_topk_plan_t* plan, const int8_t* queries_q, const fb_filter_prog_t* prog,
+                    const uint64_t* masks, uint64_t* out_ids, int32_t* out_scores, int32_t* out_count,
+                    uint64_t* out_keys, double* out_fscores, double gmin, double gmax,
+                    void* stream);
+
+/* Measurement hooks: total kernel launches issued by this library (process-wide), and
+ * CUDA-event timing of the emit scan and the selection of a plan's last execute. */
+uint64_t fb_launch_count(void);
+int fb_topk_set_timing(fb_topk_plan_t* plan, int32_t enable);
+int fb_topk_last_timing(fb_topk_plan_t* plan, float* emit_ms, float* select_ms);
+
+/* Device: merge n_lists per-query lists, each sorted by (score desc, item_id asc), into the
+ * global top-k (serve._reduce_topk semantics, serve.py:98-100). Pairs are compared directly,
+ * so shards need no global id ranks.
+ *   in_scores i32 [n_lists, n_queries, k_in], in_ids u64 [same], in_count i32 [n_lists, n_queries],
+ *   in_fscores f64 [same] (nullable); outputs [n_queries, k_out]; out_fscores nullable. */
+int fb_merge_topk(const int32_t* in_scores, const uint64_t* in_ids, const double* in_fscores,
+                  const int32_t* in_count, int32_t n_lists, int32_t n_queries, int32_t k_in,
+                  int32_t k_out, uint64_t* out_ids, int32_t* out_scores, int32_t* out_count,
+                  double* out_fscores, void* stream);
+
+/* Device: f64 dequantised dot from the int32 dot, the item row sum and the query sum
+ * (closed form of sum_j dequantize(a_j) * dequantize(b_j)). */
+int fb_dequant_scores(const int32_t* scores, const int32_t* item_row_sum, const int32_t* query_sum,
+                      int32_t n_queries, int32_t k, const int32_t* count, int32_t dim,
+                      double gmin, double gmax, double* out, void* stream);
+
+/* Device: out[r] = exact int32 dot of int8 row r (stride bytes) with vec (quantize.int8_dot_rows,
+ * quantize.py:84-102). */
+int fb_int8_dot_rows(const int8_t* rows, int64_t n_rows, int32_t dim, int32_t stride,
+                     const int8_t* vec, int32_t* out, void* stream);
+
+/* Device: out[c] = float64 dot of float32 row c with the float32 query, accumulated with
+ * numpy's pairwise-summation order (vecmath.dot_rows, vecmath.py:15-24) so centroid
+ * probing ties resolve exactly as in ivf.probe_centroids (ivf.py:261-269). */
+int fb_dot_rows_f64(const float* rows, int64_t n_rows, int32_t dim, const float* vec,
+                    double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FILTRA_B200_H */

@@ -1,0 +1,739 @@
+// SIMT kernels of filtra_b200: Bloom build, filter-program evaluation, quantisation,
+// the SIMT masked scan (sample / emit / fallback-histogram modes), per-query
+// threshold + exact selection, and the shard merge.
+//
+// Reference semantics (paths under /root/reference/pkg/src/filtra):
+//   build_bloom           bloom.py:114-144
+//   eval_compiled         filter_query.py:314-356 (NOT = ~x & valid, result & valid)
+//   quantize_vector       quantize.py:72-76 (float64, rint half-to-even)
+//   search_clusters       ivf.py:285-334  (eligible = valid & mask, exact int32 dot)
+//   _select_topk          ivf.py:272-282  (score desc, item_id asc)
+//   _reduce_topk          serve.py:98-100
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fb_internal.cuh"
+
+namespace fb {
+
+namespace {
+
+constexpr int kSelectChunk = 8192;   // keys per in-smem bitonic chunk (12 B each)
+constexpr int kSelectThreads = 1024;
+
+__device__ __forceinline__ int64_t grid_stride() { return (int64_t)gridDim.x * blockDim.x; }
+__device__ __forceinline__ int64_t grid_tid() {
+  return (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+}
+
+// ------------------------------------------------------------------------------------
+// Bloom build: one thread per (fid, value, slot) pair, 64-bit atomicOr into the plane word.
+// ------------------------------------------------------------------------------------
+__global__ void k_bloom_build(const uint64_t* __restrict__ fid, const uint64_t* __restrict__ val,
+                              const int64_t* __restrict__ slot, int64_t n, int64_t n_words,
+                              int m_bits, int k, unsigned long long* planes) {
+  for (int64_t i = grid_tid(); i < n; i += grid_stride()) {
+    int32_t pos[FB_MAX_K_HASHES];
+    const int np = leaf_positions(fid[i], val[i], m_bits, k, pos);
+    const int64_t s = slot[i];
+    const unsigned long long bit = 1ull << (s & 63);
+    for (int j = 0; j < np; ++j) atomicOr(planes + (int64_t)pos[j] * n_words + (s >> 6), bit);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Filter program: postfix stack machine over one 64-slot word.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t leaf_word(const int16_t* __restrict__ pos, int k_max,
+                                              const uint64_t* __restrict__ planes, int64_t n_words,
+                                              int64_t w) {
+  uint64_t m = ~0ull;
+  for (int j = 0; j < k_max; ++j) {
+    const int p = pos[j];
+    if (p < 0) break;
+    m &= __ldg(planes + (int64_t)p * n_words + w);
+  }
+  return m;
+}
+
+__device__ uint64_t eval_program_word(const fb_filter_prog_t& prog, int q,
+                                      const uint64_t* __restrict__ planes, int64_t n_words,
+                                      int64_t w, uint64_t valid_w) {
+  const int32_t o0 = prog.op_offset[q], o1 = prog.op_offset[q + 1];
+  if (o0 == o1) return valid_w;  // unfiltered query
+  uint64_t stk[FB_MAX_STACK];
+  int sp = 0;
+  for (int o = o0; o < o1; ++o) {
+    const uint32_t op = prog.ops[o];
+    const uint32_t code = op >> 14, arg = op & 0x3FFF;
+    if (code == FB_OP_PUSH_LEAF) {
+      stk[sp++] = leaf_word(prog.leaf_pos + (int64_t)arg * prog.k_max, prog.k_max, planes,
+                            n_words, w);
+    } else if (code == FB_OP_NOT) {
+      stk[sp - 1] = ~stk[sp - 1] & valid_w;
+    } else {
+      const uint64_t rhs = stk[--sp];
+      stk[sp - 1] = (code == FB_OP_AND) ? (stk[sp - 1] & rhs) : (stk[sp - 1] | rhs);
+    }
+  }
+  return stk[0];
+}
+
+__global__ void k_filter_eval(fb_index_t idx, fb_filter_prog_t prog, int64_t w0, int64_t w1,
+                              int apply_valid, uint64_t* __restrict__ out) {
+  const int64_t width = w1 - w0;
+  const int64_t total = width * prog.n_queries;
+  for (int64_t i = grid_tid(); i < total; i += grid_stride()) {
+    const int q = (int)(i / width);
+    const int64_t w = w0 + (i - (int64_t)q * width);
+    const uint64_t v = idx.valid[w];
+    uint64_t m = eval_program_word(prog, q, idx.planes, idx.n_words, w, v);
+    if (apply_valid) m &= v;
+    out[i] = m;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Quantisation: float64 (x - min) * scale, rint (half to even), -128, clip.
+// ------------------------------------------------------------------------------------
+template <typename T>
+__global__ void k_quantize(const T* __restrict__ x, int64_t rows, int cols, double gmin,
+                           double scale, int8_t* __restrict__ out, int out_stride) {
+  const int64_t total = rows * out_stride;
+  for (int64_t i = grid_tid(); i < total; i += grid_stride()) {
+    const int64_t r = i / out_stride;
+    const int c = (int)(i - r * out_stride);
+    int8_t q = 0;
+    if (c < cols) {
+      const double v = (double)x[r * cols + c];
+      double t = rint(__dmul_rn(__dsub_rn(v, gmin), scale)) - 128.0;
+      t = fmin(127.0, fmax(-128.0, t));
+      q = (int8_t)(int)t;
+    }
+    out[i] = q;
+  }
+}
+
+__global__ void k_dot_rows_i8(const int8_t* __restrict__ x, int64_t rows, int dim, int stride,
+                              const int8_t* __restrict__ v, int32_t* __restrict__ out) {
+  for (int64_t r = grid_tid(); r < rows; r += grid_stride()) {
+    int32_t s = 0;
+    for (int c = 0; c < dim; ++c) s += (int32_t)x[r * stride + c] * (int32_t)v[c];
+    out[r] = s;
+  }
+}
+
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src, PW_BLOCKSIZE 128)
+// over p[i] = (double)a[i] * (double)b[i]; 0.0 + pairwise(p) reproduces
+// np.sum(rows * vec, axis=1) bit-for-bit (checked in tests/test_native_cpu.py's emulation).
+__device__ double pairwise_f64(const float* __restrict__ a, const float* __restrict__ b, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, __dmul_rn((double)a[i], (double)b[i]));
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dmul_rn((double)a[j], (double)b[j]);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        r[j] = __dadd_rn(r[j], __dmul_rn((double)a[i + j], (double)b[i + j]));
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, __dmul_rn((double)a[i], (double)b[i]));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_f64(a, b, n2), pairwise_f64(a + n2, b + n2, n - n2));
+}
+
+__global__ void k_dot_rows_f64(const float* __restrict__ x, int64_t rows, int dim,
+                               const float* __restrict__ v, double* __restrict__ out) {
+  for (int64_t r = grid_tid(); r < rows; r += grid_stride())
+    out[r] = __dadd_rn(0.0, pairwise_f64(x + r * dim, v, dim));
+}
+
+__global__ void k_row_sums(const int8_t* __restrict__ x, int64_t rows, int cols, int stride,
+                           int32_t* __restrict__ out) {
+  for (int64_t r = grid_tid(); r < rows; r += grid_stride()) {
+    int32_t s = 0;
+    for (int c = 0; c < cols; ++c) s += x[r * stride + c];
+    out[r] = s;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// SIMT masked scan. One CTA per 64-slot word (grid-stride over the work list); the 64
+// item rows are staged in shared memory, each thread owns a query: program -> mask,
+// then an exact dp4a dot per admitted slot.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int32_t dot_i8(const int8_t* __restrict__ a, const int8_t* b, int n) {
+  int acc = 0;
+  for (int j = 0; j < n; j += 16) {
+    const int4 x = __ldg(reinterpret_cast<const int4*>(a + j));
+    const int4 y = *reinterpret_cast<const int4*>(b + j);
+    acc = __dp4a(x.x, y.x, acc);
+    acc = __dp4a(x.y, y.y, acc);
+    acc = __dp4a(x.z, y.z, acc);
+    acc = __dp4a(x.w, y.w, acc);
+  }
+  return acc;
+}
+
+__device__ __forceinline__ void locate_word(const ScanArgs& a, int64_t g, int64_t& w,
+                                            uint64_t& rmask) {
+  // range r with word_prefix[r] <= g < word_prefix[r + 1]
+  int lo = 0, hi = a.n_ranges - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.word_prefix[mid] <= g) lo = mid; else hi = mid - 1;
+  }
+  const int64_t s0 = a.ranges[2 * lo], s1 = a.ranges[2 * lo + 1];
+  w = (s0 >> 6) + (g - a.word_prefix[lo]);
+  const int64_t rem = s1 - w * 64;
+  rmask = rem >= 64 ? ~0ull : ((1ull << rem) - 1);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_scan_simt(ScanArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_items[];
+  if (a.active_count != nullptr && *a.active_count == 0) return;
+  const int dp = a.idx.dim_pad;
+  const int64_t n_work = (a.total_words + a.word_stride - 1) / a.word_stride;
+  for (int64_t gi = blockIdx.x; gi < n_work; gi += gridDim.x) {
+    int64_t w;
+    uint64_t rmask;
+    locate_word(a, gi * a.word_stride, w, rmask);
+    const uint64_t vword = a.idx.valid[w] & rmask;
+    const int64_t slot0 = w * 64;
+    __syncthreads();
+    if (vword != 0) {
+      const int4* src = reinterpret_cast<const int4*>(a.idx.items + slot0 * dp);
+      int4* dst = reinterpret_cast<int4*>(smem_items);
+      for (int i = threadIdx.x; i < 4 * dp; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    if (vword == 0) continue;
+    for (int q = threadIdx.x; q < a.n_queries; q += blockDim.x) {
+      if (a.fb != nullptr && a.fb[q].state != a.only_state) continue;
+      uint64_t m = a.has_prog
+                       ? eval_program_word(a.prog, q, a.idx.planes, a.idx.n_words, w, vword) & vword
+                       : vword;
+      if (a.masks != nullptr) m &= a.masks[(int64_t)q * a.idx.n_words + w];
+      if (m == 0) continue;
+      const int8_t* qrow = a.queries + (int64_t)q * dp;
+      if (MODE == SCAN_EMIT) {
+        atomicAdd(a.out_elig + q, (uint32_t)__popcll(m));
+        const uint64_t T = a.threshold ? a.threshold[q] : 0ull;
+        while (m) {
+          const int i = __ffsll((long long)m) - 1;
+          m &= m - 1;
+          const int32_t sc = dot_i8(qrow, reinterpret_cast<const int8_t*>(smem_items) + i * dp, dp);
+          const uint64_t key = make_key(sc, a.idx.id_rank[slot0 + i]);
+          if (key >= T) {
+            const uint32_t p = atomicAdd(a.out_cnt + q, 1u);
+            if (p < (uint32_t)a.cap) {
+              a.out_key[(int64_t)q * a.cap + p] = key;
+              if (a.out_slot) a.out_slot[(int64_t)q * a.cap + p] = (uint32_t)(slot0 + i);
+            }
+          }
+        }
+      } else {
+        const Fallback f = a.fb[q];
+        uint32_t* h = a.hist + (int64_t)q * kHistBins;
+        while (m) {
+          const int i = __ffsll((long long)m) - 1;
+          m &= m - 1;
+          const int32_t sc = dot_i8(qrow, reinterpret_cast<const int8_t*>(smem_items) + i * dp, dp);
+          const uint64_t key = make_key(sc, a.idx.id_rank[slot0 + i]);
+          if (key >= f.lo) {
+            const uint64_t b = (key - f.lo) >> f.shift;
+            if (b < (uint64_t)kHistBins) atomicAdd(h + b, 1u);
+          }
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Block-wide bitonic sort (descending by key) over n = power of two elements in smem.
+// ------------------------------------------------------------------------------------
+template <bool kHasVal>
+__device__ void bitonic_desc(uint64_t* key, uint32_t* val, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
+        const int i = 2 * t - (t & (stride - 1));
+        const int j = i + stride;
+        const bool desc = (i & size) == 0;
+        const uint64_t ki = key[i], kj = key[j];
+        if (desc ? (ki < kj) : (ki > kj)) {
+          key[i] = kj;
+          key[j] = ki;
+          if (kHasVal) {
+            const uint32_t t2 = val[i];
+            val[i] = val[j];
+            val[j] = t2;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int pow2_ceil(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// Per query: sort the sampled keys and pick the key whose estimated full-scan rank is
+// ~1.5k + 3 sqrt(k) + 64, so the emit pass keeps every key of the true top-k with
+// overwhelming probability (the check/fallback keeps the answer exact regardless).
+__global__ void __launch_bounds__(kSelectThreads) k_threshold(ThresholdArgs a) {
+  extern __shared__ __align__(16) uint64_t s_key[];
+  const int q = blockIdx.x;
+  if (threadIdx.x == 0) {
+    a.cnt[q] = 0;
+    a.elig[q] = 0;
+  }
+  const uint32_t ns = a.sample_cnt != nullptr ? a.sample_cnt[q] : 0u;
+  if (a.sample_fraction <= 0.0 || ns == 0) {
+    if (threadIdx.x == 0) a.threshold[q] = 0ull;
+    return;
+  }
+  const int nk = (int)min(ns, (uint32_t)a.sample_cap);
+  const double target = 1.5 * a.k + 3.0 * sqrt((double)a.k) + 64.0;
+  const double jd = target * a.sample_fraction * (double)nk / (double)ns;
+  if (jd >= (double)(nk - 1)) {
+    if (threadIdx.x == 0) a.threshold[q] = 0ull;
+    return;
+  }
+  const int n = pow2_ceil(nk);
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    s_key[i] = i < nk ? a.sample_key[(int64_t)q * a.sample_cap + i] : 0ull;
+  bitonic_desc<false>(s_key, nullptr, n);
+  if (threadIdx.x == 0) a.threshold[q] = s_key[(int)jd];
+}
+
+// Flag queries whose emit pass over- or under-flowed (or all, when forced).
+__global__ void k_check(int n_queries, int k, int cap, const uint32_t* __restrict__ cnt,
+                        const uint32_t* __restrict__ elig, int force, Fallback* fb,
+                        uint32_t* active, uint32_t* total_flagged) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_queries) return;
+  const uint32_t c = cnt[q], e = elig[q];
+  const bool ok = c <= (uint32_t)cap && (c >= (uint32_t)k || c == e);
+  Fallback f;
+  f.lo = 0;
+  f.shift = 52;
+  f.above = 0;
+  f.need = (uint64_t)k;
+  if (force || !ok) {
+    f.state = Q_FLAGGED;
+    atomicAdd(active, 1u);
+    atomicAdd(total_flagged, 1u);
+  } else {
+    f.state = Q_OK;
+  }
+  fb[q] = f;
+}
+
+__global__ void k_zero_hist(int n_queries, const Fallback* fb, uint32_t* hist,
+                            const uint32_t* active) {
+  if (*active == 0) return;
+  const int64_t total = (int64_t)n_queries * kHistBins;
+  for (int64_t i = grid_tid(); i < total; i += grid_stride()) {
+    const int q = (int)(i / kHistBins);
+    if (fb[q].state == Q_FLAGGED) hist[i] = 0;
+  }
+}
+
+// Narrow each flagged query's key window to the histogram bin holding rank `need`;
+// resolve once the keys >= that bin's lower edge fit the candidate buffer.
+__global__ void k_resolve(int n_queries, int k, int cap, Fallback* fb, const uint32_t* hist,
+                          uint64_t* threshold, uint32_t* cnt, uint32_t* elig, uint32_t* active) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_queries || fb[q].state != Q_FLAGGED) return;
+  Fallback f = fb[q];
+  const uint32_t* h = hist + (int64_t)q * kHistBins;
+  uint64_t cum = 0;
+  bool found = false;
+  uint64_t T = 0;
+  for (int b = kHistBins - 1; b >= 0; --b) {
+    const uint64_t c = h[b];
+    if (cum + c >= f.need) {
+      const uint64_t edge = f.lo + ((uint64_t)b << f.shift);
+      if (f.above + cum + c <= (uint64_t)cap || f.shift == 0) {
+        T = edge;
+        found = true;
+      } else {
+        f.above += cum;
+        f.need -= cum;
+        f.lo = edge;
+        f.shift = f.shift >= 12 ? f.shift - 12 : 0;
+        fb[q] = f;
+        return;
+      }
+      break;
+    }
+    cum += c;
+  }
+  // found: threshold at the bin edge; !found: fewer than k eligible keys -> take all
+  threshold[q] = found ? T : 0ull;
+  cnt[q] = 0;
+  elig[q] = 0;
+  f.state = Q_RESOLVED;
+  fb[q] = f;
+  atomicSub(active, 1u);
+  atomicAdd(active + 1, 1u);
+}
+
+// ------------------------------------------------------------------------------------
+// Exact selection: sort each query's candidates (chunks of kSelectChunk in smem), then
+// place every element at its global rank by binary search in the other chunks.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int count_greater(const uint64_t* a, int n, uint64_t x, bool or_equal) {
+  // a sorted descending; number of elements > x (or >= x)
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const bool before = or_equal ? (a[mid] >= x) : (a[mid] > x);
+    if (before) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void write_out(const SelectArgs& a, int q, int rank, uint64_t key,
+                                          uint32_t slot, int32_t qsum) {
+  const int64_t o = (int64_t)q * a.k + rank;
+  const int32_t sc = key_score(key);
+  a.out_ids[o] = a.item_ids[slot];
+  a.out_scores[o] = sc;
+  if (a.out_keys) a.out_keys[o] = key;
+  if (a.out_fscores) {
+    const int32_t rs = a.row_sum ? a.row_sum[slot] : 0;
+    a.out_fscores[o] = dequant_dot(sc, rs, qsum, a.dim, a.gmin, a.gmax);
+  }
+}
+
+__global__ void __launch_bounds__(kSelectThreads) k_select(SelectArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_sel[];
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(smem_sel);
+  uint32_t* s_val = reinterpret_cast<uint32_t*>(smem_sel + sizeof(uint64_t) * kSelectChunk);
+  __shared__ int32_t s_qsum;
+  const int q = blockIdx.x;
+  const int n = (int)min(a.cnt[q], (uint32_t)a.cap);
+  const int kk = min(a.k, n);
+  if (threadIdx.x == 0) {
+    a.out_count[q] = kk;
+    int32_t s = 0;
+    if (a.out_fscores)
+      for (int c = 0; c < a.dim; ++c) s += a.queries[(int64_t)q * a.dim_pad + c];
+    s_qsum = s;
+  }
+  // padding rows of the output
+  for (int r = kk + threadIdx.x; r < a.k; r += blockDim.x) {
+    const int64_t o = (int64_t)q * a.k + r;
+    a.out_ids[o] = ~0ull;
+    a.out_scores[o] = INT32_MIN;
+    if (a.out_keys) a.out_keys[o] = 0ull;
+    if (a.out_fscores) a.out_fscores[o] = 0.0;
+  }
+  __syncthreads();
+  const int32_t qsum = s_qsum;
+  uint64_t* gk = const_cast<uint64_t*>(a.cand_key) + (int64_t)q * a.cap;
+  uint32_t* gs = a.cand_slot + (int64_t)q * a.cap;
+  const int n_chunks = (n + kSelectChunk - 1) / kSelectChunk;
+  for (int c = 0; c < n_chunks; ++c) {
+    const int base = c * kSelectChunk;
+    const int len = min(kSelectChunk, n - base);
+    const int np2 = pow2_ceil(len);
+    __syncthreads();
+    for (int i = threadIdx.x; i < np2; i += blockDim.x) {
+      s_key[i] = i < len ? gk[base + i] : 0ull;
+      s_val[i] = i < len ? gs[base + i] : 0u;
+    }
+    bitonic_desc<true>(s_key, s_val, np2);
+    if (n_chunks == 1) {
+      for (int i = threadIdx.x; i < kk; i += blockDim.x) write_out(a, q, i, s_key[i], s_val[i], qsum);
+      return;
+    }
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      gk[base + i] = s_key[i];
+      gs[base + i] = s_val[i];
+    }
+  }
+  __syncthreads();
+  __threadfence_block();
+  for (int c = 0; c < n_chunks; ++c) {
+    const int base = c * kSelectChunk;
+    const int len = min(kSelectChunk, n - base);
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      const uint64_t x = gk[base + i];
+      int rank = i;
+      for (int d = 0; d < n_chunks && rank < kk; ++d) {
+        if (d == c) continue;
+        const int dbase = d * kSelectChunk;
+        const int dlen = min(kSelectChunk, n - dbase);
+        rank += count_greater(gk + dbase, dlen, x, d < c);
+      }
+      if (rank < kk) write_out(a, q, rank, x, gs[base + i], qsum);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Shard merge (serve._reduce_topk): n_lists lists per query, each sorted by
+// (score desc, item_id asc) -> global top-k. Compares (score, id) pairs directly, so
+// shards only need shard-local id ranks.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ bool pair_before(int32_t sa, uint64_t ia, int32_t sb, uint64_t ib) {
+  return sa > sb || (sa == sb && ia < ib);
+}
+
+// number of elements of list (s, ids)[0, n) ordered strictly before (x_s, x_i)
+// (or_equal: before-or-equal)
+__device__ __forceinline__ int count_before(const int32_t* s, const uint64_t* ids, int n,
+                                            int32_t xs, uint64_t xi, bool or_equal) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const bool before = pair_before(s[mid], ids[mid], xs, xi) ||
+                        (or_equal && s[mid] == xs && ids[mid] == xi);
+    if (before) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_merge(const int32_t* __restrict__ in_scores, const uint64_t* __restrict__ in_ids,
+                        const double* __restrict__ in_fs, const int32_t* __restrict__ in_count,
+                        int n_lists, int n_queries, int k_in, int k_out,
+                        uint64_t* out_ids, int32_t* out_scores, int32_t* out_count,
+                        double* out_fs) {
+  const int q = blockIdx.x;
+  int total = 0;
+  for (int l = 0; l < n_lists; ++l) total += min(in_count[l * n_queries + q], k_in);
+  const int kk = min(total, k_out);
+  if (threadIdx.x == 0) out_count[q] = kk;
+  for (int r = kk + threadIdx.x; r < k_out; r += blockDim.x) {
+    const int64_t o = (int64_t)q * k_out + r;
+    out_ids[o] = ~0ull;
+    out_scores[o] = INT32_MIN;
+    if (out_fs) out_fs[o] = 0.0;
+  }
+  for (int l = 0; l < n_lists; ++l) {
+    const int64_t lb = ((int64_t)l * n_queries + q) * k_in;
+    const int len = min(in_count[l * n_queries + q], k_in);
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      const int32_t xs = in_scores[lb + i];
+      const uint64_t xi = in_ids[lb + i];
+      int rank = i;
+      for (int d = 0; d < n_lists && rank < kk; ++d) {
+        if (d == l) continue;
+        const int64_t db = ((int64_t)d * n_queries + q) * k_in;
+        const int dlen = min(in_count[d * n_queries + q], k_in);
+        rank += count_before(in_scores + db, in_ids + db, dlen, xs, xi, d < l);
+      }
+      if (rank < kk) {
+        const int64_t o = (int64_t)q * k_out + rank;
+        out_ids[o] = xi;
+        out_scores[o] = xs;
+        if (out_fs) out_fs[o] = in_fs ? in_fs[lb + i] : 0.0;
+      }
+    }
+  }
+}
+
+__global__ void k_dequant(const int32_t* __restrict__ scores, const int32_t* __restrict__ rs,
+                          const int32_t* __restrict__ qs, int n_queries, int k,
+                          const int32_t* __restrict__ count, int dim, double gmin, double gmax,
+                          double* out) {
+  const int64_t total = (int64_t)n_queries * k;
+  for (int64_t i = grid_tid(); i < total; i += grid_stride()) {
+    const int q = (int)(i / k);
+    const int r = (int)(i - (int64_t)q * k);
+    out[i] = (count != nullptr && r >= count[q]) ? 0.0
+                                                 : dequant_dot(scores[i], rs[i], qs[q], dim, gmin, gmax);
+  }
+}
+
+int grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)g;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------
+// launchers
+// ------------------------------------------------------------------------------------
+int launch_bloom_build(const uint64_t* fid, const uint64_t* value, const int64_t* slot,
+                       int64_t n_pairs, int64_t n_words, int m_bits, int k, uint64_t* planes,
+                       cudaStream_t s) {
+  if (n_pairs == 0) return FB_OK;
+  k_bloom_build<<<grid_for(n_pairs, 256), 256, 0, s>>>(
+      fid, value, slot, n_pairs, n_words, m_bits, k,
+      reinterpret_cast<unsigned long long*>(planes));
+  FB_LAUNCH_CHECK("k_bloom_build");
+  return FB_OK;
+}
+
+int launch_filter_eval(const fb_index_t& idx, const fb_filter_prog_t& prog, int64_t w0, int64_t w1,
+                       int apply_valid, uint64_t* out, cudaStream_t s) {
+  const int64_t total = (w1 - w0) * prog.n_queries;
+  if (total <= 0) return FB_OK;
+  k_filter_eval<<<grid_for(total, 256), 256, 0, s>>>(idx, prog, w0, w1, apply_valid, out);
+  FB_LAUNCH_CHECK("k_filter_eval");
+  return FB_OK;
+}
+
+int launch_quantize(const float* x, int64_t rows, int cols, double gmin, double gmax, int8_t* out,
+                    int out_stride, cudaStream_t s) {
+  const int64_t total = rows * out_stride;
+  if (total <= 0) return FB_OK;
+  const double scale = 255.0 / (gmax - gmin);
+  k_quantize<float><<<grid_for(total, 256), 256, 0, s>>>(x, rows, cols, gmin, scale, out, out_stride);
+  FB_LAUNCH_CHECK("k_quantize");
+  return FB_OK;
+}
+
+int launch_quantize_f64(const double* x, int64_t rows, int cols, double gmin, double gmax,
+                        int8_t* out, int out_stride, cudaStream_t s) {
+  const int64_t total = rows * out_stride;
+  if (total <= 0) return FB_OK;
+  const double scale = 255.0 / (gmax - gmin);
+  k_quantize<double><<<grid_for(total, 256), 256, 0, s>>>(x, rows, cols, gmin, scale, out,
+                                                          out_stride);
+  FB_LAUNCH_CHECK("k_quantize_f64");
+  return FB_OK;
+}
+
+int launch_dot_rows_i8(const int8_t* rows, int64_t n, int dim, int stride, const int8_t* vec,
+                       int32_t* out, cudaStream_t s) {
+  if (n <= 0) return FB_OK;
+  k_dot_rows_i8<<<grid_for(n, 256), 256, 0, s>>>(rows, n, dim, stride, vec, out);
+  FB_LAUNCH_CHECK("k_dot_rows_i8");
+  return FB_OK;
+}
+
+int launch_dot_rows_f64(const float* rows, int64_t n, int dim, const float* vec, double* out,
+                        cudaStream_t s) {
+  if (n <= 0) return FB_OK;
+  k_dot_rows_f64<<<grid_for(n, 128), 128, 0, s>>>(rows, n, dim, vec, out);
+  FB_LAUNCH_CHECK("k_dot_rows_f64");
+  return FB_OK;
+}
+
+int launch_row_sums(const int8_t* x, int64_t rows, int cols, int stride, int32_t* out,
+                    cudaStream_t s) {
+  if (rows <= 0) return FB_OK;
+  k_row_sums<<<grid_for(rows, 256), 256, 0, s>>>(x, rows, cols, stride, out);
+  FB_LAUNCH_CHECK("k_row_sums");
+  return FB_OK;
+}
+
+int launch_scan_simt(const ScanArgs& a, cudaStream_t s) {
+  if (a.total_words <= 0 || a.n_queries <= 0) return FB_OK;
+  const int64_t n_work = (a.total_words + a.word_stride - 1) / a.word_stride;
+  const size_t smem = (size_t)64 * a.idx.dim_pad;
+  int grid = (int)(n_work < 148 * 8 ? n_work : 148 * 8);
+  if (a.mode == SCAN_EMIT) {
+    if (smem > 48 * 1024)
+      FB_CUDA(cudaFuncSetAttribute(k_scan_simt<SCAN_EMIT>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_scan_simt<SCAN_EMIT><<<grid, 256, smem, s>>>(a);
+  } else {
+    if (smem > 48 * 1024)
+      FB_CUDA(cudaFuncSetAttribute(k_scan_simt<SCAN_HIST>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_scan_simt<SCAN_HIST><<<grid, 256, smem, s>>>(a);
+  }
+  FB_LAUNCH_CHECK("k_scan_simt");
+  return FB_OK;
+}
+
+int launch_threshold(const ThresholdArgs& a, cudaStream_t s) {
+  if (a.n_queries <= 0) return FB_OK;
+  int n = 1;
+  while (n < a.sample_cap) n <<= 1;
+  const size_t smem = (size_t)n * sizeof(uint64_t);
+  FB_CUDA(cudaFuncSetAttribute(k_threshold, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  k_threshold<<<a.n_queries, kSelectThreads, smem, s>>>(a);
+  FB_LAUNCH_CHECK("k_threshold");
+  return FB_OK;
+}
+
+int launch_check(int32_t n_queries, int32_t k, int32_t cap, const uint32_t* cnt,
+                 const uint32_t* elig, int force, Fallback* fb, uint32_t* active,
+                 uint32_t* total_flagged, cudaStream_t s) {
+  if (n_queries <= 0) return FB_OK;
+  k_check<<<(n_queries + 255) / 256, 256, 0, s>>>(n_queries, k, cap, cnt, elig, force, fb, active,
+                                                  total_flagged);
+  FB_LAUNCH_CHECK("k_check");
+  return FB_OK;
+}
+
+int launch_zero_hist(int32_t n_queries, const Fallback* fb, uint32_t* hist,
+                     const uint32_t* active, cudaStream_t s) {
+  if (n_queries <= 0) return FB_OK;
+  k_zero_hist<<<grid_for((int64_t)n_queries * kHistBins, 256), 256, 0, s>>>(n_queries, fb, hist,
+                                                                             active);
+  FB_LAUNCH_CHECK("k_zero_hist");
+  return FB_OK;
+}
+
+int launch_resolve(int32_t n_queries, int32_t k, int32_t cap, Fallback* fb, uint32_t* hist,
+                   uint64_t* threshold, uint32_t* cnt, uint32_t* elig, uint32_t* active,
+                   int final_pass, cudaStream_t s) {
+  (void)final_pass;
+  if (n_queries <= 0) return FB_OK;
+  k_resolve<<<(n_queries + 127) / 128, 128, 0, s>>>(n_queries, k, cap, fb, hist, threshold, cnt,
+                                                    elig, active);
+  FB_LAUNCH_CHECK("k_resolve");
+  return FB_OK;
+}
+
+int launch_select(const SelectArgs& a, cudaStream_t s) {
+  if (a.n_queries <= 0) return FB_OK;
+  const size_t smem = (size_t)kSelectChunk * (sizeof(uint64_t) + sizeof(uint32_t));
+  FB_CUDA(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_select<<<a.n_queries, kSelectThreads, smem, s>>>(a);
+  FB_LAUNCH_CHECK("k_select");
+  return FB_OK;
+}
+
+int launch_merge(const int32_t* in_scores, const uint64_t* in_ids, const double* in_fscores,
+                 const int32_t* in_count, int n_lists, int n_queries, int k_in, int k_out,
+                 uint64_t* out_ids, int32_t* out_scores, int32_t* out_count, double* out_fscores,
+                 cudaStream_t s) {
+  if (n_queries <= 0) return FB_OK;
+  k_merge<<<n_queries, 512, 0, s>>>(in_scores, in_ids, in_fscores, in_count, n_lists, n_queries,
+                                    k_in, k_out, out_ids, out_scores, out_count, out_fscores);
+  FB_LAUNCH_CHECK("k_merge");
+  return FB_OK;
+}
+
+int launch_dequant(const int32_t* scores, const int32_t* item_row_sum, const int32_t* query_sum,
+                   int n_queries, int k, const int32_t* count, int dim, double gmin, double gmax,
+                   double* out, cudaStream_t s) {
+  const int64_t total = (int64_t)n_queries * k;
+  if (total <= 0) return FB_OK;
+  k_dequant<<<grid_for(total, 256), 256, 0, s>>>(scores, item_row_sum, query_sum, n_queries, k,
+                                                 count, dim, gmin, gmax, out);
+  FB_LAUNCH_CHECK("k_dequant");
+  return FB_OK;
+}
+
+}  // namespace fb

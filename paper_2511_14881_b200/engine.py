@@ -1,0 +1,290 @@
+"""Device-resident index and the batched filtered top-k operator.
+
+``DeviceIndex`` holds one shard's slot space in HBM in the layout the kernels read
+(include/filtra_b200.h ``fb_index_t``): int8 rows padded to a 32-byte multiple, the
+transposed Bloom planes ``[M, W]``, validity words, per-slot item ids, the global
+id rank (tie-break key) and per-row code sums (dequantised-score term).
+
+``TopkOp`` wraps a ``fb_topk_plan`` (scratch allocated once per shape) and runs the
+hot path -- sample -> threshold -> fused filter+scan emit -> exactness check ->
+select -- on the current CUDA stream with no host synchronisation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from ._device import device, round_up, to_dev, to_dev_u64, u64_host
+from .bloom import BloomIndex, BloomParams
+from .filter_query import FilterBatch
+from .quantize import QuantParams, quantize_device
+
+
+def _u64_order_key(ids: torch.Tensor) -> torch.Tensor:
+    """int64 tensor holding uint64 bits -> int64 with the same order as the unsigned ids."""
+    return ids ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=ids.device)
+
+
+@dataclass
+class TopkOutput:
+    """Device outputs of one batched call: rows sorted by (score desc, item_id asc)."""
+
+    ids: torch.Tensor       # int64 [B, k] holding uint64 item ids
+    scores: torch.Tensor    # int32 [B, k]
+    count: torch.Tensor     # int32 [B]
+    keys: torch.Tensor | None = None      # int64 [B, k] merge keys
+    fscores: torch.Tensor | None = None   # float64 [B, k] dequantised scores
+
+    def host(self, q: int) -> tuple[np.ndarray, np.ndarray]:
+        n = int(self.count[q])
+        return u64_host(self.ids[q, :n]), self.scores[q, :n].cpu().numpy()
+
+
+class DeviceIndex:
+    """One shard of the catalog, resident in HBM."""
+
+    def __init__(self, items: torch.Tensor, valid: torch.Tensor, item_ids: torch.Tensor,
+                 n_slots: int, dim: int, bloom: BloomIndex | None = None,
+                 qp: QuantParams | None = None, cluster_offsets: np.ndarray | None = None,
+                 centroids: torch.Tensor | None = None, id_rank: torch.Tensor | None = None,
+                 row_sum: torch.Tensor | None = None):
+        self.items = items            # int8 [n_slots_pad, dim_pad]
+        self.valid = valid            # int64 [W] (uint64 bits)
+        self.item_ids = item_ids      # int64 [n_slots_pad] (uint64 bits)
+        self.n_slots = int(n_slots)   # logical (reference) slot count
+        self.dim = int(dim)
+        self.dim_pad = int(items.shape[1])
+        self.bloom = bloom
+        self.qp = qp
+        self.cluster_offsets = (np.asarray(cluster_offsets, dtype=np.int64)
+                                if cluster_offsets is not None
+                                else np.array([[0, self.n_slots]], dtype=np.int64))
+        self.centroids = centroids
+        if id_rank is None:
+            id_rank = self._ranks_from_ids()
+        self.id_rank = id_rank        # int32 [n_slots_pad] (uint32 bits)
+        if row_sum is None:
+            row_sum = torch.empty(items.shape[0], dtype=torch.int32, device=items.device)
+            _native.check(_native.lib().fb_row_sums(items.data_ptr(), items.shape[0], self.dim,
+                                                    self.dim_pad, row_sum.data_ptr(),
+                                                    _native.stream_ptr()))
+        self.row_sum = row_sum
+        if bloom is None:
+            planes = torch.zeros((1, self.n_words), dtype=torch.int64, device=items.device)
+            self._planes = planes
+            self.m_bits, self.k_hashes = 1, 1
+        else:
+            self._planes = bloom.planes_dev
+            self.m_bits, self.k_hashes = bloom.params.m_bits, bloom.params.k_hashes
+            if bloom.n_words < self.n_words:
+                raise ValueError("Bloom planes cover fewer words than the slot space")
+
+    @property
+    def n_words(self) -> int:
+        return int(self.valid.shape[0])
+
+    @property
+    def n_slots_pad(self) -> int:
+        return int(self.items.shape[0])
+
+    def _ranks_from_ids(self) -> torch.Tensor:
+        """Rank of each valid slot's id among the valid ids (ascending u64)."""
+        n = self.n_slots_pad
+        bits = torch.arange(64, device=self.items.device, dtype=torch.int64)
+        words = self.valid.view(-1, 1)
+        vbool = ((words >> bits) & 1).view(-1)[:n].bool()
+        key = _u64_order_key(self.item_ids)
+        key = torch.where(vbool, key, torch.full_like(key, (1 << 63) - 1))
+        order = torch.argsort(key, stable=True)
+        rank = torch.empty(n, dtype=torch.int64, device=key.device)
+        rank[order] = torch.arange(n, device=key.device, dtype=torch.int64)
+        return rank.to(torch.int32)
+
+    @classmethod
+    def from_arrays(cls, items_q, valid, item_ids, *, bloom: BloomIndex | None = None,
+                    qp: QuantParams | None = None, cluster_offsets=None, centroids=None,
+                    id_rank=None) -> "DeviceIndex":
+        """Upload reference-layout arrays (int8 rows in slot order, packed validity,
+        per-slot u64 ids) -- numpy or CUDA tensors."""
+        dev = device()
+        items = to_dev(items_q, torch.int8, dev)
+        n_slots, dim = int(items.shape[0]), int(items.shape[1])
+        dim_pad = round_up(max(dim, 1), 32)
+        n_pad = round_up(max(n_slots, 1), 64)
+        if dim_pad != dim or n_pad != n_slots:
+            padded = torch.zeros((n_pad, dim_pad), dtype=torch.int8, device=dev)
+            padded[:n_slots, :dim] = items
+            items = padded
+        v = to_dev_u64(valid, dev)
+        if v.numel() < n_pad // 64:
+            v = torch.cat([v, torch.zeros(n_pad // 64 - v.numel(), dtype=torch.int64, device=dev)])
+        ids = to_dev_u64(item_ids, dev)
+        if ids.numel() < n_pad:
+            ids = torch.cat([ids, torch.zeros(n_pad - ids.numel(), dtype=torch.int64, device=dev)])
+        cent = to_dev(centroids, torch.float32, dev) if centroids is not None else None
+        rank = to_dev(id_rank, torch.int32, dev) if id_rank is not None else None
+        return cls(items, v, ids, n_slots, dim, bloom=bloom, qp=qp,
+                   cluster_offsets=cluster_offsets, centroids=cent, id_rank=rank)
+
+    def struct(self) -> _native.FbIndex:
+        return _native.FbIndex(self.items.data_ptr(), self._planes.data_ptr(),
+                               self.valid.data_ptr(), self.id_rank.data_ptr(),
+                               self.item_ids.data_ptr(), self.row_sum.data_ptr(),
+                               self.n_slots_pad, self.n_words, self.dim, self.dim_pad,
+                               self.m_bits, self.k_hashes)
+
+    def quantize_queries(self, queries: torch.Tensor) -> torch.Tensor:
+        if self.qp is None:
+            raise ValueError("index has no quantisation parameters")
+        return quantize_device(queries, self.qp, out_stride=self.dim_pad)
+
+    def pad_queries(self, query_q) -> torch.Tensor:
+        q = to_dev(query_q, torch.int8)
+        if q.dim() == 1:
+            q = q.view(1, -1)
+        if q.shape[1] == self.dim_pad:
+            return q
+        out = torch.zeros((q.shape[0], self.dim_pad), dtype=torch.int8, device=q.device)
+        out[:, : q.shape[1]] = q
+        return out
+
+
+_REF_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def device_index_for(index, bloom=None) -> DeviceIndex:
+    """A ``DeviceIndex`` for either our own index or a reference-shaped ``IvfIndex``
+    (duck-typed: ``items_q.data``, ``valid_mask``, ``item_ids``, ``cluster_offsets``),
+    uploaded once and cached on the object."""
+    if isinstance(index, DeviceIndex):
+        return index
+    key = index
+    cached = None
+    try:
+        cached = _REF_CACHE.get(key)
+    except TypeError:
+        key = None
+    if cached is not None and (bloom is None or cached.bloom is not None):
+        return cached
+    if bloom is not None and not isinstance(bloom, BloomIndex):
+        bloom = BloomIndex(BloomParams(bloom.params.m_bits, bloom.params.k_hashes),
+                           bloom.planes, bloom.n_slots)
+    qp = index.items_q.params
+    dix = DeviceIndex.from_arrays(
+        index.items_q.data, index.valid_mask, index.item_ids, bloom=bloom,
+        qp=QuantParams(float(qp.global_min), float(qp.global_max)),
+        cluster_offsets=np.asarray(index.cluster_offsets, dtype=np.int64),
+        centroids=getattr(getattr(index, "centroids", None), "vectors", None))
+    if key is not None:
+        try:
+            _REF_CACHE[key] = dix
+        except TypeError:
+            pass
+    return dix
+
+
+class TopkOp:
+    """A planned batched filtered top-k over fixed slot ranges."""
+
+    def __init__(self, index: DeviceIndex, n_queries: int, k: int, ranges: np.ndarray,
+                 flags: int = 0):
+        self.index = index
+        self.n_queries = int(n_queries)
+        self.k = int(k)
+        self.flags = int(flags)
+        r = np.ascontiguousarray(np.asarray(ranges, dtype=np.int64).reshape(-1, 2))
+        self.ranges = r
+        self._idx_struct = index.struct()
+        plan = ctypes.c_void_p()
+        _native.check(_native.lib().fb_topk_plan_create(
+            ctypes.byref(self._idx_struct), self.n_queries, self.k, r.ctypes.data, r.shape[0],
+            self.flags, ctypes.byref(plan)))
+        self._plan = plan
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan is not None and plan.value:
+            try:
+                _native.load_library().fb_topk_plan_destroy(plan)
+            except Exception:  # interpreter shutdown
+                pass
+            self._plan = None
+
+    def stats(self) -> _native.FbStats:
+        st = _native.FbStats()
+        _native.check(_native.load_library().fb_topk_plan_stats(self._plan, ctypes.byref(st)))
+        return st
+
+    def alloc_outputs(self, keys: bool = False, fscores: bool = False) -> TopkOutput:
+        dev = self.index.items.device
+        B, k = self.n_queries, max(self.k, 1)
+        return TopkOutput(
+            ids=torch.empty((B, k), dtype=torch.int64, device=dev),
+            scores=torch.empty((B, k), dtype=torch.int32, device=dev),
+            count=torch.empty((B,), dtype=torch.int32, device=dev),
+            keys=torch.empty((B, k), dtype=torch.int64, device=dev) if keys else None,
+            fscores=torch.empty((B, k), dtype=torch.float64, device=dev) if fscores else None)
+
+    def __call__(self, queries_q: torch.Tensor, filters: FilterBatch | None = None,
+                 masks: torch.Tensor | None = None, out: TopkOutput | None = None,
+                 keys: bool = False, fscores: bool = False, stream=None) -> TopkOutput:
+        if queries_q.dtype != torch.int8 or queries_q.shape != (self.n_queries, self.index.dim_pad):
+            raise ValueError(f"queries_q must be int8 [{self.n_queries}, {self.index.dim_pad}]")
+        if out is None:
+            out = self.alloc_outputs(keys=keys, fscores=fscores)
+        prog = filters.struct() if filters is not None else None
+        qp = self.index.qp
+        _native.check(_native.lib().fb_topk_execute(
+            self._plan, queries_q.data_ptr(), ctypes.byref(prog) if prog is not None else None,
+            masks.data_ptr() if masks is not None else None,
+            out.ids.data_ptr(), out.scores.data_ptr(), out.count.data_ptr(),
+            out.keys.data_ptr() if out.keys is not None else None,
+            out.fscores.data_ptr() if out.fscores is not None else None,
+            float(qp.global_min) if qp else 0.0, float(qp.global_max) if qp else 1.0,
+            _native.stream_ptr(stream)))
+        self._keep = (queries_q, filters, masks)  # keep inputs alive until the next call
+        return out
+
+
+def filtered_topk(index: DeviceIndex, queries_q: torch.Tensor, k: int,
+                  filters: FilterBatch | None = None, ranges=None, flags: int = 0,
+                  masks: torch.Tensor | None = None, keys: bool = False,
+                  fscores: bool = False) -> TopkOutput:
+    """One-shot batched filtered top-k (plans and runs)."""
+    if ranges is None:
+        ranges = np.array([[0, index.n_slots]], dtype=np.int64)
+    op = TopkOp(index, queries_q.shape[0], k, ranges, flags)
+    res = op(queries_q, filters, masks=masks, keys=keys, fscores=fscores)
+    torch.cuda.current_stream().synchronize()
+    return res
+
+
+def merge_topk(scores: torch.Tensor, ids: torch.Tensor, count: torch.Tensor, k_out: int,
+               fscores: torch.Tensor | None = None) -> TopkOutput:
+    """GPU merge of ``n_lists`` per-query lists sorted by (score desc, item_id asc)
+    (``_reduce_topk`` semantics). scores int32 / ids int64(u64 bits) [n_lists, B, k_in];
+    count int32 [n_lists, B]."""
+    n_lists, B, k_in = scores.shape
+    dev = scores.device
+    k_out = max(int(k_out), 1)
+    out = TopkOutput(ids=torch.empty((B, k_out), dtype=torch.int64, device=dev),
+                     scores=torch.empty((B, k_out), dtype=torch.int32, device=dev),
+                     count=torch.empty((B,), dtype=torch.int32, device=dev),
+                     fscores=(torch.empty((B, k_out), dtype=torch.float64, device=dev)
+                              if fscores is not None else None))
+    scores = scores.to(torch.int32).contiguous()
+    ids = ids.contiguous()
+    count = count.to(torch.int32).contiguous()
+    fs = fscores.contiguous() if fscores is not None else None
+    _native.check(_native.lib().fb_merge_topk(
+        scores.data_ptr(), ids.data_ptr(), fs.data_ptr() if fs is not None else None,
+        count.data_ptr(), n_lists, B, k_in, k_out, out.ids.data_ptr(), out.scores.data_ptr(),
+        out.count.data_ptr(), out.fscores.data_ptr() if out.fscores is not None else None,
+        _native.stream_ptr()))
+    return out

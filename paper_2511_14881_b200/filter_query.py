@@ -1,0 +1,394 @@
+"""Filter expressions: grammar, AST, postfix compiler, and the GPU evaluator.
+
+Grammar and lowering follow the reference (filter_query.py:1-311): OR binds tighter
+than AND, NOT tightest; AND/OR children are chained pairwise in post-order; leaves
+are de-duplicated per filter. ``FilterBatch`` packs a batch of compiled filters
+into the device bytecode consumed by the fused scan (leaves de-duplicated across
+the whole batch, positions hashed in C). ``eval_compiled`` runs ``fb_filter_eval``.
+"""
+
+from __future__ import annotations
+
+import re
+from dataclasses import dataclass, field
+from enum import IntEnum
+
+import numpy as np
+import torch
+
+from . import _native, bitset
+from ._device import device, to_dev_u64, u64_host
+from .bloom import BloomIndex, BloomParams, FilterStats, QueryBloom, hash_positions_batch
+from .errors import FilterSyntaxError, UnknownFeature, UnknownValue
+
+
+# --- AST ------------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class Leaf:
+    feature_id: int
+    value: int
+
+
+@dataclass(frozen=True)
+class And:
+    children: tuple
+
+
+@dataclass(frozen=True)
+class Or:
+    children: tuple
+
+
+@dataclass(frozen=True)
+class Not:
+    child: object
+
+
+FilterExpr = object  # Leaf | And | Or | Not
+
+
+@dataclass(frozen=True)
+class Vocabulary:
+    """Feature-name and string-value dictionaries (reference filter_query.py:60-77)."""
+
+    feature_ids: dict[str, int] = field(default_factory=dict)
+    values: dict[str, int] = field(default_factory=dict)
+
+    @classmethod
+    def from_schema(cls, feature_schema: dict[int, str], values: dict[str, int] | None = None):
+        return cls(feature_ids={name: fid for fid, name in feature_schema.items()},
+                   values=dict(values or {}))
+
+    def feature_name(self, fid: int) -> str | None:
+        for name, v in self.feature_ids.items():
+            if v == fid:
+                return name
+        return None
+
+
+# --- parser ---------------------------------------------------------------------------
+
+_TOKEN = re.compile(r'\s+|(?P<lpar>\()|(?P<rpar>\))|(?P<eq>=)|(?P<string>"[^"]*")|'
+                    r'(?P<int>\d+)|(?P<ident>[A-Za-z_][A-Za-z0-9_.]*)')
+_KEYWORDS = ("AND", "OR", "NOT")
+
+
+def _tokens(text: str):
+    out, pos = [], 0
+    while pos < len(text):
+        m = _TOKEN.match(text, pos)
+        if m is None:
+            raise FilterSyntaxError(pos, f"unexpected character {text[pos]!r}")
+        if m.lastgroup is not None:
+            kind, val = m.lastgroup, m.group()
+            if kind == "ident" and val.upper() in _KEYWORDS:
+                kind = val.upper()
+            out.append((kind, val, pos))
+        pos = m.end()
+    out.append(("eof", "", len(text)))
+    return out
+
+
+def parse_filter(text: str, vocab: Vocabulary | None = None) -> FilterExpr:
+    """Recursive descent: expr := or_term (AND or_term)*; or_term := factor (OR factor)*;
+    factor := [NOT] (leaf | '(' expr ')'); leaf := name '=' value."""
+    vocab = vocab or Vocabulary()
+    toks = _tokens(text)
+    i = 0
+
+    def peek():
+        return toks[i][0]
+
+    def take(kind=None):
+        nonlocal i
+        tok = toks[i]
+        if kind is not None and tok[0] != kind:
+            raise FilterSyntaxError(tok[2], f"expected {kind}, found {tok[1]!r}")
+        i += 1
+        return tok
+
+    def expr():
+        parts = [or_term()]
+        while peek() == "AND":
+            take()
+            parts.append(or_term())
+        return parts[0] if len(parts) == 1 else And(tuple(parts))
+
+    def or_term():
+        parts = [factor()]
+        while peek() == "OR":
+            take()
+            parts.append(factor())
+        return parts[0] if len(parts) == 1 else Or(tuple(parts))
+
+    def factor():
+        if peek() == "NOT":
+            take()
+            return Not(factor())
+        if peek() == "lpar":
+            take()
+            inner = expr()
+            take("rpar")
+            return inner
+        return leaf()
+
+    def leaf():
+        kind, text_, pos = take()
+        if kind == "ident":
+            if text_ not in vocab.feature_ids:
+                raise UnknownFeature(text_)
+            fid = vocab.feature_ids[text_]
+        elif kind == "int":
+            fid = int(text_)
+        else:
+            raise FilterSyntaxError(pos, f"expected feature name, found {text_!r}")
+        take("eq")
+        kind, text_, pos = take()
+        if kind == "string":
+            lit = text_[1:-1]
+            if lit not in vocab.values:
+                raise UnknownValue(lit)
+            value = vocab.values[lit]
+        elif kind == "int":
+            value = int(text_)
+        else:
+            raise FilterSyntaxError(pos, f"expected value, found {text_!r}")
+        return Leaf(feature_id=fid, value=value)
+
+    result = expr()
+    if peek() != "eof":
+        raise FilterSyntaxError(toks[i][2], f"trailing input {toks[i][1]!r}")
+    return result
+
+
+def format_filter(expr: FilterExpr, vocab: Vocabulary | None = None) -> str:
+    """Inverse of :func:`parse_filter`."""
+    vocab = vocab or Vocabulary()
+    rev = {v: s for s, v in vocab.values.items()}
+
+    def fmt(node, parent):
+        if isinstance(node, Leaf):
+            name = vocab.feature_name(node.feature_id)
+            lhs = name if name is not None else str(node.feature_id)
+            rhs = f'"{rev[node.value]}"' if node.value in rev else str(node.value)
+            return f"{lhs} = {rhs}"
+        if isinstance(node, Not):
+            inner = fmt(node.child, "not")
+            return f"NOT {inner}" if isinstance(node.child, Leaf) else f"NOT ({inner})"
+        if isinstance(node, Or):
+            body = " OR ".join(fmt(c, "or") for c in node.children)
+            return f"({body})" if parent in ("or", "not") else body
+        if isinstance(node, And):
+            body = " AND ".join(fmt(c, "and") for c in node.children)
+            return body if parent == "top" else f"({body})"
+        raise TypeError(f"not a filter node: {node!r}")
+
+    return fmt(expr, "top")
+
+
+def expr_has_not(expr: FilterExpr) -> bool:
+    if isinstance(expr, Not):
+        return True
+    if isinstance(expr, (And, Or)):
+        return any(expr_has_not(c) for c in expr.children)
+    return False
+
+
+# --- compiled form --------------------------------------------------------------------
+
+class OpCode(IntEnum):
+    PUSH_LEAF = 0
+    AND = 1
+    OR = 2
+    NOT = 3
+
+
+@dataclass(frozen=True)
+class CompiledFilter:
+    """Postfix ops + one pre-hashed Bloom query per distinct leaf
+    (reference filter_query.py:260-277)."""
+
+    ops: tuple
+    leaves: tuple
+
+    def max_stack_depth(self) -> int:
+        depth = peak = 0
+        for op, _ in self.ops:
+            if op == OpCode.PUSH_LEAF:
+                depth += 1
+            elif op in (OpCode.AND, OpCode.OR):
+                depth -= 1
+            peak = max(peak, depth)
+        if depth != 1:
+            raise ValueError(f"unbalanced operation array (net depth {depth})")
+        return peak
+
+
+def compile_filter(expr: FilterExpr, params: BloomParams) -> CompiledFilter:
+    """Post-order lowering with per-(fid, value) de-duplication (reference
+    filter_query.py:280-311); all leaf positions hashed in one ``fb_hash_leaves`` call."""
+    leaf_index: dict[tuple[int, int], int] = {}
+    keys: list[tuple[int, int]] = []
+    ops: list[tuple[OpCode, int]] = []
+
+    def emit(node):
+        if isinstance(node, Leaf):
+            key = (int(node.feature_id), int(node.value))
+            idx = leaf_index.get(key)
+            if idx is None:
+                idx = leaf_index[key] = len(keys)
+                keys.append(key)
+            ops.append((OpCode.PUSH_LEAF, idx))
+        elif isinstance(node, Not):
+            emit(node.child)
+            ops.append((OpCode.NOT, 0))
+        elif isinstance(node, (And, Or)):
+            code = OpCode.AND if isinstance(node, And) else OpCode.OR
+            emit(node.children[0])
+            for child in node.children[1:]:
+                emit(child)
+                ops.append((code, 0))
+        else:
+            raise TypeError(f"not a filter node: {node!r}")
+
+    emit(expr)
+    pos, cnt = hash_positions_batch([k[0] for k in keys], [k[1] for k in keys], params)
+    leaves = tuple((f, v, QueryBloom(tuple(int(p) for p in pos[i, : cnt[i]])))
+                   for i, (f, v) in enumerate(keys))
+    cf = CompiledFilter(ops=tuple(ops), leaves=leaves)
+    cf.max_stack_depth()
+    return cf
+
+
+class FilterBatch:
+    """Device bytecode for a batch of compiled filters (one per query, ``None`` =
+    unfiltered): leaves de-duplicated across the batch; ops ``(opcode << 14) | leaf``.
+    Mirrors ``fb_filter_prog_t`` in include/filtra_b200.h."""
+
+    def __init__(self, leaf_pos: np.ndarray, op_offset: np.ndarray, ops: np.ndarray,
+                 max_stack: int, words_per_leaf: np.ndarray, push_leaf_bits: np.ndarray):
+        self.n_queries = len(op_offset) - 1
+        self.n_leaves = leaf_pos.shape[0]
+        self.k_max = leaf_pos.shape[1]
+        self.max_stack = max_stack
+        self.host_leaf_pos = np.ascontiguousarray(leaf_pos, dtype=np.int16)
+        self.host_op_offset = np.ascontiguousarray(op_offset, dtype=np.int32)
+        self.host_ops = np.ascontiguousarray(ops, dtype=np.uint16)
+        # per query: sum over PUSH_LEAF ops of |set_bits| (FilterStats.words_read per word)
+        self.push_leaf_bits = push_leaf_bits
+        self._dev = None
+
+    def to_device(self) -> "FilterBatch":
+        """Upload the bytecode (one H2D copy per array); idempotent."""
+        if self._dev is None:
+            dev = device()
+            self._dev = (torch.from_numpy(self.host_leaf_pos).to(dev),
+                         torch.from_numpy(self.host_op_offset).to(dev),
+                         torch.from_numpy(self.host_ops.view(np.int16)).to(dev))
+        return self
+
+    @property
+    def leaf_pos(self) -> torch.Tensor:
+        return self.to_device()._dev[0]
+
+    @property
+    def op_offset(self) -> torch.Tensor:
+        return self.to_device()._dev[1]
+
+    @property
+    def ops(self) -> torch.Tensor:
+        return self.to_device()._dev[2]
+
+    @classmethod
+    def pack(cls, filters, params: BloomParams) -> "FilterBatch":
+        if params.m_bits > 32767:
+            raise NotImplementedError("device filter evaluation supports m_bits <= 32767")
+        glob: dict[tuple[int, int], int] = {}
+        leaf_rows: list[tuple[int, ...]] = []
+        ops: list[int] = []
+        offsets = [0]
+        push_bits = []
+        max_stack = 1
+        for cf in filters:
+            nbits = 0
+            if cf is not None:
+                local = []
+                for fid, val, qb in cf.leaves:
+                    key = (int(fid), int(val))
+                    g = glob.get(key)
+                    if g is None:
+                        g = glob[key] = len(leaf_rows)
+                        leaf_rows.append(tuple(qb.set_bits))
+                    local.append(g)
+                for op, arg in cf.ops:
+                    if op == OpCode.PUSH_LEAF:
+                        ops.append(local[arg])
+                        nbits += len(cf.leaves[arg][2].set_bits)
+                    else:
+                        ops.append(int(op) << 14)
+                max_stack = max(max_stack, cf.max_stack_depth())
+            offsets.append(len(ops))
+            push_bits.append(nbits)
+        if len(leaf_rows) > _native.FB_MAX_LEAVES:
+            raise NotImplementedError(f"more than {_native.FB_MAX_LEAVES} distinct leaves in a batch")
+        if max_stack > _native.FB_MAX_STACK:
+            raise NotImplementedError(f"filter stack depth {max_stack} > {_native.FB_MAX_STACK}")
+        k_max = max([1] + [len(r) for r in leaf_rows])
+        leaf_pos = np.full((max(1, len(leaf_rows)), k_max), -1, dtype=np.int16)
+        for i, r in enumerate(leaf_rows):
+            leaf_pos[i, : len(r)] = r
+        return cls(leaf_pos, np.array(offsets, dtype=np.int32),
+                   np.array(ops if ops else [0], dtype=np.uint16), max_stack,
+                   np.array([len(r) for r in leaf_rows]), np.array(push_bits, dtype=np.int64))
+
+    @classmethod
+    def from_leaf(cls, qb: QueryBloom, params: BloomParams) -> "FilterBatch":
+        cf = CompiledFilter(ops=((OpCode.PUSH_LEAF, 0),), leaves=((0, 0, qb),))
+        return cls.pack([cf], params)
+
+    def struct(self) -> _native.FbFilterProg:
+        return _native.FbFilterProg(self.n_queries, self.n_leaves, self.k_max, self.max_stack,
+                                    self.leaf_pos.data_ptr(), self.op_offset.data_ptr(),
+                                    self.ops.data_ptr())
+
+    def evaluate(self, bloom: BloomIndex, valid, w0: int, w1: int,
+                 apply_valid: bool = True) -> np.ndarray:
+        """``fb_filter_eval`` over words [w0, w1) for every query -> numpy u64 [B, w1-w0]."""
+        lib = _native.lib()
+        dev = device()
+        nw = bloom.n_words
+        if valid is None:
+            valid_t = torch.full((nw,), -1, dtype=torch.int64, device=dev)
+        else:
+            valid_t = to_dev_u64(valid, dev)
+        idx = _native.FbIndex(None, bloom.planes_dev.data_ptr(), valid_t.data_ptr(), None, None,
+                              None, nw * 64, nw, 32, 32, bloom.params.m_bits, bloom.params.k_hashes)
+        out = torch.empty((self.n_queries, max(0, w1 - w0)), dtype=torch.int64, device=dev)
+        prog = self.struct()
+        _native.check(lib.fb_filter_eval(idx, prog, int(w0), int(w1), 1 if apply_valid else 0,
+                                         out.data_ptr(), _native.stream_ptr()))
+        return u64_host(out)
+
+
+def eval_compiled(cf: CompiledFilter, index: BloomIndex, valid: np.ndarray,
+                  slot_range: tuple[int, int] | None = None,
+                  stats: FilterStats | None = None) -> np.ndarray:
+    """Stack-machine evaluation on the GPU (reference filter_query.py:314-356): NOT is
+    ``~x & valid``, the result is ANDed with ``valid``; ``slot_range`` must start on a
+    64-slot boundary; a ranged result equals the slice of the full one."""
+    if slot_range is None:
+        w0, w1 = 0, index.n_words
+    else:
+        s0, s1 = slot_range
+        if s0 % bitset.WORD_BITS:
+            raise ValueError(f"slot range start {s0} not 64-aligned")
+        w0, w1 = s0 >> 6, (s1 + bitset.WORD_BITS - 1) >> 6
+    if stats is not None:
+        stats.slots_evaluated += (w1 - w0) * bitset.WORD_BITS
+        stats.words_read += sum(len(cf.leaves[a][2].set_bits) for o, a in cf.ops
+                                if o == OpCode.PUSH_LEAF and cf.leaves[a][2].set_bits) * (w1 - w0)
+    if w1 <= w0:
+        return np.empty(0, dtype=np.uint64)
+    batch = FilterBatch.pack([cf], index.params)
+    return batch.evaluate(index, valid, w0, w1, apply_valid=True)[0].copy()

@@ -1,0 +1,132 @@
+"""Drop-in shims for the reference IVF scan API (ivf.py:43-343).
+
+``search_clusters`` / ``search`` / ``probe_centroids`` keep the reference signatures and
+return the reference result types; they accept either a ``DeviceIndex`` or a
+reference-shaped ``IvfIndex`` (uploaded to HBM once and cached). Compute runs through
+``fb_topk_execute`` (masked exact scan + exact (score desc, item_id asc) top-k) and
+``fb_dot_rows_f64`` (numpy-order float64 centroid dots).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from ._device import device, to_dev, to_dev_u64
+from .engine import DeviceIndex, TopkOp, device_index_for
+from .errors import DimMismatch
+
+TILE_ROWS = 4096  # reference tile contract (ivf.py:24); GPU tiles are 128 rows
+
+
+@dataclass(frozen=True)
+class TopkResult:
+    """Scores sorted descending, ties by ascending item id (reference ivf.py:43-56)."""
+
+    item_ids: np.ndarray
+    scores: np.ndarray
+    k_requested: int
+
+    def __len__(self) -> int:
+        return len(self.item_ids)
+
+    @property
+    def entries(self) -> list[tuple[int, float]]:
+        return [(int(i), s.item()) for i, s in zip(self.item_ids, self.scores)]
+
+
+@dataclass
+class ScanStats:
+    """Work counters (reference ivf.py:59-65), filled analytically from the plan."""
+
+    slots_scanned: int = 0
+    max_tile_rows: int = 0
+    tiles: int = 0
+
+
+def _empty(topk: int) -> TopkResult:
+    return TopkResult(item_ids=np.empty(0, dtype=np.uint64), scores=np.empty(0, dtype=np.int32),
+                      k_requested=topk)
+
+
+def cluster_ranges(dix: DeviceIndex, clusters) -> np.ndarray:
+    offs = dix.cluster_offsets
+    cl = np.asarray(clusters, dtype=np.int64).reshape(-1)
+    if cl.size == 0:
+        return np.zeros((0, 2), dtype=np.int64)
+    return np.ascontiguousarray(offs[cl].astype(np.int64))
+
+
+def run_scan(dix: DeviceIndex, query_q: np.ndarray, ranges: np.ndarray, mask, topk: int,
+             filters=None, stats: ScanStats | None = None, flags: int = 0) -> TopkResult:
+    """B = 1 view of the batched operator."""
+    total = int(sum(int(e) - int(s) for s, e in ranges))
+    if stats is not None:
+        stats.slots_scanned += total
+    if topk <= 0 or total == 0:
+        return _empty(topk)
+    k_eff = min(int(topk), total)
+    op = TopkOp(dix, 1, k_eff, ranges, flags)
+    if stats is not None:
+        st = op.stats()
+        stats.tiles += int(st.tiles)
+        stats.max_tile_rows = max(stats.max_tile_rows, int(st.max_tile_rows))
+    q = dix.pad_queries(query_q)
+    masks = None
+    if mask is not None:
+        m = to_dev_u64(mask)
+        if m.numel() < dix.n_words:
+            m = torch.cat([m, torch.zeros(dix.n_words - m.numel(), dtype=torch.int64,
+                                          device=m.device)])
+        masks = m.view(1, -1)
+    out = op(q, filters, masks=masks)
+    ids, scores = out.host(0)
+    return TopkResult(item_ids=ids, scores=scores.astype(np.int32), k_requested=topk)
+
+
+def search_clusters(index, query_q: np.ndarray, clusters, mask: np.ndarray | None, topk: int,
+                    stats: ScanStats | None = None) -> TopkResult:
+    """Exact integer top-k over the valid, mask-admitted slots of ``clusters``
+    (reference ivf.py:285-334), on the GPU."""
+    dix = device_index_for(index)
+    query_q = np.asarray(query_q, dtype=np.int8)
+    if query_q.shape[0] != dix.dim:
+        raise DimMismatch(dix.dim, query_q.shape[0])
+    return run_scan(dix, query_q, cluster_ranges(dix, clusters), mask, topk, stats=stats)
+
+
+def probe_centroids(index, query: np.ndarray, nprobe: int) -> np.ndarray:
+    """Ids of the nprobe highest float64-dot centroids, ties by ascending id
+    (reference ivf.py:261-269); dots in numpy's pairwise order on the GPU."""
+    dix = device_index_for(index)
+    query = np.asarray(query, dtype=np.float32)
+    if query.shape[0] != dix.dim:
+        raise DimMismatch(dix.dim, query.shape[0])
+    n_clusters = dix.cluster_offsets.shape[0]
+    nprobe = min(max(int(nprobe), 1), n_clusters)
+    if dix.centroids is None:
+        if n_clusters != 1:
+            raise ValueError("index has no centroids")
+        return np.zeros(1, dtype=np.int64)
+    scores = torch.empty(n_clusters, dtype=torch.float64, device=device())
+    qv = to_dev(query, torch.float32)
+    _native.check(_native.lib().fb_dot_rows_f64(dix.centroids.data_ptr(), n_clusters, dix.dim,
+                                                qv.data_ptr(), scores.data_ptr(),
+                                                _native.stream_ptr()))
+    order = torch.sort(scores, descending=True, stable=True).indices
+    return order[:nprobe].cpu().numpy().astype(np.int64)
+
+
+def search(index, query: np.ndarray, nprobe: int, topk: int, mask: np.ndarray | None = None,
+           stats: ScanStats | None = None) -> TopkResult:
+    """Quantise with the index params, probe, fused scan (reference ivf.py:337-343)."""
+    dix = device_index_for(index)
+    query = np.asarray(query, dtype=np.float32)
+    if query.shape[0] != dix.dim:
+        raise DimMismatch(dix.dim, query.shape[0])
+    qq = dix.quantize_queries(to_dev(query.reshape(1, -1), torch.float32))
+    clusters = probe_centroids(dix, query, nprobe)
+    return run_scan(dix, qq, cluster_ranges(dix, clusters), mask, topk, stats=stats)

@@ -1,0 +1,349 @@
+"""GPU parity: every drop-in entry point vs the reference golden vectors and the CPU
+oracle, bit-exact (ids, int32 scores, Bloom masks); float64 dequantised scores within
+1e-5 relative. Runs through the C-ABI library on a B200."""
+
+from __future__ import annotations
+
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import json_to_expr, json_to_oracle_expr, load_json, load_npz
+from oracle import filtra_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fb(cuda):
+    import paper_2511_14881_b200 as fb
+    return fb
+
+
+def ref_index(z, pre, fb):
+    lo, hi = (float(x) for x in z[pre + "qp"])
+    ns = SimpleNamespace
+    cent = z[pre + "centroids"] if (pre + "centroids") in z.files else None
+    return ns(items_q=ns(data=z[pre + "items_q"], params=fb.QuantParams(lo, hi)),
+              valid_mask=z[pre + "valid"], item_ids=z[pre + "item_ids"],
+              cluster_offsets=z[pre + "offsets"],
+              centroids=ns(vectors=cent) if cent is not None else None,
+              n_slots=z[pre + "items_q"].shape[0], dim=z[pre + "items_q"].shape[1])
+
+
+def test_bloom_build_golden(fb):
+    z = load_npz("bloom_cases.npz")
+    for i in range(int(z["n_cases"][0])):
+        m, k, n_slots = (int(x) for x in z[f"c{i}_meta"])
+        idx = fb.build_bloom_arrays(z[f"c{i}_fid"], z[f"c{i}_val"], z[f"c{i}_slot"], n_slots,
+                                    fb.BloomParams(m, k))
+        assert np.array_equal(idx.planes, z[f"c{i}_planes"]), i
+        assert idx.plane_bytes == m * ((n_slots + 63) // 64) * 8
+
+
+def test_build_bloom_list_front_end(fb):
+    idx = fb.build_bloom([[(1, 1)], [(2, 2)], [], [(1, 1), (3, 7)]], fb.BloomParams(64, 3))
+    p = idx.planes
+    nz = {int(r): int(p[r, 0]) for r in np.flatnonzero(p[:, 0])}
+    assert nz == {2: 0x2, 11: 0x8, 19: 0x8, 21: 0x9, 26: 0x2, 33: 0x9, 44: 0x9, 54: 0xA}
+    padded = fb.build_bloom([[(1, 1)], [(2, 2)]], fb.BloomParams(64, 3), n_slots=128)
+    for slot in range(2, 128):
+        assert not padded.signature(slot).any()
+
+
+def test_eval_compiled_golden(fb):
+    z = load_npz("filter_cases.npz")
+    exprs = load_json("filter_exprs.json")
+    m, k, n = (int(x) for x in z["meta"])
+    params = fb.BloomParams(m, k)
+    bloom = fb.BloomIndex(params, z["planes"], n)
+    ranges = [tuple(int(v) for v in r) for r in z["ranges"]]
+    for i, e in enumerate(exprs):
+        cf = fb.compile_filter(json_to_expr(e["expr"]), params)
+        full = fb.eval_compiled(cf, bloom, z["valid"])
+        assert np.array_equal(full, z["fulls"][i]), i
+        ranged = np.concatenate([fb.eval_compiled(cf, bloom, z["valid"], r) for r in ranges])
+        assert np.array_equal(ranged, z["ranged"][i]), i
+    cf = fb.compile_filter(fb.Leaf(1, 1), params)
+    with pytest.raises(ValueError):
+        fb.eval_compiled(cf, bloom, z["valid"], slot_range=(10, 64))
+    for row in z["leaf_budget"]:
+        fid, val, words_read = (int(x) for x in row[:3])
+        st = fb.FilterStats()
+        got = fb.bloom_eval_leaf(bloom, fb.hash_positions(fid, val, params), word_range=(1, 4),
+                                 stats=st)
+        assert st.words_read == words_read
+        assert np.array_equal(got, row[3:].astype(np.uint64))
+
+
+def test_eval_not_is_valid_complement(fb, rng):
+    params = fb.BloomParams(64, 3)
+    sf = [[(int(rng.integers(1, 6)), int(rng.integers(1, 6))) for _ in range(int(rng.integers(0, 6)))]
+          for _ in range(200)]
+    bloom = fb.build_bloom(sf, params)
+    valid = orc.from_bool(np.ones(200, dtype=bool))
+    leaf = fb.Leaf(1, 1)
+    a = fb.eval_compiled(fb.compile_filter(leaf, params), bloom, valid)
+    b = fb.eval_compiled(fb.compile_filter(fb.Not(leaf), params), bloom, valid)
+    assert not np.any(a & b)
+    assert np.array_equal(a | b, valid)
+
+
+def test_quantize_golden(fb):
+    z = load_npz("quantize_cases.npz")
+    for x, q, (lo, hi) in zip(z["x"], z["q"], z["params"]):
+        p = fb.QuantParams(float(lo), float(hi))
+        assert np.array_equal(fb.quantize_vector(x, p), q)
+        assert np.array_equal(fb.quantize_vector(x.astype(np.float64), p), q)
+    p = fb.QuantParams(-1.0, 1.0)
+    assert [fb.quantize_value(v, p) for v in (-1.0, 1.0, 0.0)] == [-128, 127, 0]
+    assert fb.quantize_value(-5.0, fb.QuantParams(0.0, 1.0)) == -128
+
+
+def test_int8_dot_kats(fb, rng):
+    v = np.array([127, 127, 127, 127], dtype=np.int8)
+    assert fb.int8_dot(v, v) == 64516
+    a = np.full(4096, 127, dtype=np.int8)
+    b = np.full(4096, -128, dtype=np.int8)
+    assert fb.int8_dot(a, b) == 127 * -128 * 4096
+    x = rng.integers(-128, 128, size=128).astype(np.int8)
+    y = rng.integers(-128, 128, size=128).astype(np.int8)
+    assert fb.int8_dot(x, y) == sum(int(p) * int(q) for p, q in zip(x, y))
+    from paper_2511_14881_b200.errors import LengthMismatch
+    with pytest.raises(LengthMismatch):
+        fb.int8_dot(np.zeros(3, dtype=np.int8), np.zeros(4, dtype=np.int8))
+
+
+def test_scan_golden(fb):
+    z = load_npz("scan_cases.npz")
+    meta = load_json("scan_meta.json")
+    for ci, m in enumerate(meta):
+        pre = f"s{ci}_"
+        ivf = ref_index(z, pre, fb)
+        bloom = fb.BloomIndex(fb.BloomParams(), z[pre + "planes"], ivf.n_slots)
+        for q in m["queries"]:
+            t = q["t"]
+            qf = z[pre + f"q{t}_f"]
+            assert fb.probe_centroids(ivf, qf, q["nprobe"]).tolist() == q["clusters"]
+            if q["kind"] == 0:
+                res = fb.search_clusters(ivf, z[pre + f"q{t}_q"], np.array(q["clusters"]),
+                                         z[pre + f"q{t}_mask"], q["topk"])
+            elif q["kind"] == 1:
+                cf = fb.compile_filter(json_to_expr(q["expr"]), fb.BloomParams())
+                res = fb.codesigned_search(ivf, bloom, cf, qf, q["nprobe"], q["topk"])
+            else:
+                res = fb.search(ivf, qf, q["nprobe"], q["topk"])
+            assert np.array_equal(res.item_ids, z[pre + f"q{t}_ids"]), (ci, t)
+            assert np.array_equal(res.scores, z[pre + f"q{t}_scores"]), (ci, t)
+            assert res.scores.dtype == np.int32 and res.item_ids.dtype == np.uint64
+        # exhaustive search == int8 brute force (reference tests/test_ivf.py:287-294)
+        res = fb.search(ivf, z[pre + "bf_q"], nprobe=len(z[pre + "offsets"]), topk=64)
+        assert np.array_equal(res.item_ids, z[pre + "bf_ids"])
+        assert np.array_equal(res.scores, z[pre + "bf_scores"])
+
+
+def test_ties_ascending_item_id(fb):
+    z = load_npz("scan_cases.npz")
+    ivf = ref_index(z, "tie_", fb)
+    res = fb.search_clusters(ivf, fb.quantize_vector(np.array([1.0, 0.0], np.float32),
+                                                     ivf.items_q.params), [0], None, 4)
+    assert res.item_ids.tolist() == [1, 3, 7, 9] == z["tie_ids"].tolist()
+    assert len(set(res.scores.tolist())) == 1
+
+
+def test_four_attribute_and_topk20000(fb):
+    z = load_npz("four_attr.npz")
+    ivf = ref_index(z, "", fb)
+    bloom = fb.BloomIndex(fb.BloomParams(), z["planes"], ivf.n_slots)
+    for t, c in enumerate(load_json("four_attr.json")):
+        cf = fb.compile_filter(json_to_expr(c["expr"]), fb.BloomParams())
+        res = fb.codesigned_search(ivf, bloom, cf, z[f"q{t}_f"], 1, c["k"])
+        assert np.array_equal(res.item_ids, z[f"q{t}_ids"]), t
+        assert np.array_equal(res.scores, z[f"q{t}_scores"]), t
+    y = load_npz("topk20000.npz")
+    ivf = ref_index(y, "", fb)
+    q = fb.quantize_vector(y["q"], ivf.items_q.params)
+    res = fb.search_clusters(ivf, q, np.arange(len(y["offsets"])), None, 20000)
+    assert len(res) == 20000
+    assert np.array_equal(res.item_ids, y["ids"]) and np.array_equal(res.scores, y["scores"])
+
+
+def test_reduce_topk_golden(fb):
+    z = load_npz("merge_cases.npz")
+    for c in range(int(z["n_cases"][0])):
+        ids, sc = fb._reduce_topk(z[f"c{c}_ids"], z[f"c{c}_scores"], int(z[f"c{c}_k"][0]))
+        assert np.array_equal(ids, z[f"c{c}_rids"]) and np.array_equal(sc, z[f"c{c}_rscores"])
+
+
+def test_scan_edge_cases(fb):
+    z = load_npz("scan_cases.npz")
+    ivf = ref_index(z, "s1_", fb)
+    q = z["s1_q0_q"]
+    n_cl = len(z["s1_offsets"])
+    res = fb.search_clusters(ivf, q, np.arange(n_cl), np.zeros_like(z["s1_valid"]), 10)
+    assert len(res) == 0
+    res = fb.search_clusters(ivf, q, np.arange(n_cl), None, 10 ** 6)
+    assert len(res) == 400
+    pairs = list(zip(res.scores.tolist(), res.item_ids.tolist()))
+    assert pairs == sorted(pairs, key=lambda t: (-t[0], t[1]))
+    assert len(fb.search_clusters(ivf, q, np.arange(n_cl), None, 0)) == 0
+    assert len(fb.search_clusters(ivf, q, np.array([], dtype=np.int64), None, 5)) == 0
+    from paper_2511_14881_b200.errors import DimMismatch
+    with pytest.raises(DimMismatch):
+        fb.search_clusters(ivf, np.zeros(ivf.dim + 1, np.int8), [0], None, 5)
+    with pytest.raises(DimMismatch):
+        fb.probe_centroids(ivf, np.zeros(ivf.dim + 1, np.float32), 1)
+
+
+def test_scan_stats_and_codesign_accounting(fb):
+    z = load_npz("scan_cases.npz")
+    ivf = ref_index(z, "s2_", fb)
+    bloom = fb.BloomIndex(fb.BloomParams(), z["s2_planes"], ivf.n_slots)
+    cf = fb.compile_filter(fb.Or((fb.Leaf(1, 1), fb.Leaf(2, 2))), fb.BloomParams())
+    scan, filt = fb.ScanStats(), fb.FilterStats()
+    qf = z["s2_q0_f"]
+    fb.codesigned_search(ivf, bloom, cf, qf, 3, 10, scan_stats=scan, filter_stats=filt)
+    probed = fb.probe_centroids(ivf, qf, 3)
+    expected = sum(int(e - s) for s, e in (z["s2_offsets"][int(c)] for c in probed))
+    assert scan.slots_scanned == expected and filt.slots_evaluated == expected
+    assert 0 < scan.max_tile_rows <= 4096 and scan.tiles >= 1
+    assert filt.words_read == sum(len(qb.set_bits) for _, _, qb in cf.leaves) * expected // 64
+
+
+# --- batched path vs the oracle -------------------------------------------------------
+
+def oracle_batch(wl, idx, k, ranges=None, masks=None, filtered=True):
+    from paper_2511_14881_b200 import _device
+    items = idx.items.cpu().numpy()[:, : wl.dim]
+    valid = _device.u64_host(idx.valid)
+    ids = _device.u64_host(idx.item_ids)
+    offs = np.array([[0, idx.n_slots]] if ranges is None else ranges)
+    qq = wl.queries_q.cpu().numpy()[:, : wl.dim]
+    out = []
+    for q in range(qq.shape[0]):
+        cf = wl.filters[q] if filtered else None
+        prog = None
+        if cf is not None:
+            prog = ([(int(o), int(a)) for o, a in cf.ops],
+                    [(f, v, qb.set_bits) for f, v, qb in cf.leaves])
+        clusters = list(range(len(offs)))
+        if masks is not None:
+            mask = masks[q]
+            if prog is not None:
+                mask = mask & orc.eval_compiled(prog[0], prog[1], idx.bloom.planes, valid)
+            out.append(orc.search_clusters(items, valid, ids, offs, qq[q], clusters, mask, k))
+        else:
+            out.append(orc.codesigned_search(items, valid, ids, offs, idx.bloom.planes, prog,
+                                             qq[q], clusters, k))
+    return out
+
+
+@pytest.fixture(scope="module")
+def wl_small(fb):
+    from paper_2511_14881_b200 import workload
+    return workload.make_workload(50_000, 24, dim=128, seed=11)
+
+
+@pytest.mark.parametrize("k", [1, 100, 5000])
+@pytest.mark.parametrize("flags", [0, 1])  # 1 = FB_PLAN_FORCE_FALLBACK
+def test_batched_filtered_vs_oracle(fb, wl_small, k, flags):
+    wl = wl_small
+    idx = wl.index
+    op = fb.TopkOp(idx, 24, k, np.array([[0, idx.n_slots]]), flags)
+    out = op(wl.queries_q, wl.batch)
+    torch.cuda.synchronize()
+    ref = oracle_batch(wl, idx, k)
+    for q in range(24):
+        ids, scores = out.host(q)
+        assert np.array_equal(ids, ref[q].item_ids), q
+        assert np.array_equal(scores, ref[q].scores), q
+
+
+def test_batched_ranges_masks_unfiltered(fb, wl_small, rng):
+    wl = wl_small
+    idx = wl.index
+    ranges = np.array([[0, 640], [6400, 20000], [30016, 30080], [49984, 50048]])
+    k = 700
+    masks_np = np.stack([orc.from_bool(rng.random(idx.n_slots) < 0.5) for _ in range(24)])
+    from paper_2511_14881_b200 import _device
+    masks = _device.to_dev_u64(masks_np).view(24, -1)
+    for filtered in (False, True):
+        op = fb.TopkOp(idx, 24, k, ranges)
+        out = op(wl.queries_q, wl.batch if filtered else None, masks=masks)
+        torch.cuda.synchronize()
+        ref = oracle_batch(wl, idx, k, ranges=ranges, masks=masks_np, filtered=filtered)
+        for q in range(24):
+            ids, scores = out.host(q)
+            assert np.array_equal(ids, ref[q].item_ids), (filtered, q)
+            assert np.array_equal(scores, ref[q].scores), (filtered, q)
+
+
+def test_dequantised_scores_within_1e5(fb, wl_small):
+    wl = wl_small
+    idx = wl.index
+    op = fb.TopkOp(idx, 24, 300, np.array([[0, idx.n_slots]]))
+    out = op(wl.queries_q, wl.batch, fscores=True)
+    torch.cuda.synchronize()
+    items = idx.items.cpu().numpy()[:, : wl.dim]
+    qq = wl.queries_q.cpu().numpy()[:, : wl.dim]
+    lo, hi = wl.qp.global_min, wl.qp.global_max
+    for q in range(0, 24, 5):
+        ids, _ = out.host(q)
+        n = len(ids)
+        got = out.fscores[q, :n].cpu().numpy()
+        want = (orc.dequantize(items[ids.astype(np.int64)], lo, hi) *
+                orc.dequantize(qq[q], lo, hi)).sum(axis=1)
+        scale = np.abs(orc.dequantize(items[ids.astype(np.int64)], lo, hi) *
+                       orc.dequantize(qq[q], lo, hi)).sum(axis=1)
+        assert np.all(np.abs(got - want) <= 1e-5 * np.maximum(np.abs(want), scale * 1e-3))
+
+
+def test_sampling_path_large_k(fb):
+    """Candidate buffer smaller than the scanned set: the sampled threshold path must
+    stay exact (vs brute force), with and without the forced fallback."""
+    from paper_2511_14881_b200 import _device, workload
+    wl = workload.make_workload(400_000, 6, dim=128, seed=5)
+    idx = wl.index
+    items = idx.items.cpu().numpy()[:, : wl.dim]
+    valid = _device.u64_host(idx.valid)
+    planes = idx.bloom.planes
+    for flags in (0, 1):
+        op = fb.TopkOp(idx, 6, 3000, np.array([[0, idx.n_slots]]), flags)
+        out = op(wl.queries_q, wl.batch)
+        torch.cuda.synchronize()
+        for q in range(6):
+            cf = wl.filters[q]
+            mask = orc.eval_compiled([(int(o), int(a)) for o, a in cf.ops],
+                                     [(f, v, qb.set_bits) for f, v, qb in cf.leaves], planes, valid)
+            ref = orc.brute_force_int8(items, np.arange(idx.n_slots, dtype=np.uint64),
+                                       wl.queries_q[q, : wl.dim].cpu().numpy(), 3000,
+                                       keep=orc.to_bool(mask, idx.n_slots))
+            ids, scores = out.host(q)
+            assert np.array_equal(ids, ref.item_ids), (flags, q)
+            assert np.array_equal(scores, ref.scores), (flags, q)
+
+
+def test_merge_topk_device(fb, rng):
+    n_lists, B, k = 5, 3, 50
+    scores = np.zeros((n_lists, B, k), np.int32)
+    ids = np.zeros((n_lists, B, k), np.uint64)
+    cnt = rng.integers(0, k + 1, size=(n_lists, B)).astype(np.int32)
+    for l in range(n_lists):
+        for b in range(B):
+            s = rng.integers(-5, 5, size=cnt[l, b]).astype(np.int32)
+            i = rng.choice(10_000, size=cnt[l, b], replace=False).astype(np.uint64) * 8 + l
+            o = np.lexsort((i, -s.astype(np.int64)))
+            scores[l, b, : cnt[l, b]] = s[o]
+            ids[l, b, : cnt[l, b]] = i[o]
+    from paper_2511_14881_b200 import _device
+    out = fb.merge_topk(_device.to_dev(scores, torch.int32),
+                        _device.to_dev_u64(ids).view(n_lists, B, k),
+                        _device.to_dev(cnt, torch.int32), 60)
+    for b in range(B):
+        all_i = np.concatenate([ids[l, b, : cnt[l, b]] for l in range(n_lists)])
+        all_s = np.concatenate([scores[l, b, : cnt[l, b]] for l in range(n_lists)])
+        ri, rs = orc.reduce_topk(all_i, all_s, 60)
+        gi, gs = out.host(b)
+        assert np.array_equal(gi, ri) and np.array_equal(gs, rs)
