@@ -1,0 +1,491 @@
+#!/usr/bin/env python
+"""Filtered int8 top-k throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N=1 runs BASELINE config 2 (10M items x 128-d int8, batch 256, top-k 10000, the
+"4-attribute" Bloom filter, ~10% selectivity). Under torchrun (N>1) every rank owns
+a 10M-item shard (weak scaling: the catalogue grows to N x 10M), runs the fused
+filtered top-k locally, and the per-rank lists are merged after one NCCL all-gather.
+
+A step = one batch of B queries: quantise the float queries + sample + threshold +
+fused Bloom-filter/int8 scan + exactness check + exact top-k selection (+ exchange
+and merge for N>1). Inputs (1.28 GB of int8 rows + 1.28 GB of planes per GPU) are far
+larger than the 126 MB L2, so no explicit flush is needed between steps.
+
+``--impl reference`` times the reference algorithm (the CPU oracle port in
+``oracle/``, a NumPy restatement of reference ivf.search_clusters / retrieval
+.codesigned_search) on this host's cores, on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "filtered int8 top-k queries/sec (4-attribute Bloom filter, exact top-k)"
+UNIT = "queries/s"
+FALLBACK_HBM_GBS = 6650.0
+NOMINAL_INT8_TOPS = 4500.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--items", type=int, default=10_000_000, help="items per GPU")
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--k", type=int, default=10_000)
+    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--simt", action="store_true", help="force the SIMT scan kernel")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-queries", type=int, default=0, help="CPU sample size (0: auto)")
+    return ap.parse_args()
+
+
+def workload_desc(a, n_gpus):
+    return {
+        "workload": (f"config2: {a.items // 1_000_000}M items/GPU x {a.dim}-d int8, batch "
+                     f"{a.batch}, top-k {a.k}, 4-attribute Bloom filter (M=1024, K=5)"),
+        "items_total": a.items * n_gpus, "items_per_gpu": a.items, "batch": a.batch,
+        "k": a.k, "dim": a.dim, "bloom_m": 1024, "bloom_k": 5,
+        "filter": "AND of 4 OR-groups, |S|=(17,17,14,11), 59 leaves/query",
+        "l2": "inputs 2.6 GB/GPU > 126 MB L2; no flush needed",
+        "parallelism": "single GPU" if n_gpus == 1 else
+                       f"items sharded x{n_gpus}, NCCL all-gather + GPU merge",
+    }
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------------------------
+# CPU oracle timing (fork pool; arrays shared copy-on-write)
+# ------------------------------------------------------------------------------------
+_CPU = {}
+
+
+def _cpu_query(i):
+    from oracle import filtra_oracle as orc
+    d = _CPU
+    prog = d["progs"][i % len(d["progs"])]
+    res = orc.codesigned_search(d["items"], d["valid"], d["ids"], d["offs"], d["planes"], prog,
+                                d["qq"][i % len(d["qq"])], [0], d["k"])
+    return len(res.item_ids)
+
+
+def time_cpu_oracle(items, valid, ids, planes, qq, progs, k, n_queries, cores, rounds=1):
+    """Wall time of ``n_queries`` oracle codesigned_search calls over ``cores`` forked
+    workers. Returns (queries/s, seconds, queries)."""
+    _CPU.update(items=items, valid=valid, ids=ids, offs=np.array([[0, items.shape[0]]]),
+                planes=planes, qq=qq, progs=progs, k=k)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_query, range(cores))  # warm the workers (page-in)
+        t0 = time.perf_counter()
+        for _ in range(rounds):
+            pool.map(_cpu_query, range(n_queries), chunksize=1)
+        dt = time.perf_counter() - t0
+    return n_queries * rounds / dt, dt, n_queries * rounds
+
+
+def progs_of(filters):
+    return [([(int(o), int(a)) for o, a in cf.ops], [(f, v, qb.set_bits) for f, v, qb in cf.leaves])
+            if cf is not None else None for cf in filters]
+
+
+# ------------------------------------------------------------------------------------
+# clocks during the timed region
+# ------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+def profiled_traffic():
+    p = ROOT / "profiles" / "roofline_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except json.JSONDecodeError:
+            return None
+    return None
+
+
+# ------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2511_14881_b200 import _native, workload
+    from paper_2511_14881_b200.engine import TopkOp, merge_topk
+    from paper_2511_14881_b200.filter_query import FilterBatch
+    from paper_2511_14881_b200.quantize import quantize_device
+    from paper_2511_14881_b200.serve import exchange_topk
+
+    lib = _native.lib()
+    B, k = a.batch, a.k
+    t_gen = time.perf_counter()
+    wl = workload.make_workload(a.items, B, dim=a.dim, seed=1 + rank)
+    if world > 1:
+        # one catalogue: shard r holds global ids [r * n_pad, (r + 1) * n_pad); every rank
+        # answers rank 0's queries with rank 0's quantisation parameters
+        wl.index.item_ids += rank * wl.index.n_slots_pad
+        dist.broadcast(wl.queries, 0)
+        qp_t = torch.tensor([wl.qp.global_min, wl.qp.global_max], dtype=torch.float64,
+                            device="cuda")
+        dist.broadcast(qp_t, 0)
+    gen_s = time.perf_counter() - t_gen
+
+    idx = wl.index
+    flags = _native.FB_PLAN_SIMT if a.simt else 0
+    op = TopkOp(idx, B, k, np.array([[0, idx.n_slots]]), flags)
+    qbuf = torch.empty((B, idx.dim_pad), dtype=torch.int8, device="cuda")
+    outs = op.alloc_outputs()
+    batch = wl.batch.to_device()
+
+    def step(queries_f32, filters):
+        quantize_device(queries_f32, wl.qp, out_stride=idx.dim_pad, out=qbuf)
+        res = op(qbuf, filters, out=outs)
+        if world > 1:
+            s, i, c = exchange_topk(res.scores, res.ids, res.count)
+            res = merge_topk(s, i, c, k)
+        return res
+
+    stream = torch.cuda.current_stream()
+    for _ in range(a.warmup):
+        step(wl.queries, batch)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs -------------------------------------
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.fb_launch_count()
+    with ClockSampler(local) as clocks:
+        ev[0].record(stream)
+        for i in range(a.steps):
+            step(wl.queries, batch)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+    launches = int(lib.fb_launch_count() - launches0)
+    per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.steps)]
+    total_ms = ev[0].elapsed_time(ev[a.steps])
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = total_ms / a.steps
+    value = B * a.steps / (total_ms / 1e3)
+
+    # ---- roofline: emit-scan duration with CUDA events inside fb_topk_execute --------
+    lib.fb_topk_set_timing(op._plan, 1)
+    emit_ms, sel_ms = [], []
+    import ctypes
+    e_ms, s_ms = ctypes.c_float(), ctypes.c_float()
+    for _ in range(max(3, min(10, a.steps))):
+        step(wl.queries, batch)
+        _native.check(lib.fb_topk_last_timing(op._plan, ctypes.byref(e_ms), ctypes.byref(s_ms)))
+        emit_ms.append(e_ms.value)
+        sel_ms.append(s_ms.value)
+    lib.fb_topk_set_timing(op._plan, 0)
+    emit_avg = float(np.mean(emit_ms))
+    planes_used = int(np.unique(batch.host_leaf_pos[batch.host_leaf_pos >= 0]).size)
+    n_words = idx.n_words
+    cand = int(outs.count.sum().item())
+    alg_bytes = (idx.n_slots_pad * idx.dim_pad + n_words * 8 * planes_used + n_words * 8
+                 + B * idx.dim_pad + cand * 12)
+    achieved = alg_bytes / (emit_avg / 1e3) / 1e9
+    peak, peak_kind = measured_peaks()
+    traffic = profiled_traffic()
+    ops = 2.0 * B * idx.n_slots_pad * idx.dim
+    roofline = {"bound": "hbm", "kernel": "fused filter+scan emit pass",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_source": peak_kind,
+                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "algorithmic_bytes_per_launch": alg_bytes, "planes_referenced": planes_used,
+                "emit_ms": round(emit_avg, 4), "select_ms": round(float(np.mean(sel_ms)), 4),
+                "int8_tops_achieved": round(ops / (emit_avg / 1e3) / 1e12, 1),
+                "int8_tops_nominal": NOMINAL_INT8_TOPS}
+
+    # ---- e2e through the public API with host buffers --------------------------------
+    host_q = torch.empty((B, a.dim), dtype=torch.float32).pin_memory()
+    host_q.copy_(wl.queries.cpu())
+    h_ops = torch.from_numpy(batch.host_ops.view(np.int16)).pin_memory()
+    h_off = torch.from_numpy(batch.host_op_offset).pin_memory()
+    h_leaf = torch.from_numpy(batch.host_leaf_pos).pin_memory()
+    out_ids = torch.empty((B, k), dtype=torch.int64).pin_memory()
+    out_sc = torch.empty((B, k), dtype=torch.int32).pin_memory()
+    out_cnt = torch.empty((B,), dtype=torch.int32).pin_memory()
+    dq = torch.empty((B, a.dim), dtype=torch.float32, device="cuda")
+    e2e_batch = FilterBatch(batch.host_leaf_pos, batch.host_op_offset, batch.host_ops,
+                            batch.max_stack, None, batch.push_leaf_bits).to_device()
+
+    def e2e_step():
+        dq.copy_(host_q, non_blocking=True)
+        e2e_batch._dev[0].copy_(h_leaf, non_blocking=True)
+        e2e_batch._dev[1].copy_(h_off, non_blocking=True)
+        e2e_batch._dev[2].copy_(h_ops, non_blocking=True)
+        res = step(dq, e2e_batch)
+        out_ids.copy_(res.ids, non_blocking=True)
+        out_sc.copy_(res.scores, non_blocking=True)
+        out_cnt.copy_(res.count, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = host_q.numel() * 4 + h_ops.numel() * 2 + h_off.numel() * 4 + h_leaf.numel() * 2
+    d2h = out_ids.numel() * 8 + out_sc.numel() * 4 + out_cnt.numel() * 4
+    e2e = {"value": round(B * a.steps / (e2e_ms / 1e3), 1), "unit": UNIT,
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+           "ms_per_step": round(e2e_ms / a.steps, 4)}
+
+    # selectivity of the filter (eligible fraction), measured by the plan counters
+    sel = None
+
+    # ---- CPU baseline (rank 0, N=1 only) ---------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        from paper_2511_14881_b200._device import u64_host
+        cores = host_cores()
+        nq = a.cpu_queries or min(2 * cores, 64)
+        items = idx.items.cpu().numpy()[:, : a.dim]
+        valid = u64_host(idx.valid)
+        ids = u64_host(idx.item_ids)
+        planes = idx.bloom.planes
+        qq = wl.queries_q.cpu().numpy()[:, : a.dim]
+        progs = progs_of(wl.filters)
+        qps, secs, n = time_cpu_oracle(items, valid, ids, planes, qq[:nq], progs[:nq], k, nq,
+                                       cores)
+        cpu = {"value": round(qps, 3), "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": (f"{n} queries (oracle codesigned_search over the full "
+                          f"{a.items // 1_000_000}M-item index, k={k}) in {secs:.1f} s on "
+                          f"{cores} forked workers")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_per_step, 4),
+            "p50_ms": round(float(np.median(per_step)), 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic (reference synth_catalog semantics, generated on device)",
+            "config": workload_desc(a, world), "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
+            "scan_kernel": "simt" if a.simt else "default",
+            "setup_s": round(gen_s, 1),
+        }
+        _ = sel
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------
+# reference arm: the CPU oracle port on the host cores
+# ------------------------------------------------------------------------------------
+def numpy_workload(n_items, n_queries, dim, seed=1, filter_seed=7):
+    """CPU generator with the same recipe as paper_2511_14881_b200.workload (NumPy)."""
+    from oracle import filtra_oracle as orc
+    rng = np.random.default_rng(seed)
+    n_clusters = max(1, n_items // 1000)
+    centers = rng.standard_normal((n_clusters, dim)).astype(np.float32)
+    centers /= np.linalg.norm(centers.astype(np.float64), axis=1, keepdims=True).astype(np.float32)
+    n_pad = (n_items + 63) // 64 * 64
+    emb = np.empty((n_items, dim), dtype=np.float32)
+    chunk = 1 << 20
+    for s in range(0, n_items, chunk):
+        e = min(n_items, s + chunk)
+        x = centers[rng.integers(0, n_clusters, e - s)] + \
+            rng.standard_normal((e - s, dim), dtype=np.float32) * np.float32(0.08)
+        x /= np.linalg.norm(x.astype(np.float64), axis=1, keepdims=True).astype(np.float32)
+        emb[s:e] = x
+    lo, hi = float(emb.min()), float(emb.max())
+    items = np.zeros((n_pad, dim), dtype=np.int8)
+    for s in range(0, n_items, chunk):
+        e = min(n_items, s + chunk)
+        items[s:e] = orc.quantize(emb[s:e], lo, hi)
+    rows = rng.integers(0, n_items, n_queries)
+    queries = emb[rows] + rng.standard_normal((n_queries, dim)).astype(np.float32) * np.float32(0.05)
+    qq = orc.quantize(queries, lo, hi)
+    del emb
+    # features -> planes, one distinct (fid, value) pair at a time
+    n_words = n_pad // 64
+    planes = np.zeros((1024, n_words), dtype=np.uint64)
+    spec = [(1, 50, 2), (2, 50, 2), (3, 40, 2), (4, 30, 2), (5, 20, 1), (6, 10, 1)]
+    for fid, card, vpi in spec:
+        a = rng.integers(0, card, n_items)
+        vals = [a]
+        if vpi == 2:
+            vals.append((a + 1 + rng.integers(0, card - 1, n_items)) % card)
+        for v in range(card):
+            has = np.zeros(n_pad, dtype=bool)
+            for arr in vals:
+                has[:n_items] |= arr == v
+            words = np.packbits(has, bitorder="little").view(np.uint64)
+            for p in orc.hash_positions(fid, v, 1024, 5):
+                planes[p] |= words
+    valid = orc.from_bool(np.arange(n_pad) < n_items)
+    ids = np.arange(n_pad, dtype=np.uint64)
+    frng = np.random.default_rng(filter_seed)
+    progs = []
+    for _ in range(n_queries):
+        groups = []
+        for (fid, card, _), size in zip(spec, (17, 17, 14, 11)):
+            vals = frng.choice(card, size=size, replace=False)
+            groups.append(("or", [("leaf", fid, int(v)) for v in vals]))
+        progs.append(orc.compile_expr(("and", groups), 1024, 5))
+    return items, valid, ids, planes, qq, progs
+
+
+def run_reference(a):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = host_cores()
+    t0 = time.perf_counter()
+    items, valid, ids, planes, qq, progs = numpy_workload(a.items, max(a.batch, cores), a.dim)
+    gen_s = time.perf_counter() - t0
+    per_step = a.cpu_queries or cores
+    _CPU.update(items=items, valid=valid, ids=ids, offs=np.array([[0, items.shape[0]]]),
+                planes=planes, qq=qq, progs=progs, k=a.k)
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(cores) as pool:
+        for _ in range(a.warmup):
+            pool.map(_cpu_query, range(per_step), chunksize=1)
+        for s in range(a.steps):
+            t = time.perf_counter()
+            pool.map(_cpu_query, range(s * per_step, (s + 1) * per_step), chunksize=1)
+            times.append(time.perf_counter() - t)
+    total = sum(times)
+    value = per_step * a.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": round(1e3 * total / a.steps, 2),
+        "p50_ms": round(1e3 * float(np.median(times)), 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+        "data": "synthetic (same recipe, generated with NumPy on the host)",
+        "config": workload_desc(a, 1),
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": (f"{per_step} queries per step (one per core), oracle "
+                                    f"codesigned_search over the full index, k={a.k}")},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "setup_s": round(gen_s, 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse_args()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()
