@@ -205,6 +205,7 @@ def run_ours(a):
 
     from paper_2511_14881_b200 import _native, workload
     from paper_2511_14881_b200.engine import TopkOp, merge_topk
+    from paper_2511_14881_b200.bloom import BloomParams
     from paper_2511_14881_b200.filter_query import FilterBatch
     from paper_2511_14881_b200.quantize import quantize_device
     from paper_2511_14881_b200.serve import exchange_topk
@@ -299,21 +300,17 @@ def run_ours(a):
     # ---- e2e through the public API with host buffers --------------------------------
     host_q = torch.empty((B, a.dim), dtype=torch.float32).pin_memory()
     host_q.copy_(wl.queries.cpu())
-    h_ops = torch.from_numpy(batch.host_ops.view(np.int16)).pin_memory()
-    h_off = torch.from_numpy(batch.host_op_offset).pin_memory()
-    h_leaf = torch.from_numpy(batch.host_leaf_pos).pin_memory()
     out_ids = torch.empty((B, k), dtype=torch.int64).pin_memory()
     out_sc = torch.empty((B, k), dtype=torch.int32).pin_memory()
     out_cnt = torch.empty((B,), dtype=torch.int32).pin_memory()
     dq = torch.empty((B, a.dim), dtype=torch.float32, device="cuda")
-    e2e_batch = FilterBatch(batch.host_leaf_pos, batch.host_op_offset, batch.host_ops,
-                            batch.max_stack, None, batch.push_leaf_bits).to_device()
+    e2e_batch = FilterBatch.pack(wl.filters, BloomParams()).to_device()
+    h_prog = [torch.from_numpy(x).pin_memory() for x in e2e_batch.host_arrays()]
 
     def e2e_step():
         dq.copy_(host_q, non_blocking=True)
-        e2e_batch._dev[0].copy_(h_leaf, non_blocking=True)
-        e2e_batch._dev[1].copy_(h_off, non_blocking=True)
-        e2e_batch._dev[2].copy_(h_ops, non_blocking=True)
+        for d, h in zip(e2e_batch._dev, h_prog):
+            d.copy_(h, non_blocking=True)
         res = step(dq, e2e_batch)
         out_ids.copy_(res.ids, non_blocking=True)
         out_sc.copy_(res.scores, non_blocking=True)
@@ -335,7 +332,7 @@ def run_ours(a):
         t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    h2d = host_q.numel() * 4 + h_ops.numel() * 2 + h_off.numel() * 4 + h_leaf.numel() * 2
+    h2d = host_q.numel() * 4 + sum(h.numel() * h.element_size() for h in h_prog)
     d2h = out_ids.numel() * 8 + out_sc.numel() * 4 + out_cnt.numel() * 4
     e2e = {"value": round(B * a.steps / (e2e_ms / 1e3), 1), "unit": UNIT,
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

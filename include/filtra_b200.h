@@ -90,7 +90,26 @@ typedef struct fb_filter_prog {
   const int16_t* leaf_pos;
   const int32_t* op_offset;
   const uint16_t* ops;
+  /* Register-machine form consumed by the tensor-core scan (all nullable; when absent
+   * the SIMT scan is used). The batch's distinct planes are staged per tile in
+   * plane_list order; leaf_slot holds each leaf's positions as indices into that list.
+   *   rops: (ropcode << 13) | leaf, ropcodes FB_ROP_*; rmax_stack = its max depth. */
+  int32_t n_planes;
+  int32_t rmax_stack;
+  const int16_t* plane_list;   /* [n_planes] */
+  const int16_t* leaf_slot;    /* [n_leaves * k_max] */
+  const int32_t* rop_offset;   /* [n_queries + 1] */
+  const uint16_t* rops;
 } fb_filter_prog_t;
+
+/* Register-machine opcodes: PUSH l | PUSHN l (push ~leaf) | ANDL l (top &= leaf) |
+ * ORL l (top |= leaf) | ANDS / ORS (pop, combine) | NOT (top = ~top). Peephole-lowered
+ * from the postfix ops on the host; NOT without "& valid" is exact because the final
+ * result is ANDed with validity. */
+enum fb_ropcode {
+  FB_ROP_PUSH = 0, FB_ROP_PUSHN = 1, FB_ROP_ANDL = 2, FB_ROP_ORL = 3,
+  FB_ROP_ANDS = 4, FB_ROP_ORS = 5, FB_ROP_NOT = 6
+};
 
 /* Work counters (ivf.ScanStats + bloom.FilterStats), filled analytically by the plan. */
 typedef struct fb_stats {
@@ -169,6 +188,12 @@ int fb_topk_execute(fb_topk_plan_t* plan, const int8_t* queries_q, const fb_filt
 /* Measurement hooks: total kernel launches issued by this library (process-wide), and
  * CUDA-event timing of the emit scan and the selection of a plan's last execute. */
 uint64_t fb_launch_count(void);
+/* 1 when the plan's last execute ran its emit pass on the tcgen05 kernel, 0 for SIMT. */
+int fb_topk_scan_path(const fb_topk_plan_t* plan);
+/* Testing: raw int32 scores of every (query, slot) from the tcgen05 kernel (unfiltered,
+ * all slots); out [n_queries, idx->n_slots]. Synchronous. */
+int fb_debug_tc_scores(const fb_index_t* idx, const int8_t* queries_q, int32_t n_queries,
+                       int32_t* out, void* stream);
 int fb_topk_set_timing(fb_topk_plan_t* plan, int32_t enable);
 int fb_topk_last_timing(fb_topk_plan_t* plan, float* emit_ms, float* select_ms);
 

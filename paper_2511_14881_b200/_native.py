@@ -45,7 +45,7 @@ EXPORTED = (
     "fb_filter_eval", "fb_quantize", "fb_quantize_f64", "fb_row_sums", "fb_topk_plan_create",
     "fb_topk_plan_destroy", "fb_topk_plan_stats", "fb_topk_execute", "fb_merge_topk",
     "fb_dequant_scores", "fb_int8_dot_rows", "fb_dot_rows_f64", "fb_launch_count",
-    "fb_topk_set_timing", "fb_topk_last_timing",
+    "fb_topk_set_timing", "fb_topk_last_timing", "fb_topk_scan_path", "fb_debug_tc_scores",
 )
 
 
@@ -64,6 +64,8 @@ class FbFilterProg(ctypes.Structure):
         ("n_queries", ctypes.c_int32), ("n_leaves", ctypes.c_int32),
         ("k_max", ctypes.c_int32), ("max_stack", ctypes.c_int32),
         ("leaf_pos", c_vp), ("op_offset", c_vp), ("ops", c_vp),
+        ("n_planes", ctypes.c_int32), ("rmax_stack", ctypes.c_int32),
+        ("plane_list", c_vp), ("leaf_slot", c_vp), ("rop_offset", c_vp), ("rops", c_vp),
     ]
 
 
@@ -122,6 +124,8 @@ def _declare(lib) -> None:
         "fb_int8_dot_rows": ([c_vp, i64, i32, i32, c_vp, c_vp, c_vp], i32),
         "fb_dot_rows_f64": ([c_vp, i64, i32, c_vp, c_vp, c_vp], i32),
         "fb_launch_count": ([], ctypes.c_uint64),
+        "fb_topk_scan_path": ([c_vp], i32),
+        "fb_debug_tc_scores": ([ctypes.POINTER(FbIndex), c_vp, i32, c_vp, c_vp], i32),
         "fb_topk_set_timing": ([c_vp, i32], i32),
         "fb_topk_last_timing": ([c_vp, ctypes.POINTER(ctypes.c_float),
                                  ctypes.POINTER(ctypes.c_float)], i32),

@@ -63,6 +63,11 @@ struct fb_topk_plan {
   Fallback* d_fb = nullptr;
   uint32_t* d_hist = nullptr;
   uint32_t* d_active = nullptr;  // [0] flagged & unresolved, [1] resolved, [2] total flagged
+  int32_t* d_tc_work = nullptr;  // (tile, range) pairs for the tensor-core scan
+  int64_t n_tc_work = 0;
+  int64_t tc_sample_stride = 0;
+  double tc_sample_fraction = 0.0;
+  int32_t last_scan_tc = 0;      // 1 when the last execute's emit pass ran on tcgen05
   // optional per-stage timing (CUDA events on the execute stream)
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -232,6 +237,18 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
   }
   p->n_ranges = (int32_t)(p->h_ranges.size() / 2);
   p->total_words = prefix.back();
+  // tensor-core work list: (256-slot tile, range) pairs covering every range
+  std::vector<int32_t> tc_work;
+  if (idx->n_slots % 256 == 0) {
+    for (int r = 0; r < p->n_ranges; ++r) {
+      const int64_t t0 = p->h_ranges[2 * r] / 256, t1 = (p->h_ranges[2 * r + 1] + 255) / 256;
+      for (int64_t t = t0; t < t1; ++t) {
+        tc_work.push_back((int32_t)t);
+        tc_work.push_back(r);
+      }
+    }
+  }
+  p->n_tc_work = (int64_t)tc_work.size() / 2;
   const int64_t want = std::max<int64_t>(2LL * k + 2048, 8192);
   p->cap = (int32_t)std::max<int64_t>(1, std::min<int64_t>(p->total_slots, want));
   // sampling pass only when the candidate buffer cannot simply hold everything
@@ -241,6 +258,13 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
     p->sample_stride = std::max<int64_t>(1, p->total_words / target_words);
     const int64_t sampled = (p->total_words + p->sample_stride - 1) / p->sample_stride;
     p->sample_fraction = (double)sampled / (double)p->total_words;
+    if (p->n_tc_work > 0) {
+      const int64_t target_tiles = std::max<int64_t>(std::min<int64_t>(p->n_tc_work, 1024),
+                                                     p->n_tc_work / 32);
+      p->tc_sample_stride = std::max<int64_t>(1, p->n_tc_work / target_tiles);
+      const int64_t st = (p->n_tc_work + p->tc_sample_stride - 1) / p->tc_sample_stride;
+      p->tc_sample_fraction = (double)st / (double)p->n_tc_work;
+    }
   }
   const int64_t B = std::max(1, n_queries);
   const int64_t nr = std::max(1, p->n_ranges);
@@ -263,6 +287,7 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
   const size_t o_fb = carve(sizeof(Fallback) * B);
   const size_t o_hist = carve(sizeof(uint32_t) * B * kHistBins);
   const size_t o_active = carve(sizeof(uint32_t) * 4);
+  const size_t o_tc = carve(sizeof(int32_t) * std::max<size_t>(2, tc_work.size()));
   cudaError_t e = cudaMalloc(&p->dev, off);
   if (e != cudaSuccess) {
     delete p;
@@ -282,11 +307,15 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
   p->d_fb = reinterpret_cast<Fallback*>(base + o_fb);
   p->d_hist = reinterpret_cast<uint32_t*>(base + o_hist);
   p->d_active = reinterpret_cast<uint32_t*>(base + o_active);
+  p->d_tc_work = reinterpret_cast<int32_t*>(base + o_tc);
   if (p->n_ranges > 0) {
     e = cudaMemcpy(p->d_ranges, p->h_ranges.data(), sizeof(int64_t) * p->h_ranges.size(),
                    cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
       e = cudaMemcpy(p->d_word_prefix, prefix.data(), sizeof(int64_t) * prefix.size(),
+                     cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !tc_work.empty())
+      e = cudaMemcpy(p->d_tc_work, tc_work.data(), sizeof(int32_t) * tc_work.size(),
                      cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
       cudaFree(p->dev);
@@ -351,13 +380,14 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
   a.fb = nullptr;
   a.hist = p->d_hist;
   a.active_count = nullptr;
-  const bool use_tc = !(p->flags & FB_PLAN_SIMT);
+  a.tc_work = p->d_tc_work;
+  a.n_tc_work = p->n_tc_work;
+  a.mode = SCAN_EMIT;
+  const bool use_tc = !(p->flags & FB_PLAN_SIMT) && p->n_tc_work > 0 && scan_tc_supported(a);
+  p->last_scan_tc = use_tc ? 1 : 0;
 
   auto emit = [&](ScanArgs& sa) -> int {
-    if (use_tc && scan_tc_supported(sa)) {
-      const int r = launch_scan_tc(sa, s);
-      if (r != FB_ERR_UNSUPPORTED) return r;
-    }
+    if (use_tc) return launch_scan_tc(sa, s);
     return launch_scan_simt(sa, s);
   };
 
@@ -370,7 +400,9 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
     t.sample_cap = p->sample_cap;
     t.sample_key = p->d_sample_key;
     t.sample_cnt = p->d_sample_cnt;
-    t.sample_fraction = p->sample_stride ? p->sample_fraction : 0.0;
+    t.sample_fraction = !p->sample_stride ? 0.0
+                        : use_tc          ? p->tc_sample_fraction
+                                          : p->sample_fraction;
     t.threshold = p->d_threshold;
     t.cnt = p->d_cnt;
     t.elig = p->d_elig;
@@ -379,7 +411,7 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
       FB_CUDA(cudaMemsetAsync(p->d_sample_elig, 0, sizeof(uint32_t) * p->B, s));
       ScanArgs sa = a;
       sa.mode = SCAN_EMIT;
-      sa.word_stride = p->sample_stride;
+      sa.word_stride = use_tc ? p->tc_sample_stride : p->sample_stride;
       sa.threshold = nullptr;
       sa.out_key = p->d_sample_key;
       sa.out_slot = nullptr;
@@ -407,7 +439,7 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
     if (p->timing) FB_CUDA(cudaEventRecord(p->ev[1], s));
     // 4) exactness check; 5) fallback: radix-narrow the key window (<= 6 passes, each a
     //    no-op unless some query was flagged), then re-emit the resolved queries
-    rc = launch_check(p->B, k, p->cap, p->d_cnt, p->d_elig,
+    rc = launch_check(p->B, k, p->cap, p->d_cnt, p->d_threshold,
                       (p->flags & FB_PLAN_FORCE_FALLBACK) ? 1 : 0, p->d_fb, p->d_active,
                       p->d_active + 2, s);
     if (rc) return rc;
@@ -465,6 +497,43 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
 }
 
 uint64_t fb_launch_count(void) { return g_launches.load(); }
+
+int fb_topk_scan_path(const fb_topk_plan_t* p) { return p == nullptr ? -1 : p->last_scan_tc; }
+
+int fb_debug_tc_scores(const fb_index_t* idx, const int8_t* queries_q, int32_t n_queries,
+                       int32_t* out, void* stream) {
+  const int64_t full[2] = {0, idx ? idx->n_slots : 0};
+  fb_topk_plan_t* p = nullptr;
+  int rc = fb_topk_plan_create(idx, n_queries, 1, full, 1, FB_PLAN_NO_SAMPLE, &p);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ScanArgs a{};
+  a.idx = p->idx;
+  a.queries = queries_q;
+  a.n_queries = n_queries;
+  a.ranges = p->d_ranges;
+  a.word_prefix = p->d_word_prefix;
+  a.n_ranges = p->n_ranges;
+  a.total_words = p->total_words;
+  a.mode = SCAN_EMIT;
+  a.word_stride = 1;
+  a.out_key = p->d_cand_key;
+  a.out_slot = p->d_cand_slot;
+  a.out_cnt = p->d_cnt;
+  a.out_elig = p->d_elig;
+  a.cap = p->cap;
+  a.tc_work = p->d_tc_work;
+  a.n_tc_work = p->n_tc_work;
+  a.dump = out;
+  a.dump_ld = idx->n_slots;
+  rc = p->n_tc_work > 0 ? launch_scan_tc(a, s) : FB_ERR_UNSUPPORTED;
+  if (rc == FB_ERR_UNSUPPORTED) fail(rc, "shape not supported by the tcgen05 scan");
+  cudaError_t e = cudaStreamSynchronize(s);
+  fb_topk_plan_destroy(p);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "fb_debug_tc_scores");
+  return FB_OK;
+}
 
 int fb_topk_set_timing(fb_topk_plan_t* p, int32_t enable) {
   if (p == nullptr) return fail(FB_ERR_INVALID, "plan is NULL");

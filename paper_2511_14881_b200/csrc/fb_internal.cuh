@@ -125,6 +125,12 @@ struct ScanArgs {
   uint32_t* hist;             // [B, kHistBins]
   const uint32_t* active_count;  // early-exit when *active_count == 0 (nullable)
   uint32_t only_state;        // process only queries whose fb state == only_state (if fb != null)
+  // tensor-core path: work list of (256-slot tile, range index) pairs; word_stride then
+  // strides over this list
+  const void* tc_work;        // int2 [n_tc_work]
+  int64_t n_tc_work;
+  int32_t* dump;              // testing: raw scores [B, dump_ld] (nullable)
+  int64_t dump_ld;
 };
 
 // kernels / launchers implemented in fb_kernels.cu
@@ -188,7 +194,7 @@ struct ThresholdArgs {
 int launch_threshold(const ThresholdArgs& a, cudaStream_t s);
 
 int launch_check(int32_t n_queries, int32_t k, int32_t cap, const uint32_t* cnt,
-                 const uint32_t* elig, int force, Fallback* fb, uint32_t* active_count,
+                 const uint64_t* thr, int force, Fallback* fb, uint32_t* active_count,
                  uint32_t* total_flagged, cudaStream_t s);
 int launch_resolve(int32_t n_queries, int32_t k, int32_t cap, Fallback* fb, uint32_t* hist,
                    uint64_t* threshold, uint32_t* cnt, uint32_t* elig, uint32_t* active_count,

@@ -326,12 +326,14 @@ __global__ void __launch_bounds__(kSelectThreads) k_threshold(ThresholdArgs a) {
 
 // Flag queries whose emit pass over- or under-flowed (or all, when forced).
 __global__ void k_check(int n_queries, int k, int cap, const uint32_t* __restrict__ cnt,
-                        const uint32_t* __restrict__ elig, int force, Fallback* fb,
+                        const uint64_t* __restrict__ thr, int force, Fallback* fb,
                         uint32_t* active, uint32_t* total_flagged) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n_queries) return;
-  const uint32_t c = cnt[q], e = elig[q];
-  const bool ok = c <= (uint32_t)cap && (c >= (uint32_t)k || c == e);
+  const uint32_t c = cnt[q];
+  // exact when every key >= T was kept and either k of them exist or T admits all
+  const bool ok = c <= (uint32_t)cap && (c >= (uint32_t)k || thr[q] == 0ull);
+
   Fallback f;
   f.lo = 0;
   f.shift = 52;
@@ -676,10 +678,10 @@ int launch_threshold(const ThresholdArgs& a, cudaStream_t s) {
 }
 
 int launch_check(int32_t n_queries, int32_t k, int32_t cap, const uint32_t* cnt,
-                 const uint32_t* elig, int force, Fallback* fb, uint32_t* active,
+                 const uint64_t* thr, int force, Fallback* fb, uint32_t* active,
                  uint32_t* total_flagged, cudaStream_t s) {
   if (n_queries <= 0) return FB_OK;
-  k_check<<<(n_queries + 255) / 256, 256, 0, s>>>(n_queries, k, cap, cnt, elig, force, fb, active,
+  k_check<<<(n_queries + 255) / 256, 256, 0, s>>>(n_queries, k, cap, cnt, thr, force, fb, active,
                                                   total_flagged);
   FB_LAUNCH_CHECK("k_check");
   return FB_OK;

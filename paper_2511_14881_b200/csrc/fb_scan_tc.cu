@@ -1,10 +1,601 @@
-// tcgen05 (sm_100a) emit scan -- placeholder until the tensor-core path lands.
+// Fused Bloom-filter + int8 scan emit kernel on the 5th-gen tensor cores (sm_100a).
+//
+// One persistent CTA per SM walks 256-item tiles (4 validity/plane words). Per tile:
+//   warp 0      TMA-loads the 256 x 128 B item rows (SWIZZLE_128B) and bulk-copies the
+//               batch's referenced Bloom plane words (32 B per plane) into shared memory;
+//   warp 1      issues tcgen05.mma.kind::i8 (M = 128 queries, N = 256 items, K = 4 x 32)
+//               into a double-buffered int32 accumulator in TMEM (2 x 256 columns);
+//   warps 2-3   AND each distinct leaf's planes into per-tile leaf masks (the paper's
+//               and.b64 Bloom test, 64 items per op);
+//   warps 4-11  read the scores back with tcgen05.ld (thread = query, 128 items), gate
+//               on the query's running key threshold, evaluate the query's filter
+//               program only where some score clears the gate, and append surviving
+//               (key, slot) candidates -- filtered-out items never leave the SM.
+// Semantics are those of reference ivf.search_clusters (ivf.py:285-334) restricted by
+// filter_query.eval_compiled (filter_query.py:314-356): eligible = valid & range & mask &
+// program; score = exact int32 dot; candidates = eligible with key >= threshold.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
 #include "fb_internal.cuh"
 
 namespace fb {
+namespace {
 
-bool scan_tc_supported(const ScanArgs&) { return false; }
+constexpr int kTileItems = 256;
+constexpr int kTileWords = 4;
+constexpr int kBlockM = 128;
+constexpr int kMaxMBlocks = 2;
+constexpr int kMaxQueries = kBlockM * kMaxMBlocks;
+constexpr int kKBytes = 128;
+constexpr int kUmmaK = 32;
+constexpr int kAccCols = 256;
+constexpr int kThreads = 384;
+constexpr int kLeafThreads = 64;
+constexpr int kEpiWarps = 8;
+constexpr int kRegStack = 4;
+constexpr uint32_t kItemBytes = kTileItems * kKBytes;  // 32 KB
 
-int launch_scan_tc(const ScanArgs&, cudaStream_t) { return FB_ERR_UNSUPPORTED; }
+struct TcArgs {
+  const int8_t* queries;
+  int32_t nq;
+  int32_t n_mblk;
+  const uint64_t* planes;
+  const uint64_t* valid;
+  const uint32_t* id_rank;
+  const uint64_t* masks;
+  int64_t n_words;
+  int32_t has_prog;
+  int32_t n_planes;
+  int32_t n_leaves;
+  int32_t k_max;
+  const int16_t* plane_list;
+  const int16_t* leaf_slot;
+  const int32_t* rop_offset;
+  const uint16_t* rops;
+  const int2* work;
+  int64_t n_sel;
+  int64_t work_stride;
+  const int64_t* ranges;
+  const uint64_t* threshold;
+  uint64_t* out_key;
+  uint32_t* out_slot;
+  uint32_t* out_cnt;
+  int32_t cap;
+  int32_t* dump;
+  int64_t dump_ld;
+  int32_t item_stages;
+  uint32_t off_a, off_b, off_p, off_l, off_ls, off_thr, off_bar, plane_stage_bytes,
+      leaf_stage_bytes;
+};
+
+// ---- PTX helpers ----------------------------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = su32(b);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0,
+                                            int32_t c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (8-row groups 1024 B apart).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;        // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                  // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+  return d;
+}
+
+// kind::i8 instruction descriptor: s32 accumulate, s8 x s8, both K-major, M = 128, N = 256
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ uint64_t word_range_mask(int64_t word_slot, int64_t s0, int64_t s1) {
+  const int64_t lo = s0 > word_slot ? s0 - word_slot : 0;
+  const int64_t hi = s1 - word_slot < 64 ? s1 - word_slot : 64;
+  if (hi <= lo) return 0ull;
+  const uint64_t upto = hi >= 64 ? ~0ull : ((1ull << hi) - 1);
+  return upto & ~((1ull << lo) - 1);
+}
+
+// Register-machine filter evaluation over two 64-slot words (128 items). The stack lives
+// in registers (static shifts), so the whole program runs without local memory.
+__device__ __forceinline__ void eval_rops(const uint16_t* __restrict__ rops, int o0, int o1,
+                                          const uint64_t* L, int half, uint64_t& r0,
+                                          uint64_t& r1) {
+  uint64_t a0[kRegStack], a1[kRegStack];
+#pragma unroll
+  for (int i = 0; i < kRegStack; ++i) a0[i] = a1[i] = 0ull;
+  for (int o = o0; o < o1; ++o) {
+    const uint32_t op = __ldg(rops + o);
+    const uint32_t code = op >> 13, leaf = op & 0x1FFF;
+    const ulonglong2 m = *reinterpret_cast<const ulonglong2*>(L + leaf * kTileWords + 2 * half);
+    switch (code) {
+      case FB_ROP_PUSH:
+      case FB_ROP_PUSHN: {
+        const uint64_t x0 = code == FB_ROP_PUSH ? m.x : ~m.x;
+        const uint64_t x1 = code == FB_ROP_PUSH ? m.y : ~m.y;
+#pragma unroll
+        for (int i = kRegStack - 1; i > 0; --i) { a0[i] = a0[i - 1]; a1[i] = a1[i - 1]; }
+        a0[0] = x0;
+        a1[0] = x1;
+        break;
+      }
+      case FB_ROP_ANDL: a0[0] &= m.x; a1[0] &= m.y; break;
+      case FB_ROP_ORL: a0[0] |= m.x; a1[0] |= m.y; break;
+      case FB_ROP_NOT: a0[0] = ~a0[0]; a1[0] = ~a1[0]; break;
+      default: {  // ANDS / ORS
+        const bool is_and = code == FB_ROP_ANDS;
+        a0[0] = is_and ? (a0[1] & a0[0]) : (a0[1] | a0[0]);
+        a1[0] = is_and ? (a1[1] & a1[0]) : (a1[1] | a1[0]);
+#pragma unroll
+        for (int i = 1; i < kRegStack - 1; ++i) { a0[i] = a0[i + 1]; a1[i] = a1[i + 1]; }
+        break;
+      }
+    }
+  }
+  r0 = a0[0];
+  r1 = a1[0];
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_scan_tc(const __grid_constant__ CUtensorMap tmap_items, const TcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem + a.off_a;
+  uint8_t* sB = smem + a.off_b;
+  uint8_t* sP = smem + a.off_p;
+  uint8_t* sL = smem + a.off_l;
+  int16_t* sLS = reinterpret_cast<int16_t*>(smem + a.off_ls);
+  uint64_t* sT = reinterpret_cast<uint64_t*>(smem + a.off_thr);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.off_bar);
+  uint64_t* items_full = bars;
+  uint64_t* items_empty = bars + 4;
+  uint64_t* planes_full = bars + 8;
+  uint64_t* planes_empty = bars + 10;
+  uint64_t* leaf_full = bars + 12;
+  uint64_t* leaf_empty = bars + 14;
+  uint64_t* acc_full = bars + 16;
+  uint64_t* acc_empty = bars + 18;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = a.item_stages;
+
+  // ---- prologue: queries -> swizzled smem, thresholds, leaf -> plane-slot table ------
+  const int a_rows = a.n_mblk * kBlockM;
+  for (int i = threadIdx.x; i < a_rows * 8; i += kThreads) {
+    const int r = i >> 3, c = i & 7;
+    int4 v = make_int4(0, 0, 0, 0);
+    if (r < a.nq) v = __ldg(reinterpret_cast<const int4*>(a.queries + (int64_t)r * kKBytes) + c);
+    *reinterpret_cast<int4*>(sA + r * kKBytes + ((c ^ (r & 7)) << 4)) = v;
+  }
+  for (int q = threadIdx.x; q < kMaxQueries; q += kThreads)
+    sT[q] = (a.threshold != nullptr && q < a.nq) ? a.threshold[q] : 0ull;
+  if (a.has_prog)
+    for (int i = threadIdx.x; i < a.n_leaves * a.k_max; i += kThreads) sLS[i] = a.leaf_slot[i];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(items_full + s, 1);
+      mbar_init(items_empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(planes_full + s, 1);
+      mbar_init(planes_empty + s, kLeafThreads);
+      mbar_init(leaf_full + s, kLeafThreads);
+      mbar_init(leaf_empty + s, kEpiWarps);
+      mbar_init(acc_full + s, 1);
+      mbar_init(acc_empty + s, kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int64_t n_sel = a.n_sel;
+  if (warp == 0) {
+    // ================= producer: TMA item tile + Bloom plane words ================
+    int it = 0;
+    for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
+      const int tile = a.work[i * a.work_stride].x;
+      const int s = it % S;
+      const uint32_t ph = (uint32_t)(it / S) & 1u;
+      if (lane == 0) {
+        mbar_wait(items_empty + s, ph ^ 1u);
+        mbar_expect_tx(items_full + s, kItemBytes);
+        tma_load_2d(sB + (size_t)s * kItemBytes, &tmap_items, 0, tile * kTileItems, items_full + s);
+      }
+      if (a.has_prog && a.n_planes > 0) {
+        const int ps = it & 1;
+        const uint32_t pph = (uint32_t)(it >> 1) & 1u;
+        mbar_wait(planes_empty + ps, pph ^ 1u);
+        if (lane == 0) mbar_expect_tx(planes_full + ps, (uint32_t)a.n_planes * 32u);
+        __syncwarp();
+        uint8_t* dst = sP + (size_t)ps * a.plane_stage_bytes;
+        for (int p = lane; p < a.n_planes; p += 32) {
+          const uint64_t* src = a.planes + (int64_t)a.plane_list[p] * a.n_words +
+                                (int64_t)tile * kTileWords;
+          bulk_load(dst + p * 32, src, 32u, planes_full + ps);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (one thread) ====================================
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_i8(kBlockM, kTileItems);
+      int it = 0, acc_it = 0;
+      for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
+        const int s = it % S;
+        const uint32_t ph = (uint32_t)(it / S) & 1u;
+        mbar_wait(items_full + s, ph);
+        tc_fence_after();
+        const uint32_t b_base = su32(sB + (size_t)s * kItemBytes);
+        for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
+          const int ab = acc_it & 1;
+          const uint32_t aph = (uint32_t)(acc_it >> 1) & 1u;
+          mbar_wait(acc_empty + ab, aph ^ 1u);
+          tc_fence_after();
+          const uint32_t a_base = su32(sA + mb * kBlockM * kKBytes);
+          const uint32_t d = tmem_base + (uint32_t)(ab * kAccCols);
+#pragma unroll
+          for (int kk = 0; kk < kKBytes / kUmmaK; ++kk)
+            umma_i8(d, sw128_desc(a_base + kk * kUmmaK), sw128_desc(b_base + kk * kUmmaK), idesc,
+                    kk > 0 ? 1u : 0u);
+          umma_commit(acc_full + ab);
+        }
+        umma_commit(items_empty + s);
+      }
+    }
+  } else if (warp < 4) {
+    // ================= leaf builders: AND each leaf's planes per word =============
+    if (a.has_prog) {
+      const int t = threadIdx.x - 64;
+      int it = 0;
+      for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
+        const int st = it & 1;
+        const uint32_t ph = (uint32_t)(it >> 1) & 1u;
+        if (a.n_planes > 0) mbar_wait(planes_full + st, ph);
+        mbar_wait(leaf_empty + st, ph ^ 1u);
+        const uint64_t* P = reinterpret_cast<const uint64_t*>(sP + (size_t)st * a.plane_stage_bytes);
+        uint64_t* L = reinterpret_cast<uint64_t*>(sL + (size_t)st * a.leaf_stage_bytes);
+        for (int e = t; e < a.n_leaves * kTileWords; e += kLeafThreads) {
+          const int l = e >> 2, w = e & 3;
+          uint64_t m = ~0ull;
+          for (int j = 0; j < a.k_max; ++j) {
+            const int sl = sLS[l * a.k_max + j];
+            if (sl < 0) break;
+            m &= P[sl * kTileWords + w];
+          }
+          L[e] = m;
+        }
+        if (a.n_planes > 0) mbar_arrive(planes_empty + st);
+        mbar_arrive(leaf_full + st);
+      }
+    }
+  } else {
+    // ================= epilogue: TMEM -> registers -> gate -> filter -> emit ======
+    const int ew = warp - 4;
+    const int quad = warp & 3;  // TMEM lane quadrant accessible to this warp
+    const int half = ew >> 2;   // item columns [half * 128, half * 128 + 128)
+    const int row = quad * 32 + lane;
+    int it = 0, acc_it = 0;
+    for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
+      const int2 wk = a.work[i * a.work_stride];
+      const int64_t tile = wk.x;
+      const int64_t s0 = a.ranges[2 * wk.y], s1 = a.ranges[2 * wk.y + 1];
+      const int64_t wbase = tile * kTileWords + 2 * half;
+      const uint64_t v0 = a.valid[wbase] & word_range_mask(wbase * 64, s0, s1);
+      const uint64_t v1 = a.valid[wbase + 1] & word_range_mask((wbase + 1) * 64, s0, s1);
+      const int st = it & 1;
+      const uint32_t lph = (uint32_t)(it >> 1) & 1u;
+      if (a.has_prog) mbar_wait(leaf_full + st, lph);
+      const uint64_t* L = reinterpret_cast<const uint64_t*>(sL + (size_t)st * a.leaf_stage_bytes);
+      for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
+        const int ab = acc_it & 1;
+        const uint32_t aph = (uint32_t)(acc_it >> 1) & 1u;
+        mbar_wait(acc_full + ab, aph);
+        tc_fence_after();
+        const int q = mb * kBlockM + row;
+        const bool active = q < a.nq;
+        const uint64_t T = active ? sT[q] : ~0ull;
+        const int32_t tau = T == 0ull ? INT32_MIN : key_score(T);
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kAccCols + half * 128);
+        int32_t r[32];
+        uint32_t need = 0;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          tmem_ld32(taddr + c * 32, r);
+          if (a.dump != nullptr && active) {
+            const int64_t base = tile * kTileItems + half * 128 + c * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (base + j < a.dump_ld) a.dump[(int64_t)q * a.dump_ld + base + j] = r[j];
+          }
+          int32_t mx = r[0];
+#pragma unroll
+          for (int j = 1; j < 31; j += 2) mx = __vimax3_s32(mx, r[j], r[j + 1]);
+          mx = max(mx, r[31]);
+          if (mx >= tau) need |= 1u << c;
+        }
+        uint64_t f0 = 0ull, f1 = 0ull;
+        if (active && need != 0u) {
+          f0 = v0;
+          f1 = v1;
+          if (a.has_prog) {
+            const int o0 = a.rop_offset[q], o1 = a.rop_offset[q + 1];
+            if (o1 > o0) {
+              uint64_t e0, e1;
+              eval_rops(a.rops, o0, o1, L, half, e0, e1);
+              f0 &= e0;
+              f1 &= e1;
+            }
+          }
+          if (a.masks != nullptr) {
+            f0 &= a.masks[(int64_t)q * a.n_words + wbase];
+            f1 &= a.masks[(int64_t)q * a.n_words + wbase + 1];
+          }
+        }
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          const uint64_t fw64 = c < 2 ? f0 : f1;
+          uint32_t fw = (uint32_t)(fw64 >> (32 * (c & 1)));
+          if (!((need >> c) & 1u)) fw = 0u;
+          if (__any_sync(0xffffffffu, fw != 0u)) {
+            tmem_ld32(taddr + c * 32, r);
+            if (fw != 0u) {
+              const int64_t slot0 = tile * kTileItems + half * 128 + c * 32;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (((fw >> j) & 1u) && r[j] >= tau) {
+                  const int64_t slot = slot0 + j;
+                  const uint64_t key = make_key(r[j], __ldg(a.id_rank + slot));
+                  if (key >= T) {
+                    const uint32_t p = atomicAdd(a.out_cnt + q, 1u);
+                    if (p < (uint32_t)a.cap) {
+                      a.out_key[(int64_t)q * a.cap + p] = key;
+                      if (a.out_slot) a.out_slot[(int64_t)q * a.cap + p] = (uint32_t)slot;
+                    }
+                  }
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + ab);
+      }
+      if (a.has_prog) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(leaf_empty + st);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512)
+                 : "memory");
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// shared-memory carve-up; returns total bytes (incl. 1 KB alignment slack) or 0 if too big
+size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int stages) {
+  size_t off = 0;
+  t.off_a = 0;
+  off = (size_t)n_mblk * kBlockM * kKBytes;
+  t.off_b = (uint32_t)align_up(off, 1024);
+  off = t.off_b + (size_t)stages * kItemBytes;
+  t.plane_stage_bytes = (uint32_t)align_up((size_t)(n_planes > 0 ? n_planes : 1) * 32, 128);
+  t.off_p = (uint32_t)align_up(off, 128);
+  off = t.off_p + 2ull * t.plane_stage_bytes;
+  t.leaf_stage_bytes = (uint32_t)align_up((size_t)(n_leaves > 0 ? n_leaves : 1) * 32, 128);
+  t.off_l = (uint32_t)align_up(off, 128);
+  off = t.off_l + 2ull * t.leaf_stage_bytes;
+  t.off_ls = (uint32_t)align_up(off, 16);
+  off = t.off_ls + (size_t)(n_leaves > 0 ? n_leaves : 1) * (k_max > 0 ? k_max : 1) * 2;
+  t.off_thr = (uint32_t)align_up(off, 16);
+  off = t.off_thr + (size_t)kMaxQueries * 8;
+  t.off_bar = (uint32_t)align_up(off, 16);
+  off = t.off_bar + 21 * 8 + 16;
+  return off + 1024;
+}
+
+constexpr size_t kSmemLimit = 227 * 1024;
+
+bool pick_stages(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, size_t& smem) {
+  for (int stages = 4; stages >= 2; --stages) {
+    smem = layout(t, n_mblk, n_planes, n_leaves, k_max, stages);
+    if (smem <= kSmemLimit) {
+      t.item_stages = stages;
+      return true;
+    }
+  }
+  return false;
+}
+
+}  // namespace
+
+bool scan_tc_supported(const ScanArgs& a) {
+  if (a.mode != SCAN_EMIT || a.fb != nullptr) return false;
+  if (a.idx.dim_pad != kKBytes) return false;
+  if (a.idx.n_slots % kTileItems != 0 || a.tc_work == nullptr) return false;
+  if (encode_fn() == nullptr) return false;
+  if (a.has_prog) {
+    if (a.prog.rops == nullptr || a.prog.rmax_stack > kRegStack) return false;
+    if (a.prog.n_leaves >= (1 << 13)) return false;
+    TcArgs t{};
+    size_t smem = 0;
+    const int n_mblk = a.n_queries >= kBlockM ? kMaxMBlocks : 1;
+    if (!pick_stages(t, n_mblk, a.prog.n_planes, a.prog.n_leaves, a.prog.k_max, smem))
+      return false;
+  }
+  return true;
+}
+
+int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
+  if (!scan_tc_supported(a)) return FB_ERR_UNSUPPORTED;
+  const int64_t n_sel = (a.n_tc_work + a.word_stride - 1) / a.word_stride;
+  if (n_sel <= 0 || a.n_queries <= 0) return FB_OK;
+  CUtensorMap tmap;
+  const cuuint64_t dims[2] = {(cuuint64_t)kKBytes, (cuuint64_t)a.idx.n_slots};
+  const cuuint64_t strides[1] = {(cuuint64_t)a.idx.dim_pad};
+  const cuuint32_t box[2] = {(cuuint32_t)kKBytes, (cuuint32_t)kTileItems};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                            const_cast<int8_t*>(a.idx.items), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(FB_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  int n_sm = 148;
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = (int)(n_sel < n_sm ? n_sel : n_sm);
+  for (int q0 = 0; q0 < a.n_queries; q0 += kMaxQueries) {
+    const int nq = a.n_queries - q0 < kMaxQueries ? a.n_queries - q0 : kMaxQueries;
+    TcArgs t{};
+    t.queries = a.queries + (int64_t)q0 * a.idx.dim_pad;
+    t.nq = nq;
+    t.n_mblk = (nq + kBlockM - 1) / kBlockM;
+    t.planes = a.idx.planes;
+    t.valid = a.idx.valid;
+    t.id_rank = a.idx.id_rank;
+    t.masks = a.masks ? a.masks + (int64_t)q0 * a.idx.n_words : nullptr;
+    t.n_words = a.idx.n_words;
+    t.has_prog = a.has_prog;
+    if (a.has_prog) {
+      t.n_planes = a.prog.n_planes;
+      t.n_leaves = a.prog.n_leaves;
+      t.k_max = a.prog.k_max;
+      t.plane_list = a.prog.plane_list;
+      t.leaf_slot = a.prog.leaf_slot;
+      t.rop_offset = a.prog.rop_offset + q0;
+      t.rops = a.prog.rops;
+    }
+    t.work = reinterpret_cast<const int2*>(a.tc_work);
+    t.n_sel = n_sel;
+    t.work_stride = a.word_stride;
+    t.ranges = a.ranges;
+    t.threshold = a.threshold ? a.threshold + q0 : nullptr;
+    t.out_key = a.out_key + (int64_t)q0 * a.cap;
+    t.out_slot = a.out_slot ? a.out_slot + (int64_t)q0 * a.cap : nullptr;
+    t.out_cnt = a.out_cnt + q0;
+    t.cap = a.cap;
+    t.dump = a.dump ? a.dump + (int64_t)q0 * a.dump_ld : nullptr;
+    t.dump_ld = a.dump_ld;
+    size_t smem = 0;
+    if (!pick_stages(t, t.n_mblk, t.has_prog ? t.n_planes : 0, t.has_prog ? t.n_leaves : 0,
+                     t.has_prog ? t.k_max : 0, smem))
+      return FB_ERR_UNSUPPORTED;
+    FB_CUDA(cudaFuncSetAttribute(k_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_scan_tc<<<grid, kThreads, smem, s>>>(tmap, t);
+    FB_LAUNCH_CHECK("k_scan_tc");
+  }
+  return FB_OK;
+}
 
 }  // namespace fb

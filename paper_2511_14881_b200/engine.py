@@ -83,7 +83,11 @@ class DeviceIndex:
             self._planes = bloom.planes_dev
             self.m_bits, self.k_hashes = bloom.params.m_bits, bloom.params.k_hashes
             if bloom.n_words < self.n_words:
-                raise ValueError("Bloom planes cover fewer words than the slot space")
+                # tile padding (slot space rounded up to 256): zero planes for padded words
+                pad = torch.zeros((self.m_bits, self.n_words), dtype=torch.int64,
+                                  device=items.device)
+                pad[:, : bloom.n_words] = bloom.planes_dev
+                self._planes = pad
 
     @property
     def n_words(self) -> int:
@@ -116,7 +120,7 @@ class DeviceIndex:
         items = to_dev(items_q, torch.int8, dev)
         n_slots, dim = int(items.shape[0]), int(items.shape[1])
         dim_pad = round_up(max(dim, 1), 32)
-        n_pad = round_up(max(n_slots, 1), 64)
+        n_pad = round_up(max(n_slots, 1), 256)  # whole 256-slot tensor-core tiles
         if dim_pad != dim or n_pad != n_slots:
             padded = torch.zeros((n_pad, dim_pad), dtype=torch.int8, device=dev)
             padded[:n_slots, :dim] = items

@@ -261,13 +261,53 @@ def compile_filter(expr: FilterExpr, params: BloomParams) -> CompiledFilter:
     return cf
 
 
+# register-machine opcodes (include/filtra_b200.h fb_ropcode)
+ROP_PUSH, ROP_PUSHN, ROP_ANDL, ROP_ORL, ROP_ANDS, ROP_ORS, ROP_NOT = range(7)
+ROP_MAX_LEAVES = 1 << 13
+
+
+def lower_to_register_ops(ops: list[tuple[int, int]]) -> tuple[list[int], int]:
+    """Peephole-lower postfix ``(opcode, global_leaf)`` ops to the register machine the
+    tensor-core epilogue runs: ``PUSH l; AND`` -> ``ANDL l``, ``PUSH l; OR`` -> ``ORL l``,
+    ``PUSH l; NOT`` -> ``PUSHN l``. Returns (encoded u16 ops, max stack depth)."""
+    out: list[tuple[int, int]] = []
+    for op, leaf in ops:
+        if op == OpCode.PUSH_LEAF:
+            out.append((ROP_PUSH, leaf))
+        elif op == OpCode.NOT:
+            if out and out[-1][0] == ROP_PUSH:
+                out[-1] = (ROP_PUSHN, out[-1][1])
+            else:
+                out.append((ROP_NOT, 0))
+        else:
+            combine_leaf = ROP_ANDL if op == OpCode.AND else ROP_ORL
+            if out and out[-1][0] == ROP_PUSH and len(out) >= 2:
+                out[-1] = (combine_leaf, out[-1][1])
+            else:
+                out.append((ROP_ANDS if op == OpCode.AND else ROP_ORS, 0))
+    depth = peak = 0
+    for code, _ in out:
+        if code in (ROP_PUSH, ROP_PUSHN):
+            depth += 1
+        elif code in (ROP_ANDS, ROP_ORS):
+            depth -= 1
+        peak = max(peak, depth)
+    return [(c << 13) | l for c, l in out], peak
+
+
 class FilterBatch:
     """Device bytecode for a batch of compiled filters (one per query, ``None`` =
-    unfiltered): leaves de-duplicated across the batch; ops ``(opcode << 14) | leaf``.
-    Mirrors ``fb_filter_prog_t`` in include/filtra_b200.h."""
+    unfiltered), mirroring ``fb_filter_prog_t`` (include/filtra_b200.h):
 
-    def __init__(self, leaf_pos: np.ndarray, op_offset: np.ndarray, ops: np.ndarray,
-                 max_stack: int, words_per_leaf: np.ndarray, push_leaf_bits: np.ndarray):
+    * postfix ops ``(opcode << 14) | leaf`` with leaves de-duplicated across the batch
+      (SIMT scan / ``fb_filter_eval``);
+    * the register-machine form for the tensor-core scan: the batch's distinct planes
+      (staged per tile in ``plane_list`` order), each leaf's positions as indices into
+      that list, and peephole-lowered ``rops``.
+    """
+
+    def __init__(self, leaf_pos, op_offset, ops, max_stack, push_leaf_bits, *,
+                 plane_list=None, leaf_slot=None, rop_offset=None, rops=None, rmax_stack=0):
         self.n_queries = len(op_offset) - 1
         self.n_leaves = leaf_pos.shape[0]
         self.k_max = leaf_pos.shape[1]
@@ -275,17 +315,34 @@ class FilterBatch:
         self.host_leaf_pos = np.ascontiguousarray(leaf_pos, dtype=np.int16)
         self.host_op_offset = np.ascontiguousarray(op_offset, dtype=np.int32)
         self.host_ops = np.ascontiguousarray(ops, dtype=np.uint16)
+        self.host_plane_list = (np.ascontiguousarray(plane_list, dtype=np.int16)
+                                if plane_list is not None else None)
+        self.host_leaf_slot = (np.ascontiguousarray(leaf_slot, dtype=np.int16)
+                               if leaf_slot is not None else None)
+        self.host_rop_offset = (np.ascontiguousarray(rop_offset, dtype=np.int32)
+                                if rop_offset is not None else None)
+        self.host_rops = np.ascontiguousarray(rops, dtype=np.uint16) if rops is not None else None
+        self.rmax_stack = rmax_stack
         # per query: sum over PUSH_LEAF ops of |set_bits| (FilterStats.words_read per word)
         self.push_leaf_bits = push_leaf_bits
         self._dev = None
+
+    @property
+    def n_planes(self) -> int:
+        return 0 if self.host_plane_list is None else int(self.host_plane_list.size)
+
+    def host_arrays(self) -> list[np.ndarray]:
+        arrs = [self.host_leaf_pos, self.host_op_offset, self.host_ops.view(np.int16)]
+        if self.host_rops is not None:
+            arrs += [self.host_plane_list, self.host_leaf_slot, self.host_rop_offset,
+                     self.host_rops.view(np.int16)]
+        return arrs
 
     def to_device(self) -> "FilterBatch":
         """Upload the bytecode (one H2D copy per array); idempotent."""
         if self._dev is None:
             dev = device()
-            self._dev = (torch.from_numpy(self.host_leaf_pos).to(dev),
-                         torch.from_numpy(self.host_op_offset).to(dev),
-                         torch.from_numpy(self.host_ops.view(np.int16)).to(dev))
+            self._dev = tuple(torch.from_numpy(a).to(dev) for a in self.host_arrays())
         return self
 
     @property
@@ -308,8 +365,11 @@ class FilterBatch:
         leaf_rows: list[tuple[int, ...]] = []
         ops: list[int] = []
         offsets = [0]
+        rops: list[int] = []
+        rop_offsets = [0]
         push_bits = []
         max_stack = 1
+        rmax = 0
         for cf in filters:
             nbits = 0
             if cf is not None:
@@ -321,14 +381,21 @@ class FilterBatch:
                         g = glob[key] = len(leaf_rows)
                         leaf_rows.append(tuple(qb.set_bits))
                     local.append(g)
+                gops = []
                 for op, arg in cf.ops:
                     if op == OpCode.PUSH_LEAF:
                         ops.append(local[arg])
+                        gops.append((int(op), local[arg]))
                         nbits += len(cf.leaves[arg][2].set_bits)
                     else:
                         ops.append(int(op) << 14)
+                        gops.append((int(op), 0))
                 max_stack = max(max_stack, cf.max_stack_depth())
+                enc, depth = lower_to_register_ops(gops)
+                rops.extend(enc)
+                rmax = max(rmax, depth)
             offsets.append(len(ops))
+            rop_offsets.append(len(rops))
             push_bits.append(nbits)
         if len(leaf_rows) > _native.FB_MAX_LEAVES:
             raise NotImplementedError(f"more than {_native.FB_MAX_LEAVES} distinct leaves in a batch")
@@ -338,9 +405,20 @@ class FilterBatch:
         leaf_pos = np.full((max(1, len(leaf_rows)), k_max), -1, dtype=np.int16)
         for i, r in enumerate(leaf_rows):
             leaf_pos[i, : len(r)] = r
+        planes = np.unique(leaf_pos[leaf_pos >= 0]).astype(np.int16)
+        slot_of = {int(p): i for i, p in enumerate(planes)}
+        leaf_slot = np.full_like(leaf_pos, -1)
+        for i, r in enumerate(leaf_rows):
+            leaf_slot[i, : len(r)] = [slot_of[p] for p in r]
+        reg = len(leaf_rows) <= ROP_MAX_LEAVES
         return cls(leaf_pos, np.array(offsets, dtype=np.int32),
                    np.array(ops if ops else [0], dtype=np.uint16), max_stack,
-                   np.array([len(r) for r in leaf_rows]), np.array(push_bits, dtype=np.int64))
+                   np.array(push_bits, dtype=np.int64),
+                   plane_list=planes if (reg and planes.size) else (np.zeros(1, np.int16) if reg else None),
+                   leaf_slot=leaf_slot if reg else None,
+                   rop_offset=np.array(rop_offsets, dtype=np.int32) if reg else None,
+                   rops=np.array(rops if rops else [0], dtype=np.uint16) if reg else None,
+                   rmax_stack=rmax)
 
     @classmethod
     def from_leaf(cls, qb: QueryBloom, params: BloomParams) -> "FilterBatch":
@@ -348,9 +426,14 @@ class FilterBatch:
         return cls.pack([cf], params)
 
     def struct(self) -> _native.FbFilterProg:
+        d = self.to_device()._dev
+        if self.host_rops is not None:
+            extra = (self.n_planes if self.host_plane_list is not None else 0, self.rmax_stack,
+                     d[3].data_ptr(), d[4].data_ptr(), d[5].data_ptr(), d[6].data_ptr())
+        else:
+            extra = (0, 0, None, None, None, None)
         return _native.FbFilterProg(self.n_queries, self.n_leaves, self.k_max, self.max_stack,
-                                    self.leaf_pos.data_ptr(), self.op_offset.data_ptr(),
-                                    self.ops.data_ptr())
+                                    d[0].data_ptr(), d[1].data_ptr(), d[2].data_ptr(), *extra)
 
     def evaluate(self, bloom: BloomIndex, valid, w0: int, w1: int,
                  apply_valid: bool = True) -> np.ndarray:

@@ -100,7 +100,7 @@ def make_workload(n_items: int, n_queries: int, dim: int = 128, seed: int = 1,
     lo, hi = float(emb.min()), float(emb.max())
     qp = QuantParams(lo, hi)
     dim_pad = (dim + 31) // 32 * 32
-    n_pad = (n_items + 63) // 64 * 64
+    n_pad = (n_items + 255) // 256 * 256  # whole 256-slot tensor-core tiles
     items = torch.zeros((n_pad, dim_pad), dtype=torch.int8, device=dev)
     chunk = 1 << 22
     for s in range(0, n_items, chunk):
@@ -115,10 +115,11 @@ def make_workload(n_items: int, n_queries: int, dim: int = 128, seed: int = 1,
     del emb
     # validity: all real items; padding cleared
     n_words = n_pad // 64
-    valid = torch.full((n_words,), -1, dtype=torch.int64, device=dev)
+    valid = torch.zeros((n_words,), dtype=torch.int64, device=dev)
+    valid[: n_items // 64] = -1
     rem = n_items % 64
     if rem:
-        valid[-1] = (1 << rem) - 1
+        valid[n_items // 64] = (1 << rem) - 1
     ids = torch.arange(n_pad, dtype=torch.int64, device=dev)
     ids[n_items:] = 0
     rank = torch.arange(n_pad, dtype=torch.int32, device=dev)

@@ -347,3 +347,42 @@ def test_merge_topk_device(fb, rng):
         ri, rs = orc.reduce_topk(all_i, all_s, 60)
         gi, gs = out.host(b)
         assert np.array_equal(gi, ri) and np.array_equal(gs, rs)
+
+
+# --- tensor-core scan ---------------------------------------------------------------
+
+def test_tc_raw_scores_match_int32_matmul(fb, rng):
+    """The tcgen05 kind::i8 path (TMA SWIZZLE_128B tiles, UMMA descriptors, TMEM reads)
+    reproduces the exact int32 dot of every (query, slot)."""
+    from paper_2511_14881_b200 import _device, _native
+    for n, nq in ((512, 5), (1024, 130), (2304, 256)):
+        items = rng.integers(-128, 128, size=(n, 128)).astype(np.int8)
+        items[: n // 8] = 127  # saturated rows: |dot| up to 128*128*128
+        q = rng.integers(-128, 128, size=(nq, 128)).astype(np.int8)
+        q[0] = -128
+        dix = fb.DeviceIndex.from_arrays(items, orc.from_bool(np.ones(n, bool)),
+                                         np.arange(n, dtype=np.uint64))
+        qd = _device.to_dev(q, torch.int8)
+        out = torch.empty((nq, dix.n_slots_pad), dtype=torch.int32, device=qd.device)
+        _native.check(_native.lib().fb_debug_tc_scores(dix.struct(), qd.data_ptr(), nq,
+                                                       out.data_ptr(), _native.stream_ptr()))
+        want = q.astype(np.int64) @ items.astype(np.int64).T
+        assert np.array_equal(out.cpu().numpy()[:, :n], want), (n, nq)
+
+
+@pytest.mark.parametrize("k", [1, 777, 10000])
+def test_tc_vs_simt_vs_oracle(fb, wl_small, k):
+    from paper_2511_14881_b200 import _native
+    wl = wl_small
+    idx = wl.index
+    ref = oracle_batch(wl, idx, k)
+    for flags in (0, _native.FB_PLAN_SIMT, _native.FB_PLAN_FORCE_FALLBACK):
+        op = fb.TopkOp(idx, 24, k, np.array([[0, idx.n_slots]]), flags)
+        out = op(wl.queries_q, wl.batch)
+        torch.cuda.synchronize()
+        path = _native.lib().fb_topk_scan_path(op._plan)
+        assert path == (0 if flags == _native.FB_PLAN_SIMT else 1)
+        for q in range(24):
+            ids, scores = out.host(q)
+            assert np.array_equal(ids, ref[q].item_ids), (flags, q)
+            assert np.array_equal(scores, ref[q].scores), (flags, q)
