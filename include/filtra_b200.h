@@ -96,6 +96,8 @@ typedef struct fb_filter_prog {
    *   rops: (ropcode << 13) | leaf, ropcodes FB_ROP_*; rmax_stack = its max depth. */
   int32_t n_planes;
   int32_t rmax_stack;
+  int32_t n_rops;              /* total rops (multiple of FB_ROP_ALIGN) */
+  int32_t reserved;
   const int16_t* plane_list;   /* [n_planes] */
   const int16_t* leaf_slot;    /* [n_leaves * k_max] */
   const int32_t* rop_offset;   /* [n_queries + 1] */
@@ -108,8 +110,11 @@ typedef struct fb_filter_prog {
  * result is ANDed with validity. */
 enum fb_ropcode {
   FB_ROP_PUSH = 0, FB_ROP_PUSHN = 1, FB_ROP_ANDL = 2, FB_ROP_ORL = 3,
-  FB_ROP_ANDS = 4, FB_ROP_ORS = 5, FB_ROP_NOT = 6
+  FB_ROP_ANDS = 4, FB_ROP_ORS = 5, FB_ROP_NOT = 6, FB_ROP_NOP = 7
 };
+/* Each query's rops start on an 8-op boundary (rop_offset[q] % 8 == 0) and are padded
+ * with FB_ROP_NOP to a multiple of 8, so the kernel fetches them 16 bytes at a time. */
+#define FB_ROP_ALIGN 8
 
 /* Work counters (ivf.ScanStats + bloom.FilterStats), filled analytically by the plan. */
 typedef struct fb_stats {

@@ -65,6 +65,7 @@ class FbFilterProg(ctypes.Structure):
         ("k_max", ctypes.c_int32), ("max_stack", ctypes.c_int32),
         ("leaf_pos", c_vp), ("op_offset", c_vp), ("ops", c_vp),
         ("n_planes", ctypes.c_int32), ("rmax_stack", ctypes.c_int32),
+        ("n_rops", ctypes.c_int32), ("reserved", ctypes.c_int32),
         ("plane_list", c_vp), ("leaf_slot", c_vp), ("rop_offset", c_vp), ("rops", c_vp),
     ]
 

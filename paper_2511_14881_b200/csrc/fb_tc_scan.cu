@@ -21,6 +21,8 @@
 
 #include "fb_internal.cuh"
 
+#include <algorithm>
+
 namespace fb {
 namespace {
 
@@ -34,7 +36,10 @@ constexpr int kUmmaK = 32;
 constexpr int kAccCols = 256;
 constexpr int kThreads = 384;
 constexpr int kLeafThreads = 64;
+constexpr int kEpiWarp0 = 4;   // warps 4-11: epilogue (thread = query x 128 items)
 constexpr int kEpiWarps = 8;
+constexpr int kLeafStride = 6;  // u64 per leaf in the per-tile leaf-mask stage (48 B: 4 words +
+                                // pad, so 32 lanes' 16-B loads spread over 8 bank groups)
 constexpr int kRegStack = 4;
 constexpr uint32_t kItemBytes = kTileItems * kKBytes;  // 32 KB
 
@@ -67,7 +72,9 @@ struct TcArgs {
   int32_t* dump;
   int64_t dump_ld;
   int32_t item_stages;
-  uint32_t off_a, off_b, off_p, off_l, off_ls, off_thr, off_bar, plane_stage_bytes,
+  int32_t plane_stages;
+  int32_t rops_cap;  // ops of this launch's programs that fit the shared-memory stage
+  uint32_t off_a, off_b, off_p, off_l, off_ls, off_thr, off_r, off_bar, plane_stage_bytes,
       leaf_stage_bytes;
 };
 
@@ -97,6 +104,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
   } while (!ok);
+}
+// for roles off the critical path: back off so spinning does not steal issue slots
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* b, uint32_t parity) {
+  const uint32_t a = su32(b);
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(32);
+  }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0,
                                             int32_t c1, uint64_t* bar) {
@@ -174,40 +197,47 @@ __device__ __forceinline__ uint64_t word_range_mask(int64_t word_slot, int64_t s
   return upto & ~((1ull << lo) - 1);
 }
 
-// Register-machine filter evaluation over two 64-slot words (128 items). The stack lives
-// in registers (static shifts), so the whole program runs without local memory.
-__device__ __forceinline__ void eval_rops(const uint16_t* __restrict__ rops, int o0, int o1,
-                                          const uint64_t* L, int half, uint64_t& r0,
-                                          uint64_t& r1) {
+
+// ---- filter program: register machine over one 64-slot word ---------------------------
+__device__ __forceinline__ void rop_apply(uint32_t code, uint64_t m, uint64_t (&a)[kRegStack]) {
+  if (code == FB_ROP_ORL) {
+    a[0] |= m;
+  } else if (code == FB_ROP_ANDL) {
+    a[0] &= m;
+  } else if (code <= FB_ROP_PUSHN) {
+#pragma unroll
+    for (int i = kRegStack - 1; i > 0; --i) a[i] = a[i - 1];
+    a[0] = code == FB_ROP_PUSHN ? ~m : m;
+  } else if (code == FB_ROP_NOT) {
+    a[0] = ~a[0];
+  } else if (code != FB_ROP_NOP) {  // ANDS / ORS
+    a[0] = code == FB_ROP_ANDS ? (a[1] & a[0]) : (a[1] | a[0]);
+#pragma unroll
+    for (int i = 1; i < kRegStack - 1; ++i) a[i] = a[i + 1];
+  }
+}
+
+// ``prog`` holds n_ops (a multiple of 8) ops, 16-byte aligned (shared or global memory).
+// Ops are fetched 8 at a time and the 8 leaf masks (2 words = 128 items each) are loaded
+// before any is applied, so the memory latency is paid once per batch. The stack lives in
+// registers.
+__device__ __forceinline__ void eval_half(const uint16_t* prog, int n_ops, const uint64_t* L,
+                                          int half, uint64_t& r0, uint64_t& r1) {
   uint64_t a0[kRegStack], a1[kRegStack];
 #pragma unroll
   for (int i = 0; i < kRegStack; ++i) a0[i] = a1[i] = 0ull;
-  for (int o = o0; o < o1; ++o) {
-    const uint32_t op = __ldg(rops + o);
-    const uint32_t code = op >> 13, leaf = op & 0x1FFF;
-    const ulonglong2 m = *reinterpret_cast<const ulonglong2*>(L + leaf * kTileWords + 2 * half);
-    switch (code) {
-      case FB_ROP_PUSH:
-      case FB_ROP_PUSHN: {
-        const uint64_t x0 = code == FB_ROP_PUSH ? m.x : ~m.x;
-        const uint64_t x1 = code == FB_ROP_PUSH ? m.y : ~m.y;
+  for (int b = 0; b < n_ops; b += 8) {
+    const uint4 w = *reinterpret_cast<const uint4*>(prog + b);
+    const uint32_t op[8] = {w.x & 0xFFFFu, w.x >> 16, w.y & 0xFFFFu, w.y >> 16,
+                            w.z & 0xFFFFu, w.z >> 16, w.w & 0xFFFFu, w.w >> 16};
+    ulonglong2 m[8];
 #pragma unroll
-        for (int i = kRegStack - 1; i > 0; --i) { a0[i] = a0[i - 1]; a1[i] = a1[i - 1]; }
-        a0[0] = x0;
-        a1[0] = x1;
-        break;
-      }
-      case FB_ROP_ANDL: a0[0] &= m.x; a1[0] &= m.y; break;
-      case FB_ROP_ORL: a0[0] |= m.x; a1[0] |= m.y; break;
-      case FB_ROP_NOT: a0[0] = ~a0[0]; a1[0] = ~a1[0]; break;
-      default: {  // ANDS / ORS
-        const bool is_and = code == FB_ROP_ANDS;
-        a0[0] = is_and ? (a0[1] & a0[0]) : (a0[1] | a0[0]);
-        a1[0] = is_and ? (a1[1] & a1[0]) : (a1[1] | a1[0]);
+    for (int j = 0; j < 8; ++j)
+      m[j] = *reinterpret_cast<const ulonglong2*>(L + (op[j] & 0x1FFFu) * kLeafStride + 2 * half);
 #pragma unroll
-        for (int i = 1; i < kRegStack - 1; ++i) { a0[i] = a0[i + 1]; a1[i] = a1[i + 1]; }
-        break;
-      }
+    for (int j = 0; j < 8; ++j) {
+      rop_apply(op[j] >> 13, m[j].x, a0);
+      rop_apply(op[j] >> 13, m[j].y, a1);
     }
   }
   r0 = a0[0];
@@ -226,20 +256,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   int16_t* sLS = reinterpret_cast<int16_t*>(smem + a.off_ls);
   uint64_t* sT = reinterpret_cast<uint64_t*>(smem + a.off_thr);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.off_bar);
-  uint64_t* items_full = bars;
-  uint64_t* items_empty = bars + 4;
-  uint64_t* planes_full = bars + 8;
-  uint64_t* planes_empty = bars + 10;
-  uint64_t* leaf_full = bars + 12;
-  uint64_t* leaf_empty = bars + 14;
-  uint64_t* acc_full = bars + 16;
-  uint64_t* acc_empty = bars + 18;
+  uint64_t* items_full = bars;        // [4]
+  uint64_t* items_empty = bars + 4;   // [4]
+  uint64_t* planes_full = bars + 8;   // [2]
+  uint64_t* planes_empty = bars + 10; // [2]
+  uint64_t* leaf_full = bars + 12;    // [2]
+  uint64_t* leaf_empty = bars + 14;   // [2]
+  uint64_t* acc_full = bars + 16;     // [2]
+  uint64_t* acc_empty = bars + 18;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = a.item_stages;
+  const int PS = a.plane_stages;
 
-  // ---- prologue: queries -> swizzled smem, thresholds, leaf -> plane-slot table ------
+  // ---- prologue: queries -> swizzled smem, thresholds, leaf table, filter programs ----
   const int a_rows = a.n_mblk * kBlockM;
   for (int i = threadIdx.x; i < a_rows * 8; i += kThreads) {
     const int r = i >> 3, c = i & 7;
@@ -249,8 +280,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   for (int q = threadIdx.x; q < kMaxQueries; q += kThreads)
     sT[q] = (a.threshold != nullptr && q < a.nq) ? a.threshold[q] : 0ull;
-  if (a.has_prog)
+  const uint16_t* prog_base = a.rops;
+  if (a.has_prog) {
     for (int i = threadIdx.x; i < a.n_leaves * a.k_max; i += kThreads) sLS[i] = a.leaf_slot[i];
+    const int32_t off0 = a.rop_offset[0];
+    const int32_t n_ops = a.rop_offset[a.nq] - off0;
+    if (n_ops <= a.rops_cap) {
+      uint4* dst = reinterpret_cast<uint4*>(smem + a.off_r);
+      const uint4* src = reinterpret_cast<const uint4*>(a.rops + off0);
+      for (int i = threadIdx.x; i < n_ops / 8; i += kThreads) dst[i] = __ldg(src + i);
+      prog_base = reinterpret_cast<const uint16_t*>(smem + a.off_r) - off0;
+    }
+  }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int s = 0; s < 4; ++s) {
@@ -288,14 +329,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int s = it % S;
       const uint32_t ph = (uint32_t)(it / S) & 1u;
       if (lane == 0) {
-        mbar_wait(items_empty + s, ph ^ 1u);
+        mbar_wait_idle(items_empty + s, ph ^ 1u);
         mbar_expect_tx(items_full + s, kItemBytes);
         tma_load_2d(sB + (size_t)s * kItemBytes, &tmap_items, 0, tile * kTileItems, items_full + s);
       }
       if (a.has_prog && a.n_planes > 0) {
-        const int ps = it & 1;
-        const uint32_t pph = (uint32_t)(it >> 1) & 1u;
-        mbar_wait(planes_empty + ps, pph ^ 1u);
+        const int ps = it % PS;
+        const uint32_t pph = (uint32_t)(it / PS) & 1u;
+        mbar_wait_idle(planes_empty + ps, pph ^ 1u);
         if (lane == 0) mbar_expect_tx(planes_full + ps, (uint32_t)a.n_planes * 32u);
         __syncwarp();
         uint8_t* dst = sP + (size_t)ps * a.plane_stage_bytes;
@@ -320,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
           const int ab = acc_it & 1;
           const uint32_t aph = (uint32_t)(acc_it >> 1) & 1u;
-          mbar_wait(acc_empty + ab, aph ^ 1u);
+          mbar_wait_idle(acc_empty + ab, aph ^ 1u);
           tc_fence_after();
           const uint32_t a_base = su32(sA + mb * kBlockM * kKBytes);
           const uint32_t d = tmem_base + (uint32_t)(ab * kAccCols);
@@ -333,17 +374,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(items_empty + s);
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < kEpiWarp0) {
     // ================= leaf builders: AND each leaf's planes per word =============
     if (a.has_prog) {
       const int t = threadIdx.x - 64;
       int it = 0;
       for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
+        const int ps = it % PS;
+        const uint32_t pph = (uint32_t)(it / PS) & 1u;
         const int st = it & 1;
         const uint32_t ph = (uint32_t)(it >> 1) & 1u;
-        if (a.n_planes > 0) mbar_wait(planes_full + st, ph);
-        mbar_wait(leaf_empty + st, ph ^ 1u);
-        const uint64_t* P = reinterpret_cast<const uint64_t*>(sP + (size_t)st * a.plane_stage_bytes);
+        if (a.n_planes > 0) mbar_wait_idle(planes_full + ps, pph);
+        mbar_wait_idle(leaf_empty + st, ph ^ 1u);
+        const uint64_t* P = reinterpret_cast<const uint64_t*>(sP + (size_t)ps * a.plane_stage_bytes);
         uint64_t* L = reinterpret_cast<uint64_t*>(sL + (size_t)st * a.leaf_stage_bytes);
         for (int e = t; e < a.n_leaves * kTileWords; e += kLeafThreads) {
           const int l = e >> 2, w = e & 3;
@@ -353,15 +396,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (sl < 0) break;
             m &= P[sl * kTileWords + w];
           }
-          L[e] = m;
+          L[l * kLeafStride + w] = m;
         }
-        if (a.n_planes > 0) mbar_arrive(planes_empty + st);
+        if (a.n_planes > 0) mbar_arrive(planes_empty + ps);
         mbar_arrive(leaf_full + st);
       }
     }
   } else {
-    // ================= epilogue: TMEM -> registers -> gate -> filter -> emit ======
-    const int ew = warp - 4;
+    // ================= epilogue: filter (eager) + TMEM scores + gate + emit ========
+    const int ew = warp - kEpiWarp0;
     const int quad = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int half = ew >> 2;   // item columns [half * 128, half * 128 + 128)
     const int row = quad * 32 + lane;
@@ -371,27 +414,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t tile = wk.x;
       const int64_t s0 = a.ranges[2 * wk.y], s1 = a.ranges[2 * wk.y + 1];
       const int64_t wbase = tile * kTileWords + 2 * half;
-      const uint64_t v0 = a.valid[wbase] & word_range_mask(wbase * 64, s0, s1);
-      const uint64_t v1 = a.valid[wbase + 1] & word_range_mask((wbase + 1) * 64, s0, s1);
+      const uint64_t v0 = __ldg(a.valid + wbase) & word_range_mask(wbase * 64, s0, s1);
+      const uint64_t v1 = __ldg(a.valid + wbase + 1) & word_range_mask((wbase + 1) * 64, s0, s1);
       const int st = it & 1;
-      const uint32_t lph = (uint32_t)(it >> 1) & 1u;
-      if (a.has_prog) mbar_wait(leaf_full + st, lph);
+      if (a.has_prog) mbar_wait(leaf_full + st, (uint32_t)(it >> 1) & 1u);
       const uint64_t* L = reinterpret_cast<const uint64_t*>(sL + (size_t)st * a.leaf_stage_bytes);
       for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
-        const int ab = acc_it & 1;
-        const uint32_t aph = (uint32_t)(acc_it >> 1) & 1u;
-        mbar_wait(acc_full + ab, aph);
-        tc_fence_after();
         const int q = mb * kBlockM + row;
         const bool active = q < a.nq;
+        // eligibility of this thread's 128 items: validity & range & program & mask
+        uint64_t f0 = active ? v0 : 0ull, f1 = active ? v1 : 0ull;
+        if (a.has_prog && (f0 | f1) != 0ull) {
+          const int o0 = a.rop_offset[q], o1 = a.rop_offset[q + 1];
+          if (o1 > o0) {
+            uint64_t e0, e1;
+            eval_half(prog_base + o0, o1 - o0, L, half, e0, e1);
+            f0 &= e0;
+            f1 &= e1;
+          }
+        }
+        if (a.masks != nullptr && (f0 | f1) != 0ull) {
+          f0 &= __ldg(a.masks + (int64_t)q * a.n_words + wbase);
+          f1 &= __ldg(a.masks + (int64_t)q * a.n_words + wbase + 1);
+        }
         const uint64_t T = active ? sT[q] : ~0ull;
         const int32_t tau = T == 0ull ? INT32_MIN : key_score(T);
+        const int ab = acc_it & 1;
+        mbar_wait(acc_full + ab, (uint32_t)(acc_it >> 1) & 1u);
+        tc_fence_after();
         const uint32_t taddr =
             tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kAccCols + half * 128);
-        int32_t r[32];
-        uint32_t need = 0;
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
+          int32_t r[32];
           tmem_ld32(taddr + c * 32, r);
           if (a.dump != nullptr && active) {
             const int64_t base = tile * kTileItems + half * 128 + c * 32;
@@ -399,44 +454,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j)
               if (base + j < a.dump_ld) a.dump[(int64_t)q * a.dump_ld + base + j] = r[j];
           }
-          int32_t mx = r[0];
+          const uint32_t fw = (uint32_t)((c < 2 ? f0 : f1) >> (32 * (c & 1)));
+          if (fw != 0u) {
+            int32_t mx = r[0];
 #pragma unroll
-          for (int j = 1; j < 31; j += 2) mx = __vimax3_s32(mx, r[j], r[j + 1]);
-          mx = max(mx, r[31]);
-          if (mx >= tau) need |= 1u << c;
-        }
-        uint64_t f0 = 0ull, f1 = 0ull;
-        if (active && need != 0u) {
-          f0 = v0;
-          f1 = v1;
-          if (a.has_prog) {
-            const int o0 = a.rop_offset[q], o1 = a.rop_offset[q + 1];
-            if (o1 > o0) {
-              uint64_t e0, e1;
-              eval_rops(a.rops, o0, o1, L, half, e0, e1);
-              f0 &= e0;
-              f1 &= e1;
-            }
-          }
-          if (a.masks != nullptr) {
-            f0 &= a.masks[(int64_t)q * a.n_words + wbase];
-            f1 &= a.masks[(int64_t)q * a.n_words + wbase + 1];
-          }
-        }
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          const uint64_t fw64 = c < 2 ? f0 : f1;
-          uint32_t fw = (uint32_t)(fw64 >> (32 * (c & 1)));
-          if (!((need >> c) & 1u)) fw = 0u;
-          if (__any_sync(0xffffffffu, fw != 0u)) {
-            tmem_ld32(taddr + c * 32, r);
-            if (fw != 0u) {
-              const int64_t slot0 = tile * kTileItems + half * 128 + c * 32;
+            for (int j = 1; j < 31; j += 2) mx = __vimax3_s32(mx, r[j], r[j + 1]);
+            mx = max(mx, r[31]);
+            if (mx >= tau) {
+              uint32_t cm = 0u;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (((fw >> j) & 1u) && r[j] >= tau) {
+              for (int j = 0; j < 32; ++j) cm |= (r[j] >= tau ? 1u : 0u) << j;
+              cm &= fw;
+              if (cm != 0u) {
+                const int64_t slot0 = tile * kTileItems + half * 128 + c * 32;
+                int32_t rs[32];  // dynamic indexing below: lives in local memory (rare path)
+#pragma unroll
+                for (int j = 0; j < 32; ++j) rs[j] = r[j];
+                while (cm != 0u) {
+                  const int j = __ffs(cm) - 1;
+                  cm &= cm - 1u;
                   const int64_t slot = slot0 + j;
-                  const uint64_t key = make_key(r[j], __ldg(a.id_rank + slot));
+                  const uint64_t key = make_key(rs[j], __ldg(a.id_rank + slot));
                   if (key >= T) {
                     const uint32_t p = atomicAdd(a.out_cnt + q, 1u);
                     if (p < (uint32_t)a.cap) {
@@ -483,8 +521,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// shared-memory carve-up; returns total bytes (incl. 1 KB alignment slack) or 0 if too big
-size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int stages) {
+// shared-memory carve-up; returns total bytes (incl. 1 KB alignment slack)
+size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int stages,
+              int plane_stages) {
   size_t off = 0;
   t.off_a = 0;
   off = (size_t)n_mblk * kBlockM * kKBytes;
@@ -492,8 +531,9 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
   off = t.off_b + (size_t)stages * kItemBytes;
   t.plane_stage_bytes = (uint32_t)align_up((size_t)(n_planes > 0 ? n_planes : 1) * 32, 128);
   t.off_p = (uint32_t)align_up(off, 128);
-  off = t.off_p + 2ull * t.plane_stage_bytes;
-  t.leaf_stage_bytes = (uint32_t)align_up((size_t)(n_leaves > 0 ? n_leaves : 1) * 32, 128);
+  off = t.off_p + (size_t)plane_stages * t.plane_stage_bytes;
+  t.leaf_stage_bytes =
+      (uint32_t)align_up((size_t)(n_leaves > 0 ? n_leaves : 1) * kLeafStride * 8, 128);
   t.off_l = (uint32_t)align_up(off, 128);
   off = t.off_l + 2ull * t.leaf_stage_bytes;
   t.off_ls = (uint32_t)align_up(off, 16);
@@ -502,16 +542,31 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
   off = t.off_thr + (size_t)kMaxQueries * 8;
   t.off_bar = (uint32_t)align_up(off, 16);
   off = t.off_bar + 21 * 8 + 16;
+  t.off_r = (uint32_t)align_up(off, 16);
+  off = t.off_r + (size_t)t.rops_cap * 2;
   return off + 1024;
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
+constexpr int kMaxStagedOps = 16384;  // 32 KB; whatever is left stays L1
 
-bool pick_stages(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, size_t& smem) {
-  for (int stages = 4; stages >= 2; --stages) {
-    smem = layout(t, n_mblk, n_planes, n_leaves, k_max, stages);
-    if (smem <= kSmemLimit) {
-      t.item_stages = stages;
+// Prefer 3 item stages and 2 plane stages; stage as much filter bytecode as fits.
+bool pick_stages(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int n_rops,
+                 size_t& smem) {
+  const int prefs[4][2] = {{3, 2}, {3, 1}, {2, 2}, {2, 1}};
+  // first pass: the configuration that also holds all filter bytecode; second: any
+  for (int pass = 0; pass < 2; ++pass) {
+    for (const auto& pr : prefs) {
+      t.rops_cap = 0;
+      smem = layout(t, n_mblk, n_planes, n_leaves, k_max, pr[0], pr[1]);
+      if (smem > kSmemLimit) continue;
+      const size_t room = (kSmemLimit - smem) / 2 / 8 * 8;
+      const size_t want = (size_t)std::min(n_rops > 0 ? n_rops : 0, kMaxStagedOps);
+      if (pass == 0 && room < want) continue;
+      t.rops_cap = (int32_t)std::min(room, want);
+      smem = layout(t, n_mblk, n_planes, n_leaves, k_max, pr[0], pr[1]);
+      t.item_stages = pr[0];
+      t.plane_stages = pr[1];
       return true;
     }
   }
@@ -531,7 +586,7 @@ bool scan_tc_supported(const ScanArgs& a) {
     TcArgs t{};
     size_t smem = 0;
     const int n_mblk = a.n_queries >= kBlockM ? kMaxMBlocks : 1;
-    if (!pick_stages(t, n_mblk, a.prog.n_planes, a.prog.n_leaves, a.prog.k_max, smem))
+    if (!pick_stages(t, n_mblk, a.prog.n_planes, a.prog.n_leaves, a.prog.k_max, 0, smem))
       return false;
   }
   return true;
@@ -588,7 +643,7 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
     t.dump_ld = a.dump_ld;
     size_t smem = 0;
     if (!pick_stages(t, t.n_mblk, t.has_prog ? t.n_planes : 0, t.has_prog ? t.n_leaves : 0,
-                     t.has_prog ? t.k_max : 0, smem))
+                     t.has_prog ? t.k_max : 0, t.has_prog ? a.prog.n_rops : 0, smem))
       return FB_ERR_UNSUPPORTED;
     FB_CUDA(cudaFuncSetAttribute(k_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));

@@ -262,8 +262,9 @@ def compile_filter(expr: FilterExpr, params: BloomParams) -> CompiledFilter:
 
 
 # register-machine opcodes (include/filtra_b200.h fb_ropcode)
-ROP_PUSH, ROP_PUSHN, ROP_ANDL, ROP_ORL, ROP_ANDS, ROP_ORS, ROP_NOT = range(7)
+ROP_PUSH, ROP_PUSHN, ROP_ANDL, ROP_ORL, ROP_ANDS, ROP_ORS, ROP_NOT, ROP_NOP = range(8)
 ROP_MAX_LEAVES = 1 << 13
+ROP_ALIGN = 8
 
 
 def lower_to_register_ops(ops: list[tuple[int, int]]) -> tuple[list[int], int]:
@@ -392,6 +393,7 @@ class FilterBatch:
                         gops.append((int(op), 0))
                 max_stack = max(max_stack, cf.max_stack_depth())
                 enc, depth = lower_to_register_ops(gops)
+                enc += [ROP_NOP << 13] * (-len(enc) % ROP_ALIGN)
                 rops.extend(enc)
                 rmax = max(rmax, depth)
             offsets.append(len(ops))
@@ -417,7 +419,8 @@ class FilterBatch:
                    plane_list=planes if (reg and planes.size) else (np.zeros(1, np.int16) if reg else None),
                    leaf_slot=leaf_slot if reg else None,
                    rop_offset=np.array(rop_offsets, dtype=np.int32) if reg else None,
-                   rops=np.array(rops if rops else [0], dtype=np.uint16) if reg else None,
+                   rops=(np.array(rops if rops else [ROP_NOP << 13] * ROP_ALIGN, dtype=np.uint16)
+                         if reg else None),
                    rmax_stack=rmax)
 
     @classmethod
@@ -429,9 +432,10 @@ class FilterBatch:
         d = self.to_device()._dev
         if self.host_rops is not None:
             extra = (self.n_planes if self.host_plane_list is not None else 0, self.rmax_stack,
+                     int(self.host_rops.size), 0,
                      d[3].data_ptr(), d[4].data_ptr(), d[5].data_ptr(), d[6].data_ptr())
         else:
-            extra = (0, 0, None, None, None, None)
+            extra = (0, 0, 0, 0, None, None, None, None)
         return _native.FbFilterProg(self.n_queries, self.n_leaves, self.k_max, self.max_stack,
                                     d[0].data_ptr(), d[1].data_ptr(), d[2].data_ptr(), *extra)
 
