@@ -102,6 +102,18 @@ typedef struct fb_filter_prog {
   const int16_t* leaf_slot;    /* [n_leaves * k_max] */
   const int32_t* rop_offset;   /* [n_queries + 1] */
   const uint16_t* rops;
+  /* Conjunctive normal form (nullable; set when every program is an AND of ORs of
+   * literals). Literal columns: col_leaf[c] = leaf, or ~leaf for a negated literal.
+   * qmask[q][g][w] is the column bitmask of query q's group g (cnf_words u32 words);
+   * qgroups[q] the number of groups (0 = unfiltered). A slot passes query q iff for
+   * every group some column of the group holds for it. */
+  int32_t n_cols;
+  int32_t cnf_words;           /* <= 8 */
+  int32_t cnf_gmax;            /* <= 8 */
+  int32_t reserved2;
+  const int16_t* col_leaf;     /* [n_cols] */
+  const uint32_t* qmask;       /* [n_queries][cnf_gmax][cnf_words] */
+  const int32_t* qgroups;      /* [n_queries] */
 } fb_filter_prog_t;
 
 /* Register-machine opcodes: PUSH l | PUSHN l (push ~leaf) | ANDL l (top &= leaf) |

@@ -74,9 +74,20 @@ struct TcArgs {
   int32_t item_stages;
   int32_t plane_stages;
   int32_t rops_cap;  // ops of this launch's programs that fit the shared-memory stage
+  // CNF mode
+  int32_t n_cols;
+  int32_t cnf_words;
+  int32_t cnf_gmax;
+  int32_t qm_stride;  // u32 per (query, group) in shared memory: 4 or 8
+  const int16_t* col_leaf;
+  const uint32_t* qmask;
+  const int32_t* qgroups;
   uint32_t off_a, off_b, off_p, off_l, off_ls, off_thr, off_r, off_bar, plane_stage_bytes,
-      leaf_stage_bytes;
+      leaf_stage_bytes, off_qm, off_qg, off_hit;
 };
+
+constexpr int kTbStride = 8;     // u32 per item row of the transposed column bits (<= 256 cols)
+constexpr int kHitCap = 64;      // per-warp ring buffer of hits (score >= threshold)
 
 // ---- PTX helpers ----------------------------------------------------------------------
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -221,29 +232,135 @@ __device__ __forceinline__ void rop_apply(uint32_t code, uint64_t m, uint64_t (&
 // Ops are fetched 8 at a time and the 8 leaf masks (2 words = 128 items each) are loaded
 // before any is applied, so the memory latency is paid once per batch. The stack lives in
 // registers.
-__device__ __forceinline__ void eval_half(const uint16_t* prog, int n_ops, const uint64_t* L,
-                                          int half, uint64_t& r0, uint64_t& r1) {
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+// prog_s / leaf_s are 32-bit shared-memory addresses (the program staged in smem; the
+// current tile's leaf-mask stage offset by this thread's half).
+__device__ __forceinline__ void eval_half(uint32_t prog_s, int n_ops, uint32_t leaf_s,
+                                          uint64_t& r0, uint64_t& r1) {
   uint64_t a0[kRegStack], a1[kRegStack];
 #pragma unroll
   for (int i = 0; i < kRegStack; ++i) a0[i] = a1[i] = 0ull;
   for (int b = 0; b < n_ops; b += 8) {
-    const uint4 w = *reinterpret_cast<const uint4*>(prog + b);
+    const uint4 w = lds128(prog_s + 2u * b);
     const uint32_t op[8] = {w.x & 0xFFFFu, w.x >> 16, w.y & 0xFFFFu, w.y >> 16,
                             w.z & 0xFFFFu, w.z >> 16, w.w & 0xFFFFu, w.w >> 16};
-    ulonglong2 m[8];
+    uint4 m[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      m[j] = *reinterpret_cast<const ulonglong2*>(L + (op[j] & 0x1FFFu) * kLeafStride + 2 * half);
+    for (int j = 0; j < 8; ++j) m[j] = lds128(leaf_s + (op[j] & 0x1FFFu) * (kLeafStride * 8u));
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      rop_apply(op[j] >> 13, m[j].x, a0);
-      rop_apply(op[j] >> 13, m[j].y, a1);
+      const uint32_t code = op[j] >> 13;
+      rop_apply(code, ((uint64_t)m[j].y << 32) | m[j].x, a0);
+      rop_apply(code, ((uint64_t)m[j].w << 32) | m[j].z, a1);
     }
   }
   r0 = a0[0];
   r1 = a1[0];
 }
 
+// Same, for a program left in global memory (batch too large to stage).
+__device__ __forceinline__ void eval_half_global(const uint16_t* prog, int n_ops, uint32_t leaf_s,
+                                                 uint64_t& r0, uint64_t& r1) {
+  uint64_t a0[kRegStack], a1[kRegStack];
+#pragma unroll
+  for (int i = 0; i < kRegStack; ++i) a0[i] = a1[i] = 0ull;
+  for (int b = 0; b < n_ops; b += 8) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(prog + b));
+    const uint32_t op[8] = {w.x & 0xFFFFu, w.x >> 16, w.y & 0xFFFFu, w.y >> 16,
+                            w.z & 0xFFFFu, w.z >> 16, w.w & 0xFFFFu, w.w >> 16};
+    uint4 m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = lds128(leaf_s + (op[j] & 0x1FFFu) * (kLeafStride * 8u));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t code = op[j] >> 13;
+      rop_apply(code, ((uint64_t)m[j].y << 32) | m[j].x, a0);
+      rop_apply(code, ((uint64_t)m[j].w << 32) | m[j].z, a1);
+    }
+  }
+  r0 = a0[0];
+  r1 = a1[0];
+}
+
+// ---- CNF mode helpers ---------------------------------------------------------------
+// 32x32 bit-matrix transpose across a warp: lane j holds row j on entry (bit i = (j, i)),
+// column j on exit (bit i = (i, j)).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int s = 16 >> k;
+    const uint32_t m = masks[k];
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
+  }
+  return x;
+}
+
+struct HitCtx {
+  int64_t tile;
+  uint64_t vw[kTileWords];  // validity & range words of the tile
+  uint32_t tb_s;            // shared address of this tile's transposed column bits
+  uint32_t qm_s;            // shared address of the query group masks
+  const int32_t* qg;        // shared: groups per query
+  const uint64_t* sT;
+  int mb;
+};
+
+// Full eligibility + threshold test of one hit (query row, tile item, score) and emission.
+__device__ __forceinline__ void process_hit(const TcArgs& a, const HitCtx& h, uint32_t row,
+                                            uint32_t item, int32_t score) {
+  const int q = h.mb * kBlockM + (int)row;
+  const int word = (int)(item >> 6);
+  uint64_t vw = h.vw[0];
+  vw = word == 1 ? h.vw[1] : vw;
+  vw = word == 2 ? h.vw[2] : vw;
+  vw = word == 3 ? h.vw[3] : vw;
+  bool pass = (vw >> (item & 63)) & 1ull;
+  if (pass && a.masks != nullptr)
+    pass = (__ldg(a.masks + (int64_t)q * a.n_words + h.tile * kTileWords + word) >> (item & 63)) &
+           1ull;
+  if (pass) {
+    const int ng = h.qg[q];
+    if (ng > 0) {
+      const uint4 t0 = lds128(h.tb_s + item * (kTbStride * 4u));
+      const uint4 t1 = a.qm_stride == 8 ? lds128(h.tb_s + item * (kTbStride * 4u) + 16u)
+                                        : make_uint4(0u, 0u, 0u, 0u);
+      uint32_t qaddr = h.qm_s + (uint32_t)(q * a.cnf_gmax * a.qm_stride) * 4u;
+      for (int g = 0; g < ng && pass; ++g) {
+        const uint4 m0 = lds128(qaddr);
+        uint32_t any = (t0.x & m0.x) | (t0.y & m0.y) | (t0.z & m0.z) | (t0.w & m0.w);
+        if (a.qm_stride == 8) {
+          const uint4 m1 = lds128(qaddr + 16u);
+          any |= (t1.x & m1.x) | (t1.y & m1.y) | (t1.z & m1.z) | (t1.w & m1.w);
+        }
+        pass = any != 0u;
+        qaddr += (uint32_t)a.qm_stride * 4u;
+      }
+    }
+  }
+  if (pass) {
+    const uint64_t T = h.sT[q];
+    const int64_t slot = h.tile * kTileItems + item;
+    const uint64_t key = make_key(score, __ldg(a.id_rank + slot));
+    if (key >= T) {
+      const uint32_t p = atomicAdd(a.out_cnt + q, 1u);
+      if (p < (uint32_t)a.cap) {
+        a.out_key[(int64_t)q * a.cap + p] = key;
+        if (a.out_slot) a.out_slot[(int64_t)q * a.cap + p] = (uint32_t)slot;
+      }
+    }
+  }
+}
+
+template <bool kCnf>
 __global__ void __launch_bounds__(kThreads, 1)
     k_scan_tc(const __grid_constant__ CUtensorMap tmap_items, const TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -280,18 +397,41 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   for (int q = threadIdx.x; q < kMaxQueries; q += kThreads)
     sT[q] = (a.threshold != nullptr && q < a.nq) ? a.threshold[q] : 0ull;
-  const uint16_t* prog_base = a.rops;
-  if (a.has_prog) {
+  int32_t prog_off0 = 0;
+  bool prog_staged = false;
+  if (kCnf) {
+    // column -> plane-slot table (negated columns flagged by a set bit 14 on slot 0),
+    // query group masks (zero-padded to qm_stride words), group counts, zeroed TB stages
+    for (int i = threadIdx.x; i < a.n_cols * a.k_max; i += kThreads) {
+      const int c = i / a.k_max, j = i - c * a.k_max;
+      const int cl = a.col_leaf[c];
+      const int leaf = cl >= 0 ? cl : ~cl;
+      int s = a.leaf_slot[leaf * a.k_max + j];
+      if (j == 0 && cl < 0) s |= 0x4000;
+      sLS[i] = (int16_t)s;
+    }
+    uint32_t* qm = reinterpret_cast<uint32_t*>(smem + a.off_qm);
+    const int qm_words = a.nq * a.cnf_gmax * a.qm_stride;
+    for (int i = threadIdx.x; i < qm_words; i += kThreads) {
+      const int w = i % a.qm_stride, qg = i / a.qm_stride;
+      qm[i] = w < a.cnf_words ? a.qmask[(int64_t)qg * a.cnf_words + w] : 0u;
+    }
+    int32_t* qgs = reinterpret_cast<int32_t*>(smem + a.off_qg);
+    for (int q = threadIdx.x; q < kMaxQueries; q += kThreads) qgs[q] = q < a.nq ? a.qgroups[q] : 0;
+    uint32_t* tb = reinterpret_cast<uint32_t*>(sL);
+    for (int i = threadIdx.x; i < 2 * (int)(a.leaf_stage_bytes / 4); i += kThreads) tb[i] = 0u;
+  } else if (a.has_prog) {
     for (int i = threadIdx.x; i < a.n_leaves * a.k_max; i += kThreads) sLS[i] = a.leaf_slot[i];
-    const int32_t off0 = a.rop_offset[0];
-    const int32_t n_ops = a.rop_offset[a.nq] - off0;
+    prog_off0 = a.rop_offset[0];
+    const int32_t n_ops = a.rop_offset[a.nq] - prog_off0;
     if (n_ops <= a.rops_cap) {
       uint4* dst = reinterpret_cast<uint4*>(smem + a.off_r);
-      const uint4* src = reinterpret_cast<const uint4*>(a.rops + off0);
+      const uint4* src = reinterpret_cast<const uint4*>(a.rops + prog_off0);
       for (int i = threadIdx.x; i < n_ops / 8; i += kThreads) dst[i] = __ldg(src + i);
-      prog_base = reinterpret_cast<const uint16_t*>(smem + a.off_r) - off0;
+      prog_staged = true;
     }
   }
+  const uint32_t prog_s = su32(smem + a.off_r);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int s = 0; s < 4; ++s) {
@@ -323,19 +463,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t n_sel = a.n_sel;
   if (warp == 0) {
     // ================= producer: TMA item tile + Bloom plane words ================
-    int it = 0;
-    for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
+    int s = 0, ps = 0;
+    uint32_t ph = 0, pph = 0;
+    for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x) {
       const int tile = a.work[i * a.work_stride].x;
-      const int s = it % S;
-      const uint32_t ph = (uint32_t)(it / S) & 1u;
       if (lane == 0) {
         mbar_wait_idle(items_empty + s, ph ^ 1u);
         mbar_expect_tx(items_full + s, kItemBytes);
         tma_load_2d(sB + (size_t)s * kItemBytes, &tmap_items, 0, tile * kTileItems, items_full + s);
       }
       if (a.has_prog && a.n_planes > 0) {
-        const int ps = it % PS;
-        const uint32_t pph = (uint32_t)(it / PS) & 1u;
         mbar_wait_idle(planes_empty + ps, pph ^ 1u);
         if (lane == 0) mbar_expect_tx(planes_full + ps, (uint32_t)a.n_planes * 32u);
         __syncwarp();
@@ -345,16 +482,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 (int64_t)tile * kTileWords;
           bulk_load(dst + p * 32, src, 32u, planes_full + ps);
         }
+        if (++ps == PS) { ps = 0; pph ^= 1u; }
       }
+      if (++s == S) { s = 0; ph ^= 1u; }
     }
   } else if (warp == 1) {
     // ================= MMA issuer (one thread) ====================================
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_i8(kBlockM, kTileItems);
-      int it = 0, acc_it = 0;
-      for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
-        const int s = it % S;
-        const uint32_t ph = (uint32_t)(it / S) & 1u;
+      int acc_it = 0, s = 0;
+      uint32_t ph = 0;
+      for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x) {
         mbar_wait(items_full + s, ph);
         tc_fence_after();
         const uint32_t b_base = su32(sB + (size_t)s * kItemBytes);
@@ -372,16 +510,54 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_commit(acc_full + ab);
         }
         umma_commit(items_empty + s);
+        if (++s == S) { s = 0; ph ^= 1u; }
       }
+    }
+  } else if (warp < kEpiWarp0 && kCnf) {
+    // ================= column builders (CNF): Bloom test per literal column, then a
+    // 32x32 bit transpose so each item row holds its column bits =====================
+    const int lw = warp - 2;  // 0 or 1
+    int it = 0, ps = 0;
+    uint32_t pph = 0;
+    for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
+      const int st = it & 1;
+      const uint32_t ph = (uint32_t)(it >> 1) & 1u;
+      mbar_wait_idle(planes_full + ps, pph);
+      mbar_wait_idle(leaf_empty + st, ph ^ 1u);
+      const uint32_t* P32 = reinterpret_cast<const uint32_t*>(sP + (size_t)ps * a.plane_stage_bytes);
+      uint32_t* TB = reinterpret_cast<uint32_t*>(sL + (size_t)st * a.leaf_stage_bytes);
+      for (int blk = lw; blk < a.cnf_words * 8; blk += 2) {
+        const int cb = blk >> 3, ib = blk & 7;  // 32-column block, 32-item block
+        const int col = cb * 32 + lane;
+        uint32_t m = 0u;
+        if (col < a.n_cols) {
+          m = ~0u;
+          bool neg = false;
+          for (int j = 0; j < a.k_max; ++j) {
+            int sl = sLS[col * a.k_max + j];
+            if (j == 0) {
+              neg = (sl & 0x4000) != 0;
+              sl &= ~0x4000;
+            }
+            if (sl < 0) break;
+            m &= P32[sl * (2 * kTileWords) + ib];
+          }
+          if (neg) m = ~m;
+        }
+        TB[(ib * 32 + lane) * kTbStride + cb] = transpose32(m, lane);
+      }
+      __syncwarp();
+      mbar_arrive(planes_empty + ps);  // 32 arrivals per warp, 64 in total
+      mbar_arrive(leaf_full + st);
+      if (++ps == PS) { ps = 0; pph ^= 1u; }
     }
   } else if (warp < kEpiWarp0) {
     // ================= leaf builders: AND each leaf's planes per word =============
     if (a.has_prog) {
       const int t = threadIdx.x - 64;
-      int it = 0;
+      int it = 0, ps = 0;
+      uint32_t pph = 0;
       for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
-        const int ps = it % PS;
-        const uint32_t pph = (uint32_t)(it / PS) & 1u;
         const int st = it & 1;
         const uint32_t ph = (uint32_t)(it >> 1) & 1u;
         if (a.n_planes > 0) mbar_wait_idle(planes_full + ps, pph);
@@ -400,7 +576,145 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (a.n_planes > 0) mbar_arrive(planes_empty + ps);
         mbar_arrive(leaf_full + st);
+        if (++ps == PS) { ps = 0; pph ^= 1u; }
       }
+    }
+  } else if (kCnf) {
+    // ================= epilogue (CNF): TMEM scores -> threshold gate -> hits queue ->
+    // dense per-hit filter test (transposed column bits & query group masks) -> emit ===
+    const int ew = warp - kEpiWarp0;
+    const int quad = warp & 3;
+    const int half = ew >> 2;
+    const int row = quad * 32 + lane;
+    const uint32_t hit_s = su32(smem + a.off_hit) + (uint32_t)ew * (kHitCap * 8u);
+    HitCtx h;
+    h.qm_s = su32(smem + a.off_qm);
+    h.qg = reinterpret_cast<const int32_t*>(smem + a.off_qg);
+    h.sT = sT;
+    int it = 0, acc_it = 0;
+    for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
+      const int2 wk = a.work[i * a.work_stride];
+      const int64_t s0 = a.ranges[2 * wk.y], s1 = a.ranges[2 * wk.y + 1];
+      h.tile = wk.x;
+#pragma unroll
+      for (int w = 0; w < kTileWords; ++w) {
+        const int64_t gw = h.tile * kTileWords + w;
+        h.vw[w] = __ldg(a.valid + gw) & word_range_mask(gw * 64, s0, s1);
+      }
+      const int st = it & 1;
+      mbar_wait(leaf_full + st, (uint32_t)(it >> 1) & 1u);
+      h.tb_s = su32(sL + (size_t)st * a.leaf_stage_bytes);
+      const uint64_t my_valid = (h.vw[2 * half] | h.vw[2 * half + 1]);
+#pragma unroll 1
+      for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
+        h.mb = mb;
+        const int q = mb * kBlockM + row;
+        const bool active = q < a.nq && my_valid != 0ull;
+        const uint64_t T = q < a.nq ? sT[q] : ~0ull;
+        const int32_t tau = T == 0ull ? INT32_MIN : key_score(T);
+        const int ab = acc_it & 1;
+        mbar_wait(acc_full + ab, (uint32_t)(acc_it >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kAccCols + half * 128);
+        uint32_t head = 0, tail = 0;  // warp-uniform ring-buffer cursors
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          int32_t r[32];
+          tmem_ld32(taddr + c * 32, r);
+          if (a.dump != nullptr && q < a.nq) {
+            const int64_t base = h.tile * kTileItems + half * 128 + c * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (base + j < a.dump_ld) a.dump[(int64_t)q * a.dump_ld + base + j] = r[j];
+          }
+          // maxima of the four 8-item groups, then the exact hit mask inside groups that
+          // clear the threshold
+          int32_t g8[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            g8[g] = max(__vimax3_s32(r[8 * g], r[8 * g + 1], r[8 * g + 2]),
+                        __vimax3_s32(__vimax3_s32(r[8 * g + 3], r[8 * g + 4], r[8 * g + 5]),
+                                     r[8 * g + 6], r[8 * g + 7]));
+          uint32_t hm = 0u;
+          if (active) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              if (g8[g] >= tau) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) hm |= (r[8 * g + j] >= tau ? 1u : 0u) << (8 * g + j);
+              }
+            }
+          }
+          const uint32_t n = __popc(hm);
+          // exclusive prefix of n across the warp
+          uint32_t pre = n;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, pre, d);
+            if (lane >= d) pre += y;
+          }
+          const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
+          pre -= n;
+          if (total == 0u) continue;
+          const uint32_t item0 = (uint32_t)(half * 128 + c * 32);
+          if (tail - head + total > (uint32_t)kHitCap) {
+            // dense regime (e.g. threshold 0): test this chunk's hits in place
+            if (hm != 0u) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if ((hm >> j) & 1u) process_hit(a, h, (uint32_t)row, item0 + j, r[j]);
+            }
+            continue;
+          }
+          if (hm != 0u) {
+            uint32_t k = tail + pre;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              if ((hm >> (8 * g)) & 0xFFu) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  if ((hm >> (8 * g + j)) & 1u) {
+                    const uint32_t e = hit_s + (k & (kHitCap - 1)) * 8u;
+                    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(e),
+                                 "r"(((uint32_t)row << 8) | (item0 + 8 * g + j)), "r"(r[8 * g + j])
+                                 : "memory");
+                    ++k;
+                  }
+                }
+              }
+            }
+          }
+          tail += total;
+          __syncwarp();
+          while (tail - head >= 32u) {
+            uint32_t ent, sc;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                         : "=r"(ent), "=r"(sc)
+                         : "r"(hit_s + ((head + lane) & (kHitCap - 1)) * 8u));
+            __syncwarp();
+            process_hit(a, h, ent >> 8, ent & 0xFFu, (int32_t)sc);
+            head += 32u;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + ab);
+        // drain the partial batch (no TMEM needed any more)
+        if (tail != head) {
+          uint32_t ent = 0, sc = 0;
+          const bool mine = (uint32_t)lane < tail - head;
+          if (mine)
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                         : "=r"(ent), "=r"(sc)
+                         : "r"(hit_s + ((head + lane) & (kHitCap - 1)) * 8u));
+          __syncwarp();
+          if (mine) process_hit(a, h, ent >> 8, ent & 0xFFu, (int32_t)sc);
+        }
+        __syncwarp();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(leaf_empty + st);
     }
   } else {
     // ================= epilogue: filter (eager) + TMEM scores + gate + emit ========
@@ -408,6 +722,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int half = ew >> 2;   // item columns [half * 128, half * 128 + 128)
     const int row = quad * 32 + lane;
+    // per M-block: this thread's query program (offset into the staged copy, length)
+    int p_off[kMaxMBlocks], p_len[kMaxMBlocks];
+#pragma unroll
+    for (int mb = 0; mb < kMaxMBlocks; ++mb) {
+      const int q = mb * kBlockM + row;
+      p_off[mb] = p_len[mb] = 0;
+      if (a.has_prog && q < a.nq && mb < a.n_mblk) {
+        p_off[mb] = a.rop_offset[q] - prog_off0;
+        p_len[mb] = a.rop_offset[q + 1] - a.rop_offset[q];
+      }
+    }
     int it = 0, acc_it = 0;
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
       const int2 wk = a.work[i * a.work_stride];
@@ -418,20 +743,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t v1 = __ldg(a.valid + wbase + 1) & word_range_mask((wbase + 1) * 64, s0, s1);
       const int st = it & 1;
       if (a.has_prog) mbar_wait(leaf_full + st, (uint32_t)(it >> 1) & 1u);
-      const uint64_t* L = reinterpret_cast<const uint64_t*>(sL + (size_t)st * a.leaf_stage_bytes);
+      const uint32_t leaf_s = su32(sL + (size_t)st * a.leaf_stage_bytes) + 16u * half;
+#pragma unroll 1
       for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
         const int q = mb * kBlockM + row;
         const bool active = q < a.nq;
         // eligibility of this thread's 128 items: validity & range & program & mask
         uint64_t f0 = active ? v0 : 0ull, f1 = active ? v1 : 0ull;
-        if (a.has_prog && (f0 | f1) != 0ull) {
-          const int o0 = a.rop_offset[q], o1 = a.rop_offset[q + 1];
-          if (o1 > o0) {
-            uint64_t e0, e1;
-            eval_half(prog_base + o0, o1 - o0, L, half, e0, e1);
-            f0 &= e0;
-            f1 &= e1;
-          }
+        const int plen = mb == 0 ? p_len[0] : p_len[1];
+        if (plen > 0 && (f0 | f1) != 0ull) {
+          const int poff = mb == 0 ? p_off[0] : p_off[1];
+          uint64_t e0, e1;
+          if (prog_staged)
+            eval_half(prog_s + 2u * poff, plen, leaf_s, e0, e1);
+          else
+            eval_half_global(a.rops + prog_off0 + poff, plen, leaf_s, e0, e1);
+          f0 &= e0;
+          f1 &= e1;
         }
         if (a.masks != nullptr && (f0 | f1) != 0ull) {
           f0 &= __ldg(a.masks + (int64_t)q * a.n_words + wbase);
@@ -522,8 +850,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // shared-memory carve-up; returns total bytes (incl. 1 KB alignment slack)
+// Shared-memory carve-up; returns total bytes (incl. 1 KB alignment slack). In CNF mode
+// the per-tile stage holds transposed column bits (256 items x kTbStride u32), the query
+// group masks and group counts are staged, and each epilogue warp gets a hit ring buffer.
 size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int stages,
-              int plane_stages) {
+              int plane_stages, bool cnf) {
   size_t off = 0;
   t.off_a = 0;
   off = (size_t)n_mblk * kBlockM * kKBytes;
@@ -533,15 +864,25 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
   t.off_p = (uint32_t)align_up(off, 128);
   off = t.off_p + (size_t)plane_stages * t.plane_stage_bytes;
   t.leaf_stage_bytes =
-      (uint32_t)align_up((size_t)(n_leaves > 0 ? n_leaves : 1) * kLeafStride * 8, 128);
+      cnf ? (uint32_t)(kTileItems * kTbStride * 4)
+          : (uint32_t)align_up((size_t)(n_leaves > 0 ? n_leaves : 1) * kLeafStride * 8, 128);
   t.off_l = (uint32_t)align_up(off, 128);
   off = t.off_l + 2ull * t.leaf_stage_bytes;
+  const int rows = cnf ? t.n_cols : n_leaves;
   t.off_ls = (uint32_t)align_up(off, 16);
-  off = t.off_ls + (size_t)(n_leaves > 0 ? n_leaves : 1) * (k_max > 0 ? k_max : 1) * 2;
+  off = t.off_ls + (size_t)(rows > 0 ? rows : 1) * (k_max > 0 ? k_max : 1) * 2;
   t.off_thr = (uint32_t)align_up(off, 16);
   off = t.off_thr + (size_t)kMaxQueries * 8;
   t.off_bar = (uint32_t)align_up(off, 16);
   off = t.off_bar + 21 * 8 + 16;
+  if (cnf) {
+    t.off_qm = (uint32_t)align_up(off, 16);
+    off = t.off_qm + (size_t)kMaxQueries * t.cnf_gmax * t.qm_stride * 4;
+    t.off_qg = (uint32_t)align_up(off, 16);
+    off = t.off_qg + (size_t)kMaxQueries * 4;
+    t.off_hit = (uint32_t)align_up(off, 16);
+    off = t.off_hit + (size_t)kEpiWarps * kHitCap * 8;
+  }
   t.off_r = (uint32_t)align_up(off, 16);
   off = t.off_r + (size_t)t.rops_cap * 2;
   return off + 1024;
@@ -552,25 +893,42 @@ constexpr int kMaxStagedOps = 16384;  // 32 KB; whatever is left stays L1
 
 // Prefer 3 item stages and 2 plane stages; stage as much filter bytecode as fits.
 bool pick_stages(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int n_rops,
-                 size_t& smem) {
+                 bool cnf, size_t& smem) {
   const int prefs[4][2] = {{3, 2}, {3, 1}, {2, 2}, {2, 1}};
+  if (cnf) n_rops = 0;  // the CNF epilogue does not read the bytecode
   // first pass: the configuration that also holds all filter bytecode; second: any
   for (int pass = 0; pass < 2; ++pass) {
     for (const auto& pr : prefs) {
       t.rops_cap = 0;
-      smem = layout(t, n_mblk, n_planes, n_leaves, k_max, pr[0], pr[1]);
+      smem = layout(t, n_mblk, n_planes, n_leaves, k_max, pr[0], pr[1], cnf);
       if (smem > kSmemLimit) continue;
       const size_t room = (kSmemLimit - smem) / 2 / 8 * 8;
       const size_t want = (size_t)std::min(n_rops > 0 ? n_rops : 0, kMaxStagedOps);
       if (pass == 0 && room < want) continue;
       t.rops_cap = (int32_t)std::min(room, want);
-      smem = layout(t, n_mblk, n_planes, n_leaves, k_max, pr[0], pr[1]);
+      smem = layout(t, n_mblk, n_planes, n_leaves, k_max, pr[0], pr[1], cnf);
       t.item_stages = pr[0];
       t.plane_stages = pr[1];
       return true;
     }
   }
   return false;
+}
+
+bool use_cnf(const ScanArgs& a) {
+  return a.has_prog && a.prog.col_leaf != nullptr && a.prog.cnf_words >= 1 &&
+         a.prog.cnf_words <= 8 && a.prog.cnf_gmax >= 1 && a.prog.cnf_gmax <= 8 &&
+         a.prog.n_cols <= 32 * a.prog.cnf_words;
+}
+
+void fill_cnf(TcArgs& t, const ScanArgs& a, int q0) {
+  t.n_cols = a.prog.n_cols;
+  t.cnf_words = a.prog.cnf_words;
+  t.cnf_gmax = a.prog.cnf_gmax;
+  t.qm_stride = a.prog.cnf_words <= 4 ? 4 : 8;
+  t.col_leaf = a.prog.col_leaf;
+  t.qmask = a.prog.qmask + (int64_t)q0 * a.prog.cnf_gmax * a.prog.cnf_words;
+  t.qgroups = a.prog.qgroups + q0;
 }
 
 }  // namespace
@@ -581,12 +939,14 @@ bool scan_tc_supported(const ScanArgs& a) {
   if (a.idx.n_slots % kTileItems != 0 || a.tc_work == nullptr) return false;
   if (encode_fn() == nullptr) return false;
   if (a.has_prog) {
-    if (a.prog.rops == nullptr || a.prog.rmax_stack > kRegStack) return false;
-    if (a.prog.n_leaves >= (1 << 13)) return false;
+    const bool cnf = use_cnf(a);
+    if (!cnf && (a.prog.rops == nullptr || a.prog.rmax_stack > kRegStack)) return false;
+    if (a.prog.n_leaves >= (1 << 13) || a.prog.plane_list == nullptr) return false;
     TcArgs t{};
+    if (cnf) fill_cnf(t, a, 0);
     size_t smem = 0;
     const int n_mblk = a.n_queries >= kBlockM ? kMaxMBlocks : 1;
-    if (!pick_stages(t, n_mblk, a.prog.n_planes, a.prog.n_leaves, a.prog.k_max, 0, smem))
+    if (!pick_stages(t, n_mblk, a.prog.n_planes, a.prog.n_leaves, a.prog.k_max, 0, cnf, smem))
       return false;
   }
   return true;
@@ -609,6 +969,7 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
   int n_sm = 148;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
   const int grid = (int)(n_sel < n_sm ? n_sel : n_sm);
+  const bool cnf = use_cnf(a);
   for (int q0 = 0; q0 < a.n_queries; q0 += kMaxQueries) {
     const int nq = a.n_queries - q0 < kMaxQueries ? a.n_queries - q0 : kMaxQueries;
     TcArgs t{};
@@ -629,6 +990,7 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
       t.leaf_slot = a.prog.leaf_slot;
       t.rop_offset = a.prog.rop_offset + q0;
       t.rops = a.prog.rops;
+      if (cnf) fill_cnf(t, a, q0);
     }
     t.work = reinterpret_cast<const int2*>(a.tc_work);
     t.n_sel = n_sel;
@@ -643,11 +1005,17 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
     t.dump_ld = a.dump_ld;
     size_t smem = 0;
     if (!pick_stages(t, t.n_mblk, t.has_prog ? t.n_planes : 0, t.has_prog ? t.n_leaves : 0,
-                     t.has_prog ? t.k_max : 0, t.has_prog ? a.prog.n_rops : 0, smem))
+                     t.has_prog ? t.k_max : 0, t.has_prog ? a.prog.n_rops : 0, cnf, smem))
       return FB_ERR_UNSUPPORTED;
-    FB_CUDA(cudaFuncSetAttribute(k_scan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    k_scan_tc<<<grid, kThreads, smem, s>>>(tmap, t);
+    if (cnf) {
+      FB_CUDA(cudaFuncSetAttribute(k_scan_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      k_scan_tc<true><<<grid, kThreads, smem, s>>>(tmap, t);
+    } else {
+      FB_CUDA(cudaFuncSetAttribute(k_scan_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      k_scan_tc<false><<<grid, kThreads, smem, s>>>(tmap, t);
+    }
     FB_LAUNCH_CHECK("k_scan_tc");
   }
   return FB_OK;

@@ -296,6 +296,60 @@ def lower_to_register_ops(ops: list[tuple[int, int]]) -> tuple[list[int], int]:
     return [(c << 13) | l for c, l in out], peak
 
 
+CNF_MAX_WORDS = 8    # leaf columns per batch <= 256
+CNF_MAX_GROUPS = 8
+
+
+def cnf_groups(ops: list[tuple[int, int]]):
+    """Conjunctive normal form of a postfix program over (global) leaves, or None.
+
+    NOTs are pushed down to literals (De Morgan; exact for bitwise masks because the
+    result is ANDed with validity at the end), same-operator nodes are flattened, and the
+    result must be an AND of ORs of literals. Returns a list of groups, each a list of
+    ``(leaf, negated)`` literals."""
+    stack: list = []
+    for op, leaf in ops:
+        if op == OpCode.PUSH_LEAF:
+            stack.append(("lit", leaf, False))
+        elif op == OpCode.NOT:
+            stack.append(("not", stack.pop()))
+        else:
+            rhs = stack.pop()
+            lhs = stack.pop()
+            stack.append(("and" if op == OpCode.AND else "or", [lhs, rhs]))
+    if len(stack) != 1:
+        return None
+
+    def nnf(node, neg):
+        kind = node[0]
+        if kind == "lit":
+            return ("lit", node[1], node[2] != neg)
+        if kind == "not":
+            return nnf(node[1], not neg)
+        flip = {"and": "or", "or": "and"}
+        k = flip[kind] if neg else kind
+        kids = []
+        for child in node[1]:
+            c = nnf(child, neg)
+            kids.extend(c[1] if c[0] == k else [c])
+        return (k, kids)
+
+    root = nnf(stack[0], False)
+
+    def clause(node):
+        if node[0] == "lit":
+            return [(node[1], node[2])]
+        if node[0] == "or" and all(c[0] == "lit" for c in node[1]):
+            return [(c[1], c[2]) for c in node[1]]
+        return None
+
+    if root[0] == "and":
+        groups = [clause(c) for c in root[1]]
+        return None if any(g is None for g in groups) else groups
+    g = clause(root)
+    return None if g is None else [g]
+
+
 class FilterBatch:
     """Device bytecode for a batch of compiled filters (one per query, ``None`` =
     unfiltered), mirroring ``fb_filter_prog_t`` (include/filtra_b200.h):
@@ -308,7 +362,8 @@ class FilterBatch:
     """
 
     def __init__(self, leaf_pos, op_offset, ops, max_stack, push_leaf_bits, *,
-                 plane_list=None, leaf_slot=None, rop_offset=None, rops=None, rmax_stack=0):
+                 plane_list=None, leaf_slot=None, rop_offset=None, rops=None, rmax_stack=0,
+                 col_leaf=None, qmask=None, qgroups=None, cnf_words=0, cnf_gmax=0):
         self.n_queries = len(op_offset) - 1
         self.n_leaves = leaf_pos.shape[0]
         self.k_max = leaf_pos.shape[1]
@@ -324,6 +379,15 @@ class FilterBatch:
                                 if rop_offset is not None else None)
         self.host_rops = np.ascontiguousarray(rops, dtype=np.uint16) if rops is not None else None
         self.rmax_stack = rmax_stack
+        # CNF form (all queries AND-of-OR-of-literals): literal columns (leaf, or ~leaf when
+        # negated), per query per group a column bitmask, and the group count per query
+        self.host_col_leaf = (np.ascontiguousarray(col_leaf, dtype=np.int16)
+                              if col_leaf is not None else None)
+        self.host_qmask = np.ascontiguousarray(qmask, dtype=np.uint32) if qmask is not None else None
+        self.host_qgroups = (np.ascontiguousarray(qgroups, dtype=np.int32)
+                             if qgroups is not None else None)
+        self.cnf_words = cnf_words
+        self.cnf_gmax = cnf_gmax
         # per query: sum over PUSH_LEAF ops of |set_bits| (FilterStats.words_read per word)
         self.push_leaf_bits = push_leaf_bits
         self._dev = None
@@ -332,11 +396,17 @@ class FilterBatch:
     def n_planes(self) -> int:
         return 0 if self.host_plane_list is None else int(self.host_plane_list.size)
 
+    @property
+    def is_cnf(self) -> bool:
+        return self.host_col_leaf is not None
+
     def host_arrays(self) -> list[np.ndarray]:
         arrs = [self.host_leaf_pos, self.host_op_offset, self.host_ops.view(np.int16)]
         if self.host_rops is not None:
             arrs += [self.host_plane_list, self.host_leaf_slot, self.host_rop_offset,
                      self.host_rops.view(np.int16)]
+            if self.host_col_leaf is not None:
+                arrs += [self.host_col_leaf, self.host_qmask.view(np.int32), self.host_qgroups]
         return arrs
 
     def to_device(self) -> "FilterBatch":
@@ -371,6 +441,7 @@ class FilterBatch:
         push_bits = []
         max_stack = 1
         rmax = 0
+        cnf: list | None = []
         for cf in filters:
             nbits = 0
             if cf is not None:
@@ -396,6 +467,11 @@ class FilterBatch:
                 enc += [ROP_NOP << 13] * (-len(enc) % ROP_ALIGN)
                 rops.extend(enc)
                 rmax = max(rmax, depth)
+                if cnf is not None:
+                    groups = cnf_groups(gops)
+                    cnf = None if groups is None else cnf + [groups]
+            elif cnf is not None:
+                cnf.append([])
             offsets.append(len(ops))
             rop_offsets.append(len(rops))
             push_bits.append(nbits)
@@ -413,6 +489,27 @@ class FilterBatch:
         for i, r in enumerate(leaf_rows):
             leaf_slot[i, : len(r)] = [slot_of[p] for p in r]
         reg = len(leaf_rows) <= ROP_MAX_LEAVES
+        cnf_kw = {}
+        if reg and cnf is not None and any(cnf):
+            cols: dict[tuple[int, bool], int] = {}
+            for groups in cnf:
+                for g in groups:
+                    for lit in g:
+                        cols.setdefault(lit, len(cols))
+            words = (len(cols) + 31) // 32
+            gmax = max(len(groups) for groups in cnf)
+            if words <= CNF_MAX_WORDS and gmax <= CNF_MAX_GROUPS:
+                qmask = np.zeros((len(cnf), gmax, words), dtype=np.uint32)
+                for q, groups in enumerate(cnf):
+                    for gi, g in enumerate(groups):
+                        for lit in g:
+                            c = cols[lit]
+                            qmask[q, gi, c >> 5] |= np.uint32(1 << (c & 31))
+                col_leaf = np.array([(~leaf if neg else leaf) for (leaf, neg) in cols],
+                                    dtype=np.int16)
+                cnf_kw = dict(col_leaf=col_leaf, qmask=qmask,
+                              qgroups=np.array([len(g) for g in cnf], dtype=np.int32),
+                              cnf_words=words, cnf_gmax=gmax)
         return cls(leaf_pos, np.array(offsets, dtype=np.int32),
                    np.array(ops if ops else [0], dtype=np.uint16), max_stack,
                    np.array(push_bits, dtype=np.int64),
@@ -421,7 +518,7 @@ class FilterBatch:
                    rop_offset=np.array(rop_offsets, dtype=np.int32) if reg else None,
                    rops=(np.array(rops if rops else [ROP_NOP << 13] * ROP_ALIGN, dtype=np.uint16)
                          if reg else None),
-                   rmax_stack=rmax)
+                   rmax_stack=rmax, **cnf_kw)
 
     @classmethod
     def from_leaf(cls, qb: QueryBloom, params: BloomParams) -> "FilterBatch":
@@ -436,8 +533,14 @@ class FilterBatch:
                      d[3].data_ptr(), d[4].data_ptr(), d[5].data_ptr(), d[6].data_ptr())
         else:
             extra = (0, 0, 0, 0, None, None, None, None)
+        if self.is_cnf:
+            cnf = (int(self.host_col_leaf.size), self.cnf_words, self.cnf_gmax, 0,
+                   d[7].data_ptr(), d[8].data_ptr(), d[9].data_ptr())
+        else:
+            cnf = (0, 0, 0, 0, None, None, None)
         return _native.FbFilterProg(self.n_queries, self.n_leaves, self.k_max, self.max_stack,
-                                    d[0].data_ptr(), d[1].data_ptr(), d[2].data_ptr(), *extra)
+                                    d[0].data_ptr(), d[1].data_ptr(), d[2].data_ptr(), *extra,
+                                    *cnf)
 
     def evaluate(self, bloom: BloomIndex, valid, w0: int, w1: int,
                  apply_valid: bool = True) -> np.ndarray:
