@@ -386,3 +386,73 @@ def test_tc_vs_simt_vs_oracle(fb, wl_small, k):
             ids, scores = out.host(q)
             assert np.array_equal(ids, ref[q].item_ids), (flags, q)
             assert np.array_equal(scores, ref[q].scores), (flags, q)
+
+
+def _random_filter(rng, depth=0):
+    if depth >= 3 or rng.random() < 0.3:
+        return ("leaf", int(rng.integers(1, 5)), int(rng.integers(0, 12)))
+    roll = rng.random()
+    if roll < 0.2:
+        return ("not", _random_filter(rng, depth + 1))
+    kind = "and" if roll < 0.6 else "or"
+    return (kind, [_random_filter(rng, depth + 1) for _ in range(int(rng.integers(2, 4)))])
+
+
+def _to_expr(fb, t):
+    if t[0] == "leaf":
+        return fb.Leaf(t[1], t[2])
+    if t[0] == "not":
+        return fb.Not(_to_expr(fb, t[1]))
+    cls = fb.And if t[0] == "and" else fb.Or
+    return cls(tuple(_to_expr(fb, c) for c in t[1]))
+
+
+@pytest.mark.parametrize("shape", ["cnf_neg", "random_mixed"])
+def test_tc_filter_modes_vs_oracle(fb, shape):
+    """CNF batches (with negated literals / NOT over groups) take the per-hit tensor-core
+    epilogue; batches with any non-CNF program take the bytecode epilogue. Both must match
+    the oracle exactly."""
+    from paper_2511_14881_b200 import _device, _native, workload
+    from paper_2511_14881_b200.filter_query import FilterBatch
+    wl = workload.make_workload(30_000, 40, dim=128, seed=21, filtered=False)
+    idx = wl.index
+    rng = np.random.default_rng(5)
+    p = fb.BloomParams()
+    exprs = []
+    for q in range(40):
+        if shape == "cnf_neg":
+            groups = []
+            for f in range(1, 4):
+                lits = [fb.Leaf(f, int(v)) for v in rng.choice(12, size=3, replace=False)]
+                if rng.random() < 0.4:
+                    lits[0] = fb.Not(lits[0])
+                groups.append(fb.Or(tuple(lits)))
+            e = fb.And(tuple(groups))
+            if rng.random() < 0.2:
+                e = fb.Not(fb.Or((fb.Leaf(5, int(rng.integers(0, 20))), fb.Leaf(6, 1))))
+            exprs.append(e)
+        else:
+            exprs.append(_to_expr(fb, _random_filter(rng)))
+    filters = [fb.compile_filter(e, p) for e in exprs]
+    filters[3] = None
+    batch = FilterBatch.pack(filters, p)
+    assert batch.is_cnf == (shape == "cnf_neg")
+    items = idx.items.cpu().numpy()[:, :128]
+    valid = _device.u64_host(idx.valid)
+    ids = _device.u64_host(idx.item_ids)
+    offs = np.array([[0, idx.n_slots]])
+    qq = wl.queries_q.cpu().numpy()[:, :128]
+    for k in (50, 3000):
+        op = fb.TopkOp(idx, 40, k, offs)
+        out = op(wl.queries_q, batch)
+        torch.cuda.synchronize()
+        assert _native.lib().fb_topk_scan_path(op._plan) == 1
+        for q in range(40):
+            cf = filters[q]
+            prog = None if cf is None else ([(int(o), int(a)) for o, a in cf.ops],
+                                            [(f, v, b.set_bits) for f, v, b in cf.leaves])
+            ref = orc.codesigned_search(items, valid, ids, offs, idx.bloom.planes, prog, qq[q],
+                                        [0], k)
+            got_ids, got_scores = out.host(q)
+            assert np.array_equal(got_ids, ref.item_ids), (shape, k, q)
+            assert np.array_equal(got_scores, ref.scores), (shape, k, q)
