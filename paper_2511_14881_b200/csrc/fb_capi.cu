@@ -259,8 +259,10 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
     const int64_t sampled = (p->total_words + p->sample_stride - 1) / p->sample_stride;
     p->sample_fraction = (double)sampled / (double)p->total_words;
     if (p->n_tc_work > 0) {
-      const int64_t target_tiles = std::max<int64_t>(std::min<int64_t>(p->n_tc_work, 1024),
-                                                     p->n_tc_work / 32);
+      // the sample pass runs at threshold 0 (every score is a hit): keep it to ~1/128 of
+      // the tiles (>= 256 tiles, ~65k slots) -- enough for the rank estimate
+      const int64_t target_tiles = std::max<int64_t>(std::min<int64_t>(p->n_tc_work, 256),
+                                                     p->n_tc_work / 128);
       p->tc_sample_stride = std::max<int64_t>(1, p->n_tc_work / target_tiles);
       const int64_t st = (p->n_tc_work + p->tc_sample_stride - 1) / p->tc_sample_stride;
       p->tc_sample_fraction = (double)st / (double)p->n_tc_work;

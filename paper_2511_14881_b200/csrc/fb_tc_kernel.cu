@@ -309,14 +309,34 @@ struct HitCtx {
   uint64_t vw[kTileWords];  // validity & range words of the tile
   uint32_t tb_s;            // shared address of this tile's transposed column bits
   uint32_t qm_s;            // shared address of the query group masks
+  uint32_t a_s;             // shared address of the query tile (SW128 rows)
+  uint32_t b_s;             // shared address of this tile's item stage (SW128 rows)
   const int32_t* qg;        // shared: groups per query
   const uint64_t* sT;
   int mb;
 };
 
-// Full eligibility + threshold test of one hit (query row, tile item, score) and emission.
+// Exact int32 dot of a query row (A tile) and an item row (B stage) from shared memory.
+// Both tiles use the SWIZZLE_128B layout: 16-byte chunk c of row r sits at c ^ (r & 7).
+__device__ __forceinline__ int32_t smem_dot(uint32_t a_row, uint32_t a_sw, uint32_t b_row,
+                                            uint32_t b_sw) {
+  int32_t acc = 0;
+#pragma unroll
+  for (uint32_t c = 0; c < 8; ++c) {
+    const uint4 x = lds128(a_row + ((c ^ a_sw) << 4));
+    const uint4 y = lds128(b_row + ((c ^ b_sw) << 4));
+    acc = __dp4a((int)x.x, (int)y.x, acc);
+    acc = __dp4a((int)x.y, (int)y.y, acc);
+    acc = __dp4a((int)x.z, (int)y.z, acc);
+    acc = __dp4a((int)x.w, (int)y.w, acc);
+  }
+  return acc;
+}
+
+// Eligibility (validity & range & mask & CNF filter) of one hit -- a (query row, tile
+// item) whose score cleared the threshold gate -- then the exact key test and emission.
 __device__ __forceinline__ void process_hit(const TcArgs& a, const HitCtx& h, uint32_t row,
-                                            uint32_t item, int32_t score) {
+                                            uint32_t item) {
   const int q = h.mb * kBlockM + (int)row;
   const int word = (int)(item >> 6);
   uint64_t vw = h.vw[0];
@@ -348,6 +368,8 @@ __device__ __forceinline__ void process_hit(const TcArgs& a, const HitCtx& h, ui
   }
   if (pass) {
     const uint64_t T = h.sT[q];
+    const int32_t score = smem_dot(h.a_s + (uint32_t)q * kKBytes, (uint32_t)q & 7u,
+                                   h.b_s + item * kKBytes, item & 7u);
     const int64_t slot = h.tile * kTileItems + item;
     const uint64_t key = make_key(score, __ldg(a.id_rank + slot));
     if (key >= T) {
@@ -436,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < 4; ++s) {
       mbar_init(items_full + s, 1);
-      mbar_init(items_empty + s, 1);
+      mbar_init(items_empty + s, kCnf ? 1 + kEpiWarps : 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(planes_full + s, 1);
@@ -580,18 +602,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (kCnf) {
-    // ================= epilogue (CNF): TMEM scores -> threshold gate -> hits queue ->
-    // dense per-hit filter test (transposed column bits & query group masks) -> emit ===
+    // ================= epilogue (CNF): TMEM scores -> threshold gate -> hit queue ->
+    // dense per-hit filter test (transposed column bits & query group masks); the exact
+    // score of a surviving hit is recomputed from the resident smem tiles -> emit ======
     const int ew = warp - kEpiWarp0;
     const int quad = warp & 3;
     const int half = ew >> 2;
     const int row = quad * 32 + lane;
-    const uint32_t hit_s = su32(smem + a.off_hit) + (uint32_t)ew * (kHitCap * 8u);
+    const uint32_t hit_s = su32(smem + a.off_hit) + (uint32_t)ew * (kHitCap * 2u);
     HitCtx h;
     h.qm_s = su32(smem + a.off_qm);
+    h.a_s = su32(sA);
     h.qg = reinterpret_cast<const int32_t*>(smem + a.off_qg);
     h.sT = sT;
-    int it = 0, acc_it = 0;
+    int it = 0, acc_it = 0, s = 0;
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
       const int2 wk = a.work[i * a.work_stride];
       const int64_t s0 = a.ranges[2 * wk.y], s1 = a.ranges[2 * wk.y + 1];
@@ -601,15 +625,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t gw = h.tile * kTileWords + w;
         h.vw[w] = __ldg(a.valid + gw) & word_range_mask(gw * 64, s0, s1);
       }
+      h.b_s = su32(sB + (size_t)s * kItemBytes);
       const int st = it & 1;
       mbar_wait(leaf_full + st, (uint32_t)(it >> 1) & 1u);
       h.tb_s = su32(sL + (size_t)st * a.leaf_stage_bytes);
-      const uint64_t my_valid = (h.vw[2 * half] | h.vw[2 * half + 1]);
+      const bool any_valid = (h.vw[2 * half] | h.vw[2 * half + 1]) != 0ull;
 #pragma unroll 1
       for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
         h.mb = mb;
         const int q = mb * kBlockM + row;
-        const bool active = q < a.nq && my_valid != 0ull;
+        const bool active = q < a.nq && any_valid;
         const uint64_t T = q < a.nq ? sT[q] : ~0ull;
         const int32_t tau = T == 0ull ? INT32_MIN : key_score(T);
         const int ab = acc_it & 1;
@@ -628,73 +653,49 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j)
               if (base + j < a.dump_ld) a.dump[(int64_t)q * a.dump_ld + base + j] = r[j];
           }
-          // maxima of the four 8-item groups, then the exact hit mask inside groups that
-          // clear the threshold
-          int32_t g8[4];
-#pragma unroll
-          for (int g = 0; g < 4; ++g)
-            g8[g] = max(__vimax3_s32(r[8 * g], r[8 * g + 1], r[8 * g + 2]),
-                        __vimax3_s32(__vimax3_s32(r[8 * g + 3], r[8 * g + 4], r[8 * g + 5]),
-                                     r[8 * g + 6], r[8 * g + 7]));
           uint32_t hm = 0u;
-          if (active) {
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              if (g8[g] >= tau) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) hm |= (r[8 * g + j] >= tau ? 1u : 0u) << (8 * g + j);
-              }
-            }
-          }
+          for (int j = 0; j < 32; ++j) hm |= (r[j] >= tau ? 1u : 0u) << j;
+          if (!active) hm = 0u;
+          const uint32_t item0 = (uint32_t)(half * 128 + c * 32);
           const uint32_t n = __popc(hm);
-          // exclusive prefix of n across the warp
-          uint32_t pre = n;
+          uint32_t pre = n;  // inclusive prefix of n across the warp
 #pragma unroll
           for (int d = 1; d < 32; d <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, pre, d);
             if (lane >= d) pre += y;
           }
           const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
-          pre -= n;
           if (total == 0u) continue;
-          const uint32_t item0 = (uint32_t)(half * 128 + c * 32);
-          if (tail - head + total > (uint32_t)kHitCap) {
-            // dense regime (e.g. threshold 0): test this chunk's hits in place
-            if (hm != 0u) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if ((hm >> j) & 1u) process_hit(a, h, (uint32_t)row, item0 + j, r[j]);
+          pre -= n;
+          uint32_t rank = pre;  // global rank of this lane's next unwritten hit
+          uint32_t rem = hm;
+          uint32_t done = 0u;
+          // append in rounds so the ring never overflows (dense regime: threshold 0)
+          while (done < total) {
+            const uint32_t room = (uint32_t)kHitCap - (tail - head);
+            const uint32_t take = total - done < room ? total - done : room;
+            while (rem != 0u && rank < done + take) {
+              const uint32_t j = (uint32_t)(__ffs(rem) - 1);
+              rem &= rem - 1u;
+              asm volatile("st.shared.u16 [%0], %1;" ::"r"(
+                               hit_s + ((tail + rank - done) & (kHitCap - 1)) * 2u),
+                           "h"((unsigned short)(((uint32_t)row << 8) | (item0 + j)))
+                           : "memory");
+              ++rank;
             }
-            continue;
-          }
-          if (hm != 0u) {
-            uint32_t k = tail + pre;
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              if ((hm >> (8 * g)) & 0xFFu) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  if ((hm >> (8 * g + j)) & 1u) {
-                    const uint32_t e = hit_s + (k & (kHitCap - 1)) * 8u;
-                    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(e),
-                                 "r"(((uint32_t)row << 8) | (item0 + 8 * g + j)), "r"(r[8 * g + j])
-                                 : "memory");
-                    ++k;
-                  }
-                }
-              }
-            }
-          }
-          tail += total;
-          __syncwarp();
-          while (tail - head >= 32u) {
-            uint32_t ent, sc;
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
-                         : "=r"(ent), "=r"(sc)
-                         : "r"(hit_s + ((head + lane) & (kHitCap - 1)) * 8u));
+            tail += take;
+            done += take;
             __syncwarp();
-            process_hit(a, h, ent >> 8, ent & 0xFFu, (int32_t)sc);
-            head += 32u;
+            while (tail - head >= 32u) {
+              uint16_t ent;
+              asm volatile("ld.shared.u16 %0, [%1];"
+                           : "=h"(ent)
+                           : "r"(hit_s + ((head + lane) & (kHitCap - 1)) * 2u));
+              __syncwarp();
+              process_hit(a, h, (uint32_t)ent >> 8, (uint32_t)ent & 0xFFu);
+              head += 32u;
+            }
           }
         }
         tc_fence_before();
@@ -702,19 +703,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(acc_empty + ab);
         // drain the partial batch (no TMEM needed any more)
         if (tail != head) {
-          uint32_t ent = 0, sc = 0;
+          uint16_t ent = 0;
           const bool mine = (uint32_t)lane < tail - head;
           if (mine)
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
-                         : "=r"(ent), "=r"(sc)
-                         : "r"(hit_s + ((head + lane) & (kHitCap - 1)) * 8u));
+            asm volatile("ld.shared.u16 %0, [%1];"
+                         : "=h"(ent)
+                         : "r"(hit_s + ((head + lane) & (kHitCap - 1)) * 2u));
           __syncwarp();
-          if (mine) process_hit(a, h, ent >> 8, ent & 0xFFu, (int32_t)sc);
+          if (mine) process_hit(a, h, (uint32_t)ent >> 8, (uint32_t)ent & 0xFFu);
         }
         __syncwarp();
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(leaf_empty + st);
+      if (lane == 0) {
+        mbar_arrive(leaf_empty + st);
+        mbar_arrive(items_empty + s);  // the item stage was read by the score recompute
+      }
+      if (++s == a.item_stages) s = 0;
     }
   } else {
     // ================= epilogue: filter (eager) + TMEM scores + gate + emit ========
@@ -881,7 +886,7 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
     t.off_qg = (uint32_t)align_up(off, 16);
     off = t.off_qg + (size_t)kMaxQueries * 4;
     t.off_hit = (uint32_t)align_up(off, 16);
-    off = t.off_hit + (size_t)kEpiWarps * kHitCap * 8;
+    off = t.off_hit + (size_t)kEpiWarps * kHitCap * 2;
   }
   t.off_r = (uint32_t)align_up(off, 16);
   off = t.off_r + (size_t)t.rops_cap * 2;
