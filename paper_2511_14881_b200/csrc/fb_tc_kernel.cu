@@ -546,14 +546,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ph = (uint32_t)(it >> 1) & 1u;
       mbar_wait_idle(planes_full + ps, pph);
       mbar_wait_idle(leaf_empty + st, ph ^ 1u);
-      const uint32_t* P32 = reinterpret_cast<const uint32_t*>(sP + (size_t)ps * a.plane_stage_bytes);
+      const uint32_t p_s = su32(sP + (size_t)ps * a.plane_stage_bytes);
       uint32_t* TB = reinterpret_cast<uint32_t*>(sL + (size_t)st * a.leaf_stage_bytes);
-      for (int blk = lw; blk < a.cnf_words * 8; blk += 2) {
-        const int cb = blk >> 3, ib = blk & 7;  // 32-column block, 32-item block
+      for (int cb = lw; cb < a.cnf_words; cb += 2) {  // 32-column block
         const int col = cb * 32 + lane;
-        uint32_t m = 0u;
+        // the column's 256 tile bits: AND of its planes' 32-byte rows (8 x u32, one per
+        // 32-item block); all loads are independent
+        uint32_t m[8];
+#pragma unroll
+        for (int ib = 0; ib < 8; ++ib) m[ib] = col < a.n_cols ? ~0u : 0u;
         if (col < a.n_cols) {
-          m = ~0u;
           bool neg = false;
           for (int j = 0; j < a.k_max; ++j) {
             int sl = sLS[col * a.k_max + j];
@@ -562,11 +564,33 @@ __global__ void __launch_bounds__(kThreads, 1)
               sl &= ~0x4000;
             }
             if (sl < 0) break;
-            m &= P32[sl * (2 * kTileWords) + ib];
+            const uint4 lo = lds128(p_s + (uint32_t)sl * 32u);
+            const uint4 hi = lds128(p_s + (uint32_t)sl * 32u + 16u);
+            m[0] &= lo.x; m[1] &= lo.y; m[2] &= lo.z; m[3] &= lo.w;
+            m[4] &= hi.x; m[5] &= hi.y; m[6] &= hi.z; m[7] &= hi.w;
           }
-          if (neg) m = ~m;
+          if (neg) {
+#pragma unroll
+            for (int ib = 0; ib < 8; ++ib) m[ib] = ~m[ib];
+          }
         }
-        TB[(ib * 32 + lane) * kTbStride + cb] = transpose32(m, lane);
+        // eight 32x32 transposes in lockstep (independent shuffles per round)
+        const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const int sft = 16 >> k;
+          const uint32_t mk = masks[k];
+          const bool upper = (lane & sft) != 0;
+          uint32_t y[8];
+#pragma unroll
+          for (int ib = 0; ib < 8; ++ib) y[ib] = __shfl_xor_sync(0xffffffffu, m[ib], sft);
+#pragma unroll
+          for (int ib = 0; ib < 8; ++ib)
+            m[ib] = upper ? ((m[ib] & ~mk) | ((y[ib] & ~mk) >> sft))
+                          : ((m[ib] & mk) | ((y[ib] & mk) << sft));
+        }
+#pragma unroll
+        for (int ib = 0; ib < 8; ++ib) TB[(ib * 32 + lane) * kTbStride + cb] = m[ib];
       }
       __syncwarp();
       mbar_arrive(planes_empty + ps);  // 32 arrivals per warp, 64 in total
