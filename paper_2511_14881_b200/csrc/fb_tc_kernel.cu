@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(items_empty + s, kCnf ? 1 + kEpiWarps : 1);
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(planes_full + s, 1);
+      mbar_init(planes_full + s, 32);  // one cp.async.mbarrier.arrive per producer lane
       mbar_init(planes_empty + s, kLeafThreads);
       mbar_init(leaf_full + s, kLeafThreads);
       mbar_init(leaf_empty + s, kEpiWarps);
@@ -496,14 +496,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (a.has_prog && a.n_planes > 0) {
         mbar_wait_idle(planes_empty + ps, pph ^ 1u);
-        if (lane == 0) mbar_expect_tx(planes_full + ps, (uint32_t)a.n_planes * 32u);
-        __syncwarp();
-        uint8_t* dst = sP + (size_t)ps * a.plane_stage_bytes;
-        for (int p = lane; p < a.n_planes; p += 32) {
-          const uint64_t* src = a.planes + (int64_t)a.plane_list[p] * a.n_words +
-                                (int64_t)tile * kTileWords;
-          bulk_load(dst + p * 32, src, 32u, planes_full + ps);
+        // gather the referenced planes' 32-byte rows for this tile: 16-byte cp.async per
+        // lane (two lanes per plane row, a warp covers 16 rows per instruction); each lane
+        // arrives on planes_full once its copies land
+        const uint32_t dst = su32(sP + (size_t)ps * a.plane_stage_bytes);
+        const int64_t col0 = (int64_t)tile * kTileWords;
+        for (int e = lane; e < 2 * a.n_planes; e += 32) {
+          const int p = e >> 1;
+          const uint64_t* src = a.planes + (int64_t)a.plane_list[p] * a.n_words + col0 + 2 * (e & 1);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + (uint32_t)e * 16u),
+                       "l"(src)
+                       : "memory");
         }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                         su32(planes_full + ps))
+                     : "memory");
         if (++ps == PS) { ps = 0; pph ^= 1u; }
       }
       if (++s == S) { s = 0; ph ^= 1u; }
