@@ -129,7 +129,7 @@ __device__ __forceinline__ void mbar_wait_idle(uint64_t* b, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
     if (ok) break;
-    __nanosleep(32);
+    __nanosleep(128);
   }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0,
@@ -306,15 +306,26 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 
 struct HitCtx {
   int64_t tile;
-  uint64_t vw[kTileWords];  // validity & range words of the tile
-  uint32_t tb_s;            // shared address of this tile's transposed column bits
-  uint32_t qm_s;            // shared address of the query group masks
-  uint32_t a_s;             // shared address of the query tile (SW128 rows)
-  uint32_t b_s;             // shared address of this tile's item stage (SW128 rows)
-  const int32_t* qg;        // shared: groups per query
-  const uint64_t* sT;
+  uint64_t vw0, vw1, vw2, vw3;  // validity & range words of the tile
+  uint32_t tb_s;                // shared address of this tile's transposed column bits
+  uint32_t qm_s;                // shared address of the query group masks
+  uint32_t a_s;                 // shared address of the query tile (SW128 rows)
+  uint32_t b_s;                 // shared address of this tile's item stage (SW128 rows)
+  uint32_t qg_s;                // shared address of the groups-per-query table
+  uint32_t t_s;                 // shared address of the per-query thresholds
   int mb;
 };
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds64(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+  return v;
+}
 
 // Exact int32 dot of a query row (A tile) and an item row (B stage) from shared memory.
 // Both tiles use the SWIZZLE_128B layout: 16-byte chunk c of row r sits at c ^ (r & 7).
@@ -339,16 +350,16 @@ __device__ __forceinline__ void process_hit(const TcArgs& a, const HitCtx& h, ui
                                             uint32_t item) {
   const int q = h.mb * kBlockM + (int)row;
   const int word = (int)(item >> 6);
-  uint64_t vw = h.vw[0];
-  vw = word == 1 ? h.vw[1] : vw;
-  vw = word == 2 ? h.vw[2] : vw;
-  vw = word == 3 ? h.vw[3] : vw;
+  uint64_t vw = h.vw0;
+  vw = word == 1 ? h.vw1 : vw;
+  vw = word == 2 ? h.vw2 : vw;
+  vw = word == 3 ? h.vw3 : vw;
   bool pass = (vw >> (item & 63)) & 1ull;
   if (pass && a.masks != nullptr)
     pass = (__ldg(a.masks + (int64_t)q * a.n_words + h.tile * kTileWords + word) >> (item & 63)) &
            1ull;
   if (pass) {
-    const int ng = h.qg[q];
+    const int ng = (int)lds32(h.qg_s + 4u * (uint32_t)q);
     if (ng > 0) {
       const uint4 t0 = lds128(h.tb_s + item * (kTbStride * 4u));
       const uint4 t1 = a.qm_stride == 8 ? lds128(h.tb_s + item * (kTbStride * 4u) + 16u)
@@ -367,7 +378,7 @@ __device__ __forceinline__ void process_hit(const TcArgs& a, const HitCtx& h, ui
     }
   }
   if (pass) {
-    const uint64_t T = h.sT[q];
+    const uint64_t T = lds64(h.t_s + 8u * (uint32_t)q);
     const int32_t score = smem_dot(h.a_s + (uint32_t)q * kKBytes, (uint32_t)q & 7u,
                                    h.b_s + item * kKBytes, item & 7u);
     const int64_t slot = h.tile * kTileItems + item;
@@ -644,23 +655,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     HitCtx h;
     h.qm_s = su32(smem + a.off_qm);
     h.a_s = su32(sA);
-    h.qg = reinterpret_cast<const int32_t*>(smem + a.off_qg);
-    h.sT = sT;
+    h.qg_s = su32(smem + a.off_qg);
+    h.t_s = su32(sT);
     int it = 0, acc_it = 0, s = 0;
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
       const int2 wk = a.work[i * a.work_stride];
       const int64_t s0 = a.ranges[2 * wk.y], s1 = a.ranges[2 * wk.y + 1];
       h.tile = wk.x;
-#pragma unroll
-      for (int w = 0; w < kTileWords; ++w) {
-        const int64_t gw = h.tile * kTileWords + w;
-        h.vw[w] = __ldg(a.valid + gw) & word_range_mask(gw * 64, s0, s1);
+      {
+        const int64_t gw = h.tile * kTileWords;
+        h.vw0 = __ldg(a.valid + gw) & word_range_mask(gw * 64, s0, s1);
+        h.vw1 = __ldg(a.valid + gw + 1) & word_range_mask((gw + 1) * 64, s0, s1);
+        h.vw2 = __ldg(a.valid + gw + 2) & word_range_mask((gw + 2) * 64, s0, s1);
+        h.vw3 = __ldg(a.valid + gw + 3) & word_range_mask((gw + 3) * 64, s0, s1);
       }
       h.b_s = su32(sB + (size_t)s * kItemBytes);
       const int st = it & 1;
       mbar_wait(leaf_full + st, (uint32_t)(it >> 1) & 1u);
       h.tb_s = su32(sL + (size_t)st * a.leaf_stage_bytes);
-      const bool any_valid = (h.vw[2 * half] | h.vw[2 * half + 1]) != 0ull;
+      const bool any_valid = (half == 0 ? (h.vw0 | h.vw1) : (h.vw2 | h.vw3)) != 0ull;
 #pragma unroll 1
       for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
         h.mb = mb;
