@@ -60,7 +60,7 @@ def parse_args():
 
 def workload_desc(a, n_gpus):
     return {
-        "workload": (f"config2: {a.items // 1_000_000}M items/GPU x {a.dim}-d int8, batch "
+        "workload": (f"config2: {a.items / 1e6:g}M items/GPU x {a.dim}-d int8, batch "
                      f"{a.batch}, top-k {a.k}, 4-attribute Bloom filter (M=1024, K=5)"),
         "items_total": a.items * n_gpus, "items_per_gpu": a.items, "batch": a.batch,
         "k": a.k, "dim": a.dim, "bloom_m": 1024, "bloom_k": 5,
@@ -357,7 +357,7 @@ def run_ours(a):
                                        cores)
         cpu = {"value": round(qps, 3), "unit": UNIT, "cores": cores, "kind": "port",
                "sample": (f"{n} queries (oracle codesigned_search over the full "
-                          f"{a.items // 1_000_000}M-item index, k={k}) in {secs:.1f} s on "
+                          f"{a.items / 1e6:g}M-item index, k={k}) in {secs:.1f} s on "
                           f"{cores} forked workers")}
 
     if rank == 0:
