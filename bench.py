@@ -124,13 +124,14 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
-        self.lines = []
+        self.lines = []          # (host time, csv line)
+        self.window = None       # (t0, t1) of the timed region
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -140,7 +141,15 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def wait_ready(self, timeout=5.0):
+        t = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t < timeout:
+            time.sleep(0.01)
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -153,7 +162,12 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in self.lines:
+        lines = self.lines
+        if self.window is not None:
+            t0, t1 = self.window
+            inside = [x for x in lines if t0 <= x[0] <= t1 + 0.02]
+            lines = inside if inside else sorted(lines, key=lambda x: abs(x[0] - t1))[:3]
+        for _, line in lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 8:
                 continue
@@ -251,11 +265,14 @@ def run_ours(a):
     torch.cuda.synchronize()
     launches0 = lib.fb_launch_count()
     with ClockSampler(local) as clocks:
+        clocks.wait_ready()
+        t_host0 = time.perf_counter()
         ev[0].record(stream)
         for i in range(a.steps):
             step(wl.queries, batch)
             ev[i + 1].record(stream)
         torch.cuda.synchronize()
+        clocks.mark(t_host0, time.perf_counter())
     launches = int(lib.fb_launch_count() - launches0)
     per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(a.steps)]
     total_ms = ev[0].elapsed_time(ev[a.steps])

@@ -420,6 +420,7 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
       sa.out_cnt = p->d_sample_cnt;
       sa.out_elig = p->d_sample_elig;
       sa.cap = p->sample_cap;
+      sa.dense = 1;
       rc = emit(sa);
       if (rc) return rc;
     }

@@ -129,6 +129,7 @@ struct ScanArgs {
   // strides over this list
   const void* tc_work;        // int2 [n_tc_work]
   int64_t n_tc_work;
+  int32_t dense;              // threshold 0 everywhere (sampling): word-level filter is cheaper
   int32_t* dump;              // testing: raw scores [B, dump_ld] (nullable)
   int64_t dump_ld;
 };

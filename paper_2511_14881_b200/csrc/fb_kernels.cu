@@ -317,11 +317,58 @@ __global__ void __launch_bounds__(kSelectThreads) k_threshold(ThresholdArgs a) {
     if (threadIdx.x == 0) a.threshold[q] = 0ull;
     return;
   }
-  const int n = pow2_ceil(nk);
-  for (int i = threadIdx.x; i < n; i += blockDim.x)
-    s_key[i] = i < nk ? a.sample_key[(int64_t)q * a.sample_cap + i] : 0ull;
-  bitonic_desc<false>(s_key, nullptr, n);
-  if (threadIdx.x == 0) a.threshold[q] = s_key[(int)jd];
+  for (int i = threadIdx.x; i < nk; i += blockDim.x)
+    s_key[i] = a.sample_key[(int64_t)q * a.sample_cap + i];
+  // radix select (8-bit digits, most significant first) of the key with exactly `jd`
+  // larger keys: one histogram pass over the kept sample per digit
+  __shared__ uint32_t hist[256];
+  __shared__ uint64_t s_prefix;
+  __shared__ uint32_t s_need;
+  if (threadIdx.x == 0) {
+    s_prefix = 0ull;
+    s_need = (uint32_t)jd + 1u;
+  }
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0u;
+    __syncthreads();
+    const uint64_t prefix = s_prefix;
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+      const uint64_t k = s_key[i];
+      if (shift == 56 || ((k ^ prefix) >> (shift + 8)) == 0ull)
+        atomicAdd(hist + ((k >> shift) & 0xFFu), 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // one warp: find the digit holding rank `need` (from the top)
+      const uint32_t need = s_need;
+      // lane l owns bins [255 - 8l, 255 - 8l - 7]
+      uint32_t c[8], sum = 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[255 - 8 * threadIdx.x - j];
+        sum += c[j];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if ((int)threadIdx.x >= d) incl += y;
+      }
+      const uint32_t excl = incl - sum;
+      if (excl < need && need <= incl) {
+        uint32_t cum = excl;
+        for (int j = 0; j < 8; ++j) {
+          if (cum + c[j] >= need) {
+            s_prefix = prefix | ((uint64_t)(255 - 8 * threadIdx.x - j) << shift);
+            s_need = need - cum;
+            break;
+          }
+          cum += c[j];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.threshold[q] = s_prefix;
 }
 
 // Flag queries whose emit pass over- or under-flowed (or all, when forced).

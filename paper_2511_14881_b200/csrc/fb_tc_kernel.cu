@@ -965,6 +965,9 @@ bool pick_stages(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, i
 }
 
 bool use_cnf(const ScanArgs& a) {
+  // at threshold 0 every score is a hit: the word-level bytecode epilogue is cheaper than
+  // per-hit tests, so the sampling pass takes it whenever the bytecode fits the kernel
+  if (a.dense && a.prog.rops != nullptr && a.prog.rmax_stack <= kRegStack) return false;
   return a.has_prog && a.prog.col_leaf != nullptr && a.prog.cnf_words >= 1 &&
          a.prog.cnf_words <= 8 && a.prog.cnf_gmax >= 1 && a.prog.cnf_gmax <= 8 &&
          a.prog.n_cols <= 32 * a.prog.cnf_words;
