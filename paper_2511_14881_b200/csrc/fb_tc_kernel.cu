@@ -103,35 +103,23 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: the warp is parked by the hardware until the phase
+// completes (or the hint expires) instead of spinning through issue slots that the
+// epilogue warps on the same scheduler need.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   const uint32_t a = su32(b);
   uint32_t ok = 0;
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(0x989680)
         : "memory");
   } while (!ok);
 }
-// for roles off the critical path: back off so spinning does not steal issue slots
-__device__ __forceinline__ void mbar_wait_idle(uint64_t* b, uint32_t parity) {
-  const uint32_t a = su32(b);
-  uint32_t ok = 0;
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (ok) break;
-    __nanosleep(128);
-  }
-}
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* b, uint32_t parity) { mbar_wait(b, parity); }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0,
                                             int32_t c1, uint64_t* bar) {
   asm volatile(
@@ -181,6 +169,46 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&r)[32]) {
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// Asynchronous variant: issue the load now, tmem_wait32() before the first use. The wait
+// names the destination registers so the compiler cannot read them ahead of it.
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, int32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait32(int32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
+                 "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]),
+                 "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+                 "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),
+                 "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
+// Bit j of the result = (r[j] >= tau), for |r| < 2^22 and tau clamped to [-2^23, 2^23]:
+// the sign of (tau - 1 - r[j]) is shifted in with a funnel shift (2 instructions per
+// score), in four independent 8-bit chains.
+__device__ __forceinline__ uint32_t hit_mask32(const int32_t (&r)[32], int32_t tau) {
+  const int32_t ntau = -tau;  // sign of r + ntau marks a miss
+  uint32_t m[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int j = 7; j >= 0; --j) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) m[p] = __funnelshift_l((uint32_t)(r[8 * p + j] + ntau), m[p], 1);
+  }
+  return ~(m[0] | (m[1] << 8) | (m[2] << 16) | (m[3] << 24));
 }
 
 // K-major, SWIZZLE_128B shared-memory matrix descriptor (8-row groups 1024 B apart).
@@ -304,17 +332,30 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
   return x;
 }
 
+// Per-warp state of the CNF epilogue for the current tile. Hits and survivors are queued
+// as 16-bit entries: (m-block << 14) | (row << 7) | item-within-half.
 struct HitCtx {
   int64_t tile;
-  uint64_t vw0, vw1, vw2, vw3;  // validity & range words of the tile
-  uint32_t tb_s;                // shared address of this tile's transposed column bits
-  uint32_t qm_s;                // shared address of the query group masks
-  uint32_t a_s;                 // shared address of the query tile (SW128 rows)
-  uint32_t b_s;                 // shared address of this tile's item stage (SW128 rows)
-  uint32_t qg_s;                // shared address of the groups-per-query table
-  uint32_t t_s;                 // shared address of the per-query thresholds
-  int mb;
+  uint32_t tb_s;   // shared address of this tile's transposed column bits
+  uint32_t qm_s;   // shared address of the query group masks
+  uint32_t a_s;    // shared address of the query tile (SW128 rows)
+  uint32_t b_s;    // shared address of this tile's item stage (SW128 rows)
+  uint32_t qg_s;   // shared address of the groups-per-query table
+  uint32_t t_s;    // shared address of the per-query thresholds
+  uint32_t hit_s;  // this warp's hit ring
+  uint32_t sv_s;   // this warp's survivor ring
+  uint32_t half;   // item columns [half * 128, half * 128 + 128)
+  uint32_t idr0, idr1, idr2, idr3;  // id ranks of items half*128 + 4*lane + {0..3}
 };
+// An emission whose slot reservation (atomicAdd) is in flight; stored one batch later so
+// the global round trip overlaps the next tile's work.
+struct PendingEmit {
+  uint64_t key;
+  uint32_t p;
+  uint32_t slot;
+  int32_t q;
+};
+constexpr int kSurvCap = 64;  // per-warp ring of filter survivors (exact key test pending)
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
@@ -344,52 +385,109 @@ __device__ __forceinline__ int32_t smem_dot(uint32_t a_row, uint32_t a_sw, uint3
   return acc;
 }
 
-// Eligibility (validity & range & mask & CNF filter) of one hit -- a (query row, tile
-// item) whose score cleared the threshold gate -- then the exact key test and emission.
-__device__ __forceinline__ void process_hit(const TcArgs& a, const HitCtx& h, uint32_t row,
-                                            uint32_t item) {
-  const int q = h.mb * kBlockM + (int)row;
-  const int word = (int)(item >> 6);
-  uint64_t vw = h.vw0;
-  vw = word == 1 ? h.vw1 : vw;
-  vw = word == 2 ? h.vw2 : vw;
-  vw = word == 3 ? h.vw3 : vw;
-  bool pass = (vw >> (item & 63)) & 1ull;
-  if (pass && a.masks != nullptr)
-    pass = (__ldg(a.masks + (int64_t)q * a.n_words + h.tile * kTileWords + word) >> (item & 63)) &
-           1ull;
-  if (pass) {
-    const int ng = (int)lds32(h.qg_s + 4u * (uint32_t)q);
+__device__ __forceinline__ uint32_t lds16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ void flush_pending(const TcArgs& a, PendingEmit& pd) {
+  if (pd.q >= 0 && pd.p < (uint32_t)a.cap) {
+    a.out_key[(int64_t)pd.q * a.cap + pd.p] = pd.key;
+    if (a.out_slot) a.out_slot[(int64_t)pd.q * a.cap + pd.p] = pd.slot;
+  }
+  pd.q = -1;
+}
+
+// Up to 32 filter survivors from the head of the survivor ring: exact score recomputed
+// from the resident query / item tiles, exact key test, slot reservation. The previous
+// batch's stores are completed first (their reservations have long returned).
+__device__ __forceinline__ void emit_survivors(const TcArgs& a, const HitCtx& h,
+                                               uint32_t& sv_head, uint32_t sv_tail,
+                                               PendingEmit& pd, int lane) {
+  const uint32_t n = min(32u, sv_tail - sv_head);
+  const bool mine = (uint32_t)lane < n;
+  uint32_t ent = 0;
+  if (mine) ent = lds16(h.sv_s + ((sv_head + (uint32_t)lane) & (kSurvCap - 1)) * 2u);
+  const uint32_t il = ent & 127u;
+  const uint32_t src = il >> 2;
+  const uint32_t x = __shfl_sync(0xffffffffu, h.idr0, src);
+  const uint32_t y = __shfl_sync(0xffffffffu, h.idr1, src);
+  const uint32_t z = __shfl_sync(0xffffffffu, h.idr2, src);
+  const uint32_t w = __shfl_sync(0xffffffffu, h.idr3, src);
+  __syncwarp();
+  sv_head += n;
+  flush_pending(a, pd);
+  if (mine) {
+    const uint32_t q = ((ent >> 14) << 7) | ((ent >> 7) & 127u);
+    const uint32_t item = h.half * 128u + il;
+    const uint32_t sel = il & 3u;
+    const uint32_t idr = sel == 0 ? x : (sel == 1 ? y : (sel == 2 ? z : w));
+    const uint64_t T = lds64(h.t_s + 8u * q);
+    const int32_t score =
+        smem_dot(h.a_s + q * kKBytes, q & 7u, h.b_s + item * kKBytes, item & 7u);
+    const uint64_t key = make_key(score, idr);
+    if (key >= T) {
+      pd.p = atomicAdd(a.out_cnt + q, 1u);
+      pd.key = key;
+      pd.slot = (uint32_t)(h.tile * kTileItems + item);
+      pd.q = (int32_t)q;
+    }
+  }
+}
+
+// n (<= 32) hits from the head of the hit ring -- (query, item) pairs whose score cleared
+// the threshold gate and whose item is valid, in range and in the query's mask -- get the
+// CNF filter test (item column bits & the query's group masks); survivors are queued.
+__device__ __forceinline__ void filter_hits(const TcArgs& a, const HitCtx& h, uint32_t& head,
+                                            uint32_t n, uint32_t& sv_head, uint32_t& sv_tail,
+                                            PendingEmit& pd, int lane) {
+  const bool mine = (uint32_t)lane < n;
+  uint32_t ent = 0;
+  if (mine) ent = lds16(h.hit_s + ((head + (uint32_t)lane) & (kHitCap - 1)) * 2u);
+  __syncwarp();
+  head += n;
+  bool pass = mine;
+  if (mine) {
+    const uint32_t q = ((ent >> 14) << 7) | ((ent >> 7) & 127u);
+    const uint32_t item = h.half * 128u + (ent & 127u);
+    const int ng = (int)lds32(h.qg_s + 4u * q);
     if (ng > 0) {
-      const uint4 t0 = lds128(h.tb_s + item * (kTbStride * 4u));
-      const uint4 t1 = a.qm_stride == 8 ? lds128(h.tb_s + item * (kTbStride * 4u) + 16u)
-                                        : make_uint4(0u, 0u, 0u, 0u);
-      uint32_t qaddr = h.qm_s + (uint32_t)(q * a.cnf_gmax * a.qm_stride) * 4u;
-      for (int g = 0; g < ng && pass; ++g) {
-        const uint4 m0 = lds128(qaddr);
-        uint32_t any = (t0.x & m0.x) | (t0.y & m0.y) | (t0.z & m0.z) | (t0.w & m0.w);
-        if (a.qm_stride == 8) {
-          const uint4 m1 = lds128(qaddr + 16u);
-          any |= (t1.x & m1.x) | (t1.y & m1.y) | (t1.z & m1.z) | (t1.w & m1.w);
+      const uint32_t tb = h.tb_s + item * (kTbStride * 4u);
+      const uint4 t0 = lds128(tb);
+      uint32_t qaddr = h.qm_s + q * (uint32_t)(a.cnf_gmax * a.qm_stride) * 4u;
+      if (a.qm_stride == 4) {
+        for (int g = 0; g < ng && pass; ++g) {
+          const uint4 m0 = lds128(qaddr);
+          pass = ((t0.x & m0.x) | (t0.y & m0.y) | (t0.z & m0.z) | (t0.w & m0.w)) != 0u;
+          qaddr += 16u;
         }
-        pass = any != 0u;
-        qaddr += (uint32_t)a.qm_stride * 4u;
+      } else {
+        const uint4 t1 = lds128(tb + 16u);
+        for (int g = 0; g < ng && pass; ++g) {
+          const uint4 m0 = lds128(qaddr);
+          const uint4 m1 = lds128(qaddr + 16u);
+          pass = ((t0.x & m0.x) | (t0.y & m0.y) | (t0.z & m0.z) | (t0.w & m0.w) |
+                  (t1.x & m1.x) | (t1.y & m1.y) | (t1.z & m1.z) | (t1.w & m1.w)) != 0u;
+          qaddr += 32u;
+        }
       }
     }
   }
-  if (pass) {
-    const uint64_t T = lds64(h.t_s + 8u * (uint32_t)q);
-    const int32_t score = smem_dot(h.a_s + (uint32_t)q * kKBytes, (uint32_t)q & 7u,
-                                   h.b_s + item * kKBytes, item & 7u);
-    const int64_t slot = h.tile * kTileItems + item;
-    const uint64_t key = make_key(score, __ldg(a.id_rank + slot));
-    if (key >= T) {
-      const uint32_t p = atomicAdd(a.out_cnt + q, 1u);
-      if (p < (uint32_t)a.cap) {
-        a.out_key[(int64_t)q * a.cap + p] = key;
-        if (a.out_slot) a.out_slot[(int64_t)q * a.cap + p] = (uint32_t)slot;
-      }
-    }
+  const uint32_t b = __ballot_sync(0xffffffffu, pass);
+  if (pass) sts16(h.sv_s + ((sv_tail + __popc(b & lanemask_lt())) & (kSurvCap - 1)) * 2u, ent);
+  sv_tail += (uint32_t)__popc(b);
+  if (sv_tail - sv_head >= 32u) {
+    __syncwarp();
+    emit_survivors(a, h, sv_head, sv_tail, pd, lane);
   }
 }
 
@@ -651,112 +749,112 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;
     const int half = ew >> 2;
     const int row = quad * 32 + lane;
-    const uint32_t hit_s = su32(smem + a.off_hit) + (uint32_t)ew * (kHitCap * 2u);
     HitCtx h;
     h.qm_s = su32(smem + a.off_qm);
     h.a_s = su32(sA);
     h.qg_s = su32(smem + a.off_qg);
     h.t_s = su32(sT);
+    h.hit_s = su32(smem + a.off_hit) + (uint32_t)ew * (kHitCap * 2u);
+    h.sv_s = su32(smem + a.off_hit) + (uint32_t)(kEpiWarps * kHitCap * 2) +
+             (uint32_t)ew * (kSurvCap * 2u);
+    h.half = (uint32_t)half;
+    // per query row of this thread: clamped score gate (|score| < 2^22 at dim 128)
+    int32_t tau[kMaxMBlocks];
+#pragma unroll
+    for (int mb = 0; mb < kMaxMBlocks; ++mb) {
+      const int q = mb * kBlockM + row;
+      const uint64_t T = q < a.nq ? sT[q] : ~0ull;
+      int32_t t = T == 0ull ? -(1 << 23) : key_score(T);
+      tau[mb] = min(max(t, -(1 << 23)), 1 << 23);
+    }
+    PendingEmit pd;
+    pd.q = -1;
+    pd.p = 0;
+    pd.key = 0;
+    pd.slot = 0;
     int it = 0, acc_it = 0, s = 0;
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
       const int2 wk = a.work[i * a.work_stride];
       const int64_t s0 = a.ranges[2 * wk.y], s1 = a.ranges[2 * wk.y + 1];
       h.tile = wk.x;
+      // this half's two validity & range words (warp-uniform) and the id ranks of its
+      // 128 items (4 per lane; consumed by the survivors at the end of the tile)
+      const int64_t wbase = h.tile * kTileWords + 2 * half;
+      const uint64_t v0 = __ldg(a.valid + wbase) & word_range_mask(wbase * 64, s0, s1);
+      const uint64_t v1 = __ldg(a.valid + wbase + 1) & word_range_mask((wbase + 1) * 64, s0, s1);
       {
-        const int64_t gw = h.tile * kTileWords;
-        h.vw0 = __ldg(a.valid + gw) & word_range_mask(gw * 64, s0, s1);
-        h.vw1 = __ldg(a.valid + gw + 1) & word_range_mask((gw + 1) * 64, s0, s1);
-        h.vw2 = __ldg(a.valid + gw + 2) & word_range_mask((gw + 2) * 64, s0, s1);
-        h.vw3 = __ldg(a.valid + gw + 3) & word_range_mask((gw + 3) * 64, s0, s1);
+        const uint4 ir = __ldg(reinterpret_cast<const uint4*>(a.id_rank + h.tile * kTileItems +
+                                                              half * 128) + lane);
+        h.idr0 = ir.x;
+        h.idr1 = ir.y;
+        h.idr2 = ir.z;
+        h.idr3 = ir.w;
       }
       h.b_s = su32(sB + (size_t)s * kItemBytes);
       const int st = it & 1;
       mbar_wait(leaf_full + st, (uint32_t)(it >> 1) & 1u);
       h.tb_s = su32(sL + (size_t)st * a.leaf_stage_bytes);
-      const bool any_valid = (half == 0 ? (h.vw0 | h.vw1) : (h.vw2 | h.vw3)) != 0ull;
+      uint32_t head = 0, tail = 0, sv_head = 0, sv_tail = 0;  // warp-uniform ring cursors
 #pragma unroll 1
       for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
-        h.mb = mb;
         const int q = mb * kBlockM + row;
-        const bool active = q < a.nq && any_valid;
-        const uint64_t T = q < a.nq ? sT[q] : ~0ull;
-        const int32_t tau = T == 0ull ? INT32_MIN : key_score(T);
+        uint64_t e0 = q < a.nq ? v0 : 0ull, e1 = q < a.nq ? v1 : 0ull;
+        if (a.masks != nullptr && (e0 | e1) != 0ull) {
+          e0 &= __ldg(a.masks + (int64_t)q * a.n_words + wbase);
+          e1 &= __ldg(a.masks + (int64_t)q * a.n_words + wbase + 1);
+        }
+        const int32_t tq = mb == 0 ? tau[0] : tau[kMaxMBlocks - 1];
         const int ab = acc_it & 1;
         mbar_wait(acc_full + ab, (uint32_t)(acc_it >> 1) & 1u);
         tc_fence_after();
         const uint32_t taddr =
             tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kAccCols + half * 128);
-        uint32_t head = 0, tail = 0;  // warp-uniform ring-buffer cursors
+        const uint32_t ebase = ((uint32_t)mb << 14) | ((uint32_t)row << 7);
+        int32_t r[32];
+        tmem_ld32_async(taddr, r);
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
-          int32_t r[32];
-          tmem_ld32(taddr + c * 32, r);
+          tmem_wait32(r);
           if (a.dump != nullptr && q < a.nq) {
             const int64_t base = h.tile * kTileItems + half * 128 + c * 32;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (base + j < a.dump_ld) a.dump[(int64_t)q * a.dump_ld + base + j] = r[j];
           }
-          uint32_t hm = 0u;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) hm |= (r[j] >= tau ? 1u : 0u) << j;
-          if (!active) hm = 0u;
-          const uint32_t item0 = (uint32_t)(half * 128 + c * 32);
-          const uint32_t n = __popc(hm);
-          uint32_t pre = n;  // inclusive prefix of n across the warp
-#pragma unroll
-          for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, pre, d);
-            if (lane >= d) pre += y;
-          }
-          const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
-          if (total == 0u) continue;
-          pre -= n;
-          uint32_t rank = pre;  // global rank of this lane's next unwritten hit
-          uint32_t rem = hm;
-          uint32_t done = 0u;
-          // append in rounds so the ring never overflows (dense regime: threshold 0)
-          while (done < total) {
-            const uint32_t room = (uint32_t)kHitCap - (tail - head);
-            const uint32_t take = total - done < room ? total - done : room;
-            while (rem != 0u && rank < done + take) {
-              const uint32_t j = (uint32_t)(__ffs(rem) - 1);
-              rem &= rem - 1u;
-              asm volatile("st.shared.u16 [%0], %1;" ::"r"(
-                               hit_s + ((tail + rank - done) & (kHitCap - 1)) * 2u),
-                           "h"((unsigned short)(((uint32_t)row << 8) | (item0 + j)))
-                           : "memory");
-              ++rank;
-            }
-            tail += take;
-            done += take;
+          uint32_t hm = hit_mask32(r, tq) & (uint32_t)((c < 2 ? e0 : e1) >> (32 * (c & 1)));
+          if (c < 3) {
+            tmem_ld32_async(taddr + (c + 1) * 32, r);  // overlaps the hit handling below
+          } else {
+            tc_fence_before();
             __syncwarp();
-            while (tail - head >= 32u) {
-              uint16_t ent;
-              asm volatile("ld.shared.u16 %0, [%1];"
-                           : "=h"(ent)
-                           : "r"(hit_s + ((head + lane) & (kHitCap - 1)) * 2u));
+            if (lane == 0) mbar_arrive(acc_empty + ab);
+          }
+          // append this chunk's hits to the warp's ring, one per lane per round
+          const uint32_t eb = ebase | (uint32_t)(c * 32);
+          while (true) {
+            const uint32_t b = __ballot_sync(0xffffffffu, hm != 0u);
+            if (b == 0u) break;
+            if (hm != 0u) {
+              const uint32_t j = (uint32_t)(__ffs(hm) - 1);
+              hm &= hm - 1u;
+              sts16(h.hit_s + ((tail + __popc(b & lanemask_lt())) & (kHitCap - 1)) * 2u, eb + j);
+            }
+            tail += (uint32_t)__popc(b);
+            if (tail - head >= 32u) {
               __syncwarp();
-              process_hit(a, h, (uint32_t)ent >> 8, (uint32_t)ent & 0xFFu);
-              head += 32u;
+              filter_hits(a, h, head, 32u, sv_head, sv_tail, pd, lane);
             }
           }
         }
-        tc_fence_before();
+      }
+      // drain: remaining hits, then the survivors (they read the item stage)
+      if (tail != head) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(acc_empty + ab);
-        // drain the partial batch (no TMEM needed any more)
-        if (tail != head) {
-          uint16_t ent = 0;
-          const bool mine = (uint32_t)lane < tail - head;
-          if (mine)
-            asm volatile("ld.shared.u16 %0, [%1];"
-                         : "=h"(ent)
-                         : "r"(hit_s + ((head + lane) & (kHitCap - 1)) * 2u));
-          __syncwarp();
-          if (mine) process_hit(a, h, (uint32_t)ent >> 8, (uint32_t)ent & 0xFFu);
-        }
+        filter_hits(a, h, head, tail - head, sv_head, sv_tail, pd, lane);
+      }
+      while (sv_tail != sv_head) {
         __syncwarp();
+        emit_survivors(a, h, sv_head, sv_tail, pd, lane);
       }
       __syncwarp();
       if (lane == 0) {
@@ -765,6 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (++s == a.item_stages) s = 0;
     }
+    flush_pending(a, pd);
   } else {
     // ================= epilogue: filter (eager) + TMEM scores + gate + emit ========
     const int ew = warp - kEpiWarp0;
@@ -842,7 +941,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) cm |= (r[j] >= tau ? 1u : 0u) << j;
               cm &= fw;
-              if (cm != 0u) {
+              if (cm != 0u && T == 0ull) {
+                // threshold 0 (sampling pass): every eligible item is emitted, so one slot
+                // reservation covers the chunk and the stores need no per-item round trip
+                const int64_t slot0 = tile * kTileItems + half * 128 + c * 32;
+                uint32_t p = atomicAdd(a.out_cnt + q, (uint32_t)__popc(cm));
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  if ((cm >> j) & 1u) {
+                    if (p < (uint32_t)a.cap) {
+                      a.out_key[(int64_t)q * a.cap + p] =
+                          make_key(r[j], __ldg(a.id_rank + slot0 + j));
+                      if (a.out_slot) a.out_slot[(int64_t)q * a.cap + p] = (uint32_t)(slot0 + j);
+                    }
+                    ++p;
+                  }
+                }
+              } else if (cm != 0u) {
                 const int64_t slot0 = tile * kTileItems + half * 128 + c * 32;
                 int32_t rs[32];  // dynamic indexing below: lives in local memory (rare path)
 #pragma unroll
@@ -930,7 +1045,7 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
     t.off_qg = (uint32_t)align_up(off, 16);
     off = t.off_qg + (size_t)kMaxQueries * 4;
     t.off_hit = (uint32_t)align_up(off, 16);
-    off = t.off_hit + (size_t)kEpiWarps * kHitCap * 2;
+    off = t.off_hit + (size_t)kEpiWarps * (kHitCap + kSurvCap) * 2;
   }
   t.off_r = (uint32_t)align_up(off, 16);
   off = t.off_r + (size_t)t.rops_cap * 2;
