@@ -38,6 +38,9 @@ constexpr int kThreads = 384;
 constexpr int kLeafThreads = 64;
 constexpr int kEpiWarp0 = 4;   // warps 4-11: epilogue (thread = query x 128 items)
 constexpr int kEpiWarps = 8;
+// CNF mode: 16 warps, 12 of them epilogue (3 per TMEM lane quadrant, chunks interleaved)
+constexpr int kThreadsCnf = 512;
+constexpr int kEpiWarpsCnf = 12;
 constexpr int kLeafStride = 6;  // u64 per leaf in the per-tile leaf-mask stage (48 B: 4 words +
                                 // pad, so 32 lanes' 16-B loads spread over 8 bank groups)
 constexpr int kRegStack = 4;
@@ -83,11 +86,11 @@ struct TcArgs {
   const uint32_t* qmask;
   const int32_t* qgroups;
   uint32_t off_a, off_b, off_p, off_l, off_ls, off_thr, off_r, off_bar, plane_stage_bytes,
-      leaf_stage_bytes, off_qm, off_qg, off_hit;
+      leaf_stage_bytes, off_qm, off_qg, off_hit, off_id;
 };
 
 constexpr int kTbStride = 8;     // u32 per item row of the transposed column bits (<= 256 cols)
-constexpr int kHitCap = 64;      // per-warp ring buffer of hits (score >= threshold)
+constexpr int kHitCap = 128;     // per-warp ring buffer of hits (score >= threshold)
 
 // ---- PTX helpers ----------------------------------------------------------------------
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -333,19 +336,18 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 }
 
 // Per-warp state of the CNF epilogue for the current tile. Hits and survivors are queued
-// as 16-bit entries: (m-block << 14) | (row << 7) | item-within-half.
+// as 16-bit entries: (m-block << 15) | (row << 8) | item, so entry >> 8 is the query.
 struct HitCtx {
   int64_t tile;
   uint32_t tb_s;   // shared address of this tile's transposed column bits
   uint32_t qm_s;   // shared address of the query group masks
   uint32_t a_s;    // shared address of the query tile (SW128 rows)
   uint32_t b_s;    // shared address of this tile's item stage (SW128 rows)
+  uint32_t id_s;   // shared address of this tile's id ranks (same stage index)
   uint32_t qg_s;   // shared address of the groups-per-query table
   uint32_t t_s;    // shared address of the per-query thresholds
   uint32_t hit_s;  // this warp's hit ring
   uint32_t sv_s;   // this warp's survivor ring
-  uint32_t half;   // item columns [half * 128, half * 128 + 128)
-  uint32_t idr0, idr1, idr2, idr3;  // id ranks of items half*128 + 4*lane + {0..3}
 };
 // An emission whose slot reservation (atomicAdd) is in flight; stored one batch later so
 // the global round trip overlaps the next tile's work.
@@ -417,24 +419,16 @@ __device__ __forceinline__ void emit_survivors(const TcArgs& a, const HitCtx& h,
   const bool mine = (uint32_t)lane < n;
   uint32_t ent = 0;
   if (mine) ent = lds16(h.sv_s + ((sv_head + (uint32_t)lane) & (kSurvCap - 1)) * 2u);
-  const uint32_t il = ent & 127u;
-  const uint32_t src = il >> 2;
-  const uint32_t x = __shfl_sync(0xffffffffu, h.idr0, src);
-  const uint32_t y = __shfl_sync(0xffffffffu, h.idr1, src);
-  const uint32_t z = __shfl_sync(0xffffffffu, h.idr2, src);
-  const uint32_t w = __shfl_sync(0xffffffffu, h.idr3, src);
   __syncwarp();
   sv_head += n;
   flush_pending(a, pd);
   if (mine) {
-    const uint32_t q = ((ent >> 14) << 7) | ((ent >> 7) & 127u);
-    const uint32_t item = h.half * 128u + il;
-    const uint32_t sel = il & 3u;
-    const uint32_t idr = sel == 0 ? x : (sel == 1 ? y : (sel == 2 ? z : w));
+    const uint32_t q = ent >> 8;
+    const uint32_t item = ent & 255u;
     const uint64_t T = lds64(h.t_s + 8u * q);
     const int32_t score =
         smem_dot(h.a_s + q * kKBytes, q & 7u, h.b_s + item * kKBytes, item & 7u);
-    const uint64_t key = make_key(score, idr);
+    const uint64_t key = make_key(score, lds32(h.id_s + 4u * item));
     if (key >= T) {
       pd.p = atomicAdd(a.out_cnt + q, 1u);
       pd.key = key;
@@ -457,8 +451,8 @@ __device__ __forceinline__ void filter_hits(const TcArgs& a, const HitCtx& h, ui
   head += n;
   bool pass = mine;
   if (mine) {
-    const uint32_t q = ((ent >> 14) << 7) | ((ent >> 7) & 127u);
-    const uint32_t item = h.half * 128u + (ent & 127u);
+    const uint32_t q = ent >> 8;
+    const uint32_t item = ent & 255u;
     const int ng = (int)lds32(h.qg_s + 4u * q);
     if (ng > 0) {
       const uint32_t tb = h.tb_s + item * (kTbStride * 4u);
@@ -492,8 +486,10 @@ __device__ __forceinline__ void filter_hits(const TcArgs& a, const HitCtx& h, ui
 }
 
 template <bool kCnf>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
     k_scan_tc(const __grid_constant__ CUtensorMap tmap_items, const TcArgs a) {
+  constexpr int NT = kCnf ? kThreadsCnf : kThreads;
+  constexpr int NE = kCnf ? kEpiWarpsCnf : kEpiWarps;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -520,20 +516,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ---- prologue: queries -> swizzled smem, thresholds, leaf table, filter programs ----
   const int a_rows = a.n_mblk * kBlockM;
-  for (int i = threadIdx.x; i < a_rows * 8; i += kThreads) {
+  for (int i = threadIdx.x; i < a_rows * 8; i += NT) {
     const int r = i >> 3, c = i & 7;
     int4 v = make_int4(0, 0, 0, 0);
     if (r < a.nq) v = __ldg(reinterpret_cast<const int4*>(a.queries + (int64_t)r * kKBytes) + c);
     *reinterpret_cast<int4*>(sA + r * kKBytes + ((c ^ (r & 7)) << 4)) = v;
   }
-  for (int q = threadIdx.x; q < kMaxQueries; q += kThreads)
+  for (int q = threadIdx.x; q < kMaxQueries; q += NT)
     sT[q] = (a.threshold != nullptr && q < a.nq) ? a.threshold[q] : 0ull;
   int32_t prog_off0 = 0;
   bool prog_staged = false;
   if (kCnf) {
     // column -> plane-slot table (negated columns flagged by a set bit 14 on slot 0),
     // query group masks (zero-padded to qm_stride words), group counts, zeroed TB stages
-    for (int i = threadIdx.x; i < a.n_cols * a.k_max; i += kThreads) {
+    for (int i = threadIdx.x; i < a.n_cols * a.k_max; i += NT) {
       const int c = i / a.k_max, j = i - c * a.k_max;
       const int cl = a.col_leaf[c];
       const int leaf = cl >= 0 ? cl : ~cl;
@@ -543,22 +539,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     uint32_t* qm = reinterpret_cast<uint32_t*>(smem + a.off_qm);
     const int qm_words = a.nq * a.cnf_gmax * a.qm_stride;
-    for (int i = threadIdx.x; i < qm_words; i += kThreads) {
+    for (int i = threadIdx.x; i < qm_words; i += NT) {
       const int w = i % a.qm_stride, qg = i / a.qm_stride;
       qm[i] = w < a.cnf_words ? a.qmask[(int64_t)qg * a.cnf_words + w] : 0u;
     }
     int32_t* qgs = reinterpret_cast<int32_t*>(smem + a.off_qg);
-    for (int q = threadIdx.x; q < kMaxQueries; q += kThreads) qgs[q] = q < a.nq ? a.qgroups[q] : 0;
+    for (int q = threadIdx.x; q < kMaxQueries; q += NT) qgs[q] = q < a.nq ? a.qgroups[q] : 0;
     uint32_t* tb = reinterpret_cast<uint32_t*>(sL);
-    for (int i = threadIdx.x; i < 2 * (int)(a.leaf_stage_bytes / 4); i += kThreads) tb[i] = 0u;
+    for (int i = threadIdx.x; i < 2 * (int)(a.leaf_stage_bytes / 4); i += NT) tb[i] = 0u;
   } else if (a.has_prog) {
-    for (int i = threadIdx.x; i < a.n_leaves * a.k_max; i += kThreads) sLS[i] = a.leaf_slot[i];
+    for (int i = threadIdx.x; i < a.n_leaves * a.k_max; i += NT) sLS[i] = a.leaf_slot[i];
     prog_off0 = a.rop_offset[0];
     const int32_t n_ops = a.rop_offset[a.nq] - prog_off0;
     if (n_ops <= a.rops_cap) {
       uint4* dst = reinterpret_cast<uint4*>(smem + a.off_r);
       const uint4* src = reinterpret_cast<const uint4*>(a.rops + prog_off0);
-      for (int i = threadIdx.x; i < n_ops / 8; i += kThreads) dst[i] = __ldg(src + i);
+      for (int i = threadIdx.x; i < n_ops / 8; i += NT) dst[i] = __ldg(src + i);
       prog_staged = true;
     }
   }
@@ -566,16 +562,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int s = 0; s < 4; ++s) {
-      mbar_init(items_full + s, 1);
-      mbar_init(items_empty + s, kCnf ? 1 + kEpiWarps : 1);
+      mbar_init(items_full + s, kCnf ? 1 + 32 : 1);  // CNF: + id-rank cp.async per lane
+      mbar_init(items_empty + s, kCnf ? 1 + NE : 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(planes_full + s, 32);  // one cp.async.mbarrier.arrive per producer lane
       mbar_init(planes_empty + s, kLeafThreads);
       mbar_init(leaf_full + s, kLeafThreads);
-      mbar_init(leaf_empty + s, kEpiWarps);
+      mbar_init(leaf_empty + s, NE);
       mbar_init(acc_full + s, 1);
-      mbar_init(acc_empty + s, kEpiWarps);
+      mbar_init(acc_empty + s, NE);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -598,7 +594,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ph = 0, pph = 0;
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x) {
       const int tile = a.work[i * a.work_stride].x;
-      if (lane == 0) {
+      if (kCnf) {
+        // item rows by TMA; the tile's 256 id ranks (1 KB) by 16-byte cp.async alongside,
+        // into a stage with the item stage's lifetime (read by the survivors' key build)
+        mbar_wait_idle(items_empty + s, ph ^ 1u);
+        if (lane == 0) {
+          mbar_expect_tx(items_full + s, kItemBytes);
+          tma_load_2d(sB + (size_t)s * kItemBytes, &tmap_items, 0, tile * kTileItems,
+                      items_full + s);
+        }
+        const uint32_t dst = su32(smem + a.off_id) + (uint32_t)s * (kTileItems * 4u);
+        const uint32_t* src = a.id_rank + (int64_t)tile * kTileItems;
+#pragma unroll
+        for (int e = lane; e < kTileItems / 4; e += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + (uint32_t)e * 16u),
+                       "l"(src + 4 * e)
+                       : "memory");
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                         su32(items_full + s))
+                     : "memory");
+      } else if (lane == 0) {
         mbar_wait_idle(items_empty + s, ph ^ 1u);
         mbar_expect_tx(items_full + s, kItemBytes);
         tma_load_2d(sB + (size_t)s * kItemBytes, &tmap_items, 0, tile * kTileItems, items_full + s);
@@ -742,12 +757,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (kCnf) {
-    // ================= epilogue (CNF): TMEM scores -> threshold gate -> hit queue ->
-    // dense per-hit filter test (transposed column bits & query group masks); the exact
-    // score of a surviving hit is recomputed from the resident smem tiles -> emit ======
+    // ================= epilogue (CNF): TMEM scores -> threshold gate -> hit ring ->
+    // per-hit filter test (transposed column bits & query group masks) -> survivor ring ->
+    // exact score from the resident smem tiles -> key test -> emit. Twelve warps, three
+    // per TMEM lane quadrant; a quadrant's eight 32-column chunks of each M-block are
+    // dealt round-robin with a rotating start so the three warps stay balanced. =======
     const int ew = warp - kEpiWarp0;
     const int quad = warp & 3;
-    const int half = ew >> 2;
+    const int sub = ew >> 2;
     const int row = quad * 32 + lane;
     HitCtx h;
     h.qm_s = su32(smem + a.off_qm);
@@ -755,16 +772,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     h.qg_s = su32(smem + a.off_qg);
     h.t_s = su32(sT);
     h.hit_s = su32(smem + a.off_hit) + (uint32_t)ew * (kHitCap * 2u);
-    h.sv_s = su32(smem + a.off_hit) + (uint32_t)(kEpiWarps * kHitCap * 2) +
-             (uint32_t)ew * (kSurvCap * 2u);
-    h.half = (uint32_t)half;
+    h.sv_s = su32(smem + a.off_hit) + (uint32_t)(NE * kHitCap * 2) + (uint32_t)ew * (kSurvCap * 2u);
     // per query row of this thread: clamped score gate (|score| < 2^22 at dim 128)
     int32_t tau[kMaxMBlocks];
 #pragma unroll
     for (int mb = 0; mb < kMaxMBlocks; ++mb) {
       const int q = mb * kBlockM + row;
       const uint64_t T = q < a.nq ? sT[q] : ~0ull;
-      int32_t t = T == 0ull ? -(1 << 23) : key_score(T);
+      const int32_t t = T == 0ull ? -(1 << 23) : key_score(T);
       tau[mb] = min(max(t, -(1 << 23)), 1 << 23);
     }
     PendingEmit pd;
@@ -775,22 +790,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0, acc_it = 0, s = 0;
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
       const int2 wk = a.work[i * a.work_stride];
-      const int64_t s0 = a.ranges[2 * wk.y], s1 = a.ranges[2 * wk.y + 1];
       h.tile = wk.x;
-      // this half's two validity & range words (warp-uniform) and the id ranks of its
-      // 128 items (4 per lane; consumed by the survivors at the end of the tile)
-      const int64_t wbase = h.tile * kTileWords + 2 * half;
-      const uint64_t v0 = __ldg(a.valid + wbase) & word_range_mask(wbase * 64, s0, s1);
-      const uint64_t v1 = __ldg(a.valid + wbase + 1) & word_range_mask((wbase + 1) * 64, s0, s1);
-      {
-        const uint4 ir = __ldg(reinterpret_cast<const uint4*>(a.id_rank + h.tile * kTileItems +
-                                                              half * 128) + lane);
-        h.idr0 = ir.x;
-        h.idr1 = ir.y;
-        h.idr2 = ir.z;
-        h.idr3 = ir.w;
+      // lane c < 8 holds the validity & range bits of the tile's chunk c (32 items)
+      uint32_t vchunk = 0u;
+      if (lane < 8) {
+        const int64_t s0 = a.ranges[2 * wk.y], s1 = a.ranges[2 * wk.y + 1];
+        const int64_t gw = h.tile * kTileWords + (lane >> 1);
+        const uint64_t v = __ldg(a.valid + gw) & word_range_mask(gw * 64, s0, s1);
+        vchunk = (uint32_t)(v >> (32 * (lane & 1)));
       }
       h.b_s = su32(sB + (size_t)s * kItemBytes);
+      h.id_s = su32(smem + a.off_id) + (uint32_t)s * (kTileItems * 4u);
       const int st = it & 1;
       mbar_wait(leaf_full + st, (uint32_t)(it >> 1) & 1u);
       h.tb_s = su32(sL + (size_t)st * a.leaf_stage_bytes);
@@ -798,56 +808,65 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
         const int q = mb * kBlockM + row;
-        uint64_t e0 = q < a.nq ? v0 : 0ull, e1 = q < a.nq ? v1 : 0ull;
-        if (a.masks != nullptr && (e0 | e1) != 0ull) {
-          e0 &= __ldg(a.masks + (int64_t)q * a.n_words + wbase);
-          e1 &= __ldg(a.masks + (int64_t)q * a.n_words + wbase + 1);
-        }
+        const bool qok = q < a.nq;
         const int32_t tq = mb == 0 ? tau[0] : tau[kMaxMBlocks - 1];
         const int ab = acc_it & 1;
         mbar_wait(acc_full + ab, (uint32_t)(acc_it >> 1) & 1u);
         tc_fence_after();
         const uint32_t taddr =
-            tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kAccCols + half * 128);
-        const uint32_t ebase = ((uint32_t)mb << 14) | ((uint32_t)row << 7);
+            tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kAccCols);
+        const uint32_t ebase = ((uint32_t)mb << 15) | ((uint32_t)row << 8);
+        const int c0 = (sub + mb + it) % 3;
         int32_t r[32];
-        tmem_ld32_async(taddr, r);
+        tmem_ld32_async(taddr + (uint32_t)(c0 * 32), r);
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = c0; c < 8; c += 3) {
           tmem_wait32(r);
-          if (a.dump != nullptr && q < a.nq) {
-            const int64_t base = h.tile * kTileItems + half * 128 + c * 32;
+          if (a.dump != nullptr && qok) {
+            const int64_t base = h.tile * kTileItems + c * 32;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (base + j < a.dump_ld) a.dump[(int64_t)q * a.dump_ld + base + j] = r[j];
           }
-          uint32_t hm = hit_mask32(r, tq) & (uint32_t)((c < 2 ? e0 : e1) >> (32 * (c & 1)));
-          if (c < 3) {
-            tmem_ld32_async(taddr + (c + 1) * 32, r);  // overlaps the hit handling below
+          uint32_t em = __shfl_sync(0xffffffffu, vchunk, c);
+          if (!qok) em = 0u;
+          if (a.masks != nullptr && em != 0u)
+            em &= (uint32_t)(__ldg(a.masks + (int64_t)q * a.n_words + h.tile * kTileWords +
+                                   (c >> 1)) >>
+                             (32 * (c & 1)));
+          uint32_t hm = hit_mask32(r, tq) & em;
+          if (c + 3 < 8) {
+            tmem_ld32_async(taddr + (uint32_t)((c + 3) * 32), r);  // overlaps the hit handling
           } else {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(acc_empty + ab);
           }
-          // append this chunk's hits to the warp's ring, one per lane per round
+          // append this chunk's hits to the warp's ring, up to two per lane per round
           const uint32_t eb = ebase | (uint32_t)(c * 32);
           while (true) {
-            const uint32_t b = __ballot_sync(0xffffffffu, hm != 0u);
-            if (b == 0u) break;
+            const uint32_t b1 = __ballot_sync(0xffffffffu, hm != 0u);
+            if (b1 == 0u) break;
+            const uint32_t rest = hm & (hm - 1u);
+            const uint32_t b2 = __ballot_sync(0xffffffffu, rest != 0u);
             if (hm != 0u) {
-              const uint32_t j = (uint32_t)(__ffs(hm) - 1);
-              hm &= hm - 1u;
-              sts16(h.hit_s + ((tail + __popc(b & lanemask_lt())) & (kHitCap - 1)) * 2u, eb + j);
+              const uint32_t lt = lanemask_lt();
+              const uint32_t pos = tail + (uint32_t)(__popc(b1 & lt) + __popc(b2 & lt));
+              sts16(h.hit_s + (pos & (kHitCap - 1)) * 2u, eb + (uint32_t)(__ffs(hm) - 1));
+              if (rest != 0u)
+                sts16(h.hit_s + ((pos + 1u) & (kHitCap - 1)) * 2u,
+                      eb + (uint32_t)(__ffs(rest) - 1));
             }
-            tail += (uint32_t)__popc(b);
-            if (tail - head >= 32u) {
+            hm = rest & (rest - 1u);
+            tail += (uint32_t)(__popc(b1) + __popc(b2));
+            while (tail - head >= 32u) {
               __syncwarp();
               filter_hits(a, h, head, 32u, sv_head, sv_tail, pd, lane);
             }
           }
         }
       }
-      // drain: remaining hits, then the survivors (they read the item stage)
+      // drain: remaining hits, then the survivors (they read the item and id stages)
       if (tail != head) {
         __syncwarp();
         filter_hits(a, h, head, tail - head, sv_head, sv_tail, pd, lane);
@@ -859,7 +878,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(leaf_empty + st);
-        mbar_arrive(items_empty + s);  // the item stage was read by the score recompute
+        mbar_arrive(items_empty + s);
       }
       if (++s == a.item_stages) s = 0;
     }
@@ -1045,7 +1064,9 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
     t.off_qg = (uint32_t)align_up(off, 16);
     off = t.off_qg + (size_t)kMaxQueries * 4;
     t.off_hit = (uint32_t)align_up(off, 16);
-    off = t.off_hit + (size_t)kEpiWarps * (kHitCap + kSurvCap) * 2;
+    off = t.off_hit + (size_t)kEpiWarpsCnf * (kHitCap + kSurvCap) * 2;
+    t.off_id = (uint32_t)align_up(off, 16);
+    off = t.off_id + (size_t)stages * kTileItems * 4;
   }
   t.off_r = (uint32_t)align_up(off, 16);
   off = t.off_r + (size_t)t.rops_cap * 2;
@@ -1177,7 +1198,7 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
     if (cnf) {
       FB_CUDA(cudaFuncSetAttribute(k_scan_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
-      k_scan_tc<true><<<grid, kThreads, smem, s>>>(tmap, t);
+      k_scan_tc<true><<<grid, kThreadsCnf, smem, s>>>(tmap, t);
     } else {
       FB_CUDA(cudaFuncSetAttribute(k_scan_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
