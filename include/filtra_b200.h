@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define FB_ABI_VERSION 1
+#define FB_ABI_VERSION 2
 
 enum fb_status {
   FB_OK = 0,
@@ -72,6 +72,10 @@ typedef struct fb_index {
   int32_t dim_pad;   /* row stride in bytes: dim rounded up to 32 */
   int32_t m_bits;
   int32_t k_hashes;
+  /* Nullable inverse of id_rank (slot holding each rank) when id_rank is a permutation
+   * of [0, n_slots). With it, candidates carry only their merge key and the selection
+   * sorts keys alone (radix sort in shared memory). */
+  const uint32_t* slot_of_rank;
 } fb_index_t;
 
 /*

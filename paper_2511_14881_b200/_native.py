@@ -49,6 +49,9 @@ EXPORTED = (
 )
 
 
+ABI_VERSION = 2  # include/filtra_b200.h FB_ABI_VERSION
+
+
 class FbIndex(ctypes.Structure):
     _fields_ = [
         ("items", c_vp), ("planes", c_vp), ("valid", c_vp), ("id_rank", c_vp),
@@ -56,6 +59,7 @@ class FbIndex(ctypes.Structure):
         ("n_slots", ctypes.c_int64), ("n_words", ctypes.c_int64),
         ("dim", ctypes.c_int32), ("dim_pad", ctypes.c_int32),
         ("m_bits", ctypes.c_int32), ("k_hashes", ctypes.c_int32),
+        ("slot_of_rank", c_vp),
     ]
 
 
@@ -99,6 +103,9 @@ def load_library() -> ctypes.CDLL:
             f"{_LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(str(_LIB_PATH))
     _declare(lib)
+    if lib.fb_abi_version() != ABI_VERSION:
+        raise NativeUnavailable(f"{_LIB_PATH} has ABI {lib.fb_abi_version()}, expected "
+                                f"{ABI_VERSION}: rebuild the library")
     _lib = lib
     return lib
 

@@ -434,7 +434,7 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
     ea.word_stride = 1;
     ea.threshold = p->d_threshold;
     ea.out_key = p->d_cand_key;
-    ea.out_slot = p->d_cand_slot;
+    ea.out_slot = select_by_rank(p->cap, k, p->idx.slot_of_rank) ? nullptr : p->d_cand_slot;
     ea.out_cnt = p->d_cnt;
     ea.out_elig = p->d_elig;
     rc = emit(ea);
@@ -475,6 +475,7 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
   sel.cap = p->cap;
   sel.cand_key = p->d_cand_key;
   sel.cand_slot = p->d_cand_slot;
+  sel.slot_of_rank = p->idx.slot_of_rank;
   sel.cnt = p->d_cnt;
   sel.item_ids = p->idx.item_ids;
   sel.row_sum = p->idx.row_sum;

@@ -178,8 +178,11 @@ struct SelectArgs {
   double* out_fscores;        // nullable
   uint64_t* scratch_key;      // [B, cap]
   uint32_t* scratch_slot;     // [B, cap]
+  const uint32_t* slot_of_rank;  // [n_slots] nullable (fb_index_t.slot_of_rank)
 };
 int launch_select(const SelectArgs& a, cudaStream_t s);
+// true when the key-only radix selection applies (candidates then need no slot column)
+bool select_by_rank(int32_t cap, int32_t k, const uint32_t* slot_of_rank);
 
 struct ThresholdArgs {
   int32_t n_queries;

@@ -541,6 +541,266 @@ __global__ void __launch_bounds__(kSelectThreads) k_select(SelectArgs a) {
 }
 
 // ------------------------------------------------------------------------------------
+// Key-only exact selection (index with a rank -> slot table): per query CTA,
+//   1. the candidate keys are loaded into shared memory (<= kRsMaxCand);
+//   2. an MSD radix select (8-bit digits from the highest bit where the keys differ)
+//      finds the lower edge K of the top min(k, n) keys -- it stops as soon as a digit
+//      bin completes the count, so usually after 2-4 histogram passes;
+//   3. the keys >= K are compacted (exactly min(k, n) of them, keys being unique);
+//   4. an LSD radix sort (4-bit digits, stable block-wide counting passes over the bits
+//      of key - K) orders them; output rank = kk - 1 - sorted position;
+//   5. ids / scores / dequantised scores are gathered through slot_of_rank.
+// Same output as k_select (the oracle's (score desc, item_id asc) order).
+// ------------------------------------------------------------------------------------
+constexpr int kRsThreads = 1024;
+constexpr int kRsIpt = 10;                         // sort capacity per thread
+constexpr int kRsMaxK = kRsThreads * kRsIpt;       // 10240
+constexpr int kRsMaxCand = 22528;                  // keys loaded per query (176 KB)
+constexpr size_t kRsSmem = (size_t)kRsMaxCand * 8 + (size_t)16 * kRsThreads * 2;
+
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const uint64_t o = __shfl_xor_sync(0xffffffffu, v, d);
+    v = o > v ? o : v;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const uint64_t o = __shfl_xor_sync(0xffffffffu, v, d);
+    v = o < v ? o : v;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_rs[];
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(smem_rs);
+  uint16_t* s_cnt = reinterpret_cast<uint16_t*>(smem_rs + (size_t)kRsMaxCand * 8);
+  __shared__ uint32_t hist[256];
+  __shared__ uint64_t s_red[2][32];
+  __shared__ uint64_t s_lo;       // lower edge of the selected keys
+  __shared__ uint64_t s_prefix;
+  __shared__ uint32_t s_need, s_done, s_pos;
+  __shared__ uint32_t s_wsum[32];
+  __shared__ int32_t s_qsum;
+  const int q = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int n = (int)min(a.cnt[q], (uint32_t)a.cap);
+  const int kk = min(a.k, n);
+  if (t == 0) {
+    a.out_count[q] = kk;
+    int32_t sum = 0;
+    if (a.out_fscores)
+      for (int c = 0; c < a.dim; ++c) sum += a.queries[(int64_t)q * a.dim_pad + c];
+    s_qsum = sum;
+  }
+  for (int r = kk + t; r < a.k; r += kRsThreads) {
+    const int64_t o = (int64_t)q * a.k + r;
+    a.out_ids[o] = ~0ull;
+    a.out_scores[o] = INT32_MIN;
+    if (a.out_keys) a.out_keys[o] = 0ull;
+    if (a.out_fscores) a.out_fscores[o] = 0.0;
+  }
+  if (kk == 0) return;
+  const uint64_t* gk = a.cand_key + (int64_t)q * a.cap;
+
+  // 1. load + max / min
+  uint64_t mx = 0ull, mn = ~0ull;
+  for (int i = t; i < n; i += kRsThreads) {
+    const uint64_t k = gk[i];
+    s_key[i] = k;
+    mx = k > mx ? k : mx;
+    mn = k < mn ? k : mn;
+  }
+  mx = warp_max_u64(mx);
+  mn = warp_min_u64(mn);
+  if (lane == 0) {
+    s_red[0][wid] = mx;
+    s_red[1][wid] = mn;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    mx = warp_max_u64(s_red[0][lane]);
+    mn = warp_min_u64(s_red[1][lane]);
+    if (lane == 0) {
+      s_red[0][0] = mx;
+      s_red[1][0] = mn;
+      s_lo = mn;  // n <= k: every key is selected
+      s_need = (uint32_t)kk;
+      s_done = n <= kk ? 1u : 0u;
+      const int hb = 63 - __clzll((long long)(mx ^ mn));
+      const int shift = (hb / 8) * 8;
+      s_prefix = shift + 8 >= 64 ? 0ull : (mx >> (shift + 8)) << (shift + 8);
+      s_pos = (uint32_t)shift;  // current digit position
+    }
+  }
+  __syncthreads();
+  mx = s_red[0][0];
+
+  // 2. MSD radix select of the lower edge of the top kk keys
+  while (!s_done) {
+    const int shift = (int)s_pos;
+    const uint64_t prefix = s_prefix;
+    for (int b = t; b < 256; b += kRsThreads) hist[b] = 0u;
+    __syncthreads();
+    for (int i = t; i < n; i += kRsThreads) {
+      const uint64_t k = s_key[i];
+      if (shift + 8 >= 64 || ((k ^ prefix) >> (shift + 8)) == 0ull)
+        atomicAdd(hist + ((k >> shift) & 0xFFu), 1u);
+    }
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t need = s_need;
+      uint32_t c[8], sum = 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[255 - 8 * lane - j];
+        sum += c[j];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
+      }
+      const uint32_t excl = incl - sum;
+      if (excl < need && need <= incl) {
+        uint32_t cum = excl;
+        for (int j = 0; j < 8; ++j) {
+          if (cum + c[j] >= need) {
+            const uint64_t edge = prefix | ((uint64_t)(255 - 8 * lane - j) << shift);
+            if (cum + c[j] == need || shift == 0) {
+              s_lo = edge;  // the whole bin completes the count
+              s_done = 1u;
+            } else {
+              s_prefix = edge;
+              s_need = need - cum;
+              s_pos = (uint32_t)(shift - 8);
+            }
+            break;
+          }
+          cum += c[j];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const uint64_t lo = s_lo;
+
+  // 3. compaction of the kk keys >= lo to s_key[0, kk) (re-read from global memory, so
+  //    the shared copy can be overwritten)
+  if (t == 0) s_pos = 0u;
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += kRsThreads) {
+    const int i = i0 + t;
+    const uint64_t k = i < n ? gk[i] : 0ull;
+    const bool keep = i < n && k >= lo;
+    const uint32_t b = __ballot_sync(0xffffffffu, keep);
+    uint32_t base = 0u;
+    if (lane == 0 && b != 0u) base = atomicAdd(&s_pos, (uint32_t)__popc(b));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) s_key[base + __popc(b & ((1u << lane) - 1u))] = k;
+  }
+  __syncthreads();
+
+  // 4. LSD radix sort of s_key[0, kk) on the bits of (key - lo), ping-pong with
+  //    s_key[kRsMaxK, 2 kRsMaxK)
+  const uint64_t range = mx - lo;
+  const int nbits = range == 0ull ? 0 : 64 - __clzll((long long)range);
+  uint64_t* src = s_key;
+  uint64_t* dst = s_key + kRsMaxK;
+  for (int bit = 0; bit < nbits; bit += 4) {
+    uint64_t kv[kRsIpt];
+    uint32_t dl[kRsIpt];
+#pragma unroll
+    for (int d = 0; d < 16; ++d) s_cnt[d * kRsThreads + t] = 0;
+#pragma unroll
+    for (int j = 0; j < kRsIpt; ++j) {
+      const int e = t * kRsIpt + j;
+      kv[j] = e < kk ? src[e] : 0ull;
+      if (e < kk) {
+        const uint32_t d = (uint32_t)((kv[j] - lo) >> bit) & 15u;
+        const uint32_t r = s_cnt[d * kRsThreads + t];
+        s_cnt[d * kRsThreads + t] = (uint16_t)(r + 1u);
+        dl[j] = (d << 16) | r;
+      }
+    }
+    __syncthreads();
+    // exclusive scan of the counters in (digit, thread) order; thread t owns 16
+    // consecutive entries of the flattened array
+    uint16_t* my = s_cnt + 16 * t;
+    uint4 v0 = *reinterpret_cast<uint4*>(my);
+    uint4 v1 = *reinterpret_cast<uint4*>(my + 8);
+    uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint32_t run = 0u, pre[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t a0 = w[j] & 0xFFFFu, a1 = w[j] >> 16;
+      pre[j] = run | ((run + a0) << 16);
+      run += a0 + a1;
+    }
+    uint32_t incl = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    if (lane == 31) s_wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t ws = s_wsum[lane];
+      uint32_t wi = ws;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, wi, d);
+        if (lane >= d) wi += y;
+      }
+      s_wsum[lane] = wi - ws;
+    }
+    __syncthreads();
+    const uint32_t off = s_wsum[wid] + incl - run;
+    const uint32_t off2 = off | (off << 16);
+    v0 = make_uint4(pre[0] + off2, pre[1] + off2, pre[2] + off2, pre[3] + off2);
+    v1 = make_uint4(pre[4] + off2, pre[5] + off2, pre[6] + off2, pre[7] + off2);
+    *reinterpret_cast<uint4*>(my) = v0;
+    *reinterpret_cast<uint4*>(my + 8) = v1;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kRsIpt; ++j) {
+      const int e = t * kRsIpt + j;
+      if (e < kk) {
+        const uint32_t d = dl[j] >> 16;
+        dst[s_cnt[d * kRsThreads + t] + (dl[j] & 0xFFFFu)] = kv[j];
+      }
+    }
+    __syncthreads();
+    uint64_t* tmp = src;
+    src = dst;
+    dst = tmp;
+  }
+
+  // 5. outputs (ascending sorted position p -> rank kk - 1 - p)
+  const int32_t qsum = s_qsum;
+  for (int r = t; r < kk; r += kRsThreads) {
+    const uint64_t key = src[kk - 1 - r];
+    const uint32_t rank = 0xFFFFFFFFu - (uint32_t)key;
+    const uint32_t slot = a.slot_of_rank[rank];
+    const int64_t o = (int64_t)q * a.k + r;
+    const int32_t sc = key_score(key);
+    a.out_ids[o] = a.item_ids[slot];
+    a.out_scores[o] = sc;
+    if (a.out_keys) a.out_keys[o] = key;
+    if (a.out_fscores) {
+      const int32_t rs = a.row_sum ? a.row_sum[slot] : 0;
+      a.out_fscores[o] = dequant_dot(sc, rs, qsum, a.dim, a.gmin, a.gmax);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // Shard merge (serve._reduce_topk): n_lists lists per query, each sorted by
 // (score desc, item_id asc) -> global top-k. Compares (score, id) pairs directly, so
 // shards only need shard-local id ranks.
@@ -754,8 +1014,19 @@ int launch_resolve(int32_t n_queries, int32_t k, int32_t cap, Fallback* fb, uint
   return FB_OK;
 }
 
+bool select_by_rank(int32_t cap, int32_t k, const uint32_t* slot_of_rank) {
+  return slot_of_rank != nullptr && cap <= kRsMaxCand && k <= kRsMaxK;
+}
+
 int launch_select(const SelectArgs& a, cudaStream_t s) {
   if (a.n_queries <= 0) return FB_OK;
+  if (select_by_rank(a.cap, a.k, a.slot_of_rank)) {
+    FB_CUDA(cudaFuncSetAttribute(k_select_radix, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kRsSmem));
+    k_select_radix<<<a.n_queries, kRsThreads, kRsSmem, s>>>(a);
+    FB_LAUNCH_CHECK("k_select_radix");
+    return FB_OK;
+  }
   const size_t smem = (size_t)kSelectChunk * (sizeof(uint64_t) + sizeof(uint32_t));
   FB_CUDA(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_select<<<a.n_queries, kSelectThreads, smem, s>>>(a);

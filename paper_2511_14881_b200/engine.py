@@ -69,6 +69,7 @@ class DeviceIndex:
         if id_rank is None:
             id_rank = self._ranks_from_ids()
         self.id_rank = id_rank        # int32 [n_slots_pad] (uint32 bits)
+        self.slot_of_rank = self._inverse_ranks(id_rank)  # int32 [n_slots_pad] or None
         if row_sum is None:
             row_sum = torch.empty(items.shape[0], dtype=torch.int32, device=items.device)
             _native.check(_native.lib().fb_row_sums(items.data_ptr(), items.shape[0], self.dim,
@@ -110,6 +111,20 @@ class DeviceIndex:
         rank[order] = torch.arange(n, device=key.device, dtype=torch.int64)
         return rank.to(torch.int32)
 
+    @staticmethod
+    def _inverse_ranks(rank: torch.Tensor) -> torch.Tensor | None:
+        """slot_of_rank[id_rank[s]] = s when the ranks are a permutation of the slots
+        (always for ranks computed here); None otherwise."""
+        n = int(rank.numel())
+        r = rank.to(torch.int64)
+        if n == 0 or int(r.min()) < 0 or int(r.max()) >= n:
+            return None
+        inv = torch.full((n,), -1, dtype=torch.int64, device=rank.device)
+        inv[r] = torch.arange(n, device=rank.device, dtype=torch.int64)
+        if bool((inv < 0).any()):
+            return None
+        return inv.to(torch.int32)
+
     @classmethod
     def from_arrays(cls, items_q, valid, item_ids, *, bloom: BloomIndex | None = None,
                     qp: QuantParams | None = None, cluster_offsets=None, centroids=None,
@@ -141,7 +156,9 @@ class DeviceIndex:
                                self.valid.data_ptr(), self.id_rank.data_ptr(),
                                self.item_ids.data_ptr(), self.row_sum.data_ptr(),
                                self.n_slots_pad, self.n_words, self.dim, self.dim_pad,
-                               self.m_bits, self.k_hashes)
+                               self.m_bits, self.k_hashes,
+                               self.slot_of_rank.data_ptr() if self.slot_of_rank is not None
+                               else None)
 
     def quantize_queries(self, queries: torch.Tensor) -> torch.Tensor:
         if self.qp is None:

@@ -456,3 +456,48 @@ def test_tc_filter_modes_vs_oracle(fb, shape):
             got_ids, got_scores = out.host(q)
             assert np.array_equal(got_ids, ref.item_ids), (shape, k, q)
             assert np.array_equal(got_scores, ref.scores), (shape, k, q)
+
+
+@pytest.mark.parametrize("k", [1, 777, 5000])
+def test_select_paths_agree_with_oracle(fb, wl_small, k):
+    """Key-only radix selection (index with a rank -> slot table) and the chunked
+    bitonic selection (no table) give the oracle's order."""
+    wl = wl_small
+    idx = wl.index
+    ref = oracle_batch(wl, idx, k)
+    saved = idx.slot_of_rank
+    assert saved is not None
+    try:
+        for table in (saved, None):
+            idx.slot_of_rank = table
+            op = fb.TopkOp(idx, 24, k, np.array([[0, idx.n_slots]]))
+            out = op(wl.queries_q, wl.batch, keys=True)
+            torch.cuda.synchronize()
+            for q in range(24):
+                ids, scores = out.host(q)
+                assert np.array_equal(ids, ref[q].item_ids), (table is None, q)
+                assert np.array_equal(scores, ref[q].scores), (table is None, q)
+    finally:
+        idx.slot_of_rank = saved
+
+
+def test_select_heavy_ties(fb, rng):
+    """Few distinct scores (items in {-1, 0, 1}): order by (score desc, id asc) through
+    the radix selection, against brute force; ids deliberately not in slot order."""
+    from paper_2511_14881_b200 import _device, _native
+    n = 30_000
+    items = rng.integers(-1, 2, size=(n, 128)).astype(np.int8)
+    ids = rng.permutation(n * 3)[:n].astype(np.uint64) + np.uint64(1 << 40)
+    valid = rng.random(n) < 0.9
+    dix = fb.DeviceIndex.from_arrays(items, orc.from_bool(valid), ids)
+    assert dix.slot_of_rank is not None
+    q = rng.integers(-1, 2, size=(4, 128)).astype(np.int8)
+    for k in (100, 4000, 10_000):
+        op = fb.TopkOp(dix, 4, k, np.array([[0, n]]), _native.FB_PLAN_NO_SAMPLE)
+        out = op(_device.to_dev(q, torch.int8), None)
+        torch.cuda.synchronize()
+        for b in range(4):
+            ref = orc.brute_force_int8(items, ids, q[b], k, keep=valid)
+            gi, gs = out.host(b)
+            assert np.array_equal(gi, ref.item_ids), (k, b)
+            assert np.array_equal(gs, ref.scores), (k, b)
