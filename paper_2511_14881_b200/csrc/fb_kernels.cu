@@ -556,7 +556,15 @@ constexpr int kRsThreads = 1024;
 constexpr int kRsIpt = 10;                         // sort capacity per thread
 constexpr int kRsMaxK = kRsThreads * kRsIpt;       // 10240
 constexpr int kRsMaxCand = 22528;                  // keys loaded per query (176 KB)
-constexpr size_t kRsSmem = (size_t)kRsMaxCand * 8 + (size_t)16 * kRsThreads * 2;
+constexpr int kRsBits = 8;                         // LSD digit width
+constexpr int kRsDigits = 1 << kRsBits;
+constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsCntStride = kRsWarps + 1;          // u32 counters [digit][warp], padded
+// the two sort buffers (2 x kRsMaxK keys) then the per-warp digit counters; the
+// candidate load area (kRsMaxCand keys) overlaps both and is dead once compacted
+constexpr size_t kRsCntOff = (size_t)2 * kRsMaxK * 8;
+constexpr size_t kRsSmem = kRsCntOff + (size_t)kRsDigits * kRsCntStride * 4;
+static_assert(kRsSmem >= (size_t)kRsMaxCand * 8, "load area must fit");
 
 __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
 #pragma unroll
@@ -578,7 +586,7 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
 __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
   extern __shared__ __align__(16) uint8_t smem_rs[];
   uint64_t* s_key = reinterpret_cast<uint64_t*>(smem_rs);
-  uint16_t* s_cnt = reinterpret_cast<uint16_t*>(smem_rs + (size_t)kRsMaxCand * 8);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem_rs + kRsCntOff);
   __shared__ uint32_t hist[256];
   __shared__ uint64_t s_red[2][32];
   __shared__ uint64_t s_lo;       // lower edge of the selected keys
@@ -691,7 +699,12 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
   const uint64_t lo = s_lo;
 
   // 3. compaction of the kk keys >= lo to s_key[0, kk) (re-read from global memory, so
-  //    the shared copy can be overwritten)
+  //    the shared copy can be overwritten). Keys are compressed order-preservingly to
+  //    ((score_bits - score_lo) << id_bits) | (n_slots - 1 - id_rank): ranks are a
+  //    permutation of [0, n_slots), so the id part needs only id_bits bits.
+  const uint32_t sb_lo = (uint32_t)(lo >> 32);
+  const uint32_t id_base = 0u - (uint32_t)a.n_slots;  // low word of the key at rank n-1
+  const int id_bits = a.n_slots <= 1 ? 0 : 64 - __clzll((long long)(a.n_slots - 1));
   if (t == 0) s_pos = 0u;
   __syncthreads();
   for (int i0 = 0; i0 < n; i0 += kRsThreads) {
@@ -702,100 +715,129 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
     uint32_t base = 0u;
     if (lane == 0 && b != 0u) base = atomicAdd(&s_pos, (uint32_t)__popc(b));
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (keep) s_key[base + __popc(b & ((1u << lane) - 1u))] = k;
+    if (keep)
+      s_key[base + __popc(b & ((1u << lane) - 1u))] =
+          ((uint64_t)((uint32_t)(k >> 32) - sb_lo) << id_bits) | (uint64_t)((uint32_t)k - id_base);
   }
   __syncthreads();
 
-  // 4. LSD radix sort of s_key[0, kk) on the bits of (key - lo), ping-pong with
-  //    s_key[kRsMaxK, 2 kRsMaxK)
-  const uint64_t range = mx - lo;
-  const int nbits = range == 0ull ? 0 : 64 - __clzll((long long)range);
+  // 4. LSD radix sort of the compressed keys s_key[0, kk), ping-pong with
+  //    s_key[kRsMaxK, 2 kRsMaxK), 8-bit digits. Element order within a pass is
+  //    (warp, slot j, lane): warp w owns [w * 320, w * 320 + 320). Lanes holding equal
+  //    digits are found with match.any; per-warp running digit counts give the rank
+  //    within the warp, one scan of the (digit, warp) counters the rest.
+  const uint64_t cmax = ((uint64_t)((uint32_t)(mx >> 32) - sb_lo) << id_bits) |
+                        (uint64_t)((uint32_t)mx - id_base);
+  const int nbits = cmax == 0ull ? 0 : 64 - __clzll((long long)cmax);
   uint64_t* src = s_key;
   uint64_t* dst = s_key + kRsMaxK;
-  for (int bit = 0; bit < nbits; bit += 4) {
+  const uint32_t lt = (1u << lane) - 1u;
+  constexpr int kPer = kRsMaxK / kRsWarps;  // 320 elements per warp
+  for (int bit = 0; bit < nbits; bit += kRsBits) {
+    for (int d = lane; d < kRsDigits; d += 32) s_cnt[d * kRsCntStride + wid] = 0u;
+    __syncwarp();
     uint64_t kv[kRsIpt];
-    uint32_t dl[kRsIpt];
-#pragma unroll
-    for (int d = 0; d < 16; ++d) s_cnt[d * kRsThreads + t] = 0;
+    uint32_t rk[kRsIpt];
 #pragma unroll
     for (int j = 0; j < kRsIpt; ++j) {
-      const int e = t * kRsIpt + j;
-      kv[j] = e < kk ? src[e] : 0ull;
-      if (e < kk) {
-        const uint32_t d = (uint32_t)((kv[j] - lo) >> bit) & 15u;
-        const uint32_t r = s_cnt[d * kRsThreads + t];
-        s_cnt[d * kRsThreads + t] = (uint16_t)(r + 1u);
-        dl[j] = (d << 16) | r;
+      const int e = wid * kPer + j * 32 + lane;
+      const bool valid = e < kk;
+      kv[j] = valid ? src[e] : 0ull;
+      const uint32_t d = (uint32_t)(kv[j] >> bit) & (kRsDigits - 1);
+      const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 0x100u + lane);
+      uint32_t base = 0u;
+      if (valid) base = s_cnt[d * kRsCntStride + wid];
+      __syncwarp();
+      const uint32_t below = (uint32_t)__popc(peers & lt);
+      if (valid && below == 0u) s_cnt[d * kRsCntStride + wid] = base + (uint32_t)__popc(peers);
+      __syncwarp();
+      rk[j] = valid ? ((d << 16) | (base + below)) : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    // exclusive scan of the counters in (digit, warp) order: thread t owns the 8
+    // consecutive entries t * 8 .. t * 8 + 7 (digit t / 4, warps 8 (t % 4) ..)
+    {
+      const int d = t >> 2, w0 = (t & 3) * 8;
+      uint32_t* c = s_cnt + d * kRsCntStride + w0;
+      uint32_t v[8], run = 0u;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v[i] = run;
+        run += c[i];
       }
-    }
-    __syncthreads();
-    // exclusive scan of the counters in (digit, thread) order; thread t owns 16
-    // consecutive entries of the flattened array
-    uint16_t* my = s_cnt + 16 * t;
-    uint4 v0 = *reinterpret_cast<uint4*>(my);
-    uint4 v1 = *reinterpret_cast<uint4*>(my + 8);
-    uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-    uint32_t run = 0u, pre[8];
+      uint32_t incl = run;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t a0 = w[j] & 0xFFFFu, a1 = w[j] >> 16;
-      pre[j] = run | ((run + a0) << 16);
-      run += a0 + a1;
-    }
-    uint32_t incl = run;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += y;
-    }
-    if (lane == 31) s_wsum[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      const uint32_t ws = s_wsum[lane];
-      uint32_t wi = ws;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, wi, d);
-        if (lane >= d) wi += y;
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, dd);
+        if (lane >= dd) incl += y;
       }
-      s_wsum[lane] = wi - ws;
+      if (lane == 31) s_wsum[wid] = incl;
+      __syncthreads();
+      if (wid == 0) {
+        const uint32_t ws = s_wsum[lane];
+        uint32_t wi = ws;
+#pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, wi, dd);
+          if (lane >= dd) wi += y;
+        }
+        s_wsum[lane] = wi - ws;
+      }
+      __syncthreads();
+      const uint32_t off = s_wsum[wid] + incl - run;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c[i] = v[i] + off;
     }
-    __syncthreads();
-    const uint32_t off = s_wsum[wid] + incl - run;
-    const uint32_t off2 = off | (off << 16);
-    v0 = make_uint4(pre[0] + off2, pre[1] + off2, pre[2] + off2, pre[3] + off2);
-    v1 = make_uint4(pre[4] + off2, pre[5] + off2, pre[6] + off2, pre[7] + off2);
-    *reinterpret_cast<uint4*>(my) = v0;
-    *reinterpret_cast<uint4*>(my + 8) = v1;
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kRsIpt; ++j) {
-      const int e = t * kRsIpt + j;
-      if (e < kk) {
-        const uint32_t d = dl[j] >> 16;
-        dst[s_cnt[d * kRsThreads + t] + (dl[j] & 0xFFFFu)] = kv[j];
-      }
-    }
+    for (int j = 0; j < kRsIpt; ++j)
+      if (rk[j] != 0xFFFFFFFFu) dst[s_cnt[(rk[j] >> 16) * kRsCntStride + wid] + (rk[j] & 0xFFFFu)] = kv[j];
     __syncthreads();
     uint64_t* tmp = src;
     src = dst;
     dst = tmp;
   }
 
-  // 5. outputs (ascending sorted position p -> rank kk - 1 - p)
+  // 5. outputs (ascending sorted position p -> rank kk - 1 - p); all gathers of a
+  //    thread's outputs are issued before any is consumed
   const int32_t qsum = s_qsum;
-  for (int r = t; r < kk; r += kRsThreads) {
-    const uint64_t key = src[kk - 1 - r];
-    const uint32_t rank = 0xFFFFFFFFu - (uint32_t)key;
-    const uint32_t slot = a.slot_of_rank[rank];
-    const int64_t o = (int64_t)q * a.k + r;
-    const int32_t sc = key_score(key);
-    a.out_ids[o] = a.item_ids[slot];
-    a.out_scores[o] = sc;
-    if (a.out_keys) a.out_keys[o] = key;
-    if (a.out_fscores) {
-      const int32_t rs = a.row_sum ? a.row_sum[slot] : 0;
-      a.out_fscores[o] = dequant_dot(sc, rs, qsum, a.dim, a.gmin, a.gmax);
+  constexpr int kOutU = 5;  // gathers in flight per thread
+  const uint64_t id_mask = id_bits >= 64 ? ~0ull : ((1ull << id_bits) - 1ull);
+  for (int r0 = 0; r0 < kk; r0 += kRsThreads * kOutU) {
+    uint64_t key[kOutU];
+    uint32_t slot[kOutU];
+#pragma unroll
+    for (int u = 0; u < kOutU; ++u) {
+      const int r = r0 + u * kRsThreads + t;
+      key[u] = 0ull;
+      slot[u] = 0u;
+      if (r < kk) {
+        const uint64_t c = src[kk - 1 - r];
+        const uint32_t sb = (uint32_t)(c >> id_bits) + sb_lo;
+        const uint32_t low = (uint32_t)(c & id_mask) + id_base;
+        key[u] = ((uint64_t)sb << 32) | low;
+        slot[u] = __ldg(a.slot_of_rank + (0xFFFFFFFFu - low));
+      }
+    }
+    uint64_t iid[kOutU];
+    int32_t rsum[kOutU];
+#pragma unroll
+    for (int u = 0; u < kOutU; ++u) {
+      const int r = r0 + u * kRsThreads + t;
+      iid[u] = r < kk ? __ldg(a.item_ids + slot[u]) : 0ull;
+      rsum[u] = (r < kk && a.out_fscores && a.row_sum) ? __ldg(a.row_sum + slot[u]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kOutU; ++u) {
+      const int r = r0 + u * kRsThreads + t;
+      if (r < kk) {
+        const int64_t o = (int64_t)q * a.k + r;
+        const int32_t sc = key_score(key[u]);
+        a.out_ids[o] = iid[u];
+        a.out_scores[o] = sc;
+        if (a.out_keys) a.out_keys[o] = key[u];
+        if (a.out_fscores) a.out_fscores[o] = dequant_dot(sc, rsum[u], qsum, a.dim, a.gmin, a.gmax);
+      }
     }
   }
 }

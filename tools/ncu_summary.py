@@ -82,7 +82,7 @@ def launches(path, out_md):
         scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
                  "ms": 1e3, "second": 1e6, "s": 1e6}
         seq.append((r[ki].split("(")[0].replace("fb::<unnamed>::", ""), v * scale.get(r[ui], 1.0)))
-    sel = [i for i, s in enumerate(seq) if s[0].endswith("k_select")]
+    sel = [i for i, s in enumerate(seq) if s[0].endswith(("k_select", "k_select_radix"))]
     lines = [f"# Launch list: `{path.split('/')[-1]}`", "",
              "ncu `gpu__time_duration.sum`, `--clock-control none`, kernels serialised and "
              "cold-cache: compare shares, not absolutes.", ""]
