@@ -114,7 +114,7 @@ typedef struct fb_filter_prog {
   int32_t n_cols;
   int32_t cnf_words;           /* <= 8 */
   int32_t cnf_gmax;            /* <= 8 */
-  int32_t reserved2;
+  int32_t cnf_lits_max;        /* max over queries of sum_g 4 * ceil(|group g| / 4); 0 = unknown */
   const int16_t* col_leaf;     /* [n_cols] */
   const uint32_t* qmask;       /* [n_queries][cnf_gmax][cnf_words] */
   const int32_t* qgroups;      /* [n_queries] */

@@ -363,7 +363,8 @@ class FilterBatch:
 
     def __init__(self, leaf_pos, op_offset, ops, max_stack, push_leaf_bits, *,
                  plane_list=None, leaf_slot=None, rop_offset=None, rops=None, rmax_stack=0,
-                 col_leaf=None, qmask=None, qgroups=None, cnf_words=0, cnf_gmax=0):
+                 col_leaf=None, qmask=None, qgroups=None, cnf_words=0, cnf_gmax=0,
+                 cnf_lits_max=0):
         self.n_queries = len(op_offset) - 1
         self.n_leaves = leaf_pos.shape[0]
         self.k_max = leaf_pos.shape[1]
@@ -388,6 +389,8 @@ class FilterBatch:
                              if qgroups is not None else None)
         self.cnf_words = cnf_words
         self.cnf_gmax = cnf_gmax
+        # longest per-query literal stream with every group padded to 4 literals
+        self.cnf_lits_max = cnf_lits_max
         # per query: sum over PUSH_LEAF ops of |set_bits| (FilterStats.words_read per word)
         self.push_leaf_bits = push_leaf_bits
         self._dev = None
@@ -507,9 +510,12 @@ class FilterBatch:
                             qmask[q, gi, c >> 5] |= np.uint32(1 << (c & 31))
                 col_leaf = np.array([(~leaf if neg else leaf) for (leaf, neg) in cols],
                                     dtype=np.int16)
+                pops = np.unpackbits(qmask.view(np.uint8), axis=-1).reshape(
+                    len(cnf), gmax, -1).sum(axis=-1)
+                lits_max = int(((pops + 3) // 4 * 4).sum(axis=1).max()) if len(cnf) else 0
                 cnf_kw = dict(col_leaf=col_leaf, qmask=qmask,
                               qgroups=np.array([len(g) for g in cnf], dtype=np.int32),
-                              cnf_words=words, cnf_gmax=gmax)
+                              cnf_words=words, cnf_gmax=gmax, cnf_lits_max=lits_max)
         return cls(leaf_pos, np.array(offsets, dtype=np.int32),
                    np.array(ops if ops else [0], dtype=np.uint16), max_stack,
                    np.array(push_bits, dtype=np.int64),
@@ -534,8 +540,8 @@ class FilterBatch:
         else:
             extra = (0, 0, 0, 0, None, None, None, None)
         if self.is_cnf:
-            cnf = (int(self.host_col_leaf.size), self.cnf_words, self.cnf_gmax, 0,
-                   d[7].data_ptr(), d[8].data_ptr(), d[9].data_ptr())
+            cnf = (int(self.host_col_leaf.size), self.cnf_words, self.cnf_gmax,
+                   self.cnf_lits_max, d[7].data_ptr(), d[8].data_ptr(), d[9].data_ptr())
         else:
             cnf = (0, 0, 0, 0, None, None, None)
         return _native.FbFilterProg(self.n_queries, self.n_leaves, self.k_max, self.max_stack,
