@@ -261,9 +261,14 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
     if (p->n_tc_work > 0) {
       // the sample pass runs at threshold 0 (every score is a hit): keep it to ~1/128 of
       // the tiles (>= 256 tiles, ~65k slots) -- enough for the rank estimate
+      // (rounded to whole waves of one tile per SM so no CTA runs a tile more than others)
       const int64_t target_tiles = std::max<int64_t>(std::min<int64_t>(p->n_tc_work, 256),
                                                      p->n_tc_work / 128);
-      p->tc_sample_stride = std::max<int64_t>(1, p->n_tc_work / target_tiles);
+      int n_sm = 148;
+      cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+      const int64_t waves = std::max<int64_t>(1, (target_tiles + n_sm / 2) / n_sm);
+      p->tc_sample_stride =
+          std::max<int64_t>(1, (p->n_tc_work + waves * n_sm - 1) / (waves * n_sm));
       const int64_t st = (p->n_tc_work + p->tc_sample_stride - 1) / p->tc_sample_stride;
       p->tc_sample_fraction = (double)st / (double)p->n_tc_work;
     }

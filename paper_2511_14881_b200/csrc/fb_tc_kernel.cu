@@ -562,13 +562,13 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int s = 0; s < 4; ++s) {
-      mbar_init(items_full + s, kCnf ? 1 + 32 : 1);  // CNF: + id-rank cp.async per lane
-      mbar_init(items_empty + s, kCnf ? 1 + NE : 1);
+      mbar_init(items_full + s, 1 + 32);  // TMA expect-tx + the id-rank cp.async per lane
+      mbar_init(items_empty + s, 1 + NE);  // MMA commit + every epilogue warp (id stage)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(planes_full + s, 32);  // one cp.async.mbarrier.arrive per producer lane
-      mbar_init(planes_empty + s, kLeafThreads);
-      mbar_init(leaf_full + s, kLeafThreads);
+      mbar_init(planes_empty + s, kCnf ? 2 : kLeafThreads);
+      mbar_init(leaf_full + s, kCnf ? 2 : kLeafThreads);
       mbar_init(leaf_empty + s, NE);
       mbar_init(acc_full + s, 1);
       mbar_init(acc_empty + s, NE);
@@ -594,9 +594,9 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
     uint32_t ph = 0, pph = 0;
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x) {
       const int tile = a.work[i * a.work_stride].x;
-      if (kCnf) {
+      {
         // item rows by TMA; the tile's 256 id ranks (1 KB) by 16-byte cp.async alongside,
-        // into a stage with the item stage's lifetime (read by the survivors' key build)
+        // into a stage with the item stage's lifetime (read by the epilogue's key build)
         mbar_wait_idle(items_empty + s, ph ^ 1u);
         if (lane == 0) {
           mbar_expect_tx(items_full + s, kItemBytes);
@@ -613,10 +613,6 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
                          su32(items_full + s))
                      : "memory");
-      } else if (lane == 0) {
-        mbar_wait_idle(items_empty + s, ph ^ 1u);
-        mbar_expect_tx(items_full + s, kItemBytes);
-        tma_load_2d(sB + (size_t)s * kItemBytes, &tmap_items, 0, tile * kTileItems, items_full + s);
       }
       if (a.has_prog && a.n_planes > 0) {
         mbar_wait_idle(planes_empty + ps, pph ^ 1u);
@@ -724,8 +720,10 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
         for (int ib = 0; ib < 8; ++ib) TB[(ib * 32 + lane) * kTbStride + cb] = m[ib];
       }
       __syncwarp();
-      mbar_arrive(planes_empty + ps);  // 32 arrivals per warp, 64 in total
-      mbar_arrive(leaf_full + st);
+      if (lane == 0) {  // one arrival per builder warp
+        mbar_arrive(planes_empty + ps);
+        mbar_arrive(leaf_full + st);
+      }
       if (++ps == PS) { ps = 0; pph ^= 1u; }
     }
   } else if (warp < kEpiWarp0) {
@@ -900,10 +898,12 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
         p_len[mb] = a.rop_offset[q + 1] - a.rop_offset[q];
       }
     }
-    int it = 0, acc_it = 0;
+    int it = 0, acc_it = 0, s = 0;
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
       const int2 wk = a.work[i * a.work_stride];
       const int64_t tile = wk.x;
+      const uint32_t id_s = su32(smem + a.off_id) + (uint32_t)s * (kTileItems * 4u) +
+                            (uint32_t)(half * 128) * 4u;
       const int64_t s0 = a.ranges[2 * wk.y], s1 = a.ranges[2 * wk.y + 1];
       const int64_t wbase = tile * kTileWords + 2 * half;
       const uint64_t v0 = __ldg(a.valid + wbase) & word_range_mask(wbase * 64, s0, s1);
@@ -934,6 +934,12 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
         }
         const uint64_t T = active ? sT[q] : ~0ull;
         const int32_t tau = T == 0ull ? INT32_MIN : key_score(T);
+        // threshold 0 (sampling pass): every eligible item is emitted, so one slot
+        // reservation per M-block covers all four chunks; it is issued before the scores
+        // are read so the round trip overlaps the wait
+        uint32_t pdense = 0u;
+        if (T == 0ull && (f0 | f1) != 0ull)
+          pdense = atomicAdd(a.out_cnt + q, (uint32_t)(__popcll(f0) + __popcll(f1)));
         const int ab = acc_it & 1;
         mbar_wait(acc_full + ab, (uint32_t)(acc_it >> 1) & 1u);
         tc_fence_after();
@@ -961,20 +967,21 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
               for (int j = 0; j < 32; ++j) cm |= (r[j] >= tau ? 1u : 0u) << j;
               cm &= fw;
               if (cm != 0u && T == 0ull) {
-                // threshold 0 (sampling pass): every eligible item is emitted, so one slot
-                // reservation covers the chunk and the stores need no per-item round trip
-                const int64_t slot0 = tile * kTileItems + half * 128 + c * 32;
-                uint32_t p = atomicAdd(a.out_cnt + q, (uint32_t)__popc(cm));
+                const uint32_t slot0 = (uint32_t)(tile * kTileItems + half * 128 + c * 32);
+                uint32_t p = pdense;
+                pdense += (uint32_t)__popc(cm);
+                uint64_t* okp = a.out_key + (int64_t)q * a.cap;
+                uint32_t* osp = a.out_slot ? a.out_slot + (int64_t)q * a.cap : nullptr;
+                const uint32_t ids = id_s + (uint32_t)(c * 32) * 4u;
+                const uint32_t cap = (uint32_t)a.cap;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                  if ((cm >> j) & 1u) {
-                    if (p < (uint32_t)a.cap) {
-                      a.out_key[(int64_t)q * a.cap + p] =
-                          make_key(r[j], __ldg(a.id_rank + slot0 + j));
-                      if (a.out_slot) a.out_slot[(int64_t)q * a.cap + p] = (uint32_t)(slot0 + j);
-                    }
-                    ++p;
+                  const bool on = ((cm >> j) & 1u) != 0u;
+                  if (on && p < cap) {
+                    okp[p] = make_key(r[j], lds32(ids + 4u * j));
+                    if (osp != nullptr) osp[p] = slot0 + (uint32_t)j;
                   }
+                  p += on ? 1u : 0u;
                 }
               } else if (cm != 0u) {
                 const int64_t slot0 = tile * kTileItems + half * 128 + c * 32;
@@ -985,7 +992,7 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
                   const int j = __ffs(cm) - 1;
                   cm &= cm - 1u;
                   const int64_t slot = slot0 + j;
-                  const uint64_t key = make_key(rs[j], __ldg(a.id_rank + slot));
+                  const uint64_t key = make_key(rs[j], lds32(id_s + (uint32_t)(c * 32 + j) * 4u));
                   if (key >= T) {
                     const uint32_t p = atomicAdd(a.out_cnt + q, 1u);
                     if (p < (uint32_t)a.cap) {
@@ -1002,10 +1009,12 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + ab);
       }
-      if (a.has_prog) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(leaf_empty + st);
+      __syncwarp();
+      if (lane == 0) {
+        if (a.has_prog) mbar_arrive(leaf_empty + st);
+        mbar_arrive(items_empty + s);  // id stage read
       }
+      if (++s == a.item_stages) s = 0;
     }
   }
 
@@ -1065,9 +1074,9 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
     off = t.off_qg + (size_t)kMaxQueries * 4;
     t.off_hit = (uint32_t)align_up(off, 16);
     off = t.off_hit + (size_t)kEpiWarpsCnf * (kHitCap + kSurvCap) * 2;
-    t.off_id = (uint32_t)align_up(off, 16);
-    off = t.off_id + (size_t)stages * kTileItems * 4;
   }
+  t.off_id = (uint32_t)align_up(off, 16);
+  off = t.off_id + (size_t)stages * kTileItems * 4;
   t.off_r = (uint32_t)align_up(off, 16);
   off = t.off_r + (size_t)t.rops_cap * 2;
   return off + 1024;
