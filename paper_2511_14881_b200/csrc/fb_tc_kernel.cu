@@ -200,6 +200,37 @@ __device__ __forceinline__ void tmem_wait32(int32_t (&r)[32]) {
                : "memory");
 }
 
+// 32 lanes x 32 columns <- v (every register the same value)
+__device__ __forceinline__ void tmem_st32_const(uint32_t taddr, int32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(v)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// Bit j = (r[j] >= 0), i.e. the sign bits of 32 accumulators pre-loaded with -tau
+// (one funnel shift per score, four independent 8-bit chains).
+__device__ __forceinline__ uint32_t nonneg_mask32(const int32_t (&r)[32]) {
+  uint32_t m[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int j = 7; j >= 0; --j) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) m[p] = __funnelshift_l((uint32_t)r[8 * p + j], m[p], 1);
+  }
+  return ~(m[0] | (m[1] << 8) | (m[2] << 16) | (m[3] << 24));
+}
+// Score gate of a query row from its key threshold, clamped so score - tau cannot
+// overflow (|score| < 2^22 at dim 128); rows past the batch get an unreachable gate.
+__device__ __forceinline__ int32_t gate_tau(const uint64_t* sT, int q, int nq) {
+  const uint64_t T = q < nq ? sT[q] : ~0ull;
+  const int32_t t = T == 0ull ? -(1 << 23) : key_score(T);
+  return min(max(t, -(1 << 23)), 1 << 23);
+}
+
 // Bit j of the result = (r[j] >= tau), for |r| < 2^22 and tau clamped to [-2^23, 2^23]:
 // the sign of (tau - 1 - r[j]) is shifted in with a funnel shift (2 instructions per
 // score), in four independent 8-bit chains.
@@ -357,7 +388,12 @@ struct PendingEmit {
   uint32_t slot;
   int32_t q;
 };
-constexpr int kSurvCap = 64;  // per-warp ring of filter survivors (exact key test pending)
+constexpr int kSurvCap = 64;
+// per item stage, written by the producer: the tile's id ranks, its four validity & range
+// words and its tile index
+constexpr uint32_t kMetaValid = kTileItems * 4;       // 1024
+constexpr uint32_t kMetaTile = kMetaValid + 32;       // 1056
+constexpr uint32_t kStageMeta = kMetaTile + 32;       // 1088 bytes per stage  // per-warp ring of filter survivors (exact key test pending)
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
@@ -562,7 +598,7 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int s = 0; s < 4; ++s) {
-      mbar_init(items_full + s, 1 + 32);  // TMA expect-tx + the id-rank cp.async per lane
+      mbar_init(items_full + s, 1 + 32 + 1);  // TMA expect-tx, id-rank cp.async per lane, meta
       mbar_init(items_empty + s, 1 + NE);  // MMA commit + every epilogue warp (id stage)
     }
     for (int s = 0; s < 2; ++s) {
@@ -586,6 +622,26 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (kCnf && warp >= kEpiWarp0) {
+    // CNF: both accumulator buffers start as -tau of their rows; the MMA accumulates onto
+    // them, so the epilogue's gate is a sign test. Buffer b holds M-block b (or 0).
+    const int ew = warp - kEpiWarp0;
+#pragma unroll 1
+    for (int ab = 0; ab < 2; ++ab) {
+      const int mb = a.n_mblk == kMaxMBlocks ? ab : 0;
+      const int32_t nt = -gate_tau(sT, mb * kBlockM + (warp & 3) * 32 + lane, a.nq);
+      for (int c = ew >> 2; c < 8; c += 3)
+        tmem_st32_const(tmem_base + ((uint32_t)((warp & 3) * 32) << 16) +
+                            (uint32_t)(ab * kAccCols + c * 32),
+                        nt);
+    }
+    tmem_wait_st();
+  }
+  if (kCnf) {
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   const int64_t n_sel = a.n_sel;
   if (warp == 0) {
@@ -595,24 +651,37 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x) {
       const int tile = a.work[i * a.work_stride].x;
       {
-        // item rows by TMA; the tile's 256 id ranks (1 KB) by 16-byte cp.async alongside,
-        // into a stage with the item stage's lifetime (read by the epilogue's key build)
+        // item rows by TMA; alongside, into a stage with the item stage's lifetime: the
+        // tile's 256 id ranks (1 KB, 16-byte cp.async), its validity & range words and its
+        // tile index (so the epilogue never waits on global memory for per-tile metadata)
         mbar_wait_idle(items_empty + s, ph ^ 1u);
         if (lane == 0) {
           mbar_expect_tx(items_full + s, kItemBytes);
           tma_load_2d(sB + (size_t)s * kItemBytes, &tmap_items, 0, tile * kTileItems,
                       items_full + s);
         }
-        const uint32_t dst = su32(smem + a.off_id) + (uint32_t)s * (kTileItems * 4u);
+        const uint32_t mst = su32(smem + a.off_id) + (uint32_t)s * kStageMeta;
         const uint32_t* src = a.id_rank + (int64_t)tile * kTileItems;
 #pragma unroll
         for (int e = lane; e < kTileItems / 4; e += 32)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + (uint32_t)e * 16u),
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(mst + (uint32_t)e * 16u),
                        "l"(src + 4 * e)
                        : "memory");
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
                          su32(items_full + s))
                      : "memory");
+        if (lane < kTileWords) {
+          const int rg = a.work[i * a.work_stride].y;
+          const int64_t s0 = a.ranges[2 * rg], s1 = a.ranges[2 * rg + 1];
+          const int64_t gw = (int64_t)tile * kTileWords + lane;
+          const uint64_t v = __ldg(a.valid + gw) & word_range_mask(gw * 64, s0, s1);
+          asm volatile("st.shared.u64 [%0], %1;" ::"r"(mst + kMetaValid + 8u * lane), "l"(v)
+                       : "memory");
+        }
+        if (lane == 0)
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(mst + kMetaTile), "r"(tile) : "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(items_full + s);
       }
       if (a.has_prog && a.n_planes > 0) {
         mbar_wait_idle(planes_empty + ps, pph ^ 1u);
@@ -655,7 +724,7 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kKBytes / kUmmaK; ++kk)
             umma_i8(d, sw128_desc(a_base + kk * kUmmaK), sw128_desc(b_base + kk * kUmmaK), idesc,
-                    kk > 0 ? 1u : 0u);
+                    (kk > 0 || kCnf) ? 1u : 0u);
           umma_commit(acc_full + ab);
         }
         umma_commit(items_empty + s);
@@ -771,34 +840,26 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
     h.t_s = su32(sT);
     h.hit_s = su32(smem + a.off_hit) + (uint32_t)ew * (kHitCap * 2u);
     h.sv_s = su32(smem + a.off_hit) + (uint32_t)(NE * kHitCap * 2) + (uint32_t)ew * (kSurvCap * 2u);
-    // per query row of this thread: clamped score gate (|score| < 2^22 at dim 128)
+    // per query row of this thread: clamped score gate (the accumulators start at -tau)
     int32_t tau[kMaxMBlocks];
 #pragma unroll
-    for (int mb = 0; mb < kMaxMBlocks; ++mb) {
-      const int q = mb * kBlockM + row;
-      const uint64_t T = q < a.nq ? sT[q] : ~0ull;
-      const int32_t t = T == 0ull ? -(1 << 23) : key_score(T);
-      tau[mb] = min(max(t, -(1 << 23)), 1 << 23);
-    }
+    for (int mb = 0; mb < kMaxMBlocks; ++mb) tau[mb] = gate_tau(sT, mb * kBlockM + row, a.nq);
     PendingEmit pd;
     pd.q = -1;
     pd.p = 0;
     pd.key = 0;
     pd.slot = 0;
     int it = 0, acc_it = 0, s = 0;
+    uint32_t iph = 0;
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
-      const int2 wk = a.work[i * a.work_stride];
-      h.tile = wk.x;
+      // per-tile metadata staged by the producer with the item stage
+      mbar_wait(items_full + s, iph);
+      const uint32_t mst = su32(smem + a.off_id) + (uint32_t)s * kStageMeta;
+      h.tile = (int64_t)lds32(mst + kMetaTile);
       // lane c < 8 holds the validity & range bits of the tile's chunk c (32 items)
-      uint32_t vchunk = 0u;
-      if (lane < 8) {
-        const int64_t s0 = a.ranges[2 * wk.y], s1 = a.ranges[2 * wk.y + 1];
-        const int64_t gw = h.tile * kTileWords + (lane >> 1);
-        const uint64_t v = __ldg(a.valid + gw) & word_range_mask(gw * 64, s0, s1);
-        vchunk = (uint32_t)(v >> (32 * (lane & 1)));
-      }
+      const uint32_t vchunk = lane < 8 ? lds32(mst + kMetaValid + 4u * lane) : 0u;
       h.b_s = su32(sB + (size_t)s * kItemBytes);
-      h.id_s = su32(smem + a.off_id) + (uint32_t)s * (kTileItems * 4u);
+      h.id_s = mst;
       const int st = it & 1;
       mbar_wait(leaf_full + st, (uint32_t)(it >> 1) & 1u);
       h.tb_s = su32(sL + (size_t)st * a.leaf_stage_bytes);
@@ -820,11 +881,12 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
 #pragma unroll 1
         for (int c = c0; c < 8; c += 3) {
           tmem_wait32(r);
+          tmem_st32_const(taddr + (uint32_t)(c * 32), -tq);  // re-arm for the buffer's next use
           if (a.dump != nullptr && qok) {
             const int64_t base = h.tile * kTileItems + c * 32;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (base + j < a.dump_ld) a.dump[(int64_t)q * a.dump_ld + base + j] = r[j];
+              if (base + j < a.dump_ld) a.dump[(int64_t)q * a.dump_ld + base + j] = r[j] + tq;
           }
           uint32_t em = __shfl_sync(0xffffffffu, vchunk, c);
           if (!qok) em = 0u;
@@ -832,10 +894,11 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
             em &= (uint32_t)(__ldg(a.masks + (int64_t)q * a.n_words + h.tile * kTileWords +
                                    (c >> 1)) >>
                              (32 * (c & 1)));
-          uint32_t hm = hit_mask32(r, tq) & em;
+          uint32_t hm = nonneg_mask32(r) & em;
           if (c + 3 < 8) {
             tmem_ld32_async(taddr + (uint32_t)((c + 3) * 32), r);  // overlaps the hit handling
           } else {
+            tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(acc_empty + ab);
@@ -878,7 +941,10 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
         mbar_arrive(leaf_empty + st);
         mbar_arrive(items_empty + s);
       }
-      if (++s == a.item_stages) s = 0;
+      if (++s == a.item_stages) {
+        s = 0;
+        iph ^= 1u;
+      }
     }
     flush_pending(a, pd);
   } else {
@@ -1076,7 +1142,7 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
     off = t.off_hit + (size_t)kEpiWarpsCnf * (kHitCap + kSurvCap) * 2;
   }
   t.off_id = (uint32_t)align_up(off, 16);
-  off = t.off_id + (size_t)stages * kTileItems * 4;
+  off = t.off_id + (size_t)stages * kStageMeta;
   t.off_r = (uint32_t)align_up(off, 16);
   off = t.off_r + (size_t)t.rops_cap * 2;
   return off + 1024;
