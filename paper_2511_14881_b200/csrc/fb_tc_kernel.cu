@@ -690,12 +690,27 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
         // arrives on planes_full once its copies land
         const uint32_t dst = su32(sP + (size_t)ps * a.plane_stage_bytes);
         const int64_t col0 = (int64_t)tile * kTileWords;
-        for (int e = lane; e < 2 * a.n_planes; e += 32) {
-          const int p = e >> 1;
-          const uint64_t* src = a.planes + (int64_t)a.plane_list[p] * a.n_words + col0 + 2 * (e & 1);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + (uint32_t)e * 16u),
-                       "l"(src)
-                       : "memory");
+        // (plane indices fetched eight at a time ahead of the copies: the copies' memory
+        // clobber would otherwise serialise each index load behind the previous copy)
+        const int n2 = 2 * a.n_planes;
+        for (int e0 = lane; e0 < n2; e0 += 32 * 8) {
+          int pl[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + 32 * u;
+            pl[u] = e < n2 ? __ldg(a.plane_list + (e >> 1)) : 0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + 32 * u;
+            if (e < n2) {
+              const uint64_t* src = a.planes + (int64_t)pl[u] * a.n_words + col0 + 2 * (e & 1);
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                               dst + (uint32_t)e * 16u),
+                           "l"(src)
+                           : "memory");
+            }
+          }
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
                          su32(planes_full + ps))
