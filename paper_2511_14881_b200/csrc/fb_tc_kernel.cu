@@ -646,10 +646,31 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
   const int64_t n_sel = a.n_sel;
   if (warp == 0) {
     // ================= producer: TMA item tile + Bloom plane words ================
+    // The per-tile global reads (work item, then its validity & range words) are issued
+    // one tile ahead, so their latency never sits on the producer's critical path.
     int s = 0, ps = 0;
     uint32_t ph = 0, pph = 0;
-    for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x) {
-      const int tile = a.work[i * a.work_stride].x;
+    const int64_t G = gridDim.x;
+    auto load_valid = [&](int2 w) -> uint64_t {
+      if (lane >= kTileWords) return 0ull;
+      const int64_t s0 = a.ranges[2 * w.y], s1 = a.ranges[2 * w.y + 1];
+      const int64_t gw = (int64_t)w.x * kTileWords + lane;
+      return __ldg(a.valid + gw) & word_range_mask(gw * 64, s0, s1);
+    };
+    int2 wk_cur = make_int2(0, 0), wk_next = make_int2(0, 0);
+    uint64_t v_cur = 0ull;
+    if (blockIdx.x < n_sel) {
+      wk_cur = a.work[(int64_t)blockIdx.x * a.work_stride];
+      v_cur = load_valid(wk_cur);
+      if (blockIdx.x + G < n_sel) wk_next = a.work[((int64_t)blockIdx.x + G) * a.work_stride];
+    }
+    for (int64_t i = blockIdx.x; i < n_sel; i += G) {
+      const int tile = wk_cur.x;
+      // prefetch: the next tile's validity, the tile after next's work item
+      uint64_t v_next = 0ull;
+      int2 wk_nn = make_int2(0, 0);
+      if (i + G < n_sel) v_next = load_valid(wk_next);
+      if (i + 2 * G < n_sel) wk_nn = a.work[(i + 2 * G) * a.work_stride];
       {
         // item rows by TMA; alongside, into a stage with the item stage's lifetime: the
         // tile's 256 id ranks (1 KB, 16-byte cp.async), its validity & range words and its
@@ -670,14 +691,9 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
                          su32(items_full + s))
                      : "memory");
-        if (lane < kTileWords) {
-          const int rg = a.work[i * a.work_stride].y;
-          const int64_t s0 = a.ranges[2 * rg], s1 = a.ranges[2 * rg + 1];
-          const int64_t gw = (int64_t)tile * kTileWords + lane;
-          const uint64_t v = __ldg(a.valid + gw) & word_range_mask(gw * 64, s0, s1);
-          asm volatile("st.shared.u64 [%0], %1;" ::"r"(mst + kMetaValid + 8u * lane), "l"(v)
+        if (lane < kTileWords)
+          asm volatile("st.shared.u64 [%0], %1;" ::"r"(mst + kMetaValid + 8u * lane), "l"(v_cur)
                        : "memory");
-        }
         if (lane == 0)
           asm volatile("st.shared.u32 [%0], %1;" ::"r"(mst + kMetaTile), "r"(tile) : "memory");
         __syncwarp();
@@ -718,6 +734,9 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
         if (++ps == PS) { ps = 0; pph ^= 1u; }
       }
       if (++s == S) { s = 0; ph ^= 1u; }
+      wk_cur = wk_next;
+      v_cur = v_next;
+      wk_next = wk_nn;
     }
   } else if (warp == 1) {
     // ================= MMA issuer (one thread) ====================================
