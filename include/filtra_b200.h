@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define FB_ABI_VERSION 2
+#define FB_ABI_VERSION 3
 
 enum fb_status {
   FB_OK = 0,
@@ -114,7 +114,8 @@ typedef struct fb_filter_prog {
   int32_t n_cols;
   int32_t cnf_words;           /* <= 8 */
   int32_t cnf_gmax;            /* <= 8 */
-  int32_t cnf_lits_max;        /* max over queries of sum_g 4 * ceil(|group g| / 4); 0 = unknown */
+  int32_t cnf_windowed;        /* 1: every group's columns lie in u32 words {2j, 2j+1} and
+                                  cnf_gmax <= 4 (register-resident filter test) */
   const int16_t* col_leaf;     /* [n_cols] */
   const uint32_t* qmask;       /* [n_queries][cnf_gmax][cnf_words] */
   const int32_t* qgroups;      /* [n_queries] */

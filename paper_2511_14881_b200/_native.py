@@ -49,7 +49,7 @@ EXPORTED = (
 )
 
 
-ABI_VERSION = 2  # include/filtra_b200.h FB_ABI_VERSION
+ABI_VERSION = 3  # include/filtra_b200.h FB_ABI_VERSION
 
 
 class FbIndex(ctypes.Structure):
@@ -72,7 +72,7 @@ class FbFilterProg(ctypes.Structure):
         ("n_rops", ctypes.c_int32), ("reserved", ctypes.c_int32),
         ("plane_list", c_vp), ("leaf_slot", c_vp), ("rop_offset", c_vp), ("rops", c_vp),
         ("n_cols", ctypes.c_int32), ("cnf_words", ctypes.c_int32),
-        ("cnf_gmax", ctypes.c_int32), ("cnf_lits_max", ctypes.c_int32),
+        ("cnf_gmax", ctypes.c_int32), ("cnf_windowed", ctypes.c_int32),
         ("col_leaf", c_vp), ("qmask", c_vp), ("qgroups", c_vp),
     ]
 

@@ -81,16 +81,14 @@ struct TcArgs {
   int32_t n_cols;
   int32_t cnf_words;
   int32_t cnf_gmax;
-  int32_t qm_stride;  // u32 per (query, group) in shared memory: 4 or 8
+  int32_t tb_stride;  // u32 per item row of the transposed column bits
   const int16_t* col_leaf;
   const uint32_t* qmask;
   const int32_t* qgroups;
   uint32_t off_a, off_b, off_p, off_l, off_ls, off_thr, off_r, off_bar, plane_stage_bytes,
-      leaf_stage_bytes, off_qm, off_qg, off_hit, off_id;
+      leaf_stage_bytes, off_hm, off_gate, off_sv, off_id;
 };
 
-constexpr int kTbStride = 8;     // u32 per item row of the transposed column bits (<= 256 cols)
-constexpr int kHitCap = 128;     // per-warp ring buffer of hits (score >= threshold)
 
 // ---- PTX helpers ----------------------------------------------------------------------
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -366,34 +364,11 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
   return x;
 }
 
-// Per-warp state of the CNF epilogue for the current tile. Hits and survivors are queued
-// as 16-bit entries: (m-block << 15) | (row << 8) | item, so entry >> 8 is the query.
-struct HitCtx {
-  int64_t tile;
-  uint32_t tb_s;   // shared address of this tile's transposed column bits
-  uint32_t qm_s;   // shared address of the query group masks
-  uint32_t a_s;    // shared address of the query tile (SW128 rows)
-  uint32_t b_s;    // shared address of this tile's item stage (SW128 rows)
-  uint32_t id_s;   // shared address of this tile's id ranks (same stage index)
-  uint32_t qg_s;   // shared address of the groups-per-query table
-  uint32_t t_s;    // shared address of the per-query thresholds
-  uint32_t hit_s;  // this warp's hit ring
-  uint32_t sv_s;   // this warp's survivor ring
-};
-// An emission whose slot reservation (atomicAdd) is in flight; stored one batch later so
-// the global round trip overlaps the next tile's work.
-struct PendingEmit {
-  uint64_t key;
-  uint32_t p;
-  uint32_t slot;
-  int32_t q;
-};
-constexpr int kSurvCap = 64;
 // per item stage, written by the producer: the tile's id ranks, its four validity & range
 // words and its tile index
 constexpr uint32_t kMetaValid = kTileItems * 4;       // 1024
 constexpr uint32_t kMetaTile = kMetaValid + 32;       // 1056
-constexpr uint32_t kStageMeta = kMetaTile + 32;       // 1088 bytes per stage  // per-warp ring of filter survivors (exact key test pending)
+constexpr uint32_t kStageMeta = kMetaTile + 32;       // 1088 bytes per stage
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
@@ -405,38 +380,72 @@ __device__ __forceinline__ uint64_t lds64(uint32_t addr) {
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
   return v;
 }
-
-// Exact int32 dot of a query row (A tile) and an item row (B stage) from shared memory.
-// Both tiles use the SWIZZLE_128B layout: 16-byte chunk c of row r sits at c ^ (r & 7).
-__device__ __forceinline__ int32_t smem_dot(uint32_t a_row, uint32_t a_sw, uint32_t b_row,
-                                            uint32_t b_sw) {
-  int32_t acc = 0;
-#pragma unroll
-  for (uint32_t c = 0; c < 8; ++c) {
-    const uint4 x = lds128(a_row + ((c ^ a_sw) << 4));
-    const uint4 y = lds128(b_row + ((c ^ b_sw) << 4));
-    acc = __dp4a((int)x.x, (int)y.x, acc);
-    acc = __dp4a((int)x.y, (int)y.y, acc);
-    acc = __dp4a((int)x.z, (int)y.z, acc);
-    acc = __dp4a((int)x.w, (int)y.w, acc);
-  }
-  return acc;
-}
-
-__device__ __forceinline__ uint32_t lds16(uint32_t addr) {
-  uint16_t v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+__device__ __forceinline__ uint2 lds64v(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
-  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+
+// ---- CNF gate: accumulators armed by the tensor core -----------------------------------
+// A CNF launch starts every accumulator at +127*D (D = the row's "gate digits", the sum of
+// 32 int8 digits): one extra K=32 MMA per M-block multiplies the query's digit row by a
+// constant tile of 127s. With 127*D >= -tau the score gate (score >= tau, a superset test:
+// the exact key test follows) is the accumulator's sign bit. |digits| <= 127 bounds D to
+// [-4096, 4064]: a gate below -127*4064 (and threshold 0) becomes "every score is a hit",
+// one above 127*4096 is clamped (still a superset of score >= tau).
+constexpr int32_t kGateDigitsMax = 4064;
+constexpr int32_t kGateDigitsMin = -4096;
+constexpr uint32_t kGateTileBytes = kMaxQueries * 32;  // 256 rows x 32 B (no swizzle)
+
+__host__ __device__ __forceinline__ int32_t floordiv127(int32_t a) {
+  const int32_t q = a / 127;
+  return (a % 127 != 0 && a < 0) ? q - 1 : q;
 }
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
+// gate digits of a row from its key threshold T (T == 0: no threshold -> all hits)
+__device__ __forceinline__ int32_t gate_digits(uint64_t T, bool& all) {
+  all = false;
+  if (T == 0ull) {
+    all = true;
+    return 0;
+  }
+  const int32_t D = -floordiv127(key_score(T));  // 127 D >= -tau
+  if (D > kGateDigitsMax) {
+    all = true;
+    return 0;
+  }
+  return D < kGateDigitsMin ? kGateDigitsMin : D;
+}
+// K-major, no-swizzle ("interleaved") smem descriptor: 8-row x 16-byte core matrices, the
+// two 16-byte K halves LBO apart, 8-row groups SBO apart.
+__device__ __forceinline__ uint64_t plain_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell); layout type 0 = SWIZZLE_NONE
+  return d;
+}
+// byte offset of (row, k) in the no-swizzle gate tiles (LBO = 128, SBO = 256)
+__host__ __device__ __forceinline__ uint32_t gate_off(int row, int k) {
+  return (uint32_t)((row >> 3) * 256 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15));
+}
+// one accumulator (this lane's row, column taddr) -> register
+__device__ __forceinline__ int32_t tmem_ld1(uint32_t taddr) {
+  int32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v) : : "memory");
+  return v;
 }
 
+// An emission whose slot reservation (atomicAdd) may still be in flight; its stores are
+// issued at the lane's next-but-one emission (or at the end), so the round trip overlaps
+// the scan.
+struct PendingEmit {
+  uint64_t key;
+  uint32_t p;
+  uint32_t slot;
+  int32_t q;
+};
 __device__ __forceinline__ void flush_pending(const TcArgs& a, PendingEmit& pd) {
   if (pd.q >= 0 && pd.p < (uint32_t)a.cap) {
     a.out_key[(int64_t)pd.q * a.cap + pd.p] = pd.key;
@@ -445,207 +454,93 @@ __device__ __forceinline__ void flush_pending(const TcArgs& a, PendingEmit& pd) 
   pd.q = -1;
 }
 
-// Up to 32 filter survivors from the head of the survivor ring: exact score recomputed
-// from the resident query / item tiles, exact key test, slot reservation. The previous
-// batch's stores are completed first (their reservations have long returned).
-__device__ __forceinline__ void emit_survivors(const TcArgs& a, const HitCtx& h,
-                                               uint32_t& sv_head, uint32_t sv_tail,
-                                               PendingEmit& pd, int lane) {
-  const uint32_t n = min(32u, sv_tail - sv_head);
-  const bool mine = (uint32_t)lane < n;
-  uint32_t ent = 0;
-  if (mine) ent = lds16(h.sv_s + ((sv_head + (uint32_t)lane) & (kSurvCap - 1)) * 2u);
-  __syncwarp();
-  sv_head += n;
-  flush_pending(a, pd);
-  if (mine) {
-    const uint32_t q = ent >> 8;
-    const uint32_t item = ent & 255u;
-    const uint64_t T = lds64(h.t_s + 8u * q);
-    const int32_t score =
-        smem_dot(h.a_s + q * kKBytes, q & 7u, h.b_s + item * kKBytes, item & 7u);
-    const uint64_t key = make_key(score, lds32(h.id_s + 4u * item));
-    if (key >= T) {
-      pd.p = atomicAdd(a.out_cnt + q, 1u);
-      pd.key = key;
-      pd.slot = (uint32_t)(h.tile * kTileItems + item);
-      pd.q = (int32_t)q;
-    }
+// CNF filter test of one (query, item) pair: every one of the query's OR-groups shares a
+// literal column with the item's column bits. Window form (<= 4 groups, each group's
+// columns inside one aligned u32 pair): per group a byte offset into the item row and a
+// 64-bit mask, all in registers; unused groups repeat group 0.
+__device__ __forceinline__ bool cnf_test_win(uint32_t row, const uint32_t (&wo)[4],
+                                             const uint32_t (&lo)[4], const uint32_t (&hi)[4]) {
+  uint32_t x[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const uint2 t = lds64v(row + wo[g]);
+    x[g] = (t.x & lo[g]) | (t.y & hi[g]);
   }
+  return min(min(x[0], x[1]), min(x[2], x[3])) != 0u;
+}
+// General form (<= 256 columns, <= 8 groups): group masks read from shared memory.
+__device__ __forceinline__ bool cnf_test_general(uint32_t tb_addr, uint32_t qaddr, int ng) {
+  const uint4 t0 = lds128(tb_addr);
+  const uint4 t1 = lds128(tb_addr + 16u);
+  bool pass = true;
+  for (int g = 0; g < ng && pass; ++g) {
+    const uint4 m0 = lds128(qaddr);
+    const uint4 m1 = lds128(qaddr + 16u);
+    pass = ((t0.x & m0.x) | (t0.y & m0.y) | (t0.z & m0.z) | (t0.w & m0.w) | (t1.x & m1.x) |
+            (t1.y & m1.y) | (t1.z & m1.z) | (t1.w & m1.w)) != 0u;
+    qaddr += 32u;
+  }
+  return pass;
 }
 
-// n (<= 32) hits from the head of the hit ring -- (query, item) pairs whose score cleared
-// the threshold gate and whose item is valid, in range and in the query's mask -- get the
-// CNF filter test (item column bits & the query's group masks); survivors are queued.
-__device__ __forceinline__ void filter_hits(const TcArgs& a, const HitCtx& h, uint32_t& head,
-                                            uint32_t n, uint32_t& sv_head, uint32_t& sv_tail,
-                                            PendingEmit& pd, int lane) {
-  const bool mine = (uint32_t)lane < n;
-  uint32_t ent = 0;
-  if (mine) ent = lds16(h.hit_s + ((head + (uint32_t)lane) & (kHitCap - 1)) * 2u);
-  __syncwarp();
-  head += n;
-  bool pass = mine;
-  if (mine) {
-    const uint32_t q = ent >> 8;
-    const uint32_t item = ent & 255u;
-    const int ng = (int)lds32(h.qg_s + 4u * q);
-    if (ng > 0) {
-      const uint32_t tb = h.tb_s + item * (kTbStride * 4u);
-      const uint4 t0 = lds128(tb);
-      uint32_t qaddr = h.qm_s + q * (uint32_t)(a.cnf_gmax * a.qm_stride) * 4u;
-      if (a.qm_stride == 4) {
-        for (int g = 0; g < ng && pass; ++g) {
-          const uint4 m0 = lds128(qaddr);
-          pass = ((t0.x & m0.x) | (t0.y & m0.y) | (t0.z & m0.z) | (t0.w & m0.w)) != 0u;
-          qaddr += 16u;
-        }
-      } else {
-        const uint4 t1 = lds128(tb + 16u);
-        for (int g = 0; g < ng && pass; ++g) {
-          const uint4 m0 = lds128(qaddr);
-          const uint4 m1 = lds128(qaddr + 16u);
-          pass = ((t0.x & m0.x) | (t0.y & m0.y) | (t0.z & m0.z) | (t0.w & m0.w) |
-                  (t1.x & m1.x) | (t1.y & m1.y) | (t1.z & m1.z) | (t1.w & m1.w)) != 0u;
-          qaddr += 32u;
-        }
-      }
-    }
-  }
-  const uint32_t b = __ballot_sync(0xffffffffu, pass);
-  if (pass) sts16(h.sv_s + ((sv_tail + __popc(b & lanemask_lt())) & (kSurvCap - 1)) * 2u, ent);
-  sv_tail += (uint32_t)__popc(b);
-  if (sv_tail - sv_head >= 32u) {
-    __syncwarp();
-    emit_survivors(a, h, sv_head, sv_tail, pd, lane);
-  }
-}
-
-template <bool kCnf>
-__global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
-    k_scan_tc(const __grid_constant__ CUtensorMap tmap_items, const TcArgs a) {
-  constexpr int NT = kCnf ? kThreadsCnf : kThreads;
-  constexpr int NE = kCnf ? kEpiWarpsCnf : kEpiWarps;
+// ---- shared-memory carve-up and barrier slots common to both scan kernels ------------
+struct Smem {
+  uint8_t* base;
+  uint8_t* sA;
+  uint8_t* sB;
+  uint8_t* sP;
+  uint8_t* sL;
+  int16_t* sLS;
+  uint64_t* sT;
+  uint64_t* bars;
+};
+__device__ __forceinline__ Smem carve(const TcArgs& a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* sA = smem + a.off_a;
-  uint8_t* sB = smem + a.off_b;
-  uint8_t* sP = smem + a.off_p;
-  uint8_t* sL = smem + a.off_l;
-  int16_t* sLS = reinterpret_cast<int16_t*>(smem + a.off_ls);
-  uint64_t* sT = reinterpret_cast<uint64_t*>(smem + a.off_thr);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + a.off_bar);
-  uint64_t* items_full = bars;        // [4]
-  uint64_t* items_empty = bars + 4;   // [4]
-  uint64_t* planes_full = bars + 8;   // [2]
-  uint64_t* planes_empty = bars + 10; // [2]
-  uint64_t* leaf_full = bars + 12;    // [2]
-  uint64_t* leaf_empty = bars + 14;   // [2]
-  uint64_t* acc_full = bars + 16;     // [2]
-  uint64_t* acc_empty = bars + 18;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  Smem m;
+  m.base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                      ~uintptr_t(1023));
+  m.sA = m.base + a.off_a;
+  m.sB = m.base + a.off_b;
+  m.sP = m.base + a.off_p;
+  m.sL = m.base + a.off_l;
+  m.sLS = reinterpret_cast<int16_t*>(m.base + a.off_ls);
+  m.sT = reinterpret_cast<uint64_t*>(m.base + a.off_thr);
+  m.bars = reinterpret_cast<uint64_t*>(m.base + a.off_bar);
+  return m;
+}
+// barrier slots (u64 index into bars)
+constexpr int kBarItemsFull = 0, kBarItemsEmpty = 4, kBarPlanesFull = 8, kBarPlanesEmpty = 10,
+              kBarLeafFull = 12, kBarLeafEmpty = 14, kBarAccFull = 16, kBarAccEmpty = 18,
+              kBarHmFull = 20, kBarHmEmpty = 22, kBarTmemSlot = 24, kBarCount = 25;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = a.item_stages;
-  const int PS = a.plane_stages;
-
-  // ---- prologue: queries -> swizzled smem, thresholds, leaf table, filter programs ----
+// queries -> SW128 smem rows (zero rows past the batch), per-row key thresholds
+__device__ __forceinline__ void stage_queries(const TcArgs& a, const Smem& m, int nt) {
   const int a_rows = a.n_mblk * kBlockM;
-  for (int i = threadIdx.x; i < a_rows * 8; i += NT) {
+  for (int i = threadIdx.x; i < a_rows * 8; i += nt) {
     const int r = i >> 3, c = i & 7;
     int4 v = make_int4(0, 0, 0, 0);
     if (r < a.nq) v = __ldg(reinterpret_cast<const int4*>(a.queries + (int64_t)r * kKBytes) + c);
-    *reinterpret_cast<int4*>(sA + r * kKBytes + ((c ^ (r & 7)) << 4)) = v;
+    *reinterpret_cast<int4*>(m.sA + r * kKBytes + ((c ^ (r & 7)) << 4)) = v;
   }
-  for (int q = threadIdx.x; q < kMaxQueries; q += NT)
-    sT[q] = (a.threshold != nullptr && q < a.nq) ? a.threshold[q] : 0ull;
-  int32_t prog_off0 = 0;
-  bool prog_staged = false;
-  if (kCnf) {
-    // column -> plane-slot table (negated columns flagged by a set bit 14 on slot 0),
-    // query group masks (zero-padded to qm_stride words), group counts, zeroed TB stages
-    for (int i = threadIdx.x; i < a.n_cols * a.k_max; i += NT) {
-      const int c = i / a.k_max, j = i - c * a.k_max;
-      const int cl = a.col_leaf[c];
-      const int leaf = cl >= 0 ? cl : ~cl;
-      int s = a.leaf_slot[leaf * a.k_max + j];
-      if (j == 0 && cl < 0) s |= 0x4000;
-      sLS[i] = (int16_t)s;
-    }
-    uint32_t* qm = reinterpret_cast<uint32_t*>(smem + a.off_qm);
-    const int qm_words = a.nq * a.cnf_gmax * a.qm_stride;
-    for (int i = threadIdx.x; i < qm_words; i += NT) {
-      const int w = i % a.qm_stride, qg = i / a.qm_stride;
-      qm[i] = w < a.cnf_words ? a.qmask[(int64_t)qg * a.cnf_words + w] : 0u;
-    }
-    int32_t* qgs = reinterpret_cast<int32_t*>(smem + a.off_qg);
-    for (int q = threadIdx.x; q < kMaxQueries; q += NT) qgs[q] = q < a.nq ? a.qgroups[q] : 0;
-    uint32_t* tb = reinterpret_cast<uint32_t*>(sL);
-    for (int i = threadIdx.x; i < 2 * (int)(a.leaf_stage_bytes / 4); i += NT) tb[i] = 0u;
-  } else if (a.has_prog) {
-    for (int i = threadIdx.x; i < a.n_leaves * a.k_max; i += NT) sLS[i] = a.leaf_slot[i];
-    prog_off0 = a.rop_offset[0];
-    const int32_t n_ops = a.rop_offset[a.nq] - prog_off0;
-    if (n_ops <= a.rops_cap) {
-      uint4* dst = reinterpret_cast<uint4*>(smem + a.off_r);
-      const uint4* src = reinterpret_cast<const uint4*>(a.rops + prog_off0);
-      for (int i = threadIdx.x; i < n_ops / 8; i += NT) dst[i] = __ldg(src + i);
-      prog_staged = true;
-    }
-  }
-  const uint32_t prog_s = su32(smem + a.off_r);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < 4; ++s) {
-      mbar_init(items_full + s, 1 + 32 + 1);  // TMA expect-tx, id-rank cp.async per lane, meta
-      mbar_init(items_empty + s, 1 + NE);  // MMA commit + every epilogue warp (id stage)
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(planes_full + s, 32);  // one cp.async.mbarrier.arrive per producer lane
-      mbar_init(planes_empty + s, kCnf ? 2 : kLeafThreads);
-      mbar_init(leaf_full + s, kCnf ? 2 : kLeafThreads);
-      mbar_init(leaf_empty + s, NE);
-      mbar_init(acc_full + s, 1);
-      mbar_init(acc_empty + s, NE);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     su32(tmem_slot)),
-                 "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  if (kCnf && warp >= kEpiWarp0) {
-    // CNF: both accumulator buffers start as -tau of their rows; the MMA accumulates onto
-    // them, so the epilogue's gate is a sign test. Buffer b holds M-block b (or 0).
-    const int ew = warp - kEpiWarp0;
-#pragma unroll 1
-    for (int ab = 0; ab < 2; ++ab) {
-      const int mb = a.n_mblk == kMaxMBlocks ? ab : 0;
-      const int32_t nt = -gate_tau(sT, mb * kBlockM + (warp & 3) * 32 + lane, a.nq);
-      for (int c = ew >> 2; c < 8; c += 3)
-        tmem_st32_const(tmem_base + ((uint32_t)((warp & 3) * 32) << 16) +
-                            (uint32_t)(ab * kAccCols + c * 32),
-                        nt);
-    }
-    tmem_wait_st();
-  }
-  if (kCnf) {
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-  }
+  for (int q = threadIdx.x; q < kMaxQueries; q += nt)
+    m.sT[q] = (a.threshold != nullptr && q < a.nq) ? a.threshold[q] : 0ull;
+}
 
+// ================= producer (one warp): TMA item tile + Bloom plane words ==============
+// The per-tile global reads (work item, then its validity & range words) are issued one
+// tile ahead, so their latency never sits on the producer's critical path.
+__device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap* tmap,
+                                              const Smem& m, int lane) {
+  uint8_t* smem = m.base;
+  uint8_t* sB = m.sB;
+  uint8_t* sP = m.sP;
+  uint64_t* items_full = m.bars + kBarItemsFull;
+  uint64_t* items_empty = m.bars + kBarItemsEmpty;
+  uint64_t* planes_full = m.bars + kBarPlanesFull;
+  uint64_t* planes_empty = m.bars + kBarPlanesEmpty;
+  const int S = a.item_stages;
+  const int PS = a.plane_stages;
   const int64_t n_sel = a.n_sel;
-  if (warp == 0) {
-    // ================= producer: TMA item tile + Bloom plane words ================
     // The per-tile global reads (work item, then its validity & range words) are issued
     // one tile ahead, so their latency never sits on the producer's critical path.
     int s = 0, ps = 0;
@@ -678,7 +573,7 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
         mbar_wait_idle(items_empty + s, ph ^ 1u);
         if (lane == 0) {
           mbar_expect_tx(items_full + s, kItemBytes);
-          tma_load_2d(sB + (size_t)s * kItemBytes, &tmap_items, 0, tile * kTileItems,
+          tma_load_2d(sB + (size_t)s * kItemBytes, tmap, 0, tile * kTileItems,
                       items_full + s);
         }
         const uint32_t mst = su32(smem + a.off_id) + (uint32_t)s * kStageMeta;
@@ -738,37 +633,60 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
       v_cur = v_next;
       wk_next = wk_nn;
     }
-  } else if (warp == 1) {
-    // ================= MMA issuer (one thread) ====================================
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_i8(kBlockM, kTileItems);
-      int acc_it = 0, s = 0;
-      uint32_t ph = 0;
-      for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x) {
-        mbar_wait(items_full + s, ph);
-        tc_fence_after();
-        const uint32_t b_base = su32(sB + (size_t)s * kItemBytes);
-        for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
-          const int ab = acc_it & 1;
-          const uint32_t aph = (uint32_t)(acc_it >> 1) & 1u;
-          mbar_wait_idle(acc_empty + ab, aph ^ 1u);
-          tc_fence_after();
-          const uint32_t a_base = su32(sA + mb * kBlockM * kKBytes);
-          const uint32_t d = tmem_base + (uint32_t)(ab * kAccCols);
+}
+
+// ================= MMA issuer (one thread) =============================================
+// kArm: each M-block's accumulator is first set to the row's gate (digits . 127s, K = 32,
+// no-swizzle descriptors; the 127 tile is one 256-byte pair of core matrices, SBO = 0).
+template <bool kArm>
+__device__ __forceinline__ void mma_loop(const TcArgs& a, const Smem& m, uint32_t tmem_base) {
+  uint64_t* items_full = m.bars + kBarItemsFull;
+  uint64_t* items_empty = m.bars + kBarItemsEmpty;
+  uint64_t* acc_full = m.bars + kBarAccFull;
+  uint64_t* acc_empty = m.bars + kBarAccEmpty;
+  constexpr uint32_t idesc = idesc_i8(kBlockM, kTileItems);
+  const uint32_t gate_s = su32(m.base + a.off_gate);
+  const int S = a.item_stages;
+  int acc_it = 0, s = 0;
+  uint32_t ph = 0;
+  for (int64_t i = blockIdx.x; i < a.n_sel; i += gridDim.x) {
+    mbar_wait(items_full + s, ph);
+    tc_fence_after();
+    const uint32_t b_base = su32(m.sB + (size_t)s * kItemBytes);
+    for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
+      const int ab = acc_it & 1;
+      const uint32_t aph = (uint32_t)(acc_it >> 1) & 1u;
+      mbar_wait_idle(acc_empty + ab, aph ^ 1u);
+      tc_fence_after();
+      const uint32_t a_base = su32(m.sA + mb * kBlockM * kKBytes);
+      const uint32_t d = tmem_base + (uint32_t)(ab * kAccCols);
+      if (kArm)
+        umma_i8(d, plain_desc(gate_s + (uint32_t)mb * (kBlockM / 8) * 256u, 128u, 256u),
+                plain_desc(gate_s + kGateTileBytes, 128u, 0u), idesc, 0u);
 #pragma unroll
-          for (int kk = 0; kk < kKBytes / kUmmaK; ++kk)
-            umma_i8(d, sw128_desc(a_base + kk * kUmmaK), sw128_desc(b_base + kk * kUmmaK), idesc,
-                    (kk > 0 || kCnf) ? 1u : 0u);
-          umma_commit(acc_full + ab);
-        }
-        umma_commit(items_empty + s);
-        if (++s == S) { s = 0; ph ^= 1u; }
-      }
+      for (int kk = 0; kk < kKBytes / kUmmaK; ++kk)
+        umma_i8(d, sw128_desc(a_base + kk * kUmmaK), sw128_desc(b_base + kk * kUmmaK), idesc,
+                (kk > 0 || kArm) ? 1u : 0u);
+      umma_commit(acc_full + ab);
     }
-  } else if (warp < kEpiWarp0 && kCnf) {
-    // ================= column builders (CNF): Bloom test per literal column, then a
-    // 32x32 bit transpose so each item row holds its column bits =====================
-    const int lw = warp - 2;  // 0 or 1
+    umma_commit(items_empty + s);
+    if (++s == S) { s = 0; ph ^= 1u; }
+  }
+}
+
+// ================= CNF column builders (nb warps): Bloom test per literal column, then a
+// 32x32 bit transpose so each item row holds its column bits ==========================
+__device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m, int lw, int nb,
+                                                 int lane) {
+  uint8_t* sP = m.sP;
+  uint8_t* sL = m.sL;
+  const int16_t* sLS = m.sLS;
+  uint64_t* planes_full = m.bars + kBarPlanesFull;
+  uint64_t* planes_empty = m.bars + kBarPlanesEmpty;
+  uint64_t* leaf_full = m.bars + kBarLeafFull;
+  uint64_t* leaf_empty = m.bars + kBarLeafEmpty;
+  const int PS = a.plane_stages;
+  const int64_t n_sel = a.n_sel;
     int it = 0, ps = 0;
     uint32_t pph = 0;
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
@@ -778,7 +696,7 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
       mbar_wait_idle(leaf_empty + st, ph ^ 1u);
       const uint32_t p_s = su32(sP + (size_t)ps * a.plane_stage_bytes);
       uint32_t* TB = reinterpret_cast<uint32_t*>(sL + (size_t)st * a.leaf_stage_bytes);
-      for (int cb = lw; cb < a.cnf_words; cb += 2) {  // 32-column block
+      for (int cb = lw; cb < a.cnf_words; cb += nb) {  // 32-column block
         const int col = cb * 32 + lane;
         // the column's 256 tile bits: AND of its planes' 32-byte rows (8 x u32, one per
         // 32-item block); all loads are independent
@@ -820,7 +738,7 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
                           : ((m[ib] & mk) | ((y[ib] & mk) << sft));
         }
 #pragma unroll
-        for (int ib = 0; ib < 8; ++ib) TB[(ib * 32 + lane) * kTbStride + cb] = m[ib];
+        for (int ib = 0; ib < 8; ++ib) TB[(ib * 32 + lane) * a.tb_stride + cb] = m[ib];
       }
       __syncwarp();
       if (lane == 0) {  // one arrival per builder warp
@@ -829,6 +747,95 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
       }
       if (++ps == PS) { ps = 0; pph ^= 1u; }
     }
+}
+
+// ---- tensor memory -----------------------------------------------------------------------
+__device__ __forceinline__ uint32_t tmem_alloc512(const Smem& m) {
+  uint32_t* slot = reinterpret_cast<uint32_t*>(m.bars + kBarTmemSlot);
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   su32(slot)),
+               "r"(512)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  return 0;
+}
+
+// ======================================================================================
+// Bytecode scan kernel: any filter program (stack depth <= 4) evaluated word-wise per
+// (query, 128 items) from per-tile leaf masks; also the threshold-0 sampling pass.
+// ======================================================================================
+__global__ void __launch_bounds__(kThreads, 1)
+    k_scan_tc(const __grid_constant__ CUtensorMap tmap_items, const TcArgs a) {
+  constexpr int NT = kThreads;
+  constexpr int NE = kEpiWarps;
+  const Smem m = carve(a);
+  uint8_t* smem = m.base;
+  uint8_t* sA = m.sA;
+  uint8_t* sB = m.sB;
+  uint8_t* sP = m.sP;
+  uint8_t* sL = m.sL;
+  int16_t* sLS = m.sLS;
+  uint64_t* sT = m.sT;
+  uint64_t* bars = m.bars;
+  uint64_t* items_full = bars + kBarItemsFull;
+  uint64_t* items_empty = bars + kBarItemsEmpty;
+  uint64_t* planes_full = bars + kBarPlanesFull;
+  uint64_t* planes_empty = bars + kBarPlanesEmpty;
+  uint64_t* leaf_full = bars + kBarLeafFull;
+  uint64_t* leaf_empty = bars + kBarLeafEmpty;
+  uint64_t* acc_full = bars + kBarAccFull;
+  uint64_t* acc_empty = bars + kBarAccEmpty;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kBarTmemSlot);
+  (void)sA;
+  (void)sB;
+  (void)items_full;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int PS = a.plane_stages;
+  const int64_t n_sel = a.n_sel;
+
+  // ---- prologue: queries, thresholds, leaf table, filter programs ----
+  stage_queries(a, m, NT);
+  int32_t prog_off0 = 0;
+  bool prog_staged = false;
+  if (a.has_prog) {
+    for (int i = threadIdx.x; i < a.n_leaves * a.k_max; i += NT) sLS[i] = a.leaf_slot[i];
+    prog_off0 = a.rop_offset[0];
+    const int32_t n_ops = a.rop_offset[a.nq] - prog_off0;
+    if (n_ops <= a.rops_cap) {
+      uint4* dst = reinterpret_cast<uint4*>(smem + a.off_r);
+      const uint4* src = reinterpret_cast<const uint4*>(a.rops + prog_off0);
+      for (int i = threadIdx.x; i < n_ops / 8; i += NT) dst[i] = __ldg(src + i);
+      prog_staged = true;
+    }
+  }
+  const uint32_t prog_s = su32(smem + a.off_r);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(items_full + s, 1 + 32 + 1);  // TMA expect-tx, id-rank cp.async per lane, meta
+      mbar_init(items_empty + s, 1 + NE);     // MMA commit + every epilogue warp (id stage)
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(planes_full + s, 32);  // one cp.async.mbarrier.arrive per producer lane
+      mbar_init(planes_empty + s, kLeafThreads);
+      mbar_init(leaf_full + s, kLeafThreads);
+      mbar_init(leaf_empty + s, NE);
+      mbar_init(acc_full + s, 1);
+      mbar_init(acc_empty + s, NE);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc512(m);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    producer_loop(a, &tmap_items, m, lane);
+  } else if (warp == 1) {
+    if (lane == 0) mma_loop<false>(a, m, tmem_base);
   } else if (warp < kEpiWarp0) {
     // ================= leaf builders: AND each leaf's planes per word =============
     if (a.has_prog) {
@@ -857,130 +864,6 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
         if (++ps == PS) { ps = 0; pph ^= 1u; }
       }
     }
-  } else if (kCnf) {
-    // ================= epilogue (CNF): TMEM scores -> threshold gate -> hit ring ->
-    // per-hit filter test (transposed column bits & query group masks) -> survivor ring ->
-    // exact score from the resident smem tiles -> key test -> emit. Twelve warps, three
-    // per TMEM lane quadrant; a quadrant's eight 32-column chunks of each M-block are
-    // dealt round-robin with a rotating start so the three warps stay balanced. =======
-    const int ew = warp - kEpiWarp0;
-    const int quad = warp & 3;
-    const int sub = ew >> 2;
-    const int row = quad * 32 + lane;
-    HitCtx h;
-    h.qm_s = su32(smem + a.off_qm);
-    h.a_s = su32(sA);
-    h.qg_s = su32(smem + a.off_qg);
-    h.t_s = su32(sT);
-    h.hit_s = su32(smem + a.off_hit) + (uint32_t)ew * (kHitCap * 2u);
-    h.sv_s = su32(smem + a.off_hit) + (uint32_t)(NE * kHitCap * 2) + (uint32_t)ew * (kSurvCap * 2u);
-    // per query row of this thread: clamped score gate (the accumulators start at -tau)
-    int32_t tau[kMaxMBlocks];
-#pragma unroll
-    for (int mb = 0; mb < kMaxMBlocks; ++mb) tau[mb] = gate_tau(sT, mb * kBlockM + row, a.nq);
-    PendingEmit pd;
-    pd.q = -1;
-    pd.p = 0;
-    pd.key = 0;
-    pd.slot = 0;
-    int it = 0, acc_it = 0, s = 0;
-    uint32_t iph = 0;
-    for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
-      // per-tile metadata staged by the producer with the item stage
-      mbar_wait(items_full + s, iph);
-      const uint32_t mst = su32(smem + a.off_id) + (uint32_t)s * kStageMeta;
-      h.tile = (int64_t)lds32(mst + kMetaTile);
-      // lane c < 8 holds the validity & range bits of the tile's chunk c (32 items)
-      const uint32_t vchunk = lane < 8 ? lds32(mst + kMetaValid + 4u * lane) : 0u;
-      h.b_s = su32(sB + (size_t)s * kItemBytes);
-      h.id_s = mst;
-      const int st = it & 1;
-      mbar_wait(leaf_full + st, (uint32_t)(it >> 1) & 1u);
-      h.tb_s = su32(sL + (size_t)st * a.leaf_stage_bytes);
-      uint32_t head = 0, tail = 0, sv_head = 0, sv_tail = 0;  // warp-uniform ring cursors
-#pragma unroll 1
-      for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
-        const int q = mb * kBlockM + row;
-        const bool qok = q < a.nq;
-        const int32_t tq = mb == 0 ? tau[0] : tau[kMaxMBlocks - 1];
-        const int ab = acc_it & 1;
-        mbar_wait(acc_full + ab, (uint32_t)(acc_it >> 1) & 1u);
-        tc_fence_after();
-        const uint32_t taddr =
-            tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kAccCols);
-        const uint32_t ebase = ((uint32_t)mb << 15) | ((uint32_t)row << 8);
-        const int c0 = (sub + mb + it) % 3;
-        int32_t r[32];
-        tmem_ld32_async(taddr + (uint32_t)(c0 * 32), r);
-#pragma unroll 1
-        for (int c = c0; c < 8; c += 3) {
-          tmem_wait32(r);
-          tmem_st32_const(taddr + (uint32_t)(c * 32), -tq);  // re-arm for the buffer's next use
-          if (a.dump != nullptr && qok) {
-            const int64_t base = h.tile * kTileItems + c * 32;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (base + j < a.dump_ld) a.dump[(int64_t)q * a.dump_ld + base + j] = r[j] + tq;
-          }
-          uint32_t em = __shfl_sync(0xffffffffu, vchunk, c);
-          if (!qok) em = 0u;
-          if (a.masks != nullptr && em != 0u)
-            em &= (uint32_t)(__ldg(a.masks + (int64_t)q * a.n_words + h.tile * kTileWords +
-                                   (c >> 1)) >>
-                             (32 * (c & 1)));
-          uint32_t hm = nonneg_mask32(r) & em;
-          if (c + 3 < 8) {
-            tmem_ld32_async(taddr + (uint32_t)((c + 3) * 32), r);  // overlaps the hit handling
-          } else {
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc_empty + ab);
-          }
-          // append this chunk's hits to the warp's ring, up to two per lane per round
-          const uint32_t eb = ebase | (uint32_t)(c * 32);
-          while (true) {
-            const uint32_t b1 = __ballot_sync(0xffffffffu, hm != 0u);
-            if (b1 == 0u) break;
-            const uint32_t rest = hm & (hm - 1u);
-            const uint32_t b2 = __ballot_sync(0xffffffffu, rest != 0u);
-            if (hm != 0u) {
-              const uint32_t lt = lanemask_lt();
-              const uint32_t pos = tail + (uint32_t)(__popc(b1 & lt) + __popc(b2 & lt));
-              sts16(h.hit_s + (pos & (kHitCap - 1)) * 2u, eb + (uint32_t)(__ffs(hm) - 1));
-              if (rest != 0u)
-                sts16(h.hit_s + ((pos + 1u) & (kHitCap - 1)) * 2u,
-                      eb + (uint32_t)(__ffs(rest) - 1));
-            }
-            hm = rest & (rest - 1u);
-            tail += (uint32_t)(__popc(b1) + __popc(b2));
-            while (tail - head >= 32u) {
-              __syncwarp();
-              filter_hits(a, h, head, 32u, sv_head, sv_tail, pd, lane);
-            }
-          }
-        }
-      }
-      // drain: remaining hits, then the survivors (they read the item and id stages)
-      if (tail != head) {
-        __syncwarp();
-        filter_hits(a, h, head, tail - head, sv_head, sv_tail, pd, lane);
-      }
-      while (sv_tail != sv_head) {
-        __syncwarp();
-        emit_survivors(a, h, sv_head, sv_tail, pd, lane);
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(leaf_empty + st);
-        mbar_arrive(items_empty + s);
-      }
-      if (++s == a.item_stages) {
-        s = 0;
-        iph ^= 1u;
-      }
-    }
-    flush_pending(a, pd);
   } else {
     // ================= epilogue: filter (eager) + TMEM scores + gate + emit ========
     const int ew = warp - kEpiWarp0;
@@ -1126,6 +1009,377 @@ __global__ void __launch_bounds__(kCnf ? kThreadsCnf : kThreads, 1)
                  : "memory");
 }
 
+// ======================================================================================
+// CNF scan kernel (every program an AND of OR-groups of literals). Twenty warps:
+//   warp 0       producer (TMA item rows, cp.async plane gather, per-tile metadata)
+//   warp 1       MMA: per M-block the gate-arming K=32 MMA, then 4 K-steps of kind::i8
+//   warps 2-3    column builders: per literal column the AND of its planes, transposed so
+//                each item row holds its column bits (the paper's and.b64 Bloom test)
+//   warps 4-11   dense pass, two per TMEM lane quadrant: tcgen05.ld 32 columns, the hit
+//                mask is the accumulators' sign bits (armed at +127 D), & validity/range;
+//                32-bit hit masks go to a double-buffered [chunk][query] map in smem and
+//                the accumulator is released at once
+//   warps 12-19  hit pass, lane = query: walks its hit bits, tests the CNF filter against
+//                the item's column bits (window form: 4 groups x one u32 pair, masks in
+//                registers), queues survivors per warp; survivors get their exact score
+//                from the resident smem tiles (dp4a), the exact key test and an atomic
+//                slot reservation -- filtered-out items never leave the SM.
+// ======================================================================================
+constexpr int kCnfThreads = 640;
+constexpr int kCnfBuilders = 2;
+constexpr int kCnfDense0 = 4;
+constexpr int kCnfDenseWarps = 8;
+constexpr int kCnfHit0 = 12;
+constexpr int kCnfHitWarps = 8;
+constexpr int kSurvCap = 64;  // u16 survivor entries per hit warp: (lane << 8) | item
+constexpr uint32_t kHmapBytes = 8u * kMaxQueries * 4u;  // [chunk][query] u32
+
+// Exact int32 dot of a query row (A tile) and an item row (B stage) from shared memory.
+// Both tiles use the SWIZZLE_128B layout: 16-byte chunk c of row r sits at c ^ (r & 7).
+__device__ __forceinline__ int32_t smem_dot(uint32_t a_row, uint32_t a_sw, uint32_t b_row,
+                                            uint32_t b_sw) {
+  int32_t acc0 = 0, acc1 = 0;
+#pragma unroll
+  for (uint32_t c = 0; c < 8; c += 2) {
+    const uint4 x0 = lds128(a_row + ((c ^ a_sw) << 4));
+    const uint4 y0 = lds128(b_row + ((c ^ b_sw) << 4));
+    const uint4 x1 = lds128(a_row + (((c + 1) ^ a_sw) << 4));
+    const uint4 y1 = lds128(b_row + (((c + 1) ^ b_sw) << 4));
+    acc0 = __dp4a((int)x0.x, (int)y0.x, acc0);
+    acc1 = __dp4a((int)x1.x, (int)y1.x, acc1);
+    acc0 = __dp4a((int)x0.y, (int)y0.y, acc0);
+    acc1 = __dp4a((int)x1.y, (int)y1.y, acc1);
+    acc0 = __dp4a((int)x0.z, (int)y0.z, acc0);
+    acc1 = __dp4a((int)x1.z, (int)y1.z, acc1);
+    acc0 = __dp4a((int)x0.w, (int)y0.w, acc0);
+    acc1 = __dp4a((int)x1.w, (int)y1.w, acc1);
+  }
+  return acc0 + acc1;
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t v;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(v));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// General-form filter test: masks read (L1-cached) from the batch's qmask rows.
+__device__ __forceinline__ bool cnf_test_global(uint32_t tb_addr, const uint32_t* qm, int ng,
+                                                int words) {
+  const uint4 t0 = lds128(tb_addr);
+  const uint4 t1 = lds128(tb_addr + 16u);
+  const uint32_t t[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+  bool pass = true;
+  for (int g = 0; g < ng && pass; ++g) {
+    uint32_t x = 0u;
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
+      if (w < words) x |= t[w] & __ldg(qm + g * words + w);
+    pass = x != 0u;
+  }
+  return pass;
+}
+
+// Survivors queued by one hit warp: exact score from the smem tiles, exact key test against
+// the query's threshold, slot reservation (the stores trail by two emissions per lane).
+struct EmitState {
+  PendingEmit pa, pb;
+  bool par;
+};
+__device__ __forceinline__ void emit_one(const TcArgs& a, EmitState& e, int q, uint64_t key,
+                                         uint32_t slot) {
+  if (e.par) {
+    flush_pending(a, e.pa);
+    e.pa.p = atomicAdd(a.out_cnt + q, 1u);
+    e.pa.key = key;
+    e.pa.slot = slot;
+    e.pa.q = q;
+  } else {
+    flush_pending(a, e.pb);
+    e.pb.p = atomicAdd(a.out_cnt + q, 1u);
+    e.pb.key = key;
+    e.pb.slot = slot;
+    e.pb.q = q;
+  }
+  e.par = !e.par;
+}
+__device__ __forceinline__ void drain_survivors(const TcArgs& a, const Smem& m, EmitState& e,
+                                                uint32_t sv_s, uint32_t n, int qbase,
+                                                uint32_t b_s, uint32_t mst, int64_t tile,
+                                                int lane) {
+  for (uint32_t i = (uint32_t)lane; i < n; i += 32u) {
+    const uint32_t ent = lds16(sv_s + 2u * i);
+    const int q = qbase + (int)(ent >> 8);
+    const uint32_t item = ent & 255u;
+    const int32_t score = smem_dot(su32(m.sA) + (uint32_t)q * kKBytes, (uint32_t)q & 7u,
+                                   b_s + item * kKBytes, item & 7u);
+    const uint64_t key = make_key(score, lds32(mst + 4u * item));
+    if (key >= m.sT[q]) emit_one(a, e, q, key, (uint32_t)(tile * kTileItems) + item);
+  }
+}
+
+template <bool kWin>
+__global__ void __launch_bounds__(kCnfThreads, 1)
+    k_scan_cnf(const __grid_constant__ CUtensorMap tmap_items, const TcArgs a) {
+  constexpr int NT = kCnfThreads;
+  const Smem m = carve(a);
+  uint8_t* smem = m.base;
+  uint64_t* bars = m.bars;
+  uint64_t* items_full = bars + kBarItemsFull;
+  uint64_t* items_empty = bars + kBarItemsEmpty;
+  uint64_t* planes_full = bars + kBarPlanesFull;
+  uint64_t* planes_empty = bars + kBarPlanesEmpty;
+  uint64_t* leaf_full = bars + kBarLeafFull;
+  uint64_t* leaf_empty = bars + kBarLeafEmpty;
+  uint64_t* acc_full = bars + kBarAccFull;
+  uint64_t* acc_empty = bars + kBarAccEmpty;
+  uint64_t* hm_full = bars + kBarHmFull;
+  uint64_t* hm_empty = bars + kBarHmEmpty;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kBarTmemSlot);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_sel = a.n_sel;
+
+  // ---- prologue: queries, thresholds, column table, zeroed column-bit stages, gate tiles
+  stage_queries(a, m, NT);
+  for (int i = threadIdx.x; i < a.n_cols * a.k_max; i += NT) {
+    // column -> plane-slot table (negated columns flagged by bit 14 on slot 0)
+    const int c = i / a.k_max, j = i - c * a.k_max;
+    const int cl = a.col_leaf[c];
+    const int leaf = cl >= 0 ? cl : ~cl;
+    int s = a.leaf_slot[leaf * a.k_max + j];
+    if (j == 0 && cl < 0) s |= 0x4000;
+    m.sLS[i] = (int16_t)s;
+  }
+  {
+    uint32_t* tb = reinterpret_cast<uint32_t*>(m.sL);
+    for (int i = threadIdx.x; i < 2 * (int)(a.leaf_stage_bytes / 4); i += NT) tb[i] = 0u;
+    uint8_t* gA = smem + a.off_gate;
+    uint32_t* gB = reinterpret_cast<uint32_t*>(smem + a.off_gate + kGateTileBytes);
+    for (int i = threadIdx.x; i < 64; i += NT) gB[i] = 0x7F7F7F7Fu;  // 256 B of 127s
+    for (int r = threadIdx.x; r < kMaxQueries; r += NT) {
+      bool all;
+      const uint64_t T = (a.threshold != nullptr && r < a.nq) ? a.threshold[r] : 0ull;
+      const int32_t D = r < a.nq ? gate_digits(T, all) : kGateDigitsMin;
+      const int32_t base = D >= 0 ? D / 32 : -((-D + 31) / 32);  // floor(D / 32)
+      const int32_t rem = D - 32 * base;                        // 0..31
+      for (int k = 0; k < 32; ++k)
+        gA[gate_off(r, k)] = (uint8_t)(int8_t)(base + (k < rem ? 1 : 0));
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(items_full + s, 1 + 32 + 1);          // TMA expect-tx, id ranks, meta
+      mbar_init(items_empty + s, 1 + kCnfHitWarps);   // MMA commit + hit warps
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(planes_full + s, 32);
+      mbar_init(planes_empty + s, kCnfBuilders);
+      mbar_init(leaf_full + s, kCnfBuilders);
+      mbar_init(leaf_empty + s, kCnfHitWarps);
+      mbar_init(acc_full + s, 1);
+      mbar_init(acc_empty + s, kCnfDenseWarps);
+      mbar_init(hm_full + s, kCnfDenseWarps);
+      mbar_init(hm_empty + s, kCnfHitWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc512(m);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t hm_s = su32(smem + a.off_hm);
+
+  if (warp == 0) {
+    producer_loop(a, &tmap_items, m, lane);
+  } else if (warp == 1) {
+    if (lane == 0) mma_loop<true>(a, m, tmem_base);
+  } else if (warp < kCnfDense0) {
+    cnf_builder_loop(a, m, warp - 2, kCnfBuilders, lane);
+  } else if (warp < kCnfHit0) {
+    // ================= dense pass ====================================================
+    const int quad = warp & 3;
+    const int sub = (warp - kCnfDense0) >> 2;  // chunks sub, sub + 2, sub + 4, sub + 6
+    const int row = quad * 32 + lane;
+    int it = 0, acc_it = 0, s = 0;
+    uint32_t iph = 0;
+    for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
+      mbar_wait(items_full + s, iph);
+      const uint32_t mst = su32(smem + a.off_id) + (uint32_t)s * kStageMeta;
+      const int64_t tile = (int64_t)lds32(mst + kMetaTile);
+      // lane c < 8 holds the validity & range bits of the tile's chunk c (32 items)
+      const uint32_t vchunk = lane < 8 ? lds32(mst + kMetaValid + 4u * lane) : 0u;
+      const int hb = it & 1;
+      mbar_wait(hm_empty + hb, ((uint32_t)(it >> 1) & 1u) ^ 1u);
+      const uint32_t hmap = hm_s + (uint32_t)hb * kHmapBytes;
+#pragma unroll 1
+      for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
+        const int q = mb * kBlockM + row;
+        const bool qok = q < a.nq;
+        bool all;
+        const int32_t D = gate_digits(qok ? m.sT[q] : ~0ull, all);
+        const uint32_t allmask = all ? ~0u : 0u;
+        const int ab = acc_it & 1;
+        mbar_wait(acc_full + ab, (uint32_t)(acc_it >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kAccCols);
+        int32_t r[32];
+        tmem_ld32_async(taddr + (uint32_t)(sub * 32), r);
+#pragma unroll 1
+        for (int c = sub; c < 8; c += 2) {
+          tmem_wait32(r);
+          uint32_t em = __shfl_sync(0xffffffffu, vchunk, c);
+          if (!qok) em = 0u;
+          if (a.masks != nullptr && em != 0u)
+            em &= (uint32_t)(__ldg(a.masks + (int64_t)q * a.n_words + tile * kTileWords +
+                                   (c >> 1)) >>
+                             (32 * (c & 1)));
+          if (a.dump != nullptr && qok) {
+            const int64_t base = tile * kTileItems + c * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (base + j < a.dump_ld)
+                a.dump[(int64_t)q * a.dump_ld + base + j] = r[j] - 127 * D;
+          }
+          const uint32_t hm = (nonneg_mask32(r) | allmask) & em;
+          if (c + 2 < 8) tmem_ld32_async(taddr + (uint32_t)((c + 2) * 32), r);
+          sts32(hmap + (uint32_t)(c * kMaxQueries + q) * 4u, hm);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + ab);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(hm_full + hb);
+      if (++s == a.item_stages) {
+        s = 0;
+        iph ^= 1u;
+      }
+    }
+  } else {
+    // ================= hit pass (lane = query) =========================================
+    const int qbase = (warp - kCnfHit0) * 32;
+    const int q = qbase + lane;
+    const bool qok = q < a.nq;
+    const uint64_t T = qok ? m.sT[q] : ~0ull;
+    const int ng = qok ? a.qgroups[q] : 0;
+    const bool nof = ng == 0;
+    // window form: per group (byte offset of its u32 pair in an item row, 64-bit mask);
+    // unused groups repeat group 0 (AND is idempotent)
+    uint32_t wo[4] = {0u, 0u, 0u, 0u}, lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
+    const uint32_t* qmg = a.qmask + (int64_t)(qok ? q : 0) * a.cnf_gmax * a.cnf_words;
+    if (kWin && !nof) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const uint32_t* mg = qmg + (g < ng ? g : 0) * a.cnf_words;
+        int w0 = 0;
+        while (w0 < a.cnf_words - 1 && mg[w0] == 0u) ++w0;
+        w0 &= ~1;
+        wo[g] = 4u * (uint32_t)w0;
+        lo[g] = mg[w0];
+        hi[g] = w0 + 1 < a.cnf_words ? mg[w0 + 1] : 0u;
+      }
+    }
+    const uint32_t sv_s = su32(smem + a.off_sv) + (uint32_t)(warp - kCnfHit0) * (kSurvCap * 2u);
+    EmitState e;
+    e.pa.q = e.pb.q = -1;
+    e.pa.p = e.pb.p = 0u;
+    e.pa.key = e.pb.key = 0ull;
+    e.pa.slot = e.pb.slot = 0u;
+    e.par = false;
+    int it = 0, s = 0;
+    uint32_t iph = 0;
+    for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
+      mbar_wait(items_full + s, iph);
+      const uint32_t mst = su32(smem + a.off_id) + (uint32_t)s * kStageMeta;
+      const int64_t tile = (int64_t)lds32(mst + kMetaTile);
+      const uint32_t b_s = su32(m.sB + (size_t)s * kItemBytes);
+      const int st = it & 1;
+      mbar_wait(leaf_full + st, (uint32_t)(it >> 1) & 1u);
+      const uint32_t tb_s = su32(m.sL + (size_t)st * a.leaf_stage_bytes);
+      const int hb = it & 1;
+      mbar_wait(hm_full + hb, (uint32_t)(it >> 1) & 1u);
+      const uint32_t hmap = hm_s + (uint32_t)hb * kHmapBytes + 4u * (uint32_t)q;
+      // this query's nonzero chunk words
+      uint32_t nzm = 0u;
+      if (qok) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          nzm |= (lds32(hmap + (uint32_t)c * (kMaxQueries * 4u)) != 0u ? 1u : 0u) << c;
+      }
+      int cc = nzm ? __ffs(nzm) - 1 : 0;
+      uint32_t cur = nzm ? lds32(hmap + (uint32_t)cc * (kMaxQueries * 4u)) : 0u;
+      uint32_t n_sv = 0;  // warp-uniform survivor count
+      while (__any_sync(0xffffffffu, cur != 0u)) {
+        bool surv = false;
+        uint32_t item = 0;
+        if (cur != 0u) {
+          const int j = __ffs(cur) - 1;
+          cur &= cur - 1u;
+          item = (uint32_t)(cc * 32 + j);
+          const uint32_t tb = tb_s + item * (uint32_t)a.tb_stride * 4u;
+          if (kWin)
+            surv = nof || cnf_test_win(tb, wo, lo, hi);
+          else
+            surv = cnf_test_global(tb, qmg, ng, a.cnf_words);
+          if (cur == 0u) {
+            nzm &= nzm - 1u;
+            if (nzm) {
+              cc = __ffs(nzm) - 1;
+              cur = lds32(hmap + (uint32_t)cc * (kMaxQueries * 4u));
+            }
+          }
+        }
+        const uint32_t sb = __ballot_sync(0xffffffffu, surv);
+        if (surv)
+          sts16(sv_s + 2u * (n_sv + (uint32_t)__popc(sb & lanemask_lt())),
+                ((uint32_t)lane << 8) | item);
+        n_sv += (uint32_t)__popc(sb);
+        if (n_sv > (uint32_t)(kSurvCap - 32)) {
+          __syncwarp();
+          drain_survivors(a, m, e, sv_s, n_sv, qbase, b_s, mst, tile, lane);
+          __syncwarp();
+          n_sv = 0;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(hm_empty + hb);
+      if (n_sv) drain_survivors(a, m, e, sv_s, n_sv, qbase, b_s, mst, tile, lane);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(leaf_empty + st);
+        mbar_arrive(items_empty + s);
+      }
+      if (++s == a.item_stages) {
+        s = 0;
+        iph ^= 1u;
+      }
+    }
+    flush_pending(a, e.pa);
+    flush_pending(a, e.pb);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512)
+                 : "memory");
+}
+
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (fn == nullptr) {
@@ -1141,12 +1395,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// shared-memory carve-up; returns total bytes (incl. 1 KB alignment slack)
-// Shared-memory carve-up; returns total bytes (incl. 1 KB alignment slack). In CNF mode
-// the per-tile stage holds transposed column bits (256 items x kTbStride u32), the query
-// group masks and group counts are staged, and each epilogue warp gets a hit ring buffer.
+// Shared-memory carve-up; returns total bytes (incl. 1 KB alignment slack). Bytecode mode:
+// per-tile leaf masks and the staged register-machine programs. CNF mode: per-tile column
+// bits (256 items x tb_stride u32), two [chunk][query] hit maps, the gate tiles (8 KB of
+// digits + 256 B of 127s) and the hit warps' survivor lists.
 size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int stages,
-              int plane_stages, bool cnf) {
+              int plane_stages, int mode) {
+  const bool cnf = mode != 0;
   size_t off = 0;
   t.off_a = 0;
   off = (size_t)n_mblk * kBlockM * kKBytes;
@@ -1156,7 +1411,7 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
   t.off_p = (uint32_t)align_up(off, 128);
   off = t.off_p + (size_t)plane_stages * t.plane_stage_bytes;
   t.leaf_stage_bytes =
-      cnf ? (uint32_t)(kTileItems * kTbStride * 4)
+      cnf ? (uint32_t)(kTileItems * t.tb_stride * 4)
           : (uint32_t)align_up((size_t)(n_leaves > 0 ? n_leaves : 1) * kLeafStride * 8, 128);
   t.off_l = (uint32_t)align_up(off, 128);
   off = t.off_l + 2ull * t.leaf_stage_bytes;
@@ -1166,14 +1421,14 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
   t.off_thr = (uint32_t)align_up(off, 16);
   off = t.off_thr + (size_t)kMaxQueries * 8;
   t.off_bar = (uint32_t)align_up(off, 16);
-  off = t.off_bar + 21 * 8 + 16;
+  off = t.off_bar + kBarCount * 8;
   if (cnf) {
-    t.off_qm = (uint32_t)align_up(off, 16);
-    off = t.off_qm + (size_t)kMaxQueries * t.cnf_gmax * t.qm_stride * 4;
-    t.off_qg = (uint32_t)align_up(off, 16);
-    off = t.off_qg + (size_t)kMaxQueries * 4;
-    t.off_hit = (uint32_t)align_up(off, 16);
-    off = t.off_hit + (size_t)kEpiWarpsCnf * (kHitCap + kSurvCap) * 2;
+    t.off_hm = (uint32_t)align_up(off, 128);
+    off = t.off_hm + 2ull * kHmapBytes;
+    t.off_gate = (uint32_t)align_up(off, 128);
+    off = t.off_gate + kGateTileBytes + 256;
+    t.off_sv = (uint32_t)align_up(off, 16);
+    off = t.off_sv + (size_t)kCnfHitWarps * kSurvCap * 2;
   }
   t.off_id = (uint32_t)align_up(off, 16);
   off = t.off_id + (size_t)stages * kStageMeta;
@@ -1187,7 +1442,7 @@ constexpr int kMaxStagedOps = 16384;  // 32 KB; whatever is left stays L1
 
 // Prefer 3 item stages and 2 plane stages; stage as much filter bytecode as fits.
 bool pick_stages(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int n_rops,
-                 bool cnf, size_t& smem) {
+                 int cnf, size_t& smem) {
   const int prefs[4][2] = {{3, 2}, {3, 1}, {2, 2}, {2, 1}};
   if (cnf) n_rops = 0;  // the CNF epilogue does not read the bytecode
   // first pass: the configuration that also holds all filter bytecode; second: any
@@ -1209,23 +1464,39 @@ bool pick_stages(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, i
   return false;
 }
 
-bool use_cnf(const ScanArgs& a) {
+// 0: bytecode epilogue; 1: CNF fast form; 2: CNF general form
+int cnf_mode(const ScanArgs& a) {
   // at threshold 0 every score is a hit: the word-level bytecode epilogue is cheaper than
   // per-hit tests, so the sampling pass takes it whenever the bytecode fits the kernel
-  if (a.dense && a.prog.rops != nullptr && a.prog.rmax_stack <= kRegStack) return false;
-  return a.has_prog && a.prog.col_leaf != nullptr && a.prog.cnf_words >= 1 &&
-         a.prog.cnf_words <= 8 && a.prog.cnf_gmax >= 1 && a.prog.cnf_gmax <= 8 &&
-         a.prog.n_cols <= 32 * a.prog.cnf_words;
+  if (a.dense && a.prog.rops != nullptr && a.prog.rmax_stack <= kRegStack) return 0;
+  const bool cnf = a.has_prog && a.prog.col_leaf != nullptr && a.prog.cnf_words >= 1 &&
+                   a.prog.cnf_words <= 8 && a.prog.cnf_gmax >= 1 && a.prog.cnf_gmax <= 8 &&
+                   a.prog.n_cols <= 32 * a.prog.cnf_words;
+  if (!cnf) return 0;
+  return (a.prog.cnf_windowed && a.prog.cnf_gmax <= 4) ? 1 : 2;
 }
 
-void fill_cnf(TcArgs& t, const ScanArgs& a, int q0) {
+void fill_cnf(TcArgs& t, const ScanArgs& a, int q0, int mode) {
   t.n_cols = a.prog.n_cols;
   t.cnf_words = a.prog.cnf_words;
   t.cnf_gmax = a.prog.cnf_gmax;
-  t.qm_stride = a.prog.cnf_words <= 4 ? 4 : 8;
+  // window form: rows of an odd number of u64 (conflict-free 8-byte loads at random
+  // items), at least the column words rounded up to a pair; general form: 32-byte rows
+  int u64s = (a.prog.cnf_words + 1) / 2;
+  if (u64s % 2 == 0) ++u64s;
+  t.tb_stride = mode == 1 ? 2 * u64s : 8;
   t.col_leaf = a.prog.col_leaf;
   t.qmask = a.prog.qmask + (int64_t)q0 * a.prog.cnf_gmax * a.prog.cnf_words;
   t.qgroups = a.prog.qgroups + q0;
+}
+
+template <typename K>
+int launch_kernel(K kernel, int threads, const CUtensorMap& tmap, const TcArgs& t, int grid,
+                  size_t smem, cudaStream_t s) {
+  FB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kernel<<<grid, threads, smem, s>>>(tmap, t);
+  FB_LAUNCH_CHECK("k_scan_tc");
+  return FB_OK;
 }
 
 }  // namespace
@@ -1236,11 +1507,11 @@ bool scan_tc_supported(const ScanArgs& a) {
   if (a.idx.n_slots % kTileItems != 0 || a.tc_work == nullptr) return false;
   if (encode_fn() == nullptr) return false;
   if (a.has_prog) {
-    const bool cnf = use_cnf(a);
+    const int cnf = cnf_mode(a);
     if (!cnf && (a.prog.rops == nullptr || a.prog.rmax_stack > kRegStack)) return false;
     if (a.prog.n_leaves >= (1 << 13) || a.prog.plane_list == nullptr) return false;
     TcArgs t{};
-    if (cnf) fill_cnf(t, a, 0);
+    if (cnf) fill_cnf(t, a, 0, cnf);
     size_t smem = 0;
     const int n_mblk = a.n_queries >= kBlockM ? kMaxMBlocks : 1;
     if (!pick_stages(t, n_mblk, a.prog.n_planes, a.prog.n_leaves, a.prog.k_max, 0, cnf, smem))
@@ -1266,7 +1537,7 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
   int n_sm = 148;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
   const int grid = (int)(n_sel < n_sm ? n_sel : n_sm);
-  const bool cnf = use_cnf(a);
+  const int cnf = cnf_mode(a);
   for (int q0 = 0; q0 < a.n_queries; q0 += kMaxQueries) {
     const int nq = a.n_queries - q0 < kMaxQueries ? a.n_queries - q0 : kMaxQueries;
     TcArgs t{};
@@ -1287,7 +1558,7 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
       t.leaf_slot = a.prog.leaf_slot;
       t.rop_offset = a.prog.rop_offset + q0;
       t.rops = a.prog.rops;
-      if (cnf) fill_cnf(t, a, q0);
+      if (cnf) fill_cnf(t, a, q0, cnf);
     }
     t.work = reinterpret_cast<const int2*>(a.tc_work);
     t.n_sel = n_sel;
@@ -1304,16 +1575,11 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
     if (!pick_stages(t, t.n_mblk, t.has_prog ? t.n_planes : 0, t.has_prog ? t.n_leaves : 0,
                      t.has_prog ? t.k_max : 0, t.has_prog ? a.prog.n_rops : 0, cnf, smem))
       return FB_ERR_UNSUPPORTED;
-    if (cnf) {
-      FB_CUDA(cudaFuncSetAttribute(k_scan_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-      k_scan_tc<true><<<grid, kThreadsCnf, smem, s>>>(tmap, t);
-    } else {
-      FB_CUDA(cudaFuncSetAttribute(k_scan_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-      k_scan_tc<false><<<grid, kThreads, smem, s>>>(tmap, t);
-    }
-    FB_LAUNCH_CHECK("k_scan_tc");
+    const int rc =
+        cnf == 1   ? launch_kernel(k_scan_cnf<true>, kCnfThreads, tmap, t, grid, smem, s)
+        : cnf == 2 ? launch_kernel(k_scan_cnf<false>, kCnfThreads, tmap, t, grid, smem, s)
+                   : launch_kernel(k_scan_tc, kThreads, tmap, t, grid, smem, s);
+    if (rc) return rc;
   }
   return FB_OK;
 }

@@ -350,6 +350,59 @@ def cnf_groups(ops: list[tuple[int, int]]):
     return None if g is None else [g]
 
 
+def _pack_cnf(cnf, leaf_fid):
+    """CNF column layout of a batch. Literals (leaf, negated) become columns; columns are
+    grouped by feature id and the features bin-packed (first fit, decreasing) into 64-column
+    windows, so a group whose literals share a feature -- the usual ``f in S`` group --
+    tests one aligned u32 pair of the item's column bits. Falls back to first-seen order when
+    the windows would need more than CNF_MAX_WORDS words. Returns the FilterBatch kwargs, or
+    {} when the batch does not fit the CNF limits."""
+    lits: dict[tuple[int, bool], int] = {}
+    for groups in cnf:
+        for g in groups:
+            for lit in g:
+                lits.setdefault(lit, len(lits))
+    gmax = max(len(groups) for groups in cnf)
+    if gmax > CNF_MAX_GROUPS:
+        return {}
+    by_fid: dict[int, list] = {}
+    for lit in lits:
+        by_fid.setdefault(leaf_fid[lit[0]], []).append(lit)
+    bins: list[list] = []
+    if all(len(v) <= 64 for v in by_fid.values()):
+        for fid in sorted(by_fid, key=lambda f: (-len(by_fid[f]), f)):
+            for b in bins:
+                if len(b) + len(by_fid[fid]) <= 64:
+                    b.extend(by_fid[fid])
+                    break
+            else:
+                bins.append(list(by_fid[fid]))
+    if bins and 2 * len(bins) <= CNF_MAX_WORDS:
+        cols = {lit: 64 * bi + i for bi, b in enumerate(bins) for i, lit in enumerate(b)}
+        n_cols = 64 * (len(bins) - 1) + len(bins[-1])
+    else:
+        cols, n_cols = dict(lits), len(lits)
+    words = (n_cols + 31) // 32
+    if words > CNF_MAX_WORDS:
+        return {}
+    qmask = np.zeros((len(cnf), gmax, words), dtype=np.uint32)
+    for q, groups in enumerate(cnf):
+        for gi, g in enumerate(groups):
+            for lit in g:
+                c = cols[lit]
+                qmask[q, gi, c >> 5] |= np.uint32(1 << (c & 31))
+    col_leaf = np.zeros(n_cols, dtype=np.int16)  # padding columns: leaf 0, never referenced
+    for (leaf, neg), c in cols.items():
+        col_leaf[c] = ~leaf if neg else leaf
+    nz = qmask != 0
+    first = np.where(nz.any(axis=2), nz.argmax(axis=2), 0)
+    last = np.where(nz.any(axis=2), words - 1 - nz[:, :, ::-1].argmax(axis=2), 0)
+    windowed = int(gmax <= 4 and bool(np.all((first >> 1) == (last >> 1))))
+    return dict(col_leaf=col_leaf, qmask=qmask,
+                qgroups=np.array([len(g) for g in cnf], dtype=np.int32),
+                cnf_words=words, cnf_gmax=gmax, cnf_windowed=windowed)
+
+
 class FilterBatch:
     """Device bytecode for a batch of compiled filters (one per query, ``None`` =
     unfiltered), mirroring ``fb_filter_prog_t`` (include/filtra_b200.h):
@@ -364,7 +417,7 @@ class FilterBatch:
     def __init__(self, leaf_pos, op_offset, ops, max_stack, push_leaf_bits, *,
                  plane_list=None, leaf_slot=None, rop_offset=None, rops=None, rmax_stack=0,
                  col_leaf=None, qmask=None, qgroups=None, cnf_words=0, cnf_gmax=0,
-                 cnf_lits_max=0):
+                 cnf_windowed=0):
         self.n_queries = len(op_offset) - 1
         self.n_leaves = leaf_pos.shape[0]
         self.k_max = leaf_pos.shape[1]
@@ -389,8 +442,9 @@ class FilterBatch:
                              if qgroups is not None else None)
         self.cnf_words = cnf_words
         self.cnf_gmax = cnf_gmax
-        # longest per-query literal stream with every group padded to 4 literals
-        self.cnf_lits_max = cnf_lits_max
+        # 1 when every group's columns lie in one 64-column window (u32 words 2j, 2j+1) and
+        # no query has more than 4 groups: the scan's register-resident filter test
+        self.cnf_windowed = cnf_windowed
         # per query: sum over PUSH_LEAF ops of |set_bits| (FilterStats.words_read per word)
         self.push_leaf_bits = push_leaf_bits
         self._dev = None
@@ -437,6 +491,7 @@ class FilterBatch:
             raise NotImplementedError("device filter evaluation supports m_bits <= 32767")
         glob: dict[tuple[int, int], int] = {}
         leaf_rows: list[tuple[int, ...]] = []
+        leaf_fid: list[int] = []
         ops: list[int] = []
         offsets = [0]
         rops: list[int] = []
@@ -455,6 +510,7 @@ class FilterBatch:
                     if g is None:
                         g = glob[key] = len(leaf_rows)
                         leaf_rows.append(tuple(qb.set_bits))
+                        leaf_fid.append(int(fid))
                     local.append(g)
                 gops = []
                 for op, arg in cf.ops:
@@ -494,28 +550,7 @@ class FilterBatch:
         reg = len(leaf_rows) <= ROP_MAX_LEAVES
         cnf_kw = {}
         if reg and cnf is not None and any(cnf):
-            cols: dict[tuple[int, bool], int] = {}
-            for groups in cnf:
-                for g in groups:
-                    for lit in g:
-                        cols.setdefault(lit, len(cols))
-            words = (len(cols) + 31) // 32
-            gmax = max(len(groups) for groups in cnf)
-            if words <= CNF_MAX_WORDS and gmax <= CNF_MAX_GROUPS:
-                qmask = np.zeros((len(cnf), gmax, words), dtype=np.uint32)
-                for q, groups in enumerate(cnf):
-                    for gi, g in enumerate(groups):
-                        for lit in g:
-                            c = cols[lit]
-                            qmask[q, gi, c >> 5] |= np.uint32(1 << (c & 31))
-                col_leaf = np.array([(~leaf if neg else leaf) for (leaf, neg) in cols],
-                                    dtype=np.int16)
-                pops = np.unpackbits(qmask.view(np.uint8), axis=-1).reshape(
-                    len(cnf), gmax, -1).sum(axis=-1)
-                lits_max = int(((pops + 3) // 4 * 4).sum(axis=1).max()) if len(cnf) else 0
-                cnf_kw = dict(col_leaf=col_leaf, qmask=qmask,
-                              qgroups=np.array([len(g) for g in cnf], dtype=np.int32),
-                              cnf_words=words, cnf_gmax=gmax, cnf_lits_max=lits_max)
+            cnf_kw = _pack_cnf(cnf, leaf_fid)
         return cls(leaf_pos, np.array(offsets, dtype=np.int32),
                    np.array(ops if ops else [0], dtype=np.uint16), max_stack,
                    np.array(push_bits, dtype=np.int64),
@@ -541,7 +576,7 @@ class FilterBatch:
             extra = (0, 0, 0, 0, None, None, None, None)
         if self.is_cnf:
             cnf = (int(self.host_col_leaf.size), self.cnf_words, self.cnf_gmax,
-                   self.cnf_lits_max, d[7].data_ptr(), d[8].data_ptr(), d[9].data_ptr())
+                   self.cnf_windowed, d[7].data_ptr(), d[8].data_ptr(), d[9].data_ptr())
         else:
             cnf = (0, 0, 0, 0, None, None, None)
         return _native.FbFilterProg(self.n_queries, self.n_leaves, self.k_max, self.max_stack,

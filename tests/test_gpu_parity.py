@@ -407,20 +407,37 @@ def _to_expr(fb, t):
     return cls(tuple(_to_expr(fb, c) for c in t[1]))
 
 
-@pytest.mark.parametrize("shape", ["cnf_neg", "random_mixed"])
-def test_tc_filter_modes_vs_oracle(fb, shape):
+@pytest.mark.parametrize("shape,nq", [("cnf_neg", 40), ("cnf_neg", 200), ("cnf_bins", 40),
+                                      ("cnf_bins", 256), ("cnf_wide", 40), ("cnf_wide", 150),
+                                      ("random_mixed", 40)])
+def test_tc_filter_modes_vs_oracle(fb, shape, nq):
     """CNF batches (with negated literals / NOT over groups) take the per-hit tensor-core
-    epilogue; batches with any non-CNF program take the bytecode epilogue. Both must match
-    the oracle exactly."""
+    epilogue: the fast form (<= 64 literal columns, <= 4 groups) or the general form (wide
+    batches); batches with any non-CNF program take the bytecode epilogue. All must match
+    the oracle exactly, with one or two 128-query M-blocks."""
     from paper_2511_14881_b200 import _device, _native, workload
     from paper_2511_14881_b200.filter_query import FilterBatch
-    wl = workload.make_workload(30_000, 40, dim=128, seed=21, filtered=False)
+    wl = workload.make_workload(30_000, nq, dim=128, seed=21, filtered=False)
     idx = wl.index
     rng = np.random.default_rng(5)
     p = fb.BloomParams()
     exprs = []
-    for q in range(40):
-        if shape == "cnf_neg":
+    for q in range(nq):
+        if shape == "cnf_bins":  # 4 features x up to 40 values: windowed, 8 column words
+            groups = []
+            for f in range(1, 5):
+                lits = [fb.Leaf(f, int(v)) for v in rng.choice(40, size=6, replace=False)]
+                groups.append(fb.Or(tuple(lits)))
+            exprs.append(fb.And(tuple(groups)))
+        elif shape == "cnf_wide":
+            groups = []
+            for f in range(1, 7):
+                lits = [fb.Leaf(f, int(v)) for v in rng.choice(12, size=4, replace=False)]
+                if rng.random() < 0.2:
+                    lits[1] = fb.Not(lits[1])
+                groups.append(fb.Or(tuple(lits)))
+            exprs.append(fb.And(tuple(groups)))
+        elif shape == "cnf_neg":
             groups = []
             for f in range(1, 4):
                 lits = [fb.Leaf(f, int(v)) for v in rng.choice(12, size=3, replace=False)]
@@ -436,18 +453,22 @@ def test_tc_filter_modes_vs_oracle(fb, shape):
     filters = [fb.compile_filter(e, p) for e in exprs]
     filters[3] = None
     batch = FilterBatch.pack(filters, p)
-    assert batch.is_cnf == (shape == "cnf_neg")
+    assert batch.is_cnf == shape.startswith("cnf")
+    if shape.startswith("cnf"):
+        assert batch.cnf_windowed == (shape != "cnf_wide")
+    if shape == "cnf_bins":
+        assert batch.cnf_words > 2
     items = idx.items.cpu().numpy()[:, :128]
     valid = _device.u64_host(idx.valid)
     ids = _device.u64_host(idx.item_ids)
     offs = np.array([[0, idx.n_slots]])
     qq = wl.queries_q.cpu().numpy()[:, :128]
     for k in (50, 3000):
-        op = fb.TopkOp(idx, 40, k, offs)
+        op = fb.TopkOp(idx, nq, k, offs)
         out = op(wl.queries_q, batch)
         torch.cuda.synchronize()
         assert _native.lib().fb_topk_scan_path(op._plan) == 1
-        for q in range(40):
+        for q in range(nq):
             cf = filters[q]
             prog = None if cf is None else ([(int(o), int(a)) for o, a in cf.ops],
                                             [(f, v, b.set_bits) for f, v, b in cf.leaves])

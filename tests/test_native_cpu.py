@@ -31,7 +31,7 @@ def test_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.fb_abi_version() == _native.ABI_VERSION == 2
+    assert lib.fb_abi_version() == _native.ABI_VERSION == 3
 
 
 def test_library_is_sm100a_only():
@@ -163,3 +163,67 @@ def test_golden_fixtures_present():
                  "four_attr.npz", "topk20000.npz", "merge_cases.npz", "quantize_cases.npz"):
         assert (Path(ROOT) / "tests" / "golden" / name).exists()
     assert load_npz("merge_cases.npz")["n_cases"][0] == 5
+
+
+def _cnf_eval(batch, planes, q):
+    """The scan's CNF semantics on the host: column bits = AND of the literal's planes
+    (complemented when negated); query q passes a slot iff each of its groups shares a
+    column with it. Returns u64 words (validity not applied)."""
+    nw = planes.shape[1]
+    cols = []
+    for cl in batch.host_col_leaf:
+        leaf = int(cl) if cl >= 0 else ~int(cl)
+        m = np.full(nw, ~np.uint64(0), dtype=np.uint64)
+        for pos in batch.host_leaf_pos[leaf]:
+            if pos >= 0:
+                m &= planes[pos]
+        cols.append(~m if cl < 0 else m)
+    out = np.full(nw, ~np.uint64(0), dtype=np.uint64)
+    for g in range(int(batch.host_qgroups[q])):
+        acc = np.zeros(nw, dtype=np.uint64)
+        for c in range(len(cols)):
+            if (int(batch.host_qmask[q, g, c >> 5]) >> (c & 31)) & 1:
+                acc |= cols[c]
+        out &= acc
+    return out
+
+
+@pytest.mark.parametrize("n_feat,n_vals,windowed", [(3, 12, 1), (4, 50, 1), (6, 12, 0)])
+def test_cnf_packing_matches_compiled_programs(n_feat, n_vals, windowed):
+    """FilterBatch.pack's CNF form (feature-binned 64-column windows) evaluates exactly like
+    the compiled postfix programs (oracle eval_compiled) on random planes; batches whose
+    groups each sit in one aligned u32 pair with <= 4 groups are flagged windowed."""
+    from oracle import filtra_oracle as orc
+    rng = np.random.default_rng(n_feat * 100 + n_vals)
+    p = BloomParams()
+    exprs = []
+    for q in range(24):
+        groups = []
+        for f in range(1, n_feat + 1):
+            k = int(rng.integers(1, 6))
+            lits = [Leaf(f, int(v)) for v in rng.choice(n_vals, size=k, replace=False)]
+            if rng.random() < 0.3:
+                lits[0] = Not(lits[0])
+            groups.append(Or(tuple(lits)) if len(lits) > 1 else lits[0])
+        exprs.append(And(tuple(groups)))
+    filters = [compile_filter(e, p) for e in exprs]
+    filters[5] = None
+    batch = FilterBatch.pack(filters, p)
+    assert batch.is_cnf and batch.cnf_windowed == windowed
+    planes = rng.integers(0, 2**63, size=(p.m_bits, 3), dtype=np.int64).astype(np.uint64)
+    planes |= rng.integers(0, 2**63, size=(p.m_bits, 3), dtype=np.int64).astype(np.uint64)
+    valid = np.full(3, ~np.uint64(0), dtype=np.uint64)
+    for q, cf in enumerate(filters):
+        got = _cnf_eval(batch, planes, q)
+        if cf is None:
+            assert int(batch.host_qgroups[q]) == 0
+            continue
+        ref = orc.eval_compiled([(int(o), int(a)) for o, a in cf.ops],
+                                [(f, v, qb.set_bits) for f, v, qb in cf.leaves], planes, valid)
+        assert np.array_equal(got, ref), q
+    if windowed:
+        nz = batch.host_qmask != 0
+        for q in range(batch.n_queries):
+            for g in range(int(batch.host_qgroups[q])):
+                w = np.nonzero(nz[q, g])[0]
+                assert len(w) and w.min() // 2 == w.max() // 2
