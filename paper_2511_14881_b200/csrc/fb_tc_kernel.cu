@@ -22,6 +22,8 @@
 #include "fb_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
 
 namespace fb {
 namespace {
@@ -47,6 +49,7 @@ constexpr int kRegStack = 4;
 constexpr uint32_t kItemBytes = kTileItems * kKBytes;  // 32 KB
 
 struct TcArgs {
+  const int8_t* items;    // [n_slots, 128] (survivor scores are recomputed from L2)
   const int8_t* queries;
   int32_t nq;
   int32_t n_mblk;
@@ -81,12 +84,16 @@ struct TcArgs {
   int32_t n_cols;
   int32_t cnf_words;
   int32_t cnf_gmax;
-  int32_t tb_stride;  // u32 per item row of the transposed column bits
+  int32_t tb_stride;
+  int32_t dbg;        // timing experiments only (FB_SCAN_DEBUG): bit 0 no plane copies,
+                      // bit 1 no hit work, bit 2 no column builds, bit 3 no dense work,
+                      // bit 7 no gate arm, bit 8 no TMEM drain,
+                      // bit 9 no MMA, bit 10 timeline trace (FB_TR)
   const int16_t* col_leaf;
   const uint32_t* qmask;
   const int32_t* qgroups;
   uint32_t off_a, off_b, off_p, off_l, off_ls, off_thr, off_r, off_bar, plane_stage_bytes,
-      leaf_stage_bytes, off_hm, off_gate, off_sv, off_id;
+      leaf_stage_bytes, off_hm, off_gate, off_sv, off_id, off_pl;
 };
 
 
@@ -105,8 +112,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
 // try_wait with a suspend-time hint: the warp is parked by the hardware until the phase
-// completes (or the hint expires) instead of spinning through issue slots that the
-// epilogue warps on the same scheduler need.
+// completes (or the hint expires) instead of spinning through issue slots that the other
+// roles on the same scheduler need.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   const uint32_t a = su32(b);
   uint32_t ok = 0;
@@ -120,6 +127,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
   } while (!ok);
 }
+// Timeline trace (compile with -DFB_TRACE, run with FB_SCAN_DEBUG bit 10): CTA 0 records
+// clock64 at pipeline events of its first 16 tiles and prints them at exit.
+#ifdef FB_TRACE
+__device__ long long g_tr[16][12];
+#define FB_TR(a, t, e)                                                          \
+  do {                                                                          \
+    if (((a).dbg & 1024) && blockIdx.x == 0 && (t) < 16 && (threadIdx.x & 31) == 0) \
+      g_tr[(t)][(e)] = clock64();                                               \
+  } while (0)
+#else
+#define FB_TR(a, t, e) \
+  do {                 \
+  } while (0)
+#endif
 __device__ __forceinline__ void mbar_wait_idle(uint64_t* b, uint32_t parity) { mbar_wait(b, parity); }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0,
                                             int32_t c1, uint64_t* bar) {
@@ -375,6 +396,11 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ uint32_t lds16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ uint64_t lds64(uint32_t addr) {
   uint64_t v;
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
@@ -524,13 +550,18 @@ __device__ __forceinline__ void stage_queries(const TcArgs& a, const Smem& m, in
   }
   for (int q = threadIdx.x; q < kMaxQueries; q += nt)
     m.sT[q] = (a.threshold != nullptr && q < a.nq) ? a.threshold[q] : 0ull;
+  int16_t* pl = reinterpret_cast<int16_t*>(m.base + a.off_pl);
+  for (int i = threadIdx.x; i < a.n_planes; i += nt) pl[i] = a.plane_list[i];
 }
 
 // ================= producer (one warp): TMA item tile + Bloom plane words ==============
 // The per-tile global reads (work item, then its validity & range words) are issued one
 // tile ahead, so their latency never sits on the producer's critical path.
+// do_items: TMA item rows + per-tile metadata; do_planes: the plane gather (one warp can
+// do both, or two warps split them so the gather never queues behind an item stage).
 __device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap* tmap,
-                                              const Smem& m, int lane) {
+                                              const Smem& m, int lane, bool do_items,
+                                              bool do_planes) {
   uint8_t* smem = m.base;
   uint8_t* sB = m.sB;
   uint8_t* sP = m.sP;
@@ -541,6 +572,7 @@ __device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap
   const int S = a.item_stages;
   const int PS = a.plane_stages;
   const int64_t n_sel = a.n_sel;
+  const uint32_t pl_s = su32(m.base + a.off_pl);  // plane ids, staged by stage_queries
     // The per-tile global reads (work item, then its validity & range words) are issued
     // one tile ahead, so their latency never sits on the producer's critical path.
     int s = 0, ps = 0;
@@ -566,11 +598,12 @@ __device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap
       int2 wk_nn = make_int2(0, 0);
       if (i + G < n_sel) v_next = load_valid(wk_next);
       if (i + 2 * G < n_sel) wk_nn = a.work[(i + 2 * G) * a.work_stride];
-      {
+      if (do_items) {
         // item rows by TMA; alongside, into a stage with the item stage's lifetime: the
         // tile's 256 id ranks (1 KB, 16-byte cp.async), its validity & range words and its
         // tile index (so the epilogue never waits on global memory for per-tile metadata)
         mbar_wait_idle(items_empty + s, ph ^ 1u);
+        FB_TR(a, (int)((i - blockIdx.x) / G), 0);
         if (lane == 0) {
           mbar_expect_tx(items_full + s, kItemBytes);
           tma_load_2d(sB + (size_t)s * kItemBytes, tmap, 0, tile * kTileItems,
@@ -594,8 +627,9 @@ __device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap
         __syncwarp();
         if (lane == 0) mbar_arrive(items_full + s);
       }
-      if (a.has_prog && a.n_planes > 0) {
+      if (do_planes && a.has_prog && a.n_planes > 0) {
         mbar_wait_idle(planes_empty + ps, pph ^ 1u);
+        FB_TR(a, (int)((i - blockIdx.x) / G), 10);
         // gather the referenced planes' 32-byte rows for this tile: 16-byte cp.async per
         // lane (two lanes per plane row, a warp covers 16 rows per instruction); each lane
         // arrives on planes_full once its copies land
@@ -603,13 +637,13 @@ __device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap
         const int64_t col0 = (int64_t)tile * kTileWords;
         // (plane indices fetched eight at a time ahead of the copies: the copies' memory
         // clobber would otherwise serialise each index load behind the previous copy)
-        const int n2 = 2 * a.n_planes;
+        const int n2 = (a.dbg & 1) ? 0 : 2 * a.n_planes;
         for (int e0 = lane; e0 < n2; e0 += 32 * 8) {
           int pl[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int e = e0 + 32 * u;
-            pl[u] = e < n2 ? __ldg(a.plane_list + (e >> 1)) : 0;
+            pl[u] = e < n2 ? (int)lds16(pl_s + 2u * (uint32_t)(e >> 1)) : 0;
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
@@ -652,6 +686,7 @@ __device__ __forceinline__ void mma_loop(const TcArgs& a, const Smem& m, uint32_
   for (int64_t i = blockIdx.x; i < a.n_sel; i += gridDim.x) {
     mbar_wait(items_full + s, ph);
     tc_fence_after();
+    FB_TR(a, (int)((i - blockIdx.x) / gridDim.x), 1);
     const uint32_t b_base = su32(m.sB + (size_t)s * kItemBytes);
     for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
       const int ab = acc_it & 1;
@@ -660,14 +695,16 @@ __device__ __forceinline__ void mma_loop(const TcArgs& a, const Smem& m, uint32_
       tc_fence_after();
       const uint32_t a_base = su32(m.sA + mb * kBlockM * kKBytes);
       const uint32_t d = tmem_base + (uint32_t)(ab * kAccCols);
-      if (kArm)
+      const bool arm = kArm && !(a.dbg & 128);
+      if (arm)
         umma_i8(d, plain_desc(gate_s + (uint32_t)mb * (kBlockM / 8) * 256u, 128u, 256u),
                 plain_desc(gate_s + kGateTileBytes, 128u, 0u), idesc, 0u);
 #pragma unroll
-      for (int kk = 0; kk < kKBytes / kUmmaK; ++kk)
+      for (int kk = 0; kk < ((a.dbg & 512) ? 0 : kKBytes / kUmmaK); ++kk)
         umma_i8(d, sw128_desc(a_base + kk * kUmmaK), sw128_desc(b_base + kk * kUmmaK), idesc,
-                (kk > 0 || kArm) ? 1u : 0u);
+                (kk > 0 || arm) ? 1u : 0u);
       umma_commit(acc_full + ab);
+      if (mb == 0) FB_TR(a, (int)((i - blockIdx.x) / gridDim.x), 2);
     }
     umma_commit(items_empty + s);
     if (++s == S) { s = 0; ph ^= 1u; }
@@ -696,7 +733,7 @@ __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m,
       mbar_wait_idle(leaf_empty + st, ph ^ 1u);
       const uint32_t p_s = su32(sP + (size_t)ps * a.plane_stage_bytes);
       uint32_t* TB = reinterpret_cast<uint32_t*>(sL + (size_t)st * a.leaf_stage_bytes);
-      for (int cb = lw; cb < a.cnf_words; cb += nb) {  // 32-column block
+      for (int cb = lw; cb < ((a.dbg & 4) ? 0 : a.cnf_words); cb += nb) {  // 32-column block
         const int col = cb * 32 + lane;
         // the column's 256 tile bits: AND of its planes' 32-byte rows (8 x u32, one per
         // 32-item block); all loads are independent
@@ -833,7 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    producer_loop(a, &tmap_items, m, lane);
+    producer_loop(a, &tmap_items, m, lane, true, true);
   } else if (warp == 1) {
     if (lane == 0) mma_loop<false>(a, m, tmem_base);
   } else if (warp < kEpiWarp0) {
@@ -1011,14 +1048,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ======================================================================================
 // CNF scan kernel (every program an AND of OR-groups of literals). Twenty warps:
-//   warp 0       producer (TMA item rows, cp.async plane gather, per-tile metadata)
+//   warp 0       item producer (TMA item rows, per-tile id ranks / validity / tile index)
 //   warp 1       MMA: per M-block the gate-arming K=32 MMA, then 4 K-steps of kind::i8
-//   warps 2-3    column builders: per literal column the AND of its planes, transposed so
+//   warp 2       plane producer (cp.async gather of the batch's planes, 32 B per tile)
+//   warps 3-7    column builders: per literal column the AND of its planes, transposed so
 //                each item row holds its column bits (the paper's and.b64 Bloom test)
-//   warps 4-11   dense pass, two per TMEM lane quadrant: tcgen05.ld 32 columns, the hit
-//                mask is the accumulators' sign bits (armed at +127 D), & validity/range;
-//                32-bit hit masks go to a double-buffered [chunk][query] map in smem and
-//                the accumulator is released at once
+//   warps 8-11   dense pass, one per TMEM lane quadrant: tcgen05.ld 32 columns (double
+//                buffered), the hit mask is the accumulators' sign bits (armed at +127 D),
+//                & validity/range; 32-bit hit masks go to a double-buffered [chunk][query]
+//                map in smem and the accumulator is released at once
 //   warps 12-19  hit pass, lane = query: walks its hit bits, tests the CNF filter against
 //                the item's column bits (window form: 4 groups x one u32 pair, masks in
 //                registers), queues survivors per warp; survivors get their exact score
@@ -1026,9 +1064,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 //                slot reservation -- filtered-out items never leave the SM.
 // ======================================================================================
 constexpr int kCnfThreads = 640;
-constexpr int kCnfBuilders = 2;
-constexpr int kCnfDense0 = 4;
-constexpr int kCnfDenseWarps = 8;
+constexpr int kCnfBuilders = 5;
+constexpr int kCnfDense0 = 8;
+constexpr int kCnfDenseWarps = 4;
 constexpr int kCnfHit0 = 12;
 constexpr int kCnfHitWarps = 8;
 constexpr int kSurvCap = 64;  // u16 survivor entries per hit warp: (lane << 8) | item
@@ -1059,11 +1097,6 @@ __device__ __forceinline__ int32_t smem_dot(uint32_t a_row, uint32_t a_sw, uint3
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t v;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(v));
-  return v;
-}
-__device__ __forceinline__ uint32_t lds16(uint32_t addr) {
-  uint16_t v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
@@ -1180,7 +1213,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < 4; ++s) {
       mbar_init(items_full + s, 1 + 32 + 1);          // TMA expect-tx, id ranks, meta
-      mbar_init(items_empty + s, 1 + kCnfHitWarps);   // MMA commit + hit warps
+      mbar_init(items_empty + s, 1 + kCnfHitWarps);  // MMA commit + hit warps (B tile, ids)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(planes_full + s, 32);
@@ -1202,15 +1235,16 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
   const uint32_t hm_s = su32(smem + a.off_hm);
 
   if (warp == 0) {
-    producer_loop(a, &tmap_items, m, lane);
+    producer_loop(a, &tmap_items, m, lane, true, false);
   } else if (warp == 1) {
     if (lane == 0) mma_loop<true>(a, m, tmem_base);
+  } else if (warp == 2) {
+    producer_loop(a, &tmap_items, m, lane, false, true);
   } else if (warp < kCnfDense0) {
-    cnf_builder_loop(a, m, warp - 2, kCnfBuilders, lane);
+    cnf_builder_loop(a, m, warp - 3, kCnfBuilders, lane);
   } else if (warp < kCnfHit0) {
-    // ================= dense pass ====================================================
+    // ================= dense pass (one warp per TMEM lane quadrant) ======================
     const int quad = warp & 3;
-    const int sub = (warp - kCnfDense0) >> 2;  // chunks sub, sub + 2, sub + 4, sub + 6
     const int row = quad * 32 + lane;
     int it = 0, acc_it = 0, s = 0;
     uint32_t iph = 0;
@@ -1220,6 +1254,10 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
       const int64_t tile = (int64_t)lds32(mst + kMetaTile);
       // lane c < 8 holds the validity & range bits of the tile's chunk c (32 items)
       const uint32_t vchunk = lane < 8 ? lds32(mst + kMetaValid + 4u * lane) : 0u;
+      if (++s == a.item_stages) {
+        s = 0;
+        iph ^= 1u;
+      }
       const int hb = it & 1;
       mbar_wait(hm_empty + hb, ((uint32_t)(it >> 1) & 1u) ^ 1u);
       const uint32_t hmap = hm_s + (uint32_t)hb * kHmapBytes;
@@ -1233,13 +1271,11 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
         const int ab = acc_it & 1;
         mbar_wait(acc_full + ab, (uint32_t)(acc_it >> 1) & 1u);
         tc_fence_after();
+        if (quad == 0) FB_TR(a, it, 4 + 2 * mb);
         const uint32_t taddr =
             tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kAccCols);
-        int32_t r[32];
-        tmem_ld32_async(taddr + (uint32_t)(sub * 32), r);
-#pragma unroll 1
-        for (int c = sub; c < 8; c += 2) {
-          tmem_wait32(r);
+        // hit mask of chunk c from its 32 accumulators (validity, range, explicit mask)
+        auto chunk_mask = [&](int c, const int32_t (&r)[32]) -> uint32_t {
           uint32_t em = __shfl_sync(0xffffffffu, vchunk, c);
           if (!qok) em = 0u;
           if (a.masks != nullptr && em != 0u)
@@ -1253,20 +1289,27 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
               if (base + j < a.dump_ld)
                 a.dump[(int64_t)q * a.dump_ld + base + j] = r[j] - 127 * D;
           }
-          const uint32_t hm = (nonneg_mask32(r) | allmask) & em;
-          if (c + 2 < 8) tmem_ld32_async(taddr + (uint32_t)((c + 2) * 32), r);
-          sts32(hmap + (uint32_t)(c * kMaxQueries + q) * 4u, hm);
+          return (a.dbg & 8) ? 0u : (nonneg_mask32(r) | allmask) & em;
+        };
+        // two register buffers: chunk c + 1 loads while chunk c is reduced to its mask
+        int32_t ra[32], rb[32];
+        tmem_ld32_async(taddr, ra);
+#pragma unroll 1
+        for (int c = 0; c < ((a.dbg & 256) ? 0 : 8); c += 2) {
+          tmem_wait32(ra);
+          tmem_ld32_async(taddr + (uint32_t)((c + 1) * 32), rb);
+          sts32(hmap + (uint32_t)(c * kMaxQueries + q) * 4u, chunk_mask(c, ra));
+          tmem_wait32(rb);
+          if (c + 2 < 8) tmem_ld32_async(taddr + (uint32_t)((c + 2) * 32), ra);
+          sts32(hmap + (uint32_t)((c + 1) * kMaxQueries + q) * 4u, chunk_mask(c + 1, rb));
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + ab);
+        if (quad == 0) FB_TR(a, it, 5 + 2 * mb);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(hm_full + hb);
-      if (++s == a.item_stages) {
-        s = 0;
-        iph ^= 1u;
-      }
     }
   } else {
     // ================= hit pass (lane = query) =========================================
@@ -1274,6 +1317,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
     const int q = qbase + lane;
     const bool qok = q < a.nq;
     const uint64_t T = qok ? m.sT[q] : ~0ull;
+    (void)T;
     const int ng = qok ? a.qgroups[q] : 0;
     const bool nof = ng == 0;
     // window form: per group (byte offset of its u32 pair in an item row, 64-bit mask);
@@ -1311,10 +1355,11 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
       const uint32_t tb_s = su32(m.sL + (size_t)st * a.leaf_stage_bytes);
       const int hb = it & 1;
       mbar_wait(hm_full + hb, (uint32_t)(it >> 1) & 1u);
+      if (warp == kCnfHit0) FB_TR(a, it, 8);
       const uint32_t hmap = hm_s + (uint32_t)hb * kHmapBytes + 4u * (uint32_t)q;
       // this query's nonzero chunk words
       uint32_t nzm = 0u;
-      if (qok) {
+      if (qok && !(a.dbg & 2)) {
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           nzm |= (lds32(hmap + (uint32_t)c * (kMaxQueries * 4u)) != 0u ? 1u : 0u) << c;
@@ -1322,7 +1367,10 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
       int cc = nzm ? __ffs(nzm) - 1 : 0;
       uint32_t cur = nzm ? lds32(hmap + (uint32_t)cc * (kMaxQueries * 4u)) : 0u;
       uint32_t n_sv = 0;  // warp-uniform survivor count
+      int n_rounds = 0;
       while (__any_sync(0xffffffffu, cur != 0u)) {
+        ++n_rounds;
+        (void)n_rounds;
         bool surv = false;
         uint32_t item = 0;
         if (cur != 0u) {
@@ -1356,6 +1404,11 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(hm_empty + hb);
+      if (warp == kCnfHit0) FB_TR(a, it, 11);
+#ifdef FB_TRACE
+      if ((a.dbg & 1024) && blockIdx.x == 0 && warp == kCnfHit0 && lane == 0 && it < 16)
+        g_tr[it][3] = (long long)n_rounds * 1000 + n_sv;
+#endif
       if (n_sv) drain_survivors(a, m, e, sv_s, n_sv, qbase, b_s, mst, tile, lane);
       __syncwarp();
       if (lane == 0) {
@@ -1366,6 +1419,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
         s = 0;
         iph ^= 1u;
       }
+      if (warp == kCnfHit0) FB_TR(a, it, 9);
     }
     flush_pending(a, e.pa);
     flush_pending(a, e.pb);
@@ -1374,6 +1428,17 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+#ifdef FB_TRACE
+  if ((a.dbg & 1024) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long t0 = g_tr[0][0];
+    for (int t = 0; t < 16; ++t)
+      printf("tile %2d: prodI %6lld mmaSee %6lld c0 %6lld rounds*1000+surv %6lld | d0 %6lld r0 %6lld d1 %6lld "
+             "r1 %6lld | h %6lld loop %6lld hdone %6lld | prodP %6lld\n",
+             t, g_tr[t][0] - t0, g_tr[t][1] - t0, g_tr[t][2] - t0, g_tr[t][3],
+             g_tr[t][4] - t0, g_tr[t][5] - t0, g_tr[t][6] - t0, g_tr[t][7] - t0,
+             g_tr[t][8] - t0, g_tr[t][11] - t0, g_tr[t][9] - t0, g_tr[t][10] - t0);
+  }
+#endif
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512)
                  : "memory");
@@ -1422,6 +1487,8 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
   off = t.off_thr + (size_t)kMaxQueries * 8;
   t.off_bar = (uint32_t)align_up(off, 16);
   off = t.off_bar + kBarCount * 8;
+  t.off_pl = (uint32_t)align_up(off, 16);
+  off = t.off_pl + (size_t)(n_planes > 0 ? n_planes : 1) * 2;
   if (cnf) {
     t.off_hm = (uint32_t)align_up(off, 128);
     off = t.off_hm + 2ull * kHmapBytes;
@@ -1541,6 +1608,7 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
   for (int q0 = 0; q0 < a.n_queries; q0 += kMaxQueries) {
     const int nq = a.n_queries - q0 < kMaxQueries ? a.n_queries - q0 : kMaxQueries;
     TcArgs t{};
+    t.items = a.idx.items;
     t.queries = a.queries + (int64_t)q0 * a.idx.dim_pad;
     t.nq = nq;
     t.n_mblk = (nq + kBlockM - 1) / kBlockM;
@@ -1571,6 +1639,7 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
     t.cap = a.cap;
     t.dump = a.dump ? a.dump + (int64_t)q0 * a.dump_ld : nullptr;
     t.dump_ld = a.dump_ld;
+    if (const char* d = getenv("FB_SCAN_DEBUG")) t.dbg = atoi(d);
     size_t smem = 0;
     if (!pick_stages(t, t.n_mblk, t.has_prog ? t.n_planes : 0, t.has_prog ? t.n_leaves : 0,
                      t.has_prog ? t.k_max : 0, t.has_prog ? a.prog.n_rops : 0, cnf, smem))

@@ -10,8 +10,8 @@ import sys
 from collections import defaultdict
 
 
-def line_map(sass_path, kernel):
-    out, cur, inside, line = {}, None, False, None
+def line_map(sass_path, kernel, inner=False):
+    out, cur, inside, line, in_run = {}, None, False, None, False
     for raw in open(sass_path):
         if raw.startswith("//-----") and ".text." in raw:
             inside = kernel in raw
@@ -20,8 +20,14 @@ def line_map(sass_path, kernel):
             continue
         if raw.lstrip().startswith("//## File"):
             pairs = re.findall(r'"[^"]*?([^/"]+)", line (\d+)', raw)
-            line = pairs[-1][1] if pairs else None  # outermost caller (the kernel body)
+            own = [ln for f, ln in pairs if f.endswith(".cu")]
+            # outermost caller (the kernel body), or with --inner the innermost .cu line
+            # (nvdisasm repeats the location as a run of comments, innermost first)
+            if not (inner and in_run):
+                line = (own[0] if inner else own[-1]) if own else (pairs[-1][1] if pairs else None)
+            in_run = True
             continue
+        in_run = False
         m = re.match(r"\s+/\*([0-9a-f]{4,})\*/", raw)
         if m:
             out[int(m.group(1), 16)] = line
@@ -31,7 +37,7 @@ def line_map(sass_path, kernel):
 def main():
     ncu_csv, sass, kernel = sys.argv[1:4]
     top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 50
-    lm = line_map(sass, kernel)
+    lm = line_map(sass, kernel, "--inner" in sys.argv)
     rows = list(csv.reader(open(ncu_csv)))
     h = rows[1]
     ia, iex = h.index("Address"), h.index("Instructions Executed")
