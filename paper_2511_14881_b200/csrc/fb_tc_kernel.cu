@@ -142,6 +142,15 @@ __device__ long long g_tr[16][12];
   } while (0)
 #endif
 __device__ __forceinline__ void mbar_wait_idle(uint64_t* b, uint32_t parity) { mbar_wait(b, parity); }
+// Hardware named barriers for warp-to-warp stage handoffs (the waiting warps block in the
+// barrier unit instead of polling an mbarrier): the producing warps bar.arrive on a stage's
+// "full" barrier and the consumers bar.sync on it; "empty" runs the other way.
+__device__ __forceinline__ void nb_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nb_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0,
                                             int32_t c1, uint64_t* bar) {
   asm volatile(
@@ -711,6 +720,19 @@ __device__ __forceinline__ void mma_loop(const TcArgs& a, const Smem& m, uint32_
   }
 }
 
+// ---- CNF kernel warp layout (see k_scan_cnf) ----
+constexpr int kCnfThreads = 640;
+constexpr int kCnfBuilders = 5;
+constexpr int kCnfDense0 = 8;
+constexpr int kCnfDenseWarps = 4;
+constexpr int kCnfHit0 = 12;
+constexpr int kCnfHitWarps = 8;
+constexpr int kSurvCap = 64;  // u16 survivor entries per hit warp: (lane << 8) | item
+// named barrier ids (0 is __syncthreads) and their thread counts
+constexpr int kNbHmFull = 1, kNbHmEmpty = 3, kNbLeafFull = 5, kNbLeafEmpty = 7;  // + stage
+constexpr int kNbHmCount = 32 * (kCnfDenseWarps + kCnfHitWarps);
+constexpr int kNbLeafCount = 32 * (kCnfBuilders + kCnfHitWarps);
+
 // ================= CNF column builders (nb warps): Bloom test per literal column, then a
 // 32x32 bit transpose so each item row holds its column bits ==========================
 __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m, int lw, int nb,
@@ -720,8 +742,6 @@ __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m,
   const int16_t* sLS = m.sLS;
   uint64_t* planes_full = m.bars + kBarPlanesFull;
   uint64_t* planes_empty = m.bars + kBarPlanesEmpty;
-  uint64_t* leaf_full = m.bars + kBarLeafFull;
-  uint64_t* leaf_empty = m.bars + kBarLeafEmpty;
   const int PS = a.plane_stages;
   const int64_t n_sel = a.n_sel;
     int it = 0, ps = 0;
@@ -729,8 +749,9 @@ __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m,
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
       const int st = it & 1;
       const uint32_t ph = (uint32_t)(it >> 1) & 1u;
+      (void)ph;
       mbar_wait_idle(planes_full + ps, pph);
-      mbar_wait_idle(leaf_empty + st, ph ^ 1u);
+      if (it >= 2) nb_sync(kNbLeafEmpty + st, kNbLeafCount);
       const uint32_t p_s = su32(sP + (size_t)ps * a.plane_stage_bytes);
       uint32_t* TB = reinterpret_cast<uint32_t*>(sL + (size_t)st * a.leaf_stage_bytes);
       for (int cb = lw; cb < ((a.dbg & 4) ? 0 : a.cnf_words); cb += nb) {  // 32-column block
@@ -778,12 +799,13 @@ __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m,
         for (int ib = 0; ib < 8; ++ib) TB[(ib * 32 + lane) * a.tb_stride + cb] = m[ib];
       }
       __syncwarp();
-      if (lane == 0) {  // one arrival per builder warp
-        mbar_arrive(planes_empty + ps);
-        mbar_arrive(leaf_full + st);
-      }
+      if (lane == 0) mbar_arrive(planes_empty + ps);  // one arrival per builder warp
+      nb_arrive(kNbLeafFull + st, kNbLeafCount);
       if (++ps == PS) { ps = 0; pph ^= 1u; }
     }
+    // retire the hit pass's releases of the last two stages (every barrier phase completes)
+    for (int t = it; t < it + 2; ++t)
+      if (t >= 2) nb_sync(kNbLeafEmpty + (t & 1), kNbLeafCount);
 }
 
 // ---- tensor memory -----------------------------------------------------------------------
@@ -1063,13 +1085,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 //                from the resident smem tiles (dp4a), the exact key test and an atomic
 //                slot reservation -- filtered-out items never leave the SM.
 // ======================================================================================
-constexpr int kCnfThreads = 640;
-constexpr int kCnfBuilders = 5;
-constexpr int kCnfDense0 = 8;
-constexpr int kCnfDenseWarps = 4;
-constexpr int kCnfHit0 = 12;
-constexpr int kCnfHitWarps = 8;
-constexpr int kSurvCap = 64;  // u16 survivor entries per hit warp: (lane << 8) | item
 constexpr uint32_t kHmapBytes = 8u * kMaxQueries * 4u;  // [chunk][query] u32
 
 // Exact int32 dot of a query row (A tile) and an item row (B stage) from shared memory.
@@ -1172,12 +1187,8 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
   uint64_t* items_empty = bars + kBarItemsEmpty;
   uint64_t* planes_full = bars + kBarPlanesFull;
   uint64_t* planes_empty = bars + kBarPlanesEmpty;
-  uint64_t* leaf_full = bars + kBarLeafFull;
-  uint64_t* leaf_empty = bars + kBarLeafEmpty;
   uint64_t* acc_full = bars + kBarAccFull;
   uint64_t* acc_empty = bars + kBarAccEmpty;
-  uint64_t* hm_full = bars + kBarHmFull;
-  uint64_t* hm_empty = bars + kBarHmEmpty;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kBarTmemSlot);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_sel = a.n_sel;
@@ -1218,12 +1229,8 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(planes_full + s, 32);
       mbar_init(planes_empty + s, kCnfBuilders);
-      mbar_init(leaf_full + s, kCnfBuilders);
-      mbar_init(leaf_empty + s, kCnfHitWarps);
       mbar_init(acc_full + s, 1);
       mbar_init(acc_empty + s, kCnfDenseWarps);
-      mbar_init(hm_full + s, kCnfDenseWarps);
-      mbar_init(hm_empty + s, kCnfHitWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1259,7 +1266,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
         iph ^= 1u;
       }
       const int hb = it & 1;
-      mbar_wait(hm_empty + hb, ((uint32_t)(it >> 1) & 1u) ^ 1u);
+      if (it >= 2) nb_sync(kNbHmEmpty + hb, kNbHmCount);
       const uint32_t hmap = hm_s + (uint32_t)hb * kHmapBytes;
 #pragma unroll 1
       for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
@@ -1309,8 +1316,10 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
         if (quad == 0) FB_TR(a, it, 5 + 2 * mb);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(hm_full + hb);
+      nb_arrive(kNbHmFull + hb, kNbHmCount);
     }
+    for (int t = it; t < it + 2; ++t)
+      if (t >= 2) nb_sync(kNbHmEmpty + (t & 1), kNbHmCount);
   } else {
     // ================= hit pass (lane = query) =========================================
     const int qbase = (warp - kCnfHit0) * 32;
@@ -1351,10 +1360,10 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
       const int64_t tile = (int64_t)lds32(mst + kMetaTile);
       const uint32_t b_s = su32(m.sB + (size_t)s * kItemBytes);
       const int st = it & 1;
-      mbar_wait(leaf_full + st, (uint32_t)(it >> 1) & 1u);
+      nb_sync(kNbLeafFull + st, kNbLeafCount);
       const uint32_t tb_s = su32(m.sL + (size_t)st * a.leaf_stage_bytes);
       const int hb = it & 1;
-      mbar_wait(hm_full + hb, (uint32_t)(it >> 1) & 1u);
+      nb_sync(kNbHmFull + hb, kNbHmCount);
       if (warp == kCnfHit0) FB_TR(a, it, 8);
       const uint32_t hmap = hm_s + (uint32_t)hb * kHmapBytes + 4u * (uint32_t)q;
       // this query's nonzero chunk words
@@ -1403,7 +1412,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(hm_empty + hb);
+      nb_arrive(kNbHmEmpty + hb, kNbHmCount);
       if (warp == kCnfHit0) FB_TR(a, it, 11);
 #ifdef FB_TRACE
       if ((a.dbg & 1024) && blockIdx.x == 0 && warp == kCnfHit0 && lane == 0 && it < 16)
@@ -1411,10 +1420,8 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
 #endif
       if (n_sv) drain_survivors(a, m, e, sv_s, n_sv, qbase, b_s, mst, tile, lane);
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(leaf_empty + st);
-        mbar_arrive(items_empty + s);
-      }
+      nb_arrive(kNbLeafEmpty + st, kNbLeafCount);
+      if (lane == 0) mbar_arrive(items_empty + s);
       if (++s == a.item_stages) {
         s = 0;
         iph ^= 1u;
