@@ -76,6 +76,9 @@ typedef struct fb_index {
    * of [0, n_slots). With it, candidates carry only their merge key and the selection
    * sorts keys alone (radix sort in shared memory). */
   const uint32_t* slot_of_rank;
+  /* Nullable: item id of each rank (item_ids[slot_of_rank[r]]), so the selection gathers
+   * an output id with one load instead of two dependent ones. */
+  const uint64_t* id_of_rank;
 } fb_index_t;
 
 /*

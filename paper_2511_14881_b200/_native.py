@@ -59,7 +59,7 @@ class FbIndex(ctypes.Structure):
         ("n_slots", ctypes.c_int64), ("n_words", ctypes.c_int64),
         ("dim", ctypes.c_int32), ("dim_pad", ctypes.c_int32),
         ("m_bits", ctypes.c_int32), ("k_hashes", ctypes.c_int32),
-        ("slot_of_rank", c_vp),
+        ("slot_of_rank", c_vp), ("id_of_rank", c_vp),
     ]
 
 

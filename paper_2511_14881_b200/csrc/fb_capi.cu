@@ -481,6 +481,7 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
   sel.cand_key = p->d_cand_key;
   sel.cand_slot = p->d_cand_slot;
   sel.slot_of_rank = p->idx.slot_of_rank;
+  sel.id_of_rank = p->idx.id_of_rank;
   sel.n_slots = p->idx.n_slots;
   sel.cnt = p->d_cnt;
   sel.item_ids = p->idx.item_ids;

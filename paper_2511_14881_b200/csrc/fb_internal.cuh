@@ -179,6 +179,7 @@ struct SelectArgs {
   uint64_t* scratch_key;      // [B, cap]
   uint32_t* scratch_slot;     // [B, cap]
   const uint32_t* slot_of_rank;  // [n_slots] nullable (fb_index_t.slot_of_rank)
+  const uint64_t* id_of_rank;    // [n_slots] nullable (fb_index_t.id_of_rank)
   int64_t n_slots;               // ranks are a permutation of [0, n_slots)
 };
 int launch_select(const SelectArgs& a, cudaStream_t s);

@@ -803,6 +803,8 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
   const int32_t qsum = s_qsum;
   constexpr int kOutU = 5;  // gathers in flight per thread
   const uint64_t id_mask = id_bits >= 64 ? ~0ull : ((1ull << id_bits) - 1ull);
+  // ids straight from the rank (one gather) unless the dequantised scores need the slot
+  const bool by_id = a.id_of_rank != nullptr && a.out_fscores == nullptr;
   for (int r0 = 0; r0 < kk; r0 += kRsThreads * kOutU) {
     uint64_t key[kOutU];
     uint32_t slot[kOutU];
@@ -816,7 +818,8 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
         const uint32_t sb = (uint32_t)(c >> id_bits) + sb_lo;
         const uint32_t low = (uint32_t)(c & id_mask) + id_base;
         key[u] = ((uint64_t)sb << 32) | low;
-        slot[u] = __ldg(a.slot_of_rank + (0xFFFFFFFFu - low));
+        slot[u] = 0xFFFFFFFFu - low;  // the rank
+        if (!by_id) slot[u] = __ldg(a.slot_of_rank + slot[u]);
       }
     }
     uint64_t iid[kOutU];
@@ -824,7 +827,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
 #pragma unroll
     for (int u = 0; u < kOutU; ++u) {
       const int r = r0 + u * kRsThreads + t;
-      iid[u] = r < kk ? __ldg(a.item_ids + slot[u]) : 0ull;
+      iid[u] = r < kk ? __ldg((by_id ? a.id_of_rank : a.item_ids) + slot[u]) : 0ull;
       rsum[u] = (r < kk && a.out_fscores && a.row_sum) ? __ldg(a.row_sum + slot[u]) : 0;
     }
 #pragma unroll

@@ -70,6 +70,8 @@ class DeviceIndex:
             id_rank = self._ranks_from_ids()
         self.id_rank = id_rank        # int32 [n_slots_pad] (uint32 bits)
         self.slot_of_rank = self._inverse_ranks(id_rank)  # int32 [n_slots_pad] or None
+        self.id_of_rank = (self.item_ids[self.slot_of_rank.long()]  # int64 (u64 bits) or None
+                           if self.slot_of_rank is not None else None)
         if row_sum is None:
             row_sum = torch.empty(items.shape[0], dtype=torch.int32, device=items.device)
             _native.check(_native.lib().fb_row_sums(items.data_ptr(), items.shape[0], self.dim,
@@ -158,6 +160,8 @@ class DeviceIndex:
                                self.n_slots_pad, self.n_words, self.dim, self.dim_pad,
                                self.m_bits, self.k_hashes,
                                self.slot_of_rank.data_ptr() if self.slot_of_rank is not None
+                               else None,
+                               self.id_of_rank.data_ptr() if self.id_of_rank is not None
                                else None)
 
     def quantize_queries(self, queries: torch.Tensor) -> torch.Tensor:

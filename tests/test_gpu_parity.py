@@ -325,6 +325,31 @@ def test_sampling_path_large_k(fb):
             assert np.array_equal(scores, ref.scores), (flags, q)
 
 
+def test_config3_shape_batch1024_k20000(fb):
+    """Config-3 shape at 2M items: 1024 queries (four 256-query chunks of the scan kernel),
+    top-k 20000, the 4-attribute filter; sampled queries from every chunk vs brute force."""
+    from paper_2511_14881_b200 import _device, workload
+    wl = workload.make_workload(2_000_000, 1024, dim=128, seed=17)
+    idx = wl.index
+    op = fb.TopkOp(idx, 1024, 20000, np.array([[0, idx.n_slots]]))
+    out = op(wl.queries_q, wl.batch)
+    torch.cuda.synchronize()
+    assert _device is not None and out.count.shape[0] == 1024
+    items = idx.items.cpu().numpy()[:, : wl.dim]
+    valid = _device.u64_host(idx.valid)
+    ids_all = _device.u64_host(idx.item_ids)
+    planes = idx.bloom.planes
+    for q in (0, 255, 256, 600, 1023):
+        cf = wl.filters[q]
+        mask = orc.eval_compiled([(int(o), int(a)) for o, a in cf.ops],
+                                 [(f, v, qb.set_bits) for f, v, qb in cf.leaves], planes, valid)
+        ref = orc.brute_force_int8(items, ids_all, wl.queries_q[q, : wl.dim].cpu().numpy(),
+                                   20000, keep=orc.to_bool(mask, idx.n_slots))
+        ids, scores = out.host(q)
+        assert np.array_equal(ids, ref.item_ids), q
+        assert np.array_equal(scores, ref.scores), q
+
+
 def test_merge_topk_device(fb, rng):
     n_lists, B, k = 5, 3, 50
     scores = np.zeros((n_lists, B, k), np.int32)
@@ -408,8 +433,8 @@ def _to_expr(fb, t):
 
 
 @pytest.mark.parametrize("shape,nq", [("cnf_neg", 40), ("cnf_neg", 200), ("cnf_bins", 40),
-                                      ("cnf_bins", 256), ("cnf_wide", 40), ("cnf_wide", 150),
-                                      ("random_mixed", 40)])
+                                      ("cnf_bins", 256), ("cnf_bins", 300), ("cnf_wide", 40),
+                                      ("cnf_wide", 150), ("random_mixed", 40)])
 def test_tc_filter_modes_vs_oracle(fb, shape, nq):
     """CNF batches (with negated literals / NOT over groups) take the per-hit tensor-core
     epilogue: the fast form (<= 64 literal columns, <= 4 groups) or the general form (wide
