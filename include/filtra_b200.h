@@ -249,6 +249,15 @@ int fb_int8_dot_rows(const int8_t* rows, int64_t n_rows, int32_t dim, int32_t st
 int fb_dot_rows_f64(const float* rows, int64_t n_rows, int32_t dim, const float* vec,
                     double* out, void* stream);
 
+/* Device, multi-task re-scoring (config 5; retrieval.retrieve re-rank with the identity
+ * mixture-of-logits scorer, scoring.py:99-130, retrieval.py:180-186): for request b and task
+ * t, out[(b * n_tasks + t) * n_cand + c] = float64 dot of cache row rows[b * n_cand + c]
+ * (float32, dim wide) with users[(b * n_tasks + t) * dim ..], in numpy's pairwise order (so
+ * the scores are bit-identical to the reference); c >= count[b] gives 0. */
+int fb_task_dots_f64(const float* cache, int64_t n_rows, int32_t dim, const int64_t* rows,
+                     const int32_t* count, int64_t n_cand, const float* users, int32_t n_req,
+                     int32_t n_tasks, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

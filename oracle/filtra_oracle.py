@@ -351,3 +351,121 @@ def brute_force_int8(items_q: np.ndarray, item_ids: np.ndarray, query_q: np.ndar
         ids, scores = ids[idx], scores[idx]
     order = np.lexsort((ids, -scores.astype(np.int64)))[:topk]
     return OracleTopk(item_ids=ids[order], scores=scores[order].astype(np.int32))
+
+
+# --------------------------------------------------------------------------------------
+# multi-task retrieval: merge, re-scoring, value model, final top-k (config 5;
+# ref/retrieval.py:147-199, ref/scoring.py:61-130, ref/value_model.py:97-221)
+# --------------------------------------------------------------------------------------
+def merge_candidates(per_task: list, merge: str) -> np.ndarray:
+    """Union keeps any task's ids, intersection the common ones; ascending unique
+    (ref/retrieval.py:147-160)."""
+    if merge == "union":
+        out = per_task[0]
+        for ids in per_task[1:]:
+            out = np.union1d(out, ids)
+        return out
+    out = np.unique(per_task[0])
+    for ids in per_task[1:]:
+        out = np.intersect1d(out, ids, assume_unique=False)
+    return out
+
+
+def score_dot(user: np.ndarray, items: np.ndarray) -> np.ndarray:
+    """Identity mixture-of-logits = the f64 dot product, pairwise-summed per row
+    (ref/scoring.py:99-130 with identity projections; ref/vecmath.py:15-24)."""
+    items64 = np.atleast_2d(np.asarray(items, dtype=np.float32)).astype(np.float64)
+    return np.sum(items64 * np.asarray(user, dtype=np.float32).astype(np.float64), axis=1)
+
+
+def score_mlp(hidden, heads, task, user, items) -> np.ndarray:
+    """ReLU MLP on user||item, per-task linear head, f64 (ref/scoring.py:61-84)."""
+    items = np.atleast_2d(np.asarray(items, dtype=np.float32))
+    x = np.concatenate(
+        [np.broadcast_to(np.asarray(user, dtype=np.float64), (items.shape[0], len(user))),
+         items.astype(np.float64)], axis=1)
+    for w, b in hidden:
+        x = x @ w.astype(np.float64).T + b.astype(np.float64)
+        np.maximum(x, 0.0, out=x)
+    w, b = heads[task]
+    return x @ w.astype(np.float64) + float(b)
+
+
+def score_mol(components, gate_w, gate_b, user, items) -> np.ndarray:
+    """Softmax-gated sum of projected dot products, f64 (ref/scoring.py:87-119)."""
+    items64 = np.atleast_2d(np.asarray(items, dtype=np.float32)).astype(np.float64)
+    user64 = np.asarray(user, dtype=np.float32).astype(np.float64)
+    n = items64.shape[0]
+    dots = np.empty((n, len(components)), dtype=np.float64)
+    for j, (u_proj, i_proj) in enumerate(components):
+        u_p = u_proj.astype(np.float64) @ user64
+        i_p = items64 @ i_proj.astype(np.float64).T
+        dots[:, j] = np.sum(i_p * u_p, axis=1)
+    logits = (np.concatenate([np.broadcast_to(user64, (n, len(user64))), items64], axis=1)
+              @ gate_w.astype(np.float64).T + gate_b.astype(np.float64))
+    logits -= logits.max(axis=1, keepdims=True)
+    gates = np.exp(logits)
+    gates /= gates.sum(axis=1, keepdims=True)
+    return np.sum(gates * dots, axis=1)
+
+
+def value_model_eval(spec, task_scores: dict):
+    """JSON formula over per-item f64 arrays, strict (both if-branches evaluated); a zero
+    divisor in any lane raises ZeroDivisionError (ref/value_model.py:97-129, 164-213).
+    ``spec=None`` is the per-request mean of the tasks (ref/value_model.py:216-221)."""
+    if spec is None:
+        names = list(task_scores)
+        if len(names) == 1:
+            spec = {"op": "task", "task": names[0]}
+        else:
+            spec = {"op": "mul", "args": [{"op": "const", "value": 1.0 / len(names)},
+                                          {"op": "add", "args": [{"op": "task", "task": t}
+                                                                 for t in names]}]}
+
+    def walk(n):
+        op = n["op"]
+        if op == "const":
+            return float(n["value"])
+        if op == "task":
+            return np.asarray(task_scores[n["task"]], dtype=np.float64)
+        if op in ("add", "mul", "min", "max"):
+            acc = walk(n["args"][0])
+            for x in n["args"][1:]:
+                v = walk(x)
+                acc = (acc + v if op == "add" else acc * v if op == "mul"
+                       else np.minimum(acc, v) if op == "min" else np.maximum(acc, v))
+            return acc
+        if op == "sub":
+            return walk(n["args"][0]) - walk(n["args"][1])
+        if op == "div":
+            den = walk(n["args"][1])
+            if np.any(np.asarray(den) == 0.0):
+                raise ZeroDivisionError("division by zero in value model")
+            return walk(n["args"][0]) / den
+        if op == "clamp":
+            return np.clip(walk(n["args"][0]), float(n["lo"]), float(n["hi"]))
+        if op == "if":
+            c = n["cond"]
+            cmp = {"<": np.less, "<=": np.less_equal, ">": np.greater,
+                   ">=": np.greater_equal, "==": np.equal}[c["cmp"]]
+            return np.where(cmp(walk(c["left"]), walk(c["right"])), walk(n["then"]),
+                            walk(n["else"]))
+        raise ValueError(f"unknown formula op {op!r}")
+
+    return walk(spec)
+
+
+def retrieve(per_task_ids: list, merge: str, cache_ids: np.ndarray, cache_vectors: np.ndarray,
+             score_fn, task_names: list, users: np.ndarray, vm_spec, topk: int):
+    """Merge -> cache gather -> per-task scores -> value model -> (score desc, id asc)
+    top-k (ref/retrieval.py:163-199). ``score_fn(task, user, vectors)`` re-scores."""
+    merged = merge_candidates(per_task_ids, merge)
+    if len(merged) == 0:
+        return merged, np.empty(0), np.empty((0, len(task_names)))
+    row_of = {int(i): r for r, i in enumerate(cache_ids)}
+    vectors = cache_vectors[np.array([row_of[int(i)] for i in merged], dtype=np.int64)]
+    ts = {t: score_fn(t, users[j], vectors) for j, t in enumerate(task_names)}
+    final = np.asarray(value_model_eval(vm_spec, ts), dtype=np.float64)
+    order = np.lexsort((merged, -final))[:topk]
+    return (merged[order], final[order],
+            np.stack([ts[t][order] for t in task_names], axis=1))

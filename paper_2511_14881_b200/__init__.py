@@ -16,6 +16,8 @@ from .quantize import (QuantParams, QuantizedMatrix, compute_quant_params, dequa
                        int8_dot_rows, quantize_matrix, quantize_value, quantize_vector)
 from .retrieval import StageTimings, codesigned_search
 from .serve import ShardedSearch, _reduce_topk, shard_ranges
+from .overarch import (DeviceCache, DeviceScorer, MultiTaskOp, MultiTaskOutput, merge_device,
+                       retrieve, value_model_device)
 
 __version__ = "0.1.0"
 
@@ -29,5 +31,6 @@ __all__ = [
     "filtered_topk", "format_filter", "hash_positions", "hash_seed", "heuristic_bits",
     "int8_dot", "int8_dot_rows", "merge_topk", "parse_filter", "positions_from_seed",
     "probe_centroids", "quantize_matrix", "quantize_value", "quantize_vector", "search",
-    "search_clusters", "shard_ranges",
+    "search_clusters", "shard_ranges", "DeviceCache", "DeviceScorer", "MultiTaskOp",
+    "MultiTaskOutput", "merge_device", "retrieve", "value_model_device",
 ]

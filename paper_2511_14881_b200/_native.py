@@ -46,6 +46,7 @@ EXPORTED = (
     "fb_topk_plan_destroy", "fb_topk_plan_stats", "fb_topk_execute", "fb_merge_topk",
     "fb_dequant_scores", "fb_int8_dot_rows", "fb_dot_rows_f64", "fb_launch_count",
     "fb_topk_set_timing", "fb_topk_last_timing", "fb_topk_scan_path", "fb_debug_tc_scores",
+    "fb_task_dots_f64",
 )
 
 
@@ -134,6 +135,7 @@ def _declare(lib) -> None:
         "fb_dequant_scores": ([c_vp, c_vp, c_vp, i32, i32, c_vp, i32, dbl, dbl, c_vp, c_vp], i32),
         "fb_int8_dot_rows": ([c_vp, i64, i32, i32, c_vp, c_vp, c_vp], i32),
         "fb_dot_rows_f64": ([c_vp, i64, i32, c_vp, c_vp, c_vp], i32),
+        "fb_task_dots_f64": ([c_vp, i64, i32, c_vp, c_vp, i64, c_vp, i32, i32, c_vp, c_vp], i32),
         "fb_launch_count": ([], ctypes.c_uint64),
         "fb_topk_scan_path": ([c_vp], i32),
         "fb_debug_tc_scores": ([ctypes.POINTER(FbIndex), c_vp, i32, c_vp, c_vp], i32),

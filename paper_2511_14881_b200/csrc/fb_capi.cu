@@ -585,6 +585,15 @@ int fb_dot_rows_f64(const float* rows, int64_t n_rows, int32_t dim, const float*
   return launch_dot_rows_f64(rows, n_rows, dim, vec, out, static_cast<cudaStream_t>(stream));
 }
 
+int fb_task_dots_f64(const float* cache, int64_t n_rows, int32_t dim, const int64_t* rows,
+                     const int32_t* count, int64_t n_cand, const float* users, int32_t n_req,
+                     int32_t n_tasks, double* out, void* stream) {
+  if (dim < 0 || n_rows < 0 || n_cand < 0 || n_req < 0 || n_tasks < 0)
+    return fail(FB_ERR_INVALID, "negative size");
+  return launch_task_dots_f64(cache, n_rows, dim, rows, count, n_cand, users, n_req, n_tasks,
+                              out, static_cast<cudaStream_t>(stream));
+}
+
 int fb_dequant_scores(const int32_t* scores, const int32_t* item_row_sum, const int32_t* query_sum,
                       int32_t n_queries, int32_t k, const int32_t* count, int32_t dim, double gmin,
                       double gmax, double* out, void* stream) {

@@ -147,6 +147,9 @@ int launch_quantize(const float* x, int64_t rows, int cols, double gmin, double 
                     int out_stride, cudaStream_t s);
 int launch_dot_rows_i8(const int8_t* rows, int64_t n, int dim, int stride, const int8_t* vec,
                        int32_t* out, cudaStream_t s);
+int launch_task_dots_f64(const float* cache, int64_t n_rows, int dim, const int64_t* rows,
+                         const int32_t* count, int64_t n_cand, const float* users, int n_req,
+                         int n_tasks, double* out, cudaStream_t s);
 int launch_dot_rows_f64(const float* rows, int64_t n, int dim, const float* vec, double* out,
                         cudaStream_t s);
 int launch_row_sums(const int8_t* x, int64_t rows, int cols, int stride, int32_t* out,

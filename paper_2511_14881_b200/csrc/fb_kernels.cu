@@ -158,6 +158,25 @@ __global__ void k_dot_rows_f64(const float* __restrict__ x, int64_t rows, int di
     out[r] = __dadd_rn(0.0, pairwise_f64(x + r * dim, v, dim));
 }
 
+// Multi-task re-scoring: one thread per (request, candidate) computes the candidate's
+// dot with every task's user vector (numpy pairwise order, float64).
+__global__ void k_task_dots_f64(const float* __restrict__ cache, int64_t n_rows, int dim,
+                                const int64_t* __restrict__ rows, const int32_t* __restrict__ count,
+                                int64_t n_cand, const float* __restrict__ users, int n_req,
+                                int n_tasks, double* __restrict__ out) {
+  const int64_t total = (int64_t)n_req * n_cand;
+  for (int64_t g = grid_tid(); g < total; g += grid_stride()) {
+    const int64_t b = g / n_cand, c = g - b * n_cand;
+    const int64_t r = rows[g];
+    const bool ok = c < count[b] && r >= 0 && r < n_rows;
+    for (int t = 0; t < n_tasks; ++t) {
+      const int64_t o = (b * n_tasks + t) * n_cand + c;
+      out[o] = ok ? __dadd_rn(0.0, pairwise_f64(cache + r * dim, users + (b * n_tasks + t) * dim, dim))
+                  : 0.0;
+    }
+  }
+}
+
 __global__ void k_row_sums(const int8_t* __restrict__ x, int64_t rows, int cols, int stride,
                            int32_t* __restrict__ out) {
   for (int64_t r = grid_tid(); r < rows; r += grid_stride()) {
@@ -986,6 +1005,17 @@ int launch_dot_rows_f64(const float* rows, int64_t n, int dim, const float* vec,
   if (n <= 0) return FB_OK;
   k_dot_rows_f64<<<grid_for(n, 128), 128, 0, s>>>(rows, n, dim, vec, out);
   FB_LAUNCH_CHECK("k_dot_rows_f64");
+  return FB_OK;
+}
+
+int launch_task_dots_f64(const float* cache, int64_t n_rows, int dim, const int64_t* rows,
+                         const int32_t* count, int64_t n_cand, const float* users, int n_req,
+                         int n_tasks, double* out, cudaStream_t s) {
+  const int64_t total = (int64_t)n_req * n_cand;
+  if (total <= 0 || n_tasks <= 0) return FB_OK;
+  k_task_dots_f64<<<grid_for(total, 128), 128, 0, s>>>(cache, n_rows, dim, rows, count, n_cand,
+                                                       users, n_req, n_tasks, out);
+  FB_LAUNCH_CHECK("k_task_dots_f64");
   return FB_OK;
 }
 

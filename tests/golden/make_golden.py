@@ -14,7 +14,9 @@ Functions exercised (reference ``pkg/src/filtra``):
   bloom_eval_leaf (160-181), filter_query.compile_filter / eval_compiled
   (280-356), quantize.quantize_vector (72-76), ivf.build_ivf / probe_centroids /
   search_clusters / search (207-343), retrieval.codesigned_search (110-144),
-  serve._reduce_topk (98-100), evaluation.brute_force_topk (45-69).
+  serve._reduce_topk (98-100), evaluation.brute_force_topk (45-69),
+  retrieval.merge_candidates / retrieve (147-199), scoring (61-130),
+  value_model (97-221).
 """
 
 from __future__ import annotations
@@ -347,6 +349,107 @@ def gen_merge(filtra):
     print("merge_cases.npz")
 
 
+VM_SPECS = [
+    None,  # per-request mean of the task scores (ref/value_model.py:216-221)
+    {"op": "add", "args": [
+        {"op": "mul", "args": [{"op": "const", "value": 0.5}, {"op": "task", "task": "t0"}]},
+        {"op": "mul", "args": [{"op": "const", "value": 0.3}, {"op": "task", "task": "t1"}]},
+        {"op": "clamp", "lo": -0.1, "hi": 0.4, "args": [{"op": "task", "task": "t2"}]},
+        {"op": "if", "cond": {"left": {"op": "task", "task": "t3"}, "cmp": ">",
+                              "right": {"op": "const", "value": 0.2}},
+         "then": {"op": "max", "args": [{"op": "task", "task": "t0"},
+                                        {"op": "task", "task": "t3"}]},
+         "else": {"op": "div", "args": [{"op": "sub", "args": [{"op": "task", "task": "t1"},
+                                                               {"op": "const", "value": 1.0}]},
+                                        {"op": "const", "value": 4.0}]}}]},
+]
+
+
+def gen_retrieve(filtra):
+    """Config-5 shape: multi-task requests (4 towers sharing one filter), exhaustive
+    co-designed search per task, merge, identity-MoL (f64 dot) / MLP / MoL re-scoring,
+    value-model aggregation, final (score desc, id asc) top-k
+    (ref/retrieval.py:147-199, scoring.py:61-130, value_model.py:164-221)."""
+    from filtra.catalog import default_features_spec, synth_catalog
+    from filtra.retrieval import (MERGE_INTERSECTION, MERGE_UNION, RetrievalRequest,
+                                  TaskQuery, merge_candidates, retrieve)
+    from filtra.scoring import LinearHead, MlpScorer, MolScorer
+    from filtra.snapshot import PublishConfig, build_engine
+    from filtra.value_model import parse_value_model
+    dim = 32
+    cat = synth_catalog(6000, dim, 12, default_features_spec(), seed=31, blob_std=0.08)
+    rng = np.random.default_rng(5)
+    mlp = MlpScorer(hidden=((rng.standard_normal((16, 2 * dim)).astype(np.float32) * 0.2,
+                             rng.standard_normal(16).astype(np.float32) * 0.1),),
+                    heads={f"t{i}": LinearHead(rng.standard_normal(16).astype(np.float32),
+                                               float(rng.standard_normal())) for i in range(4)})
+    mol = MolScorer(components=tuple((rng.standard_normal((8, dim)).astype(np.float32) * 0.3,
+                                      rng.standard_normal((8, dim)).astype(np.float32) * 0.3)
+                                     for _ in range(3)),
+                    gate_weight=rng.standard_normal((3, 2 * dim)).astype(np.float32) * 0.2,
+                    gate_bias=rng.standard_normal(3).astype(np.float32) * 0.1)
+    arrays, meta = {}, []
+    base = build_engine(cat, PublishConfig(n_clusters=1, seed=31))
+    arrays["items_q"] = base.ivf.items_q.data
+    arrays["valid"] = base.ivf.valid_mask
+    arrays["item_ids"] = base.ivf.item_ids
+    arrays["offsets"] = base.ivf.cluster_offsets
+    arrays["planes"] = base.bloom.planes
+    arrays["qp"] = np.array([base.ivf.items_q.params.global_min,
+                             base.ivf.items_q.params.global_max])
+    arrays["cache_ids"] = base.cache.item_ids
+    arrays["cache_vectors"] = base.cache.vectors
+    arrays["mlp_w"] = mlp.hidden[0][0]
+    arrays["mlp_b"] = mlp.hidden[0][1]
+    for i in range(4):
+        arrays[f"mlp_head{i}_w"] = mlp.heads[f"t{i}"].weight
+        arrays[f"mlp_head{i}_b"] = np.array([mlp.heads[f"t{i}"].bias])
+    for j, (u, it) in enumerate(mol.components):
+        arrays[f"mol_u{j}"] = u
+        arrays[f"mol_i{j}"] = it
+    arrays["mol_gw"] = mol.gate_weight
+    arrays["mol_gb"] = mol.gate_bias
+    engines = {"dot": base}
+    for name, sc in (("mlp", mlp), ("mol", mol)):
+        e = build_engine(cat, PublishConfig(n_clusters=1, seed=31, scorer=sc))
+        assert np.array_equal(e.ivf.items_q.data, base.ivf.items_q.data)
+        engines[name] = e
+    r = 0
+    for scorer_name in ("dot", "mlp", "mol"):
+        for vi, spec in enumerate(VM_SPECS):
+            for merge in (MERGE_UNION, MERGE_INTERSECTION):
+                if scorer_name != "dot" and merge == MERGE_INTERSECTION:
+                    continue
+                expr = four_attribute_expr(rng)
+                tasks = tuple(TaskQuery(f"t{i}", cat.embeddings[int(rng.integers(len(cat)))])
+                              for i in range(4))
+                vm = parse_value_model(spec) if spec is not None else None
+                req = RetrievalRequest(tasks=tasks, filter=expr, nprobe=1, k0=300, topk=100,
+                                       merge=merge, value_model=vm)
+                res = retrieve(engines[scorer_name], req)
+                pre = f"r{r}_"
+                arrays[pre + "users"] = np.stack([t.user_embedding for t in tasks])
+                arrays[pre + "ids"] = np.array([it.item_id for it in res.items], dtype=np.uint64)
+                arrays[pre + "scores"] = np.array([it.score for it in res.items])
+                arrays[pre + "task_scores"] = np.array(
+                    [[it.task_scores[f"t{i}"] for i in range(4)] for it in res.items])
+                meta.append({"r": r, "scorer": scorer_name, "vm": spec, "merge": merge,
+                             "expr": expr_to_json(expr), "k0": 300, "topk": 100})
+                r += 1
+    # merge_candidates algebra
+    for c in range(4):
+        lists = [np.sort(rng.choice(500, size=int(rng.integers(0, 80)), replace=False)).astype(np.uint64)
+                 for _ in range(int(rng.integers(1, 5)))]
+        for li, x in enumerate(lists):
+            arrays[f"m{c}_l{li}"] = x
+        arrays[f"m{c}_union"] = merge_candidates(lists, MERGE_UNION)
+        arrays[f"m{c}_inter"] = merge_candidates(lists, MERGE_INTERSECTION)
+        arrays[f"m{c}_n"] = np.array([len(lists)])
+    np.savez_compressed(OUT / "retrieve_cases.npz", **arrays)
+    (OUT / "retrieve_meta.json").write_text(json.dumps(meta))
+    print("retrieve_cases.npz", len(meta))
+
+
 def main():
     filtra = _import_reference()
     gen_hash(filtra)
@@ -357,6 +460,7 @@ def main():
     gen_four_attr(filtra)
     gen_topk20000(filtra)
     gen_merge(filtra)
+    gen_retrieve(filtra)
 
 
 if __name__ == "__main__":

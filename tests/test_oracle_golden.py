@@ -143,3 +143,52 @@ def test_reduce_topk_matches_reference():
     for c in range(int(z["n_cases"][0])):
         ids, sc = orc.reduce_topk(z[f"c{c}_ids"], z[f"c{c}_scores"], int(z[f"c{c}_k"][0]))
         assert np.array_equal(ids, z[f"c{c}_rids"]) and np.array_equal(sc, z[f"c{c}_rscores"])
+
+
+def _retrieve_fixture():
+    z = load_npz("retrieve_cases.npz")
+    meta = load_json("retrieve_meta.json")
+    return z, meta
+
+
+def oracle_score_fn(z, scorer):
+    if scorer == "dot":
+        return lambda t, u, v: orc.score_dot(u, v)
+    if scorer == "mlp":
+        hidden = [(z["mlp_w"], z["mlp_b"])]
+        heads = {f"t{i}": (z[f"mlp_head{i}_w"], float(z[f"mlp_head{i}_b"][0])) for i in range(4)}
+        return lambda t, u, v: orc.score_mlp(hidden, heads, t, u, v)
+    comps = [(z[f"mol_u{j}"], z[f"mol_i{j}"]) for j in range(3)]
+    return lambda t, u, v: orc.score_mol(comps, z["mol_gw"], z["mol_gb"], u, v)
+
+
+def test_oracle_retrieve_matches_reference():
+    """Config-5 pipeline: per-task exhaustive co-designed search, merge, re-score, value
+    model, final top-k -- the oracle reproduces the reference's ids and floats exactly."""
+    z, meta = _retrieve_fixture()
+    items = z["items_q"]
+    qp = (float(z["qp"][0]), float(z["qp"][1]))
+    for m in meta:
+        pre = f"r{m['r']}_"
+        users = z[pre + "users"]
+        prog = orc.compile_expr(json_to_oracle_expr(m["expr"]), 1024, 5)
+        per_task = []
+        for j in range(4):
+            qq = orc.quantize(users[j], *qp)
+            res = orc.codesigned_search(items, z["valid"], z["item_ids"], z["offsets"], z["planes"],
+                                        prog, qq, [0], m["k0"])
+            per_task.append(res.item_ids)
+        ids, final, ts = orc.retrieve(per_task, m["merge"], z["cache_ids"], z["cache_vectors"],
+                                      oracle_score_fn(z, m["scorer"]), [f"t{i}" for i in range(4)],
+                                      users, m["vm"], m["topk"])
+        assert np.array_equal(ids, z[pre + "ids"]), m["r"]
+        assert np.array_equal(final, z[pre + "scores"]), m["r"]
+        assert np.array_equal(ts, z[pre + "task_scores"]), m["r"]
+
+
+def test_oracle_merge_candidates_matches_reference():
+    z = load_npz("retrieve_cases.npz")
+    for c in range(4):
+        lists = [z[f"m{c}_l{i}"] for i in range(int(z[f"m{c}_n"][0]))]
+        assert np.array_equal(orc.merge_candidates(lists, "union"), z[f"m{c}_union"])
+        assert np.array_equal(orc.merge_candidates(lists, "intersection"), z[f"m{c}_inter"])
