@@ -2,6 +2,7 @@
 """Filtered int8 top-k throughput on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 2|3|4|5]
 
 N=1 runs BASELINE config 2 (10M items x 128-d int8, batch 256, top-k 10000, the
 "4-attribute" Bloom filter, ~10% selectivity). Under torchrun (N>1) every rank owns
@@ -12,6 +13,12 @@ A step = one batch of B queries: quantise the float queries + sample + threshold
 fused Bloom-filter/int8 scan + exactness check + exact top-k selection (+ exchange
 and merge for N>1). Inputs (1.28 GB of int8 rows + 1.28 GB of planes per GPU) are far
 larger than the 126 MB L2, so no explicit flush is needed between steps.
+
+``--config`` selects another BASELINE.json configuration (the default run is config 2):
+3 = 12.5M items/GPU, batch 1024, top-k 20000 (100M over 8 GPUs under torchrun);
+4 = the filter-selectivity sweep at 10M (one JSON line per selectivity);
+5 = multi-task retrieval: 64 requests x 4 query towers sharing a filter, k0 = topk = 5000,
+merge + float64 re-scoring + value model (metric: requests/s).
 
 ``--impl reference`` times the reference algorithm (the CPU oracle port in
 ``oracle/``, a NumPy restatement of reference ivf.search_clusters / retrieval
@@ -48,19 +55,26 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--items", type=int, default=10_000_000, help="items per GPU")
-    ap.add_argument("--batch", type=int, default=256)
-    ap.add_argument("--k", type=int, default=10_000)
+    ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2)
+    ap.add_argument("--items", type=int, default=None, help="items per GPU")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--dim", type=int, default=128)
     ap.add_argument("--simt", action="store_true", help="force the SIMT scan kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=0, help="CPU sample size (0: auto)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    items, batch, k = {2: (10_000_000, 256, 10_000), 3: (12_500_000, 1024, 20_000),
+                       4: (10_000_000, 256, 10_000), 5: (10_000_000, 64, 5_000)}[a.config]
+    a.items = items if a.items is None else a.items
+    a.batch = batch if a.batch is None else a.batch
+    a.k = k if a.k is None else a.k
+    return a
 
 
 def workload_desc(a, n_gpus):
     return {
-        "workload": (f"config2: {a.items / 1e6:g}M items/GPU x {a.dim}-d int8, batch "
+        "workload": (f"config{a.config}: {a.items / 1e6:g}M items/GPU x {a.dim}-d int8, batch "
                      f"{a.batch}, top-k {a.k}, 4-attribute Bloom filter (M=1024, K=5)"),
         "items_total": a.items * n_gpus, "items_per_gpu": a.items, "batch": a.batch,
         "k": a.k, "dim": a.dim, "bloom_m": 1024, "bloom_k": 5,
@@ -493,10 +507,150 @@ def run_reference(a):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------------------------
+# config 4: filter-selectivity sweep; config 5: multi-task retrieval
+# ------------------------------------------------------------------------------------
+SWEEP = (0.01, 0.02, 0.05, 0.10, 0.20, 0.50, 1.0)
+
+
+def sweep_sizes(p, cards=(50, 50, 40, 30)):
+    """|S_g| per group so that the 4-group AND passes ~p of the items (each item holds
+    two values per feature: one group passes 1 - (1 - s)^2)."""
+    s = 1.0 - math.sqrt(1.0 - p ** 0.25)
+    return tuple(max(1, min(c, round(s * c))) for c in cards)
+
+
+def device_loop(step, steps, warmup, stream, local):
+    import torch
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    with ClockSampler(local) as clocks:
+        clocks.wait_ready()
+        t0 = time.perf_counter()
+        ev[0].record(stream)
+        for i in range(steps):
+            step()
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+        clocks.mark(t0, time.perf_counter())
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    return ev[0].elapsed_time(ev[steps]), per, clocks.summary()
+
+
+def run_sweep(a):
+    import torch
+    from paper_2511_14881_b200 import _native, workload
+    from paper_2511_14881_b200.bloom import BloomParams
+    from paper_2511_14881_b200.engine import TopkOp
+    from paper_2511_14881_b200.filter_query import FilterBatch, compile_filter
+    torch.cuda.set_device(0)
+    lib = _native.lib()
+    B, k = a.batch, a.k
+    wl = workload.make_workload(a.items, B, dim=a.dim, seed=1)
+    idx = wl.index
+    op = TopkOp(idx, B, k, np.array([[0, idx.n_slots]]))
+    outs = op.alloc_outputs()
+    stream = torch.cuda.current_stream()
+    for p in SWEEP:
+        if p >= 1.0:
+            batch, sizes, sel = None, None, 1.0
+        else:
+            sizes = sweep_sizes(p)
+            rng = np.random.default_rng(7)
+            filters = [compile_filter(workload.four_attribute_filter(rng, sizes), BloomParams())
+                       for _ in range(B)]
+            batch = FilterBatch.pack(filters, BloomParams()).to_device()
+            m = FilterBatch.pack(filters[:8], BloomParams()).evaluate(idx.bloom, idx.valid, 0,
+                                                                      idx.n_words)
+            sel = float(np.unpackbits(m.view(np.uint8)).sum()) / (8 * a.items)
+        total, per, clocks = device_loop(lambda: op(wl.queries_q, batch, out=outs), a.steps,
+                                         a.warmup, stream, 0)
+        lib.fb_topk_set_timing(op._plan, 1)
+        op(wl.queries_q, batch, out=outs)
+        import ctypes
+        e_ms, s_ms = ctypes.c_float(), ctypes.c_float()
+        _native.check(lib.fb_topk_last_timing(op._plan, ctypes.byref(e_ms), ctypes.byref(s_ms)))
+        lib.fb_topk_set_timing(op._plan, 0)
+        cfg = workload_desc(a, 1)
+        cfg.update({"filter": ("none (100% pass)" if sizes is None else
+                               f"AND of 4 OR-groups, |S|={sizes}"),
+                    "selectivity_target": p, "selectivity_measured": round(sel, 4)})
+        print(json.dumps({
+            "metric": METRIC, "value": round(B * a.steps / (total / 1e3), 2), "unit": UNIT,
+            "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": round(total / a.steps, 4), "p50_ms": round(float(np.median(per)), 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic", "config": cfg, "emit_ms": round(e_ms.value, 4),
+            "select_ms": round(s_ms.value, 4), "clocks": clocks,
+            "scan_kernel": "tc" if lib.fb_topk_scan_path(op._plan) else "simt"}), flush=True)
+
+
+def run_multitask(a):
+    import torch
+    from paper_2511_14881_b200 import _device, _native, workload
+    from paper_2511_14881_b200.overarch import DeviceCache, MultiTaskOp
+    torch.cuda.set_device(0)
+    lib = _native.lib()
+    R, T, k = a.batch, 4, a.k
+    tasks = [f"task{t}" for t in range(T)]
+    wl = workload.make_workload(a.items, R * T, dim=a.dim, seed=1)
+    idx = wl.index
+    dev = idx.items.device
+    vecs = workload.make_items(a.items, a.dim, 1, dev)     # float32 cache = the item tower
+    cache = DeviceCache(_device.u64_host(idx.item_ids)[: a.items], vecs)
+    del vecs
+    op = MultiTaskOp(idx, cache, R, tasks, k, k)  # value model: mean of the task scores
+    filters = [wl.filters[r * T] for r in range(R)]
+    batch = op.pack_filters(filters).to_device()
+    users = wl.queries.view(R, T, -1)
+    stream = torch.cuda.current_stream()
+    launches0 = lib.fb_launch_count()
+    total, per, clocks = device_loop(lambda: op(users, batch), a.steps, a.warmup, stream, 0)
+    launches = int(lib.fb_launch_count() - launches0) * a.steps // (a.steps + a.warmup)
+    # e2e: pinned host task embeddings + filter arrays in, final ids / scores out
+    host_u = users.cpu().pin_memory()
+    h_prog = [torch.from_numpy(x).pin_memory() for x in batch.host_arrays()]
+    du = torch.empty_like(users)
+    out_ids = torch.empty((R, k), dtype=torch.int64).pin_memory()
+    out_sc = torch.empty((R, k), dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        du.copy_(host_u, non_blocking=True)
+        for d, h in zip(batch._dev, h_prog):
+            d.copy_(h, non_blocking=True)
+        res = op(du, batch)
+        out_ids.copy_(res.ids, non_blocking=True)
+        out_sc.copy_(res.scores, non_blocking=True)
+
+    e2e_total, _, _ = device_loop(e2e_step, a.steps, 2, stream, 0)
+    h2d = host_u.numel() * 4 + sum(h.numel() * h.element_size() for h in h_prog)
+    cfg = {"workload": (f"config5: {a.items / 1e6:g}M items x {a.dim}-d int8, {R} requests x "
+                        f"{T} query towers sharing a 4-attribute filter, k0 = topk = {k}, "
+                        "union merge, identity-MoL float64 re-scoring, mean-of-tasks value model"),
+           "requests": R, "towers": T, "k0": k, "topk": k, "items": a.items, "dim": a.dim,
+           "l2": "inputs far larger than the 126 MB L2; no flush needed"}
+    print(json.dumps({
+        "metric": "multi-task filtered retrieval requests/sec (4 towers, OverArch value model)",
+        "value": round(R * a.steps / (total / 1e3), 2), "unit": "requests/s", "n_gpus": 1,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(total / a.steps, 4),
+        "p50_ms": round(float(np.median(per)), 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8 scan, float64 re-scoring", "data": "synthetic",
+        "config": cfg, "gpu_launches": launches, "clocks": clocks,
+        "e2e": {"value": round(R * a.steps / (e2e_total / 1e3), 2), "unit": "requests/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": R * k * 16,
+                "ms_per_step": round(e2e_total / a.steps, 4)}}), flush=True)
+
+
 def main():
     a = parse_args()
     if a.impl == "reference":
         run_reference(a)
+    elif a.config == 4:
+        run_sweep(a)
+    elif a.config == 5:
+        run_multitask(a)
     else:
         run_ours(a)
 

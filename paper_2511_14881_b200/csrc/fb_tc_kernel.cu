@@ -944,7 +944,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
       const int2 wk = a.work[i * a.work_stride];
       const int64_t tile = wk.x;
-      const uint32_t id_s = su32(smem + a.off_id) + (uint32_t)s * (kTileItems * 4u) +
+      const uint32_t id_s = su32(smem + a.off_id) + (uint32_t)s * kStageMeta +
                             (uint32_t)(half * 128) * 4u;
       const int64_t s0 = a.ranges[2 * wk.y], s1 = a.ranges[2 * wk.y + 1];
       const int64_t wbase = tile * kTileWords + 2 * half;

@@ -350,6 +350,42 @@ def test_config3_shape_batch1024_k20000(fb):
         assert np.array_equal(scores, ref.scores), q
 
 
+@pytest.mark.parametrize("filtered", [False, True])
+def test_bytecode_kernel_multi_tile_per_cta(fb, filtered):
+    """Enough tiles that every CTA cycles through all item stages (the per-stage id-rank
+    area is found at the right offset), unfiltered (no program) and with a non-CNF
+    program batch; vs brute force."""
+    from paper_2511_14881_b200 import _device, workload
+    from paper_2511_14881_b200.filter_query import FilterBatch
+    wl = workload.make_workload(300_000, 16, dim=128, seed=23, filtered=False)
+    idx = wl.index
+    batch = None
+    filters = [None] * 16
+    if filtered:
+        rng = np.random.default_rng(8)
+        filters = [fb.compile_filter(_to_expr(fb, _random_filter(rng)), fb.BloomParams())
+                   for _ in range(16)]
+        batch = FilterBatch.pack(filters, fb.BloomParams())
+        assert not batch.is_cnf
+    op = fb.TopkOp(idx, 16, 2000, np.array([[0, idx.n_slots]]))
+    out = op(wl.queries_q, batch)
+    torch.cuda.synchronize()
+    items = idx.items.cpu().numpy()[:, :128]
+    valid = _device.u64_host(idx.valid)
+    ids_all = _device.u64_host(idx.item_ids)
+    for q in range(16):
+        keep = orc.to_bool(valid, idx.n_slots)
+        if filters[q] is not None:
+            cf = filters[q]
+            m = orc.eval_compiled([(int(o), int(a)) for o, a in cf.ops],
+                                  [(f, v, b.set_bits) for f, v, b in cf.leaves], idx.bloom.planes, valid)
+            keep = orc.to_bool(m, idx.n_slots)
+        ref = orc.brute_force_int8(items, ids_all, wl.queries_q[q, :128].cpu().numpy(), 2000, keep=keep)
+        ids, scores = out.host(q)
+        assert np.array_equal(ids, ref.item_ids), q
+        assert np.array_equal(scores, ref.scores), q
+
+
 def test_merge_topk_device(fb, rng):
     n_lists, B, k = 5, 3, 50
     scores = np.zeros((n_lists, B, k), np.int32)
