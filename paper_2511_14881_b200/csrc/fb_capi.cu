@@ -249,7 +249,10 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
     }
   }
   p->n_tc_work = (int64_t)tc_work.size() / 2;
-  const int64_t want = std::max<int64_t>(2LL * k + 2048, 8192);
+  // candidate buffer: room for the sampling threshold's spread; while the exact radix
+  // selection applies (k <= 10240) up to its staging capacity
+  int64_t want = std::max<int64_t>(2LL * k + 2048, 8192);
+  if (k <= 10240) want = std::max<int64_t>(want, std::min<int64_t>(kSelectMaxCand, (8LL * k) / 3));
   p->cap = (int32_t)std::max<int64_t>(1, std::min<int64_t>(p->total_slots, want));
   // sampling pass only when the candidate buffer cannot simply hold everything
   if (!(flags & FB_PLAN_NO_SAMPLE) && p->total_slots > p->cap && k > 0) {
@@ -272,6 +275,11 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
       const int64_t st = (p->n_tc_work + p->tc_sample_stride - 1) / p->tc_sample_stride;
       p->tc_sample_fraction = (double)st / (double)p->n_tc_work;
     }
+    // keep every eligible sampled key up to the whole sample (an unfiltered query keeps
+    // ~N/128): the threshold's rank estimate stays precise at any selectivity
+    const double f = p->n_tc_work > 0 ? p->tc_sample_fraction : p->sample_fraction;
+    const int64_t want_s = (int64_t)((double)p->total_slots * f * 1.05) + 1024;
+    p->sample_cap = (int32_t)std::min<int64_t>(std::max<int64_t>(16384, want_s), 1 << 18);
   }
   const int64_t B = std::max(1, n_queries);
   const int64_t nr = std::max(1, p->n_ranges);
@@ -354,7 +362,13 @@ int fb_topk_plan_stats(const fb_topk_plan_t* plan, fb_stats_t* st) {
     st->max_tile_rows = std::max<int64_t>(st->max_tile_rows, std::min<int64_t>(len, 128));
   }
   st->slots_evaluated = plan->total_words * 64;
-  st->fallback_queries = 0;
+  // queries the last execute sent through the exact fallback (synchronises the device)
+  uint32_t flagged = 0;
+  if (plan->d_active != nullptr &&
+      cudaMemcpy(&flagged, plan->d_active + 2, sizeof(uint32_t), cudaMemcpyDeviceToHost) !=
+          cudaSuccess)
+    return fail(FB_ERR_CUDA, "reading the fallback counter failed");
+  st->fallback_queries = flagged;
   return FB_OK;
 }
 
@@ -405,6 +419,7 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
     t.n_queries = p->B;
     t.k = k;
     t.sample_cap = p->sample_cap;
+    t.cap = p->cap;
     t.sample_key = p->d_sample_key;
     t.sample_cnt = p->d_sample_cnt;
     t.sample_fraction = !p->sample_stride ? 0.0

@@ -193,6 +193,7 @@ struct ThresholdArgs {
   int32_t n_queries;
   int32_t k;
   int32_t sample_cap;
+  int32_t cap;                 // emit-pass candidate capacity per query
   const uint64_t* sample_key;  // [B, sample_cap]
   const uint32_t* sample_cnt;  // [B] eligible keys seen (may exceed cap)
   double sample_fraction;      // sampled slots / scanned slots (0 -> no sample: T = 0)
@@ -201,6 +202,8 @@ struct ThresholdArgs {
   uint32_t* elig;              // [B] zeroed
 };
 int launch_threshold(const ThresholdArgs& a, cudaStream_t s);
+// candidate capacity the exact radix selection can take per query (keys staged in smem)
+constexpr int32_t kSelectMaxCand = 26624;
 
 int launch_check(int32_t n_queries, int32_t k, int32_t cap, const uint32_t* cnt,
                  const uint64_t* thr, int force, Fallback* fb, uint32_t* active_count,

@@ -14,6 +14,9 @@
 
 #include "fb_internal.cuh"
 
+#include <algorithm>
+#include <cstdio>
+
 namespace fb {
 
 namespace {
@@ -314,9 +317,14 @@ __device__ __forceinline__ int pow2_ceil(int n) {
   return p;
 }
 
-// Per query: sort the sampled keys and pick the key whose estimated full-scan rank is
-// ~1.5k + 3 sqrt(k) + 64, so the emit pass keeps every key of the true top-k with
-// overwhelming probability (the check/fallback keeps the answer exact regardless).
+// Per query: radix-select the sampled key of rank jd from the top, where mu = k * f_eff is
+// the expected sample rank of the true k-th key (f_eff = the sampled fraction times the
+// kept share of the eligible sample keys) and jd sits between mu and the emit capacity
+// with >= 5 sigma on each side when the sample allows, so the emit pass keeps every key
+// of the true top-k and fits the buffer with overwhelming probability at any selectivity
+// (the check/fallback keeps the answer exact regardless). Samples that fit are staged in
+// shared memory; larger ones are re-read from global memory (L2) per digit pass.
+constexpr int kThrSmemKeys = 26624;  // 208 KB
 __global__ void __launch_bounds__(kSelectThreads) k_threshold(ThresholdArgs a) {
   extern __shared__ __align__(16) uint64_t s_key[];
   const int q = blockIdx.x;
@@ -330,14 +338,25 @@ __global__ void __launch_bounds__(kSelectThreads) k_threshold(ThresholdArgs a) {
     return;
   }
   const int nk = (int)min(ns, (uint32_t)a.sample_cap);
-  const double target = 1.5 * a.k + 3.0 * sqrt((double)a.k) + 64.0;
-  const double jd = target * a.sample_fraction * (double)nk / (double)ns;
+  // sample rank of the threshold: aim the expected candidate count at the middle of
+  // [k, cap], at least 5 sigma above the true k-th key, and (when possible) 5 sigma below
+  // the capacity
+  const double fe = a.sample_fraction * (double)nk / (double)ns;
+  const double mu = (double)a.k * fe;
+  const double cf = (double)a.cap * fe;
+  const double lo = mu + 5.0 * sqrt(mu) + 8.0;
+  const double hi = cf - 5.0 * sqrt(cf);
+  double jd = 0.5 * (mu + cf);
+  jd = jd > hi ? hi : jd;
+  jd = jd < lo ? lo : jd;
   if (jd >= (double)(nk - 1)) {
     if (threadIdx.x == 0) a.threshold[q] = 0ull;
     return;
   }
-  for (int i = threadIdx.x; i < nk; i += blockDim.x)
-    s_key[i] = a.sample_key[(int64_t)q * a.sample_cap + i];
+  const uint64_t* gkey = a.sample_key + (int64_t)q * a.sample_cap;
+  const bool staged = nk <= kThrSmemKeys;
+  if (staged)
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) s_key[i] = gkey[i];
   // radix select (8-bit digits, most significant first) of the key with exactly `jd`
   // larger keys: one histogram pass over the kept sample per digit
   __shared__ uint32_t hist[256];
@@ -352,7 +371,7 @@ __global__ void __launch_bounds__(kSelectThreads) k_threshold(ThresholdArgs a) {
     __syncthreads();
     const uint64_t prefix = s_prefix;
     for (int i = threadIdx.x; i < nk; i += blockDim.x) {
-      const uint64_t k = s_key[i];
+      const uint64_t k = staged ? s_key[i] : __ldcg(gkey + i);
       if (shift == 56 || ((k ^ prefix) >> (shift + 8)) == 0ull)
         atomicAdd(hist + ((k >> shift) & 0xFFu), 1u);
     }
@@ -405,6 +424,9 @@ __global__ void k_check(int n_queries, int k, int cap, const uint32_t* __restric
   f.shift = 52;
   f.above = 0;
   f.need = (uint64_t)k;
+#ifdef FB_CHECK_PRINT
+  printf("k_check: query %d count %u cap %d k %d flagged %d\n", q, c, cap, k, (int)(force || !ok));
+#endif
   if (force || !ok) {
     f.state = Q_FLAGGED;
     atomicAdd(active, 1u);
@@ -574,7 +596,7 @@ __global__ void __launch_bounds__(kSelectThreads) k_select(SelectArgs a) {
 constexpr int kRsThreads = 1024;
 constexpr int kRsIpt = 10;                         // sort capacity per thread
 constexpr int kRsMaxK = kRsThreads * kRsIpt;       // 10240
-constexpr int kRsMaxCand = 22528;                  // keys loaded per query (176 KB)
+constexpr int kRsMaxCand = kSelectMaxCand;         // keys loaded per query (208 KB)
 constexpr int kRsBits = 8;                         // LSD digit width
 constexpr int kRsDigits = 1 << kRsBits;
 constexpr int kRsWarps = kRsThreads / 32;
@@ -582,7 +604,8 @@ constexpr int kRsCntStride = kRsWarps + 1;          // u32 counters [digit][warp
 // the two sort buffers (2 x kRsMaxK keys) then the per-warp digit counters; the
 // candidate load area (kRsMaxCand keys) overlaps both and is dead once compacted
 constexpr size_t kRsCntOff = (size_t)2 * kRsMaxK * 8;
-constexpr size_t kRsSmem = kRsCntOff + (size_t)kRsDigits * kRsCntStride * 4;
+constexpr size_t kRsSmem = std::max(kRsCntOff + (size_t)kRsDigits * kRsCntStride * 4,
+                                    (size_t)kRsMaxCand * 8);
 static_assert(kRsSmem >= (size_t)kRsMaxCand * 8, "load area must fit");
 
 __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
@@ -1049,9 +1072,7 @@ int launch_scan_simt(const ScanArgs& a, cudaStream_t s) {
 
 int launch_threshold(const ThresholdArgs& a, cudaStream_t s) {
   if (a.n_queries <= 0) return FB_OK;
-  int n = 1;
-  while (n < a.sample_cap) n <<= 1;
-  const size_t smem = (size_t)n * sizeof(uint64_t);
+  const size_t smem = (size_t)std::min(a.sample_cap, kThrSmemKeys) * sizeof(uint64_t);
   FB_CUDA(cudaFuncSetAttribute(k_threshold, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   k_threshold<<<a.n_queries, kSelectThreads, smem, s>>>(a);
