@@ -460,32 +460,34 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
     rc = emit(ea);
     if (rc) return rc;
     if (p->timing) FB_CUDA(cudaEventRecord(p->ev[1], s));
-    // 4) exactness check; 5) fallback: radix-narrow the key window (<= 6 passes, each a
-    //    no-op unless some query was flagged), then re-emit the resolved queries
+    // 4) exactness check; 5) fallback, one cooperative launch that only reads a flag
+    //    unless some query was flagged: radix-narrow the key window (<= 6 grid-synchronised
+    //    histogram passes), then re-emit the resolved queries
     rc = launch_check(p->B, k, p->cap, p->d_cnt, p->d_threshold,
                       (p->flags & FB_PLAN_FORCE_FALLBACK) ? 1 : 0, p->d_fb, p->d_active,
                       p->d_active + 2, s);
     if (rc) return rc;
-    for (int pass = 0; pass < 6; ++pass) {
-      rc = launch_zero_hist(p->B, p->d_fb, p->d_hist, p->d_active, s);
-      if (rc) return rc;
-      ScanArgs ha = a;
-      ha.mode = SCAN_HIST;
-      ha.word_stride = 1;
-      ha.fb = p->d_fb;
-      ha.only_state = Q_FLAGGED;
-      ha.active_count = p->d_active;
-      rc = launch_scan_simt(ha, s);
-      if (rc) return rc;
-      rc = launch_resolve(p->B, k, p->cap, p->d_fb, p->d_hist, p->d_threshold, p->d_cnt,
-                          p->d_elig, p->d_active, pass == 5, s);
-      if (rc) return rc;
-    }
-    ScanArgs ra = ea;
-    ra.fb = p->d_fb;
-    ra.only_state = Q_RESOLVED;
-    ra.active_count = p->d_active + 1;
-    rc = launch_scan_simt(ra, s);
+    FallbackArgs fa{};
+    fa.hist = a;
+    fa.hist.mode = SCAN_HIST;
+    fa.hist.word_stride = 1;
+    fa.hist.fb = p->d_fb;
+    fa.hist.only_state = Q_FLAGGED;
+    fa.hist.active_count = nullptr;
+    fa.emit = ea;
+    fa.emit.fb = p->d_fb;
+    fa.emit.only_state = Q_RESOLVED;
+    fa.emit.active_count = nullptr;
+    fa.n_queries = p->B;
+    fa.k = k;
+    fa.cap = p->cap;
+    fa.fb = p->d_fb;
+    fa.hist_buf = p->d_hist;
+    fa.threshold = p->d_threshold;
+    fa.cnt = p->d_cnt;
+    fa.elig = p->d_elig;
+    fa.active = p->d_active;
+    rc = launch_fallback(fa, s);
     if (rc) return rc;
   }
   // 6) exact selection + outputs

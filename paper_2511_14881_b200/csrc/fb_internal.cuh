@@ -202,6 +202,19 @@ struct ThresholdArgs {
   uint32_t* elig;              // [B] zeroed
 };
 int launch_threshold(const ThresholdArgs& a, cudaStream_t s);
+
+struct FallbackArgs {
+  ScanArgs hist;   // SCAN_HIST over the flagged queries
+  ScanArgs emit;   // SCAN_EMIT of the resolved queries
+  int32_t n_queries, k, cap;
+  Fallback* fb;
+  uint32_t* hist_buf;
+  uint64_t* threshold;
+  uint32_t* cnt;
+  uint32_t* elig;
+  uint32_t* active;  // [0] flagged & unresolved, [1] resolved
+};
+int launch_fallback(const FallbackArgs& f, cudaStream_t s);
 // candidate capacity the exact radix selection can take per query (keys staged in smem)
 constexpr int32_t kSelectMaxCand = 26624;
 

@@ -9,10 +9,13 @@
 //   search_clusters       ivf.py:285-334  (eligible = valid & mask, exact int32 dot)
 //   _select_topk          ivf.py:272-282  (score desc, item_id asc)
 //   _reduce_topk          serve.py:98-100
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "fb_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 #include <algorithm>
 #include <cstdio>
@@ -222,9 +225,7 @@ __device__ __forceinline__ void locate_word(const ScanArgs& a, int64_t g, int64_
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256) k_scan_simt(ScanArgs a) {
-  extern __shared__ __align__(16) uint8_t smem_items[];
-  if (a.active_count != nullptr && *a.active_count == 0) return;
+__device__ void scan_simt_body(const ScanArgs& a, uint8_t* smem_items) {
   const int dp = a.idx.dim_pad;
   const int64_t n_work = (a.total_words + a.word_stride - 1) / a.word_stride;
   for (int64_t gi = blockIdx.x; gi < n_work; gi += gridDim.x) {
@@ -281,6 +282,13 @@ __global__ void __launch_bounds__(256) k_scan_simt(ScanArgs a) {
       }
     }
   }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_scan_simt(ScanArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_items[];
+  if (a.active_count != nullptr && *a.active_count == 0) return;
+  scan_simt_body<MODE>(a, smem_items);
 }
 
 // ------------------------------------------------------------------------------------
@@ -449,10 +457,10 @@ __global__ void k_zero_hist(int n_queries, const Fallback* fb, uint32_t* hist,
 
 // Narrow each flagged query's key window to the histogram bin holding rank `need`;
 // resolve once the keys >= that bin's lower edge fit the candidate buffer.
-__global__ void k_resolve(int n_queries, int k, int cap, Fallback* fb, const uint32_t* hist,
-                          uint64_t* threshold, uint32_t* cnt, uint32_t* elig, uint32_t* active) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= n_queries || fb[q].state != Q_FLAGGED) return;
+__device__ void resolve_query(int q, int k, int cap, Fallback* fb, const uint32_t* hist,
+                              uint64_t* threshold, uint32_t* cnt, uint32_t* elig,
+                              uint32_t* active) {
+  if (fb[q].state != Q_FLAGGED) return;
   Fallback f = fb[q];
   const uint32_t* h = hist + (int64_t)q * kHistBins;
   uint64_t cum = 0;
@@ -485,6 +493,35 @@ __global__ void k_resolve(int n_queries, int k, int cap, Fallback* fb, const uin
   fb[q] = f;
   atomicSub(active, 1u);
   atomicAdd(active + 1, 1u);
+}
+
+__global__ void k_resolve(int n_queries, int k, int cap, Fallback* fb, const uint32_t* hist,
+                          uint64_t* threshold, uint32_t* cnt, uint32_t* elig, uint32_t* active) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n_queries) resolve_query(q, k, cap, fb, hist, threshold, cnt, elig, active);
+}
+
+// The whole exact fallback in ONE cooperative launch: nothing but a flag read when no
+// query was flagged (the common case); otherwise up to 6 rounds of (zero histograms ->
+// SIMT histogram scan of the flagged queries -> narrow/resolve), grid-synchronised, then
+// the re-emit of the resolved queries.
+__global__ void __launch_bounds__(256) k_fallback(FallbackArgs f) {
+  extern __shared__ __align__(16) uint8_t smem_items[];
+  if (__ldcg(f.active) == 0u) return;  // written by k_check: uniform across the grid
+  cg::grid_group g = cg::this_grid();
+  const int64_t n_hist = (int64_t)f.n_queries * kHistBins;
+  for (int pass = 0; pass < 6; ++pass) {
+    for (int64_t i = grid_tid(); i < n_hist; i += grid_stride())
+      if (f.fb[i / kHistBins].state == Q_FLAGGED) f.hist_buf[i] = 0u;
+    g.sync();
+    scan_simt_body<SCAN_HIST>(f.hist, smem_items);
+    g.sync();
+    for (int64_t q = grid_tid(); q < f.n_queries; q += grid_stride())
+      resolve_query((int)q, f.k, f.cap, f.fb, f.hist_buf, f.threshold, f.cnt, f.elig, f.active);
+    g.sync();
+    if (__ldcg(f.active) == 0u) break;  // read after the sync: uniform
+  }
+  scan_simt_body<SCAN_EMIT>(f.emit, smem_items);
 }
 
 // ------------------------------------------------------------------------------------
@@ -1107,6 +1144,24 @@ int launch_resolve(int32_t n_queries, int32_t k, int32_t cap, Fallback* fb, uint
   k_resolve<<<(n_queries + 127) / 128, 128, 0, s>>>(n_queries, k, cap, fb, hist, threshold, cnt,
                                                     elig, active);
   FB_LAUNCH_CHECK("k_resolve");
+  return FB_OK;
+}
+
+int launch_fallback(const FallbackArgs& f, cudaStream_t s) {
+  if (f.n_queries <= 0) return FB_OK;
+  const size_t smem = (size_t)64 * f.hist.idx.dim_pad;
+  if (smem > 48 * 1024)
+    FB_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  int per_sm = 0, n_sm = 148;
+  FB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fallback, 256, smem));
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = std::max(1, std::min(per_sm, 4) * n_sm);
+  FallbackArgs args = f;
+  void* params[] = {&args};
+  FB_CUDA(cudaLaunchCooperativeKernel((const void*)k_fallback, dim3(grid), dim3(256), params,
+                                      smem, s));
+  FB_LAUNCH_CHECK("k_fallback");
   return FB_OK;
 }
 
