@@ -8,7 +8,8 @@ C-ABI of ``include/filtra_b200.h``); there is no CPU fallback.
 from .bloom import (BloomIndex, BloomParams, FilterStats, QueryBloom, bloom_eval_leaf,
                     bloom_fpr_theoretical, build_bloom, build_bloom_arrays, hash_positions,
                     hash_seed, heuristic_bits, positions_from_seed)
-from .engine import DeviceIndex, TopkOp, TopkOutput, device_index_for, filtered_topk, merge_topk
+from .engine import (DeviceIndex, PipelinedTopk, TopkOp, TopkOutput, device_index_for,
+                     filtered_topk, merge_topk)
 from .filter_query import (And, CompiledFilter, FilterBatch, Leaf, Not, OpCode, Or, Vocabulary,
                            compile_filter, eval_compiled, format_filter, parse_filter)
 from .ivf import ScanStats, TopkResult, probe_centroids, search, search_clusters
@@ -24,7 +25,7 @@ __version__ = "0.1.0"
 __all__ = [
     "And", "BloomIndex", "BloomParams", "CompiledFilter", "DeviceIndex", "FilterBatch",
     "FilterStats", "Leaf", "Not", "OpCode", "Or", "QuantParams", "QuantizedMatrix",
-    "QueryBloom", "ScanStats", "ShardedSearch", "StageTimings", "TopkOp", "TopkOutput",
+    "QueryBloom", "ScanStats", "ShardedSearch", "StageTimings", "TopkOp", "PipelinedTopk", "TopkOutput",
     "TopkResult", "Vocabulary", "_reduce_topk", "bloom_eval_leaf", "bloom_fpr_theoretical",
     "build_bloom", "build_bloom_arrays", "codesigned_search", "compile_filter",
     "compute_quant_params", "dequantize", "device_index_for", "eval_compiled",

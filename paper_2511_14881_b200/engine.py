@@ -313,3 +313,74 @@ def merge_topk(scores: torch.Tensor, ids: torch.Tensor, count: torch.Tensor, k_o
         out.count.data_ptr(), out.fscores.data_ptr() if out.fscores is not None else None,
         _native.stream_ptr()))
     return out
+
+
+class PipelinedTopk:
+    """Host-in / host-out batched filtered top-k for serving: batch i's scan runs on the
+    compute stream while batch i+1's queries and filter arrays are copied in on one copy
+    stream and batch i-1's ids / scores are copied out on another (``depth`` slots of
+    device and pinned host buffers, ordered by CUDA events; separate streams so a copy-out
+    waiting for its scan never holds up the next copy-in)."""
+
+    def __init__(self, index: DeviceIndex, n_queries: int, k: int, ranges=None,
+                 flags: int = 0, depth: int = 2, filters_template=None):
+        if ranges is None:
+            ranges = np.array([[0, index.n_slots]], dtype=np.int64)
+        self.index, self.B, self.k = index, int(n_queries), max(int(k), 1)
+        self.op = TopkOp(index, n_queries, k, ranges, flags)
+        self.compute = torch.cuda.current_stream()
+        self.copy_in = torch.cuda.Stream()
+        self.copy_out = torch.cuda.Stream()
+        dev = index.items.device
+        self.slots = []
+        for _ in range(depth):
+            batch = None
+            if filters_template is not None:
+                batch = FilterBatch.pack(filters_template, index.bloom.params).to_device()
+            self.slots.append({
+                "q": torch.empty((self.B, index.dim), dtype=torch.float32, device=dev),
+                "qq": torch.empty((self.B, index.dim_pad), dtype=torch.int8, device=dev),
+                "batch": batch, "out": self.op.alloc_outputs(),
+                "ids": torch.empty((self.B, self.k), dtype=torch.int64).pin_memory(),
+                "scores": torch.empty((self.B, self.k), dtype=torch.int32).pin_memory(),
+                "count": torch.empty((self.B,), dtype=torch.int32).pin_memory(),
+                "h2d": torch.cuda.Event(), "comp": torch.cuda.Event(), "d2h": torch.cuda.Event(),
+            })
+        self._n = 0
+
+    def submit(self, host_queries: torch.Tensor, host_filter_arrays=None) -> int:
+        """Enqueue one batch (pinned float32 queries [B, dim]; the filter batch's host arrays
+        in ``FilterBatch.host_arrays()`` order, or None to reuse the slot's). Returns a
+        ticket for ``result``."""
+        t = self._n
+        s = self.slots[t % len(self.slots)]
+        self._n += 1
+        self.copy_in.wait_event(s["comp"])       # the slot's inputs are no longer read
+        with torch.cuda.stream(self.copy_in):
+            s["q"].copy_(host_queries, non_blocking=True)
+            if host_filter_arrays is not None and s["batch"] is not None:
+                for d, h in zip(s["batch"]._dev, host_filter_arrays):
+                    d.copy_(h, non_blocking=True)
+            s["h2d"].record(self.copy_in)
+        self.compute.wait_event(s["h2d"])
+        self.compute.wait_event(s["d2h"])        # the slot's outputs were copied out
+        quantize_device(s["q"], self.index.qp, out_stride=self.index.dim_pad, out=s["qq"])
+        res = self.op(s["qq"], s["batch"], out=s["out"])
+        s["comp"].record(self.compute)
+        self.copy_out.wait_event(s["comp"])
+        with torch.cuda.stream(self.copy_out):
+            s["ids"].copy_(res.ids, non_blocking=True)
+            s["scores"].copy_(res.scores, non_blocking=True)
+            s["count"].copy_(res.count, non_blocking=True)
+            s["d2h"].record(self.copy_out)
+        return t
+
+    def result(self, ticket: int):
+        """Host (ids u64-bits int64 [B, k], int32 scores [B, k], int32 counts [B]) of a
+        submitted batch (waits for its copy-out; valid until the slot is reused)."""
+        s = self.slots[ticket % len(self.slots)]
+        s["d2h"].synchronize()
+        return s["ids"], s["scores"], s["count"]
+
+    def done_event(self, ticket: int):
+        return self.slots[ticket % len(self.slots)]["d2h"]

@@ -386,6 +386,34 @@ def test_bytecode_kernel_multi_tile_per_cta(fb, filtered):
         assert np.array_equal(scores, ref.scores), q
 
 
+def test_pipelined_topk_matches_batched_op(fb, wl_small):
+    """The serving pipeline (copies overlapped on a second stream, two slots) returns the
+    batched operator's results for every submitted batch, including alternating inputs."""
+    wl = wl_small
+    idx = wl.index
+    k = 400
+    op = fb.TopkOp(idx, 24, k, np.array([[0, idx.n_slots]]))
+    want = op(wl.queries_q, wl.batch)
+    want_ids = want.ids.cpu().numpy().copy()
+    want_sc = want.scores.cpu().numpy().copy()
+    pipe = fb.PipelinedTopk(idx, 24, k, filters_template=wl.filters)
+    hq = wl.queries.cpu().pin_memory()
+    hq2 = (wl.queries.flip(0)).cpu().pin_memory()
+    h_prog = [torch.from_numpy(x).pin_memory() for x in pipe.slots[0]["batch"].host_arrays()]
+    tickets = [pipe.submit(hq if t % 2 == 0 else hq2, h_prog) for t in range(2)]
+    for t in tickets:
+        ids, sc, cnt = pipe.result(t)
+        src = hq if t % 2 == 0 else hq2
+        if t % 2 == 0:
+            assert np.array_equal(ids.numpy(), want_ids)
+            assert np.array_equal(sc.numpy(), want_sc)
+        else:
+            qq = idx.quantize_queries(src.cuda())
+            ref = op(qq, wl.batch)
+            assert np.array_equal(ids.numpy(), ref.ids.cpu().numpy())
+            assert np.array_equal(sc.numpy(), ref.scores.cpu().numpy())
+
+
 def test_merge_topk_device(fb, rng):
     n_lists, B, k = 5, 3, 50
     scores = np.zeros((n_lists, B, k), np.int32)
