@@ -346,17 +346,15 @@ __global__ void __launch_bounds__(kSelectThreads) k_threshold(ThresholdArgs a) {
     return;
   }
   const int nk = (int)min(ns, (uint32_t)a.sample_cap);
-  // sample rank of the threshold: aim the expected candidate count at the middle of
-  // [k, cap], at least 5 sigma above the true k-th key, and (when possible) 5 sigma below
-  // the capacity
+  // sample rank of the threshold: 5 sigma above the true k-th key's expected sample rank
+  // when that stays 5 sigma below the capacity, else the middle of [k, cap]
   const double fe = a.sample_fraction * (double)nk / (double)ns;
   const double mu = (double)a.k * fe;
   const double cf = (double)a.cap * fe;
   const double lo = mu + 5.0 * sqrt(mu) + 8.0;
   const double hi = cf - 5.0 * sqrt(cf);
-  double jd = 0.5 * (mu + cf);
-  jd = jd > hi ? hi : jd;
-  jd = jd < lo ? lo : jd;
+  // (the lower edge: every extra candidate costs hit-filter and selection work)
+  const double jd = lo < hi ? lo : (0.5 * (mu + cf) > lo ? lo : 0.5 * (mu + cf));
   if (jd >= (double)(nk - 1)) {
     if (threadIdx.x == 0) a.threshold[q] = 0ull;
     return;
@@ -800,82 +798,71 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
   }
   __syncthreads();
 
-  // 4. LSD radix sort of the compressed keys s_key[0, kk), ping-pong with
-  //    s_key[kRsMaxK, 2 kRsMaxK), 8-bit digits. Element order within a pass is
-  //    (warp, slot j, lane): warp w owns [w * 320, w * 320 + 320). Lanes holding equal
-  //    digits are found with match.any; per-warp running digit counts give the rank
-  //    within the warp, one scan of the (digit, warp) counters the rest.
+  // 4. bucket sort of the compressed keys s_key[0, kk) into ascending order: 4096 bins on
+  //    the top bits (one histogram pass, one scan, one scatter), then each key's rank
+  //    inside its bin by counting the bin's smaller keys (bins hold a few keys: the top
+  //    bits are the score). Result in s_key[0, kk); s_key[kRsMaxK, ...) is the scratch.
   const uint64_t cmax = ((uint64_t)((uint32_t)(mx >> 32) - sb_lo) << id_bits) |
                         (uint64_t)((uint32_t)mx - id_base);
   const int nbits = cmax == 0ull ? 0 : 64 - __clzll((long long)cmax);
+  constexpr int kBins = 4096;
+  const int bshift = nbits > 12 ? nbits - 12 : 0;
+  uint32_t* s_bcnt = s_cnt;           // [kBins] counts, then fill pointers = bin ends
+  uint32_t* s_bstart = s_cnt + kBins; // [kBins] bin starts
   uint64_t* src = s_key;
   uint64_t* dst = s_key + kRsMaxK;
-  const uint32_t lt = (1u << lane) - 1u;
-  constexpr int kPer = kRsMaxK / kRsWarps;  // 320 elements per warp
-  for (int bit = 0; bit < nbits; bit += kRsBits) {
-    for (int d = lane; d < kRsDigits; d += 32) s_cnt[d * kRsCntStride + wid] = 0u;
-    __syncwarp();
-    uint64_t kv[kRsIpt];
-    uint32_t rk[kRsIpt];
+  for (int b = t; b < kBins; b += kRsThreads) s_bcnt[b] = 0u;
+  __syncthreads();
+  for (int i = t; i < kk; i += kRsThreads) atomicAdd(s_bcnt + (int)(src[i] >> bshift), 1u);
+  __syncthreads();
+  {  // exclusive scan of the bin counts: thread t owns bins 4t .. 4t + 3
+    uint32_t v[4], run = 0u;
 #pragma unroll
-    for (int j = 0; j < kRsIpt; ++j) {
-      const int e = wid * kPer + j * 32 + lane;
-      const bool valid = e < kk;
-      kv[j] = valid ? src[e] : 0ull;
-      const uint32_t d = (uint32_t)(kv[j] >> bit) & (kRsDigits - 1);
-      const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 0x100u + lane);
-      uint32_t base = 0u;
-      if (valid) base = s_cnt[d * kRsCntStride + wid];
-      __syncwarp();
-      const uint32_t below = (uint32_t)__popc(peers & lt);
-      if (valid && below == 0u) s_cnt[d * kRsCntStride + wid] = base + (uint32_t)__popc(peers);
-      __syncwarp();
-      rk[j] = valid ? ((d << 16) | (base + below)) : 0xFFFFFFFFu;
+    for (int i = 0; i < 4; ++i) {
+      v[i] = run;
+      run += s_bcnt[4 * t + i];
+    }
+    uint32_t incl = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    if (lane == 31) s_wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t ws = s_wsum[lane];
+      uint32_t wi = ws;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, wi, d);
+        if (lane >= d) wi += y;
+      }
+      s_wsum[lane] = wi - ws;
     }
     __syncthreads();
-    // exclusive scan of the counters in (digit, warp) order: thread t owns the 8
-    // consecutive entries t * 8 .. t * 8 + 7 (digit t / 4, warps 8 (t % 4) ..)
-    {
-      const int d = t >> 2, w0 = (t & 3) * 8;
-      uint32_t* c = s_cnt + d * kRsCntStride + w0;
-      uint32_t v[8], run = 0u;
+    const uint32_t off = s_wsum[wid] + incl - run;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        v[i] = run;
-        run += c[i];
-      }
-      uint32_t incl = run;
-#pragma unroll
-      for (int dd = 1; dd < 32; dd <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, dd);
-        if (lane >= dd) incl += y;
-      }
-      if (lane == 31) s_wsum[wid] = incl;
-      __syncthreads();
-      if (wid == 0) {
-        const uint32_t ws = s_wsum[lane];
-        uint32_t wi = ws;
-#pragma unroll
-        for (int dd = 1; dd < 32; dd <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, wi, dd);
-          if (lane >= dd) wi += y;
-        }
-        s_wsum[lane] = wi - ws;
-      }
-      __syncthreads();
-      const uint32_t off = s_wsum[wid] + incl - run;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) c[i] = v[i] + off;
+    for (int i = 0; i < 4; ++i) {
+      s_bstart[4 * t + i] = v[i] + off;
+      s_bcnt[4 * t + i] = v[i] + off;  // fill pointer
     }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kRsIpt; ++j)
-      if (rk[j] != 0xFFFFFFFFu) dst[s_cnt[(rk[j] >> 16) * kRsCntStride + wid] + (rk[j] & 0xFFFFu)] = kv[j];
-    __syncthreads();
-    uint64_t* tmp = src;
-    src = dst;
-    dst = tmp;
   }
+  __syncthreads();
+  for (int i = t; i < kk; i += kRsThreads) {
+    const uint64_t c = src[i];
+    dst[atomicAdd(s_bcnt + (int)(c >> bshift), 1u)] = c;
+  }
+  __syncthreads();
+  for (int i = t; i < kk; i += kRsThreads) {
+    const uint64_t c = dst[i];
+    const int b = (int)(c >> bshift);
+    const uint32_t lo_b = s_bstart[b], hi_b = s_bcnt[b];
+    uint32_t r = lo_b;
+    for (uint32_t j = lo_b; j < hi_b; ++j) r += dst[j] < c ? 1u : 0u;
+    src[r] = c;
+  }
+  __syncthreads();
 
   // 5. outputs (ascending sorted position p -> rank kk - 1 - p); all gathers of a
   //    thread's outputs are issued before any is consumed
