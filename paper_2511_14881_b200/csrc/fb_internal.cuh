@@ -215,8 +215,9 @@ struct FallbackArgs {
   uint32_t* active;  // [0] flagged & unresolved, [1] resolved
 };
 int launch_fallback(const FallbackArgs& f, cudaStream_t s);
-// candidate capacity the exact radix selection can take per query (keys staged in smem)
-constexpr int32_t kSelectMaxCand = 26624;
+// keys the exact radix selection stages / sorts in shared memory per query (larger
+// candidate sets are selected from L2; k up to this many)
+constexpr int32_t kSelectMaxCand = 24576;
 
 int launch_check(int32_t n_queries, int32_t k, int32_t cap, const uint32_t* cnt,
                  const uint64_t* thr, int force, Fallback* fb, uint32_t* active_count,

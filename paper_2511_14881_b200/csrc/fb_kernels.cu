@@ -618,30 +618,26 @@ __global__ void __launch_bounds__(kSelectThreads) k_select(SelectArgs a) {
 
 // ------------------------------------------------------------------------------------
 // Key-only exact selection (index with a rank -> slot table): per query CTA,
-//   1. the candidate keys are loaded into shared memory (<= kRsMaxCand);
+//   1. the candidate keys are staged in shared memory (<= kRsMaxK of them; larger sets
+//      are re-read from L2 by each pass);
 //   2. an MSD radix select (8-bit digits from the highest bit where the keys differ)
 //      finds the lower edge K of the top min(k, n) keys -- it stops as soon as a digit
 //      bin completes the count, so usually after 2-4 histogram passes;
 //   3. the keys >= K are compacted (exactly min(k, n) of them, keys being unique);
-//   4. an LSD radix sort (4-bit digits, stable block-wide counting passes over the bits
-//      of key - K) orders them; output rank = kk - 1 - sorted position;
-//   5. ids / scores / dequantised scores are gathered through slot_of_rank.
+//   4. a bucket sort orders them (4096 bins on the top bits of the compressed key, one
+//      scatter through the dead candidate buffer, ranks within the bins); output rank =
+//      kk - 1 - sorted position;
+//   5. ids come from id_of_rank (one gather), scores from the key, dequantised scores
+//      through slot_of_rank.
 // Same output as k_select (the oracle's (score desc, item_id asc) order).
 // ------------------------------------------------------------------------------------
 constexpr int kRsThreads = 1024;
-constexpr int kRsIpt = 10;                         // sort capacity per thread
-constexpr int kRsMaxK = kRsThreads * kRsIpt;       // 10240
-constexpr int kRsMaxCand = kSelectMaxCand;         // keys loaded per query (208 KB)
-constexpr int kRsBits = 8;                         // LSD digit width
-constexpr int kRsDigits = 1 << kRsBits;
-constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsCntStride = kRsWarps + 1;          // u32 counters [digit][warp], padded
-// the two sort buffers (2 x kRsMaxK keys) then the per-warp digit counters; the
-// candidate load area (kRsMaxCand keys) overlaps both and is dead once compacted
-constexpr size_t kRsCntOff = (size_t)2 * kRsMaxK * 8;
-constexpr size_t kRsSmem = std::max(kRsCntOff + (size_t)kRsDigits * kRsCntStride * 4,
-                                    (size_t)kRsMaxCand * 8);
-static_assert(kRsSmem >= (size_t)kRsMaxCand * 8, "load area must fit");
+constexpr int kRsMaxK = kSelectMaxCand;            // 24576 selected keys sorted in smem
+// shared memory: the compacted / sorted keys (kRsMaxK u64; also the staging area of the
+// candidates when they fit), then the bucket-sort bin counters and starts
+constexpr size_t kRsCntOff = (size_t)kRsMaxK * 8;
+constexpr int kRsBins = 4096;
+constexpr size_t kRsSmem = kRsCntOff + (size_t)2 * kRsBins * 4;
 
 __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
 #pragma unroll
@@ -692,11 +688,13 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
   if (kk == 0) return;
   const uint64_t* gk = a.cand_key + (int64_t)q * a.cap;
 
-  // 1. load + max / min
+  // 1. load (staged in smem when the candidates fit, else re-read from L2 per pass) +
+  //    max / min
+  const bool staged = n <= kRsMaxK;
   uint64_t mx = 0ull, mn = ~0ull;
   for (int i = t; i < n; i += kRsThreads) {
     const uint64_t k = gk[i];
-    s_key[i] = k;
+    if (staged) s_key[i] = k;
     mx = k > mx ? k : mx;
     mn = k < mn ? k : mn;
   }
@@ -732,7 +730,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
     for (int b = t; b < 256; b += kRsThreads) hist[b] = 0u;
     __syncthreads();
     for (int i = t; i < n; i += kRsThreads) {
-      const uint64_t k = s_key[i];
+      const uint64_t k = staged ? s_key[i] : __ldcg(gk + i);
       if (shift + 8 >= 64 || ((k ^ prefix) >> (shift + 8)) == 0ull)
         atomicAdd(hist + ((k >> shift) & 0xFFu), 1u);
     }
@@ -805,12 +803,15 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
   const uint64_t cmax = ((uint64_t)((uint32_t)(mx >> 32) - sb_lo) << id_bits) |
                         (uint64_t)((uint32_t)mx - id_base);
   const int nbits = cmax == 0ull ? 0 : 64 - __clzll((long long)cmax);
-  constexpr int kBins = 4096;
+  constexpr int kBins = kRsBins;
   const int bshift = nbits > 12 ? nbits - 12 : 0;
   uint32_t* s_bcnt = s_cnt;           // [kBins] counts, then fill pointers = bin ends
   uint32_t* s_bstart = s_cnt + kBins; // [kBins] bin starts
   uint64_t* src = s_key;
-  uint64_t* dst = s_key + kRsMaxK;
+  // scatter scratch: the upper half of the shared buffer when kk fits there, else the
+  // query's candidate buffer (dead after the compaction; cap >= kk)
+  const bool dst_smem = kk <= kRsMaxK / 2;
+  uint64_t* dst = dst_smem ? s_key + kRsMaxK / 2 : const_cast<uint64_t*>(gk);
   for (int b = t; b < kBins; b += kRsThreads) s_bcnt[b] = 0u;
   __syncthreads();
   for (int i = t; i < kk; i += kRsThreads) atomicAdd(s_bcnt + (int)(src[i] >> bshift), 1u);
@@ -855,11 +856,14 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
   }
   __syncthreads();
   for (int i = t; i < kk; i += kRsThreads) {
-    const uint64_t c = dst[i];
+    const uint64_t c = dst_smem ? dst[i] : __ldcg(dst + i);
     const int b = (int)(c >> bshift);
     const uint32_t lo_b = s_bstart[b], hi_b = s_bcnt[b];
     uint32_t r = lo_b;
-    for (uint32_t j = lo_b; j < hi_b; ++j) r += dst[j] < c ? 1u : 0u;
+    if (dst_smem)
+      for (uint32_t j = lo_b; j < hi_b; ++j) r += dst[j] < c ? 1u : 0u;
+    else
+      for (uint32_t j = lo_b; j < hi_b; ++j) r += __ldcg(dst + j) < c ? 1u : 0u;
     src[r] = c;
   }
   __syncthreads();
@@ -1153,7 +1157,8 @@ int launch_fallback(const FallbackArgs& f, cudaStream_t s) {
 }
 
 bool select_by_rank(int32_t cap, int32_t k, const uint32_t* slot_of_rank) {
-  return slot_of_rank != nullptr && cap <= kRsMaxCand && k <= kRsMaxK;
+  (void)cap;  // any candidate count: beyond kRsMaxK the select reads them from L2
+  return slot_of_rank != nullptr && k <= kRsMaxK;
 }
 
 int launch_select(const SelectArgs& a, cudaStream_t s) {
