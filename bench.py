@@ -61,6 +61,8 @@ def parse_args():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--dim", type=int, default=128)
     ap.add_argument("--simt", action="store_true", help="force the SIMT scan kernel")
+    ap.add_argument("--exchange", choices=["pruned", "all_gather"], default="pruned",
+                    help="N>1 shard exchange: pruned owner-partitioned all-to-all, or all-gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=0, help="CPU sample size (0: auto)")
     a = ap.parse_args()
@@ -81,7 +83,10 @@ def workload_desc(a, n_gpus):
         "filter": "AND of 4 OR-groups, |S|=(17,17,14,11), 59 leaves/query",
         "l2": "inputs 2.6 GB/GPU > 126 MB L2; no flush needed",
         "parallelism": "single GPU" if n_gpus == 1 else
-                       f"items sharded x{n_gpus}, NCCL all-gather + GPU merge",
+                       (f"items sharded x{n_gpus}, NCCL all-reduce(max) of local k-th scores + "
+                        "pruned all-to-all to query owners + GPU merge"
+                        if getattr(a, "exchange", "pruned") == "pruned" else
+                        f"items sharded x{n_gpus}, NCCL all-gather + GPU merge"),
     }
 
 
@@ -236,7 +241,7 @@ def run_ours(a):
     from paper_2511_14881_b200.bloom import BloomParams
     from paper_2511_14881_b200.filter_query import FilterBatch
     from paper_2511_14881_b200.quantize import quantize_device
-    from paper_2511_14881_b200.serve import exchange_topk
+    from paper_2511_14881_b200.serve import exchange_pruned, exchange_topk
 
     lib = _native.lib()
     B, k = a.batch, a.k
@@ -263,7 +268,10 @@ def run_ours(a):
         quantize_device(queries_f32, wl.qp, out_stride=idx.dim_pad, out=qbuf)
         res = op(qbuf, filters, out=outs)
         if world > 1:
-            s, i, c = exchange_topk(res.scores, res.ids, res.count)
+            if a.exchange == "pruned":  # each rank merges its query slice
+                _, _, s, i, c = exchange_pruned(res.scores, res.ids, res.count, k)
+            else:
+                s, i, c = exchange_topk(res.scores, res.ids, res.count)
             res = merge_topk(s, i, c, k)
         return res
 

@@ -72,6 +72,71 @@ def exchange_topk(local_scores: torch.Tensor, local_ids: torch.Tensor, local_cou
     return torch.stack(gs), torch.stack(gi), torch.stack(gc)
 
 
+def query_owner_slices(n_queries: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous query slice each rank merges in the owner-partitioned exchange."""
+    return [(r * n_queries // world, (r + 1) * n_queries // world) for r in range(world)]
+
+
+def exchange_pruned(local_scores: torch.Tensor, local_ids: torch.Tensor,
+                    local_count: torch.Tensor, k: int, group=None):
+    """Owner-partitioned, pruned exchange (SURVEY §8(e) "optimised"): one all-reduce(MAX)
+    of every query's local k-th score gives a bound tau* the global k-th score cannot fall
+    below (the union of the ranks' lists holds >= k pairs scoring >= it), so each rank
+    ships only its pairs with score >= tau*, and only to the rank owning the query
+    (all-to-all). Per rank the traffic drops from (world - 1) * B * k pairs (all-gather) to
+    about B * k / world.
+
+    Returns (q0, q1, scores [world, q1-q0, kmax], ids [...], counts [world, q1-q0]): the
+    lists of this rank's query slice, ready for the merge (ties at tau* are all kept, so
+    the merge of the pruned lists equals the merge of the full ones)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    B, kin = local_scores.shape
+    dev = local_scores.device
+    cnt = local_count.to(torch.int64).clamp(max=kin)
+    pos = torch.arange(kin, device=dev)[None, :]
+    # local k-th score (INT32_MIN when a rank holds fewer than k pairs for the query)
+    kth = torch.where(cnt >= k, local_scores.gather(1, (cnt.clamp(min=1) - 1)[:, None]
+                                                    .clamp(max=k - 1))[:, 0].to(torch.int64),
+                      torch.full((B,), -2**31, dtype=torch.int64, device=dev))
+    tau = kth.clone()
+    dist.all_reduce(tau, op=dist.ReduceOp.MAX, group=group)
+    keep = (pos < cnt[:, None]) & (local_scores.to(torch.int64) >= tau[:, None])
+    n_keep = keep.sum(dim=1)                                        # lists are sorted: a prefix
+    slices = query_owner_slices(B, world)
+    send_counts = torch.stack([n_keep[a:b].sum() for a, b in slices]).to(torch.int64)
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    q0, q1 = slices[rank]
+    nq = q1 - q0
+    # per-query kept counts for the owner
+    send_nk = torch.cat([n_keep[a:b] for a, b in slices]).to(torch.int64)
+    recv_nk = torch.empty((world * nq,), dtype=torch.int64, device=dev)
+    dist.all_to_all_single(recv_nk, send_nk, output_split_sizes=[nq] * world,
+                           input_split_sizes=[b - a for a, b in slices], group=group)
+    flat_s = local_scores[keep]
+    flat_i = local_ids[keep]
+    sc = send_counts.tolist()
+    rc = recv_counts.tolist()
+    rs = torch.empty((sum(rc),), dtype=local_scores.dtype, device=dev)
+    ri = torch.empty((sum(rc),), dtype=local_ids.dtype, device=dev)
+    dist.all_to_all_single(rs, flat_s, output_split_sizes=rc, input_split_sizes=sc, group=group)
+    dist.all_to_all_single(ri, flat_i, output_split_sizes=rc, input_split_sizes=sc, group=group)
+    nk = recv_nk.view(world, nq)
+    kmax = max(1, int(nk.max().item()) if nk.numel() else 1)
+    out_s = torch.full((world * nq, kmax), -2**31, dtype=local_scores.dtype, device=dev)
+    out_i = torch.zeros((world * nq, kmax), dtype=local_ids.dtype, device=dev)
+    flat = recv_nk                                   # received in (source rank, query) order
+    if rs.numel():
+        seg = torch.repeat_interleave(torch.arange(world * nq, device=dev), flat)
+        start = torch.cumsum(flat, 0) - flat
+        slot = torch.arange(rs.numel(), device=dev) - start[seg]
+        out_s[seg, slot] = rs
+        out_i[seg, slot] = ri
+    return (q0, q1, out_s.view(world, nq, kmax), out_i.view(world, nq, kmax),
+            nk.to(torch.int32))
+
+
 @dataclass
 class ShardedSearch:
     """One rank's part of an item-sharded filtered top-k.
@@ -83,13 +148,20 @@ class ShardedSearch:
     op: TopkOp
     group: object = None
     merge: object = None  # injectable merge (tests on CPU/gloo); default: fb_merge_topk
+    exchange: str = "all_gather"  # or "pruned": owner-partitioned, see exchange_pruned
 
     def __call__(self, queries_q: torch.Tensor, filters=None, k: int | None = None) -> TopkOutput:
+        """Global top-k: every query on every rank ("all_gather"), or with ``exchange=
+        "pruned"`` the rows of this rank's query slice (``query_owner_slices``)."""
         local = self.op(queries_q, filters)
         k = self.op.k if k is None else k
-        s, i, c = exchange_topk(local.scores, local.ids, local.count, self.group)
         merge = self.merge or merge_topk
+        if self.exchange == "pruned":
+            _, _, s, i, c = exchange_pruned(local.scores, local.ids, local.count, k, self.group)
+            return merge(s, i, c, k)
+        s, i, c = exchange_topk(local.scores, local.ids, local.count, self.group)
         return merge(s, i, c, k)
 
 
-__all__ = ["_reduce_topk", "shard_ranges", "exchange_topk", "ShardedSearch", "DeviceIndex"]
+__all__ = ["_reduce_topk", "shard_ranges", "exchange_topk", "exchange_pruned",
+           "query_owner_slices", "ShardedSearch", "DeviceIndex"]

@@ -61,7 +61,7 @@ def _oracle_merge(scores, ids, count, k):
     return TopkOutput(ids=out_i, scores=out_s, count=out_c)
 
 
-def _worker(rank, world, port, n_items, k, result_q):
+def _worker(rank, world, port, n_items, k, result_q, exchange="all_gather"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -75,22 +75,30 @@ def _worker(rank, world, port, n_items, k, result_q):
         s0, s1 = shard_ranges(n_items, world)[rank]
         op = _OracleOp(items[s0:s1], ids[s0:s1], queries, k)
         op.k = k
-        search = ShardedSearch(op=op, merge=_oracle_merge)
+        search = ShardedSearch(op=op, merge=_oracle_merge, exchange=exchange)
         out = search(torch.from_numpy(queries), None, k)
-        got = [(out.ids[q, : out.count[q]].numpy().view(np.uint64).tolist(),
-                out.scores[q, : out.count[q]].tolist()) for q in range(5)]
+        if exchange == "pruned":
+            from paper_2511_14881_b200.serve import query_owner_slices
+            q0, q1 = query_owner_slices(5, world)[rank]
+        else:
+            q0, q1 = 0, 5
+        got = {q0 + j: (out.ids[j, : out.count[j]].numpy().view(np.uint64).tolist(),
+                        out.scores[j, : out.count[j]].tolist()) for j in range(q1 - q0)}
         result_q.put((rank, got, (s0, s1)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_items,k", [(1000, 50), (130, 200)])
-def test_sharded_search_equals_unsharded(n_items, k):
+@pytest.mark.parametrize("n_items,k,exchange", [(1000, 50, "all_gather"), (130, 200, "all_gather"),
+                                                (1000, 50, "pruned"), (130, 200, "pruned"),
+                                                (3000, 40, "pruned")])
+def test_sharded_search_equals_unsharded(n_items, k, exchange):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n_items, k, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_items, k, q, exchange))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=120) for _ in range(world)]
@@ -104,11 +112,14 @@ def test_sharded_search_equals_unsharded(n_items, k):
     queries = rng.integers(-128, 128, size=(5, 16)).astype(np.int8)
     ranges = sorted(r[2] for r in results)
     assert ranges[0][0] == 0 and ranges[-1][1] == n_items and ranges[0][1] == ranges[1][0]
+    seen = set()
     for rank, got, _ in results:
-        for qi in range(5):
+        for qi, (gi, gs) in got.items():
             ref = orc.brute_force_int8(items, ids, queries[qi], k)
-            assert got[qi][0] == ref.item_ids.tolist(), (rank, qi)
-            assert got[qi][1] == ref.scores.tolist(), (rank, qi)
+            assert gi == ref.item_ids.tolist(), (rank, qi)
+            assert gs == ref.scores.tolist(), (rank, qi)
+            seen.add(qi)
+    assert seen == set(range(5))
 
 
 def test_shard_ranges_partition():
