@@ -368,15 +368,18 @@ def run_ours(a):
         dq = torch.empty((B, a.dim), dtype=torch.float32, device="cuda")
         e2e_batch = FilterBatch.pack(wl.filters, BloomParams()).to_device()
         h_prog = [torch.from_numpy(x).pin_memory() for x in e2e_batch.host_arrays()]
+        rows = [B]
 
         def e2e_step():
             dq.copy_(host_q, non_blocking=True)
             for d, h in zip(e2e_batch._dev, h_prog):
                 d.copy_(h, non_blocking=True)
             res = step(dq, e2e_batch)
-            out_ids.copy_(res.ids, non_blocking=True)
-            out_sc.copy_(res.scores, non_blocking=True)
-            out_cnt.copy_(res.count, non_blocking=True)
+            n = res.ids.shape[0]  # this rank's query slice under the pruned exchange
+            out_ids[:n].copy_(res.ids, non_blocking=True)
+            out_sc[:n].copy_(res.scores, non_blocking=True)
+            out_cnt[:n].copy_(res.count, non_blocking=True)
+            rows[0] = n
 
         for _ in range(2):
             e2e_step()
@@ -392,7 +395,7 @@ def run_ours(a):
         t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-        d2h = out_ids.numel() * 8 + out_sc.numel() * 4 + out_cnt.numel() * 4
+        d2h = rows[0] * (k * 12 + 4)
     h2d = host_q.numel() * 4 + sum(h.numel() * h.element_size() for h in h_prog)
     e2e = {"value": round(B * a.steps / (e2e_ms / 1e3), 1), "unit": UNIT,
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
