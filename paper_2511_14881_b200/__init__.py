@@ -12,7 +12,7 @@ from .engine import (DeviceIndex, PipelinedTopk, TopkOp, TopkOutput, device_inde
                      filtered_topk, merge_topk)
 from .filter_query import (And, CompiledFilter, FilterBatch, Leaf, Not, OpCode, Or, Vocabulary,
                            compile_filter, eval_compiled, format_filter, parse_filter)
-from .ivf import ScanStats, TopkResult, probe_centroids, search, search_clusters
+from .ivf import IvfSearchOp, ScanStats, TopkResult, probe_centroids, search, search_clusters
 from .quantize import (QuantParams, QuantizedMatrix, compute_quant_params, dequantize, int8_dot,
                        int8_dot_rows, quantize_matrix, quantize_value, quantize_vector)
 from .retrieval import StageTimings, codesigned_search
@@ -33,5 +33,5 @@ __all__ = [
     "int8_dot", "int8_dot_rows", "merge_topk", "parse_filter", "positions_from_seed",
     "probe_centroids", "quantize_matrix", "quantize_value", "quantize_vector", "search",
     "search_clusters", "shard_ranges", "DeviceCache", "DeviceScorer", "MultiTaskOp",
-    "MultiTaskOutput", "merge_device", "retrieve", "value_model_device",
+    "MultiTaskOutput", "merge_device", "retrieve", "value_model_device", "IvfSearchOp",
 ]

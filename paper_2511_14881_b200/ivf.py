@@ -130,3 +130,68 @@ def search(index, query: np.ndarray, nprobe: int, topk: int, mask: np.ndarray | 
     qq = dix.quantize_queries(to_dev(query.reshape(1, -1), torch.float32))
     clusters = probe_centroids(dix, query, nprobe)
     return run_scan(dix, qq, cluster_ranges(dix, clusters), mask, topk, stats=stats)
+
+
+class IvfSearchOp:
+    """Batched IVF-probed co-designed search (reference ``retrieval.codesigned_search`` with
+    ``nprobe < n_clusters``, ref/retrieval.py:110-144, for B queries at once).
+
+    On the device: every query's centroid dots (``fb_task_dots_f64``, numpy's pairwise
+    order, so probe ties resolve as in ``probe_centroids``), its top-``nprobe`` clusters
+    (stable sort: ties by ascending cluster id), a per-query probe mask over the slot
+    words of those clusters (difference array + prefix sum), then one batched filtered
+    top-k whose per-query masks confine each query to its probed clusters. The filter is
+    evaluated inside the scan, so restricting it to the probed ranges is implicit and the
+    result equals the reference's range-restricted evaluation exactly. (The scan covers
+    the clusters probed by any query of the batch; per-query work is pruned by the mask.)
+    """
+
+    def __init__(self, index, n_queries: int, nprobe: int, k0: int, flags: int = 0):
+        self.dix = device_index_for(index)
+        if self.dix.centroids is None and self.dix.cluster_offsets.shape[0] != 1:
+            raise ValueError("index has no centroids")
+        self.B = int(n_queries)
+        self.C = int(self.dix.cluster_offsets.shape[0])
+        self.nprobe = min(max(int(nprobe), 1), self.C)
+        self.k0 = int(k0)
+        dev = device()
+        offs = torch.as_tensor(self.dix.cluster_offsets, dtype=torch.int64, device=dev)
+        self._w0 = offs[:, 0] >> 6
+        self._w1 = (offs[:, 1] + 63) >> 6
+        self._rows = torch.arange(self.C, dtype=torch.int64, device=dev).repeat(self.B, 1)
+        self._cnt = torch.full((self.B,), self.C, dtype=torch.int32, device=dev)
+        self.op = TopkOp(self.dix, self.B, self.k0,
+                         np.array([[0, self.dix.n_slots]], dtype=np.int64), flags)
+
+    def probe(self, queries: torch.Tensor) -> torch.Tensor:
+        """int64 [B, nprobe] probed cluster ids per query."""
+        if self.dix.centroids is None:
+            return torch.zeros((self.B, 1), dtype=torch.int64, device=queries.device)
+        dots = torch.empty((self.B, 1, self.C), dtype=torch.float64, device=queries.device)
+        u = queries.to(torch.float32).contiguous()
+        _native.check(_native.lib().fb_task_dots_f64(
+            self.dix.centroids.data_ptr(), self.C, self.dix.dim, self._rows.data_ptr(),
+            self._cnt.data_ptr(), self.C, u.data_ptr(), self.B, 1, dots.data_ptr(),
+            _native.stream_ptr()))
+        order = torch.sort(dots[:, 0, :], dim=1, descending=True, stable=True).indices
+        return order[:, : self.nprobe]
+
+    def masks(self, clusters: torch.Tensor) -> torch.Tensor:
+        """Per-query probe masks int64 [B, n_words] (u64 bits)."""
+        W = self.dix.n_words
+        diff = torch.zeros((self.B, W + 1), dtype=torch.int32, device=clusters.device)
+        ones = torch.ones_like(clusters, dtype=torch.int32)
+        diff.scatter_add_(1, self._w0[clusters], ones)
+        diff.scatter_add_(1, self._w1[clusters], -ones)
+        cover = torch.cumsum(diff, dim=1)[:, :W] > 0
+        return torch.where(cover, torch.full_like(cover, -1, dtype=torch.int64),
+                           torch.zeros_like(cover, dtype=torch.int64))
+
+    def __call__(self, queries: torch.Tensor, filters=None):
+        """queries float32 [B, dim] (device) -> TopkOutput; also returns the probed ids."""
+        if queries.shape != (self.B, self.dix.dim):
+            raise DimMismatch(self.dix.dim, int(queries.shape[-1]))
+        clusters = self.probe(queries)
+        qq = self.dix.quantize_queries(queries)
+        out = self.op(qq, filters, masks=self.masks(clusters))
+        return out, clusters

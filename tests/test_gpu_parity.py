@@ -414,6 +414,43 @@ def test_pipelined_topk_matches_batched_op(fb, wl_small):
             assert np.array_equal(sc.numpy(), ref.scores.cpu().numpy())
 
 
+@pytest.mark.parametrize("case,nprobe,filtered", [(0, 3, True), (3, 7, True), (2, 1, False),
+                                                (1, 5, True)])
+def test_ivf_batched_probe_vs_oracle(fb, case, nprobe, filtered):
+    """Batched IVF-probed co-designed search (IvfSearchOp): per-query centroid probe on the
+    GPU (numpy-order float64 dots, ties by cluster id) + per-query probe masks + one
+    batched filtered top-k == the oracle's codesigned_search with nprobe, per query."""
+    from paper_2511_14881_b200.filter_query import FilterBatch
+    z = load_npz("scan_cases.npz")
+    pre = f"s{case}_"
+    idx = ref_index(z, pre, fb)
+    dix = fb.device_index_for(idx, bloom=fb.BloomIndex(fb.BloomParams(), z[pre + "planes"],
+                                                        z[pre + "items_q"].shape[0]))
+    qs = np.stack([z[pre + f"q{t}_f"] for t in range(12)])
+    rng = np.random.default_rng(case * 10 + nprobe)
+    filters = [fb.compile_filter(_to_expr(fb, _random_filter(rng)), fb.BloomParams())
+               if filtered else None for _ in range(12)]
+    batch = FilterBatch.pack(filters, fb.BloomParams()) if filtered else None
+    k = 60
+    op = fb.IvfSearchOp(dix, 12, nprobe, k)
+    out, clusters = op(torch.as_tensor(qs, device="cuda"), batch)
+    torch.cuda.synchronize()
+    lo, hi = (float(x) for x in z[pre + "qp"])
+    for t in range(12):
+        cl = orc.probe_centroids(z[pre + "centroids"], qs[t], nprobe)
+        assert np.array_equal(np.sort(clusters[t].cpu().numpy()), np.sort(cl)), t
+        prog = None
+        if filters[t] is not None:
+            cf = filters[t]
+            prog = ([(int(o), int(a)) for o, a in cf.ops], [(f, v, b.set_bits) for f, v, b in cf.leaves])
+        ref = orc.codesigned_search(z[pre + "items_q"], z[pre + "valid"], z[pre + "item_ids"],
+                                    z[pre + "offsets"], z[pre + "planes"], prog,
+                                    orc.quantize(qs[t], lo, hi), cl, k)
+        ids, scores = out.host(t)
+        assert np.array_equal(ids, ref.item_ids), t
+        assert np.array_equal(scores, ref.scores), t
+
+
 def test_merge_topk_device(fb, rng):
     n_lists, B, k = 5, 3, 50
     scores = np.zeros((n_lists, B, k), np.int32)
