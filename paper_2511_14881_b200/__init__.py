@@ -17,6 +17,7 @@ from .quantize import (QuantParams, QuantizedMatrix, compute_quant_params, dequa
                        int8_dot_rows, quantize_matrix, quantize_value, quantize_vector)
 from .retrieval import StageTimings, codesigned_search
 from .serve import ShardedSearch, _reduce_topk, shard_ranges
+from . import snapshot
 from .overarch import (DeviceCache, DeviceScorer, MultiTaskOp, MultiTaskOutput, merge_device,
                        retrieve, value_model_device)
 

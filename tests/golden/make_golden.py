@@ -450,6 +450,35 @@ def gen_retrieve(filtra):
     print("retrieve_cases.npz", len(meta))
 
 
+def gen_snapshot(filtra):
+    """A reference-published FLTRSNP1 file (ref/snapshot.py:157-174) plus its describe()
+    and, for two multi-task requests over all clusters, the reference retrieve() output."""
+    from filtra.catalog import default_features_spec, synth_catalog
+    from filtra.retrieval import RetrievalRequest, TaskQuery, retrieve
+    from filtra.snapshot import PublishConfig, describe, load, publish
+    cat = synth_catalog(3000, 32, 12, default_features_spec(), seed=44, blob_std=0.08)
+    vm = {"op": "add", "args": [{"op": "task", "task": "a"},
+                                {"op": "mul", "args": [{"op": "const", "value": 0.5},
+                                                       {"op": "task", "task": "b"}]}]}
+    path = OUT / "snapshot_small.fsnap"
+    publish(cat, path, version=7, config=PublishConfig(n_clusters=8, seed=44, value_model=vm))
+    engine = load(path)
+    rng = np.random.default_rng(12)
+    out = {"describe": describe(path), "requests": []}
+    for r in range(2):
+        expr = four_attribute_expr(rng, sizes=(20, 20, 16, 12))
+        tasks = [cat.embeddings[int(rng.integers(len(cat)))] for _ in range(2)]
+        req = RetrievalRequest(tasks=(TaskQuery("a", tasks[0]), TaskQuery("b", tasks[1])),
+                               filter=expr, nprobe=8, k0=200, topk=50)
+        res = retrieve(engine, req)
+        out["requests"].append({"expr": expr_to_json(expr),
+                                "users": [t.tolist() for t in tasks],
+                                "ids": [int(it.item_id) for it in res.items],
+                                "scores": [float(it.score).hex() for it in res.items]})
+    (OUT / "snapshot_small.json").write_text(json.dumps(out))
+    print("snapshot_small.fsnap", path.stat().st_size)
+
+
 def main():
     filtra = _import_reference()
     gen_hash(filtra)
@@ -461,6 +490,7 @@ def main():
     gen_topk20000(filtra)
     gen_merge(filtra)
     gen_retrieve(filtra)
+    gen_snapshot(filtra)
 
 
 if __name__ == "__main__":
