@@ -251,8 +251,16 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
   p->n_tc_work = (int64_t)tc_work.size() / 2;
   // candidate buffer: room for the sampling threshold's spread; while the exact radix
   // selection applies (k <= 10240) up to its staging capacity
+  // The sampled threshold lands ~jd / f above the k-th key (jd = mu + 5 sqrt(mu) + 8,
+  // mu = k f, f ~ 1/128) with a spread of ~sqrt(jd) / f; room for 5.5 sigma of it.
   int64_t want = std::max<int64_t>(2LL * k + 2048, 8192);
-  if (k <= 10240) want = std::max<int64_t>(want, std::min<int64_t>(kSelectMaxCand, (8LL * k) / 3));
+  {
+    const double mu = (double)k / 128.0;
+    const double jd = mu + 5.0 * std::sqrt(mu) + 8.0;
+    const int64_t noise = (int64_t)std::ceil(128.0 * (jd + 5.5 * std::sqrt(jd)));
+    // k <= 10240: stay within the selection's shared-memory staging when that is close
+    want = std::max<int64_t>(want, k <= 10240 ? std::min<int64_t>(kSelectMaxCand, noise) : noise);
+  }
   p->cap = (int32_t)std::max<int64_t>(1, std::min<int64_t>(p->total_slots, want));
   // sampling pass only when the candidate buffer cannot simply hold everything
   if (!(flags & FB_PLAN_NO_SAMPLE) && p->total_slots > p->cap && k > 0) {

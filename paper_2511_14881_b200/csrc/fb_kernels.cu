@@ -164,8 +164,92 @@ __global__ void k_dot_rows_f64(const float* __restrict__ x, int64_t rows, int di
     out[r] = __dadd_rn(0.0, pairwise_f64(x + r * dim, v, dim));
 }
 
-// Multi-task re-scoring: one thread per (request, candidate) computes the candidate's
-// dot with every task's user vector (numpy pairwise order, float64).
+// Multi-task re-scoring, dim <= 128: a block stages 128 candidates' rows (coalesced
+// gathers, rows padded to dim + 1 floats so the per-thread row walks are conflict-free)
+// and the request's task vectors in shared memory; one thread per candidate then runs
+// numpy's pairwise float64 dot against every task.
+constexpr int kTdRows = 128;
+__global__ void __launch_bounds__(kTdRows) k_task_dots_f64_smem(
+    const float* __restrict__ cache, int64_t n_rows, int dim, const int64_t* __restrict__ rows,
+    const int32_t* __restrict__ count, int64_t n_cand, const float* __restrict__ users,
+    int n_tasks, double* __restrict__ out) {
+  extern __shared__ double s_td[];
+  const int stride = dim + 4;  // 16-byte rows; float4 reads by 8-thread phases hit distinct banks
+  double* s_users = s_td;                                       // [n_tasks][dim], widened once
+  float* s_rows = reinterpret_cast<float*>(s_td + n_tasks * dim);  // [kTdRows][stride]
+  const int64_t b = blockIdx.y;
+  const int64_t c0 = (int64_t)blockIdx.x * kTdRows;
+  const int64_t nb = count[b];
+  if (c0 >= n_cand) return;
+  // rows: all 16-byte chunks of the block's rows in flight at once (cp.async, zero-fill for
+  // padding lanes), then the task vectors while they land
+  const int q4 = dim >> 2;
+  for (int e = threadIdx.x; e < kTdRows * q4; e += blockDim.x) {
+    const int r = e / q4, k = e - r * q4;
+    const int64_t c = c0 + r;
+    const int64_t row = (c < nb && c < n_cand) ? rows[b * n_cand + c] : -1;
+    const bool ok = row >= 0 && row < n_rows;
+    const float* src = cache + (ok ? row * dim + 4 * k : 0);
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_rows + r * stride + 4 * k);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+                 "r"(ok ? 16 : 0) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  for (int i = threadIdx.x; i < n_tasks * dim; i += blockDim.x)
+    s_users[i] = (double)users[b * n_tasks * dim + i];
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  const int64_t c = c0 + threadIdx.x;
+  if (c >= n_cand) return;
+  const int64_t row = c < nb ? rows[b * n_cand + c] : -1;
+  const bool ok = row >= 0 && row < n_rows;
+  const float* a = s_rows + threadIdx.x * stride;
+  // numpy pairwise order for 8 <= n <= 128 (see pairwise_f64): eight strided partial sums,
+  // a fixed combine tree, then the tail; four tasks share each widened row element.
+  const int n = dim, body = n - (n % 8);
+  for (int t0 = 0; t0 < n_tasks; t0 += 4) {
+    const double* u[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) u[q] = s_users + min(t0 + q, n_tasks - 1) * dim;
+    double r[4][8];
+    float xs0[8];
+    *reinterpret_cast<float4*>(xs0) = *reinterpret_cast<const float4*>(a);
+    *reinterpret_cast<float4*>(xs0 + 4) = *reinterpret_cast<const float4*>(a + 4);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double x = (double)xs0[j];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) r[q][j] = __dmul_rn(x, u[q][j]);
+    }
+    for (int i = 8; i < body; i += 8) {
+      float xs[8];
+      *reinterpret_cast<float4*>(xs) = *reinterpret_cast<const float4*>(a + i);
+      *reinterpret_cast<float4*>(xs + 4) = *reinterpret_cast<const float4*>(a + i + 4);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double x = (double)xs[j];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) r[q][j] = __dadd_rn(r[q][j], __dmul_rn(x, u[q][i + j]));
+      }
+    }
+    double res[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      res[q] = __dadd_rn(__dadd_rn(__dadd_rn(r[q][0], r[q][1]), __dadd_rn(r[q][2], r[q][3])),
+                         __dadd_rn(__dadd_rn(r[q][4], r[q][5]), __dadd_rn(r[q][6], r[q][7])));
+    for (int i = body; i < n; ++i) {
+      const double x = (double)a[i];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) res[q] = __dadd_rn(res[q], __dmul_rn(x, u[q][i]));
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (t0 + q < n_tasks) out[(b * n_tasks + t0 + q) * n_cand + c] = ok ? __dadd_rn(0.0, res[q]) : 0.0;
+  }
+}
+
+// Multi-task re-scoring, any dim: one thread per (request, candidate) computes the
+// candidate's dot with every task's user vector (numpy pairwise order, float64).
 __global__ void k_task_dots_f64(const float* __restrict__ cache, int64_t n_rows, int dim,
                                 const int64_t* __restrict__ rows, const int32_t* __restrict__ count,
                                 int64_t n_cand, const float* __restrict__ users, int n_req,
@@ -1064,6 +1148,17 @@ int launch_task_dots_f64(const float* cache, int64_t n_rows, int dim, const int6
                          int n_tasks, double* out, cudaStream_t s) {
   const int64_t total = (int64_t)n_req * n_cand;
   if (total <= 0 || n_tasks <= 0) return FB_OK;
+  const size_t smem = (size_t)kTdRows * (dim + 4) * sizeof(float) + (size_t)n_tasks * dim * sizeof(double);
+  if (dim >= 8 && dim <= 128 && dim % 4 == 0 && (reinterpret_cast<uintptr_t>(cache) & 15) == 0 && smem <= 200 * 1024 && n_req <= 65535) {
+    if (smem > 48 * 1024)
+      FB_CUDA(cudaFuncSetAttribute(k_task_dots_f64_smem,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const dim3 grid((unsigned)((n_cand + kTdRows - 1) / kTdRows), (unsigned)n_req);
+    k_task_dots_f64_smem<<<grid, kTdRows, smem, s>>>(cache, n_rows, dim, rows, count, n_cand,
+                                                     users, n_tasks, out);
+    FB_LAUNCH_CHECK("k_task_dots_f64_smem");
+    return FB_OK;
+  }
   k_task_dots_f64<<<grid_for(total, 128), 128, 0, s>>>(cache, n_rows, dim, rows, count, n_cand,
                                                        users, n_req, n_tasks, out);
   FB_LAUNCH_CHECK("k_task_dots_f64");
