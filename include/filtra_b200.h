@@ -258,6 +258,46 @@ int fb_task_dots_f64(const float* cache, int64_t n_rows, int32_t dim, const int6
                      const int32_t* count, int64_t n_cand, const float* users, int32_t n_req,
                      int32_t n_tasks, double* out, void* stream);
 
+/* ---- publish-side k-means (ivf.kmeans_pp_init / kmeans_train / kmeans_inertia,
+ * ivf.py:68-145). data is float64 [n, dim] row-major on the device. ---- */
+
+/* Device: D^2 seeding distances, best[i] = (init ? d_i : min(best[i], d_i)) with
+ * d_i = np.sum((data[i] - data[center_row]) ** 2) in numpy's pairwise order (ivf.py:86, 97). */
+int fb_kmeans_min_sqdist(const double* data, int64_t n, int32_t dim, int64_t center_row,
+                         double* best, int32_t init, void* stream);
+
+/* Scratch doubles fb_pairwise_sum_f64 needs for n elements. */
+int64_t fb_pairwise_sum_scratch(int64_t n);
+
+/* Device: *out = numpy's x.sum() for a contiguous float64 vector (pairwise summation tree,
+ * bit-identical; ivf.py:89 best.sum(), ivf.py:135 inertia). */
+int fb_pairwise_sum_f64(const double* x, int64_t n, double* out, double* scratch,
+                        int64_t scratch_len, void* stream);
+
+/* Device: the D^2 draw of ivf.py:94-96, *out_idx = min(searchsorted(cumsum(best), u * total,
+ * 'right'), n - 1), exact: approx_prefix (any-order prefix sums of best) decides the crossing
+ * when its error bound separates it, else the sequential cumsum is walked; exact_walks
+ * (optional) counts those walks. scratch: one uint64. */
+int fb_kmeans_draw(const double* best, const double* approx_prefix, int64_t n,
+                   const double* total, double u, int64_t* out_idx, uint64_t* scratch,
+                   int32_t* exact_walks, void* stream);
+
+/* Device: out[i] = |x[i]|^2 (pairwise order) for float64 rows (ivf.py:70-72). */
+int fb_row_sqnorm_f64(const double* x, int64_t n, int32_t dim, double* out, void* stream);
+
+/* Device: Lloyd assignment (ivf.py:68-73, 119-120): d2 = max((data_sq - 2 x.c) + center_sq, 0)
+ * in fp64, assign[i] = first argmin over the k centres, min_d2[i] its d2. */
+int fb_kmeans_assign(const double* data, int64_t n, int32_t dim, const double* centers, int32_t k,
+                     const double* data_sq, const double* center_sq, int64_t* assign,
+                     double* min_d2, void* stream);
+
+/* Device: centers[c] = mean of data rows order[seg_start[c] .. + seg_count[c]] (ascending row
+ * index), summed sequentially per column then divided by the count, bit-identical to
+ * data64[members].mean(axis=0) (ivf.py:131-133). */
+int fb_kmeans_means(const double* data, int32_t dim, const int64_t* order,
+                    const int64_t* seg_start, const int64_t* seg_count, int32_t k,
+                    double* centers, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

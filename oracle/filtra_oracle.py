@@ -469,3 +469,93 @@ def retrieve(per_task_ids: list, merge: str, cache_ids: np.ndarray, cache_vector
     order = np.lexsort((merged, -final))[:topk]
     return (merged[order], final[order],
             np.stack([ts[t][order] for t in task_names], axis=1))
+
+
+# --------------------------------------------------------------------------------------
+# publish-side k-means and IVF layout (ref/ivf.py:68-258)
+# --------------------------------------------------------------------------------------
+
+def kmeans_pp_init(data: np.ndarray, k: int, seed: int) -> np.ndarray:
+    """D^2 seeding (ref/ivf.py:76-101): row indices of the k chosen centres. The first is
+    uniform; each next one is drawn with probability proportional to the squared distance
+    to the nearest chosen centre (cumsum + searchsorted 'right' on u * total); with zero
+    total mass, uniformly among the rows not yet chosen."""
+    x = np.asarray(data, dtype=np.float64)
+    n = x.shape[0]
+    if k > n:
+        raise ValueError(f"k={k} exceeds number of rows n={n}")
+    gen = np.random.default_rng(seed)
+    picks = [int(gen.integers(n))]
+    dist = ((x - x[picks[0]]) ** 2).sum(axis=1)
+    used = np.zeros(n, dtype=bool)
+    used[picks[0]] = True
+    while len(picks) < k:
+        mass = dist.sum()
+        if mass <= 0.0:
+            free = np.nonzero(~used)[0]
+            nxt = int(free[gen.integers(free.size)])
+        else:
+            target = gen.random() * mass
+            nxt = min(int(np.searchsorted(np.cumsum(dist), target, side="right")), n - 1)
+        picks.append(nxt)
+        used[nxt] = True
+        dist = np.minimum(dist, ((x - x[nxt]) ** 2).sum(axis=1))
+    return np.array(picks, dtype=np.int64)
+
+
+def sq_dists(x: np.ndarray, c: np.ndarray) -> np.ndarray:
+    """(|x|^2 - 2 x.c) + |c|^2 clamped at 0 (ref/ivf.py:68-73)."""
+    xx = np.einsum("ij,ij->i", x, x)
+    cc = np.einsum("ij,ij->i", c, c)
+    return np.maximum(xx[:, None] - 2.0 * (x @ c.T) + cc[None, :], 0.0)
+
+
+def kmeans_train(data: np.ndarray, k: int, max_iters: int = 25, tol: float = 1e-4,
+                 seed: int = 0):
+    """Lloyd from D^2 seeding (ref/ivf.py:104-145) -> (centres float32 [k, d], assign i64).
+    Empty clusters take the costliest point of the first largest cluster before the means;
+    stop when the relative inertia gain is <= tol or after max_iters."""
+    x = np.asarray(data, dtype=np.float64)
+    n = x.shape[0]
+    cen = x[kmeans_pp_init(x, k, seed)].astype(np.float32).astype(np.float64)
+    last = None
+    lab = np.zeros(n, dtype=np.int64)
+    for _ in range(max_iters):
+        d2 = sq_dists(x, cen)
+        lab = d2.argmin(axis=1)
+        size = np.bincount(lab, minlength=k)
+        cost = d2[np.arange(n), lab]
+        for c in np.nonzero(size == 0)[0]:
+            big = int(size.argmax())
+            mem = np.nonzero(lab == big)[0]
+            j = mem[cost[mem].argmax()]
+            lab[j] = c
+            cost[j] = 0.0
+            size[big] -= 1
+            size[c] += 1
+        for c in range(k):
+            cen[c] = x[lab == c].mean(axis=0)
+        d2 = sq_dists(x, cen)
+        lab = d2.argmin(axis=1)
+        cur = float(d2[np.arange(n), lab].sum())
+        if last is not None and last - cur <= tol * last:
+            break
+        last = cur
+    return cen.astype(np.float32), lab
+
+
+def ivf_layout(assign: np.ndarray, item_ids: np.ndarray, k: int):
+    """Cluster-major slot layout (ref/ivf.py:229-249) -> (perm i64 [n_slots], offsets u64
+    [k, 2]): members of each cluster by ascending item id, ranges padded to 64."""
+    parts, offs, pos = [], np.zeros((k, 2), dtype=np.uint64), 0
+    for c in range(k):
+        mem = np.nonzero(assign == c)[0]
+        mem = mem[np.argsort(item_ids[mem], kind="stable")]
+        width = -(-mem.size // WORD_BITS) * WORD_BITS
+        block = np.full(width, -1, dtype=np.int64)
+        block[: mem.size] = mem
+        parts.append(block)
+        offs[c] = (pos, pos + width)
+        pos += width
+    perm = np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
+    return perm, offs

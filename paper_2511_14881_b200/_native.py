@@ -46,7 +46,9 @@ EXPORTED = (
     "fb_topk_plan_destroy", "fb_topk_plan_stats", "fb_topk_execute", "fb_merge_topk",
     "fb_dequant_scores", "fb_int8_dot_rows", "fb_dot_rows_f64", "fb_launch_count",
     "fb_topk_set_timing", "fb_topk_last_timing", "fb_topk_scan_path", "fb_debug_tc_scores",
-    "fb_task_dots_f64",
+    "fb_task_dots_f64", "fb_kmeans_min_sqdist", "fb_pairwise_sum_scratch",
+    "fb_pairwise_sum_f64", "fb_kmeans_draw", "fb_row_sqnorm_f64", "fb_kmeans_assign",
+    "fb_kmeans_means",
 )
 
 
@@ -136,6 +138,13 @@ def _declare(lib) -> None:
         "fb_int8_dot_rows": ([c_vp, i64, i32, i32, c_vp, c_vp, c_vp], i32),
         "fb_dot_rows_f64": ([c_vp, i64, i32, c_vp, c_vp, c_vp], i32),
         "fb_task_dots_f64": ([c_vp, i64, i32, c_vp, c_vp, i64, c_vp, i32, i32, c_vp, c_vp], i32),
+        "fb_kmeans_min_sqdist": ([c_vp, i64, i32, i64, c_vp, i32, c_vp], i32),
+        "fb_pairwise_sum_scratch": ([i64], i64),
+        "fb_pairwise_sum_f64": ([c_vp, i64, c_vp, c_vp, i64, c_vp], i32),
+        "fb_kmeans_draw": ([c_vp, c_vp, i64, c_vp, dbl, c_vp, c_vp, c_vp, c_vp], i32),
+        "fb_row_sqnorm_f64": ([c_vp, i64, i32, c_vp, c_vp], i32),
+        "fb_kmeans_assign": ([c_vp, i64, i32, c_vp, i32, c_vp, c_vp, c_vp, c_vp, c_vp], i32),
+        "fb_kmeans_means": ([c_vp, i32, c_vp, c_vp, c_vp, i32, c_vp, c_vp], i32),
         "fb_launch_count": ([], ctypes.c_uint64),
         "fb_topk_scan_path": ([c_vp], i32),
         "fb_debug_tc_scores": ([ctypes.POINTER(FbIndex), c_vp, i32, c_vp, c_vp], i32),

@@ -28,7 +28,7 @@ from .quantize import QuantParams, quantize_device
 
 def _u64_order_key(ids: torch.Tensor) -> torch.Tensor:
     """int64 tensor holding uint64 bits -> int64 with the same order as the unsigned ids."""
-    return ids ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=ids.device)
+    return torch.bitwise_xor(ids, -(1 << 63))
 
 
 @dataclass

@@ -278,10 +278,14 @@ def merge_device(ids: torch.Tensor, counts: torch.Tensor, merge: str):
             ahead = torch.full_like(key, _PAD)
             ahead[:, : T * k - (T - 1)] = key[:, T - 1:]
             keep &= ahead == key
-    mcount = keep.sum(dim=1).to(torch.int32)
-    # the kept keys are ascending already: one more sort moves the dropped ones (PAD) last
-    merged = torch.sort(torch.where(keep, key, torch.full_like(key, _PAD)), dim=1).values
-    return _u64_order_key(merged), mcount
+    # the kept keys are ascending already: compact them to the front (dropped slots go to
+    # a spill column past the end)
+    pos = torch.cumsum(keep, dim=1)
+    mcount = pos[:, -1].to(torch.int32)
+    dst = torch.where(keep, pos - 1, torch.full_like(pos, T * k))
+    merged = torch.full((B, T * k + 1), _PAD, dtype=key.dtype, device=key.device)
+    merged.scatter_(1, dst, key)
+    return _u64_order_key(merged[:, : T * k]), mcount
 
 
 # ------------------------------------------------------------------------------------

@@ -479,6 +479,63 @@ def gen_snapshot(filtra):
     print("snapshot_small.fsnap", path.stat().st_size)
 
 
+def _blobs(n_per=50, dim=4, gap=10.0, seed=0):
+    """The reference's tests/test_ivf.py:14-18 data shape."""
+    rng = np.random.default_rng(seed)
+    return np.vstack([rng.standard_normal((n_per, dim)) * 0.1,
+                      rng.standard_normal((n_per, dim)) * 0.1 + gap])
+
+
+def gen_kmeans(filtra):
+    """KMeans++ seeding, Lloyd and the build_ivf layout (ref ivf.py:76-258)."""
+    from filtra.catalog import default_features_spec, synth_catalog
+    from filtra.ivf import build_ivf, kmeans_pp_init, kmeans_train
+    rng = np.random.default_rng(77)
+    pp = {
+        "normal128": (rng.standard_normal((1500, 128)), 40, 3),
+        "unit_f32": (None, 30, 11),
+        "blobs": (_blobs(), 5, 9),
+        "dups": (np.repeat(_blobs(n_per=10), 10, axis=0), 8, 21),
+        "zero_mass": (np.repeat(rng.standard_normal((3, 8)), 5, axis=0), 6, 4),
+        "k_eq_n": (np.arange(12, dtype=np.float64).reshape(6, 2), 6, 5),
+        "dim13": (rng.standard_normal((500, 13)), 20, 6),
+        "dim200": (rng.standard_normal((300, 200)), 10, 7),
+    }
+    e = rng.standard_normal((2000, 64)).astype(np.float32)
+    pp["unit_f32"] = ((e / np.linalg.norm(e, axis=1, keepdims=True)).astype(np.float32), 30, 11)
+    arrays, meta = {}, {"pp": [], "train": []}
+    for name, (x, k, seed) in pp.items():
+        arrays[f"pp_{name}_x"] = x
+        arrays[f"pp_{name}_c"] = kmeans_pp_init(x, k, seed).vectors
+        meta["pp"].append({"name": name, "k": k, "seed": seed})
+    centres4 = np.array([[0, 0], [0, 8], [8, 0], [8, 8]], dtype=np.float64)
+    r2 = np.random.default_rng(2)
+    train = {
+        "four_blobs": (np.vstack([r2.standard_normal((100, 2)) * 0.5 + c for c in centres4]),
+                       4, 0, 25, 1e-4),
+        "two_blobs6": (_blobs(n_per=100, dim=6, gap=3.0, seed=8), 5, 13, 12, 0.0),
+        "dups": (np.repeat(_blobs(n_per=10), 10, axis=0), 8, 21, 25, 1e-4),
+        "normal16": (rng.standard_normal((2000, 16)), 12, 2, 25, 1e-4),
+    }
+    for name, (x, k, seed, iters, tol) in train.items():
+        c, a = kmeans_train(x, k, max_iters=iters, tol=tol, seed=seed)
+        arrays[f"tr_{name}_x"] = x
+        arrays[f"tr_{name}_c"] = c.vectors
+        arrays[f"tr_{name}_a"] = a
+        meta["train"].append({"name": name, "k": k, "seed": seed, "max_iters": iters, "tol": tol})
+    cat = synth_catalog(3000, 16, 30, default_features_spec()[:2], seed=5, blob_std=0.08)
+    index = build_ivf(cat, k=7, seed=3)
+    arrays.update(ivf_emb=cat.embeddings, ivf_ids=cat.item_ids, ivf_perm=index.perm,
+                  ivf_inv_perm=index.inv_perm, ivf_offsets=index.cluster_offsets,
+                  ivf_items_q=index.items_q.data, ivf_valid=index.valid_mask,
+                  ivf_slot_ids=index.item_ids, ivf_centroids=index.centroids.vectors,
+                  ivf_qp=np.array([index.items_q.params.global_min, index.items_q.params.global_max]))
+    meta["ivf"] = {"k": 7, "seed": 3}
+    np.savez_compressed(OUT / "kmeans_cases.npz", **arrays)
+    (OUT / "kmeans_meta.json").write_text(json.dumps(meta))
+    print("kmeans_cases.npz")
+
+
 def main():
     filtra = _import_reference()
     gen_hash(filtra)
@@ -491,6 +548,7 @@ def main():
     gen_merge(filtra)
     gen_retrieve(filtra)
     gen_snapshot(filtra)
+    gen_kmeans(filtra)
 
 
 if __name__ == "__main__":

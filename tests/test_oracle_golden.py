@@ -192,3 +192,23 @@ def test_oracle_merge_candidates_matches_reference():
         lists = [z[f"m{c}_l{i}"] for i in range(int(z[f"m{c}_n"][0]))]
         assert np.array_equal(orc.merge_candidates(lists, "union"), z[f"m{c}_union"])
         assert np.array_equal(orc.merge_candidates(lists, "intersection"), z[f"m{c}_inter"])
+
+
+def test_oracle_kmeans_matches_reference():
+    """KMeans++ seeding, Lloyd and the IVF slot layout (ref ivf.py:76-258)."""
+    z = load_npz("kmeans_cases.npz")
+    meta = load_json("kmeans_meta.json")
+    for m in meta["pp"]:
+        x = z[f"pp_{m['name']}_x"]
+        got = np.asarray(x, dtype=np.float64)[orc.kmeans_pp_init(x, m["k"], m["seed"])]
+        assert np.array_equal(got.astype(np.float32), z[f"pp_{m['name']}_c"]), m["name"]
+    for m in meta["train"]:
+        c, a = orc.kmeans_train(z[f"tr_{m['name']}_x"], m["k"], m["max_iters"], m["tol"], m["seed"])
+        assert np.array_equal(c, z[f"tr_{m['name']}_c"]), m["name"]
+        assert np.array_equal(a, z[f"tr_{m['name']}_a"]), m["name"]
+    k, seed = meta["ivf"]["k"], meta["ivf"]["seed"]
+    c, a = orc.kmeans_train(z["ivf_emb"], k, seed=seed)
+    assert np.array_equal(c, z["ivf_centroids"])
+    perm, offs = orc.ivf_layout(a, z["ivf_ids"], k)
+    assert np.array_equal(perm, z["ivf_perm"])
+    assert np.array_equal(offs, z["ivf_offsets"])
