@@ -21,7 +21,7 @@ from paper_2511_14881_b200.filter_query import (And, FilterBatch, Leaf, Not, OpC
 
 def header_symbols() -> set[str]:
     text = (ROOT / "include" / "filtra_b200.h").read_text()
-    return set(re.findall(r"^\s*(?:int|const char\*|uint64_t)\s+(fb_\w+)\(", text, flags=re.M))
+    return set(re.findall(r"^\s*(?:int|int64_t|const char\*|uint64_t)\s+(fb_\w+)\(", text, flags=re.M))
 
 
 def test_library_exports_every_header_symbol():
