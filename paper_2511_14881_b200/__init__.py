@@ -17,7 +17,8 @@ from .quantize import (QuantParams, QuantizedMatrix, compute_quant_params, dequa
                        int8_dot_rows, quantize_matrix, quantize_value, quantize_vector)
 from .retrieval import StageTimings, codesigned_search
 from .serve import ShardedSearch, _reduce_topk, shard_ranges
-from . import snapshot
+from . import kmeans, snapshot
+from .kmeans import Centroids, IvfIndex, build_ivf, kmeans_inertia, kmeans_pp_init, kmeans_train
 from .overarch import (DeviceCache, DeviceScorer, MultiTaskOp, MultiTaskOutput, merge_device,
                        retrieve, value_model_device)
 
@@ -35,4 +36,5 @@ __all__ = [
     "probe_centroids", "quantize_matrix", "quantize_value", "quantize_vector", "search",
     "search_clusters", "shard_ranges", "DeviceCache", "DeviceScorer", "MultiTaskOp",
     "MultiTaskOutput", "merge_device", "retrieve", "value_model_device", "IvfSearchOp",
+    "Centroids", "IvfIndex", "build_ivf", "kmeans_inertia", "kmeans_pp_init", "kmeans_train",
 ]
