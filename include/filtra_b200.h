@@ -258,6 +258,21 @@ int fb_task_dots_f64(const float* cache, int64_t n_rows, int32_t dim, const int6
                      const int32_t* count, int64_t n_cand, const float* users, int32_t n_req,
                      int32_t n_tasks, double* out, void* stream);
 
+/* Device, IVF-probed batched search (retrieval.codesigned_search with nprobe < n_clusters,
+ * retrieval.py:110-144; ivf.search_clusters over the probed clusters, ivf.py:285-334): for
+ * query b, probe_words[(b * nprobe + j) * 2 ..] is the 64-slot word range [w0, w1) of its
+ * j-th probed cluster. Every slot there that is valid and passes the query's filter program
+ * (evaluated over the probed words only, as the reference does) is scored exactly and its
+ * key kept in cand_key[b * cap ..]; then the exact (score desc, item_id asc) top-k is written
+ * as by fb_topk_execute. cap must be >= the largest number of slots one query probes (the
+ * selection is exact only then); cand_slot may be NULL when idx->slot_of_rank is set and
+ * k <= 24576. */
+int fb_ivf_topk(const fb_index_t* idx, const int8_t* queries_q, int32_t n_queries,
+                const fb_filter_prog_t* prog, const int64_t* probe_words, int32_t nprobe, int32_t k,
+                int32_t cap, uint64_t* cand_key, uint32_t* cand_slot, uint32_t* cand_cnt,
+                uint64_t* out_ids, int32_t* out_scores, int32_t* out_count, uint64_t* out_keys,
+                double* out_fscores, double gmin, double gmax, void* stream);
+
 /* ---- publish-side k-means (ivf.kmeans_pp_init / kmeans_train / kmeans_inertia,
  * ivf.py:68-145). data is float64 [n, dim] row-major on the device. ---- */
 

@@ -532,6 +532,69 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
   return FB_OK;
 }
 
+int fb_ivf_topk(const fb_index_t* idx, const int8_t* queries_q, int32_t n_queries,
+                const fb_filter_prog_t* prog, const int64_t* probe_words, int32_t nprobe, int32_t k,
+                int32_t cap, uint64_t* cand_key, uint32_t* cand_slot, uint32_t* cand_cnt,
+                uint64_t* out_ids, int32_t* out_scores, int32_t* out_count, uint64_t* out_keys,
+                double* out_fscores, double gmin, double gmax, void* stream) {
+  int rc = validate_index(idx);
+  if (rc) return rc;
+  if (n_queries < 0 || nprobe < 0 || k < 0 || cap < 0) return fail(FB_ERR_INVALID, "negative size");
+  if (prog != nullptr && prog->ops != nullptr) {
+    rc = validate_prog(prog, n_queries);
+    if (rc) return rc;
+  }
+  if (idx->dim_pad % 16 != 0 || idx->dim_pad > kIvfMaxDimPad)
+    return fail(FB_ERR_UNSUPPORTED, "dim_pad must be a multiple of 16 and <= 1024");
+  if (out_fscores && !(gmax > gmin)) return fail(FB_ERR_DEGENERATE, "fscores need gmax > gmin");
+  const bool by_rank = select_by_rank(cap, k, idx->slot_of_rank);
+  if (!by_rank && cand_slot == nullptr) return fail(FB_ERR_INVALID, "cand_slot needed for this k");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n_queries == 0) return FB_OK;
+  FB_CUDA(cudaMemsetAsync(cand_cnt, 0, sizeof(uint32_t) * n_queries, s));
+  if (k == 0) {
+    FB_CUDA(cudaMemsetAsync(out_count, 0, sizeof(int32_t) * n_queries, s));
+    return FB_OK;
+  }
+  IvfScanArgs a{};
+  a.idx = *idx;
+  a.queries = queries_q;
+  a.n_queries = n_queries;
+  a.has_prog = prog != nullptr && prog->ops != nullptr ? 1 : 0;
+  if (a.has_prog) a.prog = *prog;
+  a.probe_words = probe_words;
+  a.nprobe = nprobe;
+  a.out_key = cand_key;
+  a.out_slot = by_rank ? nullptr : cand_slot;
+  a.out_cnt = cand_cnt;
+  a.cap = cap;
+  rc = launch_ivf_scan(a, s);
+  if (rc) return rc;
+  SelectArgs sel{};
+  sel.n_queries = n_queries;
+  sel.k = k;
+  sel.cap = cap;
+  sel.cand_key = cand_key;
+  sel.cand_slot = cand_slot;
+  sel.slot_of_rank = idx->slot_of_rank;
+  sel.id_of_rank = idx->id_of_rank;
+  sel.n_slots = idx->n_slots;
+  sel.cnt = cand_cnt;
+  sel.item_ids = idx->item_ids;
+  sel.row_sum = idx->row_sum;
+  sel.queries = queries_q;
+  sel.dim = idx->dim;
+  sel.dim_pad = idx->dim_pad;
+  sel.gmin = gmin;
+  sel.gmax = gmax;
+  sel.out_ids = out_ids;
+  sel.out_scores = out_scores;
+  sel.out_count = out_count;
+  sel.out_keys = out_keys;
+  sel.out_fscores = out_fscores;
+  return launch_select(sel, s);
+}
+
 uint64_t fb_launch_count(void) { return g_launches.load(); }
 
 int fb_topk_scan_path(const fb_topk_plan_t* p) { return p == nullptr ? -1 : p->last_scan_tc; }

@@ -134,6 +134,23 @@ struct ScanArgs {
   int64_t dump_ld;
 };
 
+// IVF-probed scan: per (query, probed cluster) pair, every eligible slot's key
+constexpr int kIvfMaxDimPad = 1024;
+struct IvfScanArgs {
+  fb_index_t idx;
+  const int8_t* queries;       // [B, dim_pad]
+  int32_t n_queries;
+  fb_filter_prog_t prog;
+  int32_t has_prog;
+  const int64_t* probe_words;  // [B, nprobe, 2] word range [w0, w1) of each probed cluster
+  int32_t nprobe;
+  uint64_t* out_key;           // [B, cap]
+  uint32_t* out_slot;          // [B, cap] (nullable)
+  uint32_t* out_cnt;           // [B] (zeroed by the caller)
+  int32_t cap;
+};
+int launch_ivf_scan(const IvfScanArgs& a, cudaStream_t s);
+
 // kernels / launchers implemented in fb_kernels.cu
 int launch_scan_simt(const ScanArgs& a, cudaStream_t s);
 int launch_bloom_build(const uint64_t* fid, const uint64_t* value, const int64_t* slot,

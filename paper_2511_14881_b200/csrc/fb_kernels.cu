@@ -376,6 +376,47 @@ __global__ void __launch_bounds__(256) k_scan_simt(ScanArgs a) {
 }
 
 // ------------------------------------------------------------------------------------
+// IVF-probed scan (ref retrieval.codesigned_search with nprobe < n_clusters,
+// retrieval.py:124-135 + ivf.search_clusters, ivf.py:285-334): one CTA per (query, probed
+// cluster) pair, one thread per 64-slot word of the cluster. The thread evaluates the
+// query's filter program on its word (coalesced plane loads across the warp's consecutive
+// words), then scores every eligible slot with dp4a against the query staged in shared
+// memory and appends its key. The caller sizes cap to the largest possible eligible count,
+// so every eligible pair is kept and the selection is exact without a threshold.
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(64) k_ivf_scan(IvfScanArgs a) {
+  __shared__ __align__(16) int8_t s_q[kIvfMaxDimPad];
+  const int dp = a.idx.dim_pad;
+  const int64_t pairs = (int64_t)a.n_queries * a.nprobe;
+  for (int64_t pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+    const int q = (int)(pr / a.nprobe);
+    const int64_t w0 = a.probe_words[2 * pr], w1 = a.probe_words[2 * pr + 1];
+    __syncthreads();
+    for (int i = threadIdx.x; i < dp / 16; i += blockDim.x)
+      reinterpret_cast<int4*>(s_q)[i] =
+          __ldg(reinterpret_cast<const int4*>(a.queries + (int64_t)q * dp) + i);
+    __syncthreads();
+    for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
+      const uint64_t v = a.idx.valid[w];
+      uint64_t m = a.has_prog ? eval_program_word(a.prog, q, a.idx.planes, a.idx.n_words, w, v) & v
+                              : v;
+      const int64_t slot0 = w * 64;
+      while (m) {
+        const int i = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        const int32_t sc = dot_i8(a.idx.items + (slot0 + i) * dp, s_q, dp);
+        const uint32_t p = atomicAdd(a.out_cnt + q, 1u);
+        if (p < (uint32_t)a.cap) {
+          a.out_key[(int64_t)q * a.cap + p] = make_key(sc, a.idx.id_rank[slot0 + i]);
+          if (a.out_slot) a.out_slot[(int64_t)q * a.cap + p] = (uint32_t)(slot0 + i);
+        }
+      }
+    }
+  }
+}
+
+
+// ------------------------------------------------------------------------------------
 // Block-wide bitonic sort (descending by key) over n = power of two elements in smem.
 // ------------------------------------------------------------------------------------
 template <bool kHasVal>
@@ -1269,6 +1310,15 @@ int launch_select(const SelectArgs& a, cudaStream_t s) {
   FB_CUDA(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_select<<<a.n_queries, kSelectThreads, smem, s>>>(a);
   FB_LAUNCH_CHECK("k_select");
+  return FB_OK;
+}
+
+int launch_ivf_scan(const IvfScanArgs& a, cudaStream_t s) {
+  const int64_t pairs = (int64_t)a.n_queries * a.nprobe;
+  if (pairs <= 0) return FB_OK;
+  const int grid = (int)std::min<int64_t>(pairs, 148LL * 64);
+  k_ivf_scan<<<grid, 64, 0, s>>>(a);
+  FB_LAUNCH_CHECK("k_ivf_scan");
   return FB_OK;
 }
 

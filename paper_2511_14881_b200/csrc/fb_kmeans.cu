@@ -217,14 +217,14 @@ __global__ void k_draw_first_above(const double* __restrict__ approx, int64_t n,
     }
 }
 
-constexpr int kSeqChunk = 4096;
+constexpr int kSeqChunk = 2048;
 __global__ void __launch_bounds__(256) k_draw_resolve(const double* __restrict__ x,
                                                       const double* __restrict__ approx, int64_t n,
                                                       const double* __restrict__ total, double u,
                                                       const unsigned long long* lo,
                                                       int64_t* __restrict__ out,
                                                       int32_t* __restrict__ exact_walks) {
-  __shared__ double buf[kSeqChunk];
+  __shared__ __align__(16) double buf[2][kSeqChunk];
   __shared__ int64_t s_idx;
   __shared__ int s_found;
   double r, delta;
@@ -238,27 +238,50 @@ __global__ void __launch_bounds__(256) k_draw_resolve(const double* __restrict__
     if (threadIdx.x == 0) *out = l;
     return;
   }
-  // ambiguous: the exact sequential cumsum, staged through shared memory in chunks
+  // ambiguous: thread 0 walks the exact sequential cumsum (c_0 = x_0 since x_0 >= 0) while
+  // warps 1.. stage the next chunk; chunks are zero-padded (adding +0 leaves c unchanged)
   if (threadIdx.x == 0) {
     s_idx = n - 1;
     s_found = 0;
     if (exact_walks) atomicAdd(exact_walks, 1);
   }
-  double c = 0.0;  // thread 0's running cumsum (c_0 = x_0 since x_0 >= 0)
-  for (int64_t c0 = 0; c0 < n; c0 += kSeqChunk) {
+  auto stage = [&](int64_t c0, double* dst, int t0, int nt) {
+    for (int i = t0; i < kSeqChunk; i += nt) dst[i] = c0 + i < n ? x[c0 + i] : 0.0;
+  };
+  stage(0, buf[0], threadIdx.x, blockDim.x);
+  double c = 0.0;
+  int cur = 0;
+  for (int64_t c0 = 0;; c0 += kSeqChunk, cur ^= 1) {
     __syncthreads();
-    if (s_found) break;
-    const int64_t m = min((int64_t)kSeqChunk, n - c0);
-    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) buf[i] = x[c0 + i];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int64_t i = 0; i < m; ++i) {
-        c = __dadd_rn(c, buf[i]);
-        if (c > r) {
-          s_idx = c0 + i;
+    if (s_found || c0 >= n) break;
+    if (threadIdx.x >= 32) {
+      if (c0 + kSeqChunk < n) stage(c0 + kSeqChunk, buf[cur ^ 1], threadIdx.x - 32, blockDim.x - 32);
+    } else if (threadIdx.x == 0) {
+      const double* b = buf[cur];
+      for (int i = 0; i < kSeqChunk; i += 16) {
+        double v[16];
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(b + i + j);
+          v[j] = t.x;
+          v[j + 1] = t.y;
+        }
+        double t = c;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) t = __dadd_rn(t, v[j]);
+        if (t > r) {  // the crossing is inside this block of 16: locate it
+#pragma unroll 1
+          for (int j = 0; j < 16; ++j) {
+            c = __dadd_rn(c, v[j]);
+            if (c > r) {
+              s_idx = c0 + i + j;
+              break;
+            }
+          }
           s_found = 1;
           break;
         }
+        c = t;
       }
     }
   }

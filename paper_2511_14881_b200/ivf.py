@@ -9,6 +9,7 @@ reference-shaped ``IvfIndex`` (uploaded to HBM once and cached). Compute runs th
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -16,7 +17,7 @@ import torch
 
 from . import _native
 from ._device import device, to_dev, to_dev_u64
-from .engine import DeviceIndex, TopkOp, device_index_for
+from .engine import DeviceIndex, TopkOp, TopkOutput, device_index_for
 from .errors import DimMismatch
 
 TILE_ROWS = 4096  # reference tile contract (ivf.py:24); GPU tiles are 128 rows
@@ -137,16 +138,18 @@ class IvfSearchOp:
     ``nprobe < n_clusters``, ref/retrieval.py:110-144, for B queries at once).
 
     On the device: every query's centroid dots (``fb_task_dots_f64``, numpy's pairwise
-    order, so probe ties resolve as in ``probe_centroids``), its top-``nprobe`` clusters
-    (stable sort: ties by ascending cluster id), a per-query probe mask over the slot
-    words of those clusters (difference array + prefix sum), then one batched filtered
-    top-k whose per-query masks confine each query to its probed clusters. The filter is
-    evaluated inside the scan, so restricting it to the probed ranges is implicit and the
-    result equals the reference's range-restricted evaluation exactly. (The scan covers
-    the clusters probed by any query of the batch; per-query work is pruned by the mask.)
+    order, so probe ties resolve as in ``probe_centroids``) and its top-``nprobe`` clusters
+    (stable sort: ties by ascending cluster id). Then, by default (``path="probe"``), the
+    grouped scan ``fb_ivf_topk``: one CTA per (query, probed cluster) evaluates the query's
+    filter on that cluster's words only and scores its eligible slots -- work proportional
+    to nprobe, not to the index -- followed by the exact top-k selection. ``path="masked"``
+    runs the exhaustive tensor-core scan with per-query probe masks instead (same results).
     """
 
-    def __init__(self, index, n_queries: int, nprobe: int, k0: int, flags: int = 0):
+    def __init__(self, index, n_queries: int, nprobe: int, k0: int, flags: int = 0,
+                 path: str = "probe"):
+        if path not in ("probe", "masked"):
+            raise ValueError(f"unknown path {path!r}")
         self.dix = device_index_for(index)
         if self.dix.centroids is None and self.dix.cluster_offsets.shape[0] != 1:
             raise ValueError("index has no centroids")
@@ -154,14 +157,29 @@ class IvfSearchOp:
         self.C = int(self.dix.cluster_offsets.shape[0])
         self.nprobe = min(max(int(nprobe), 1), self.C)
         self.k0 = int(k0)
+        self.path = path
         dev = device()
         offs = torch.as_tensor(self.dix.cluster_offsets, dtype=torch.int64, device=dev)
         self._w0 = offs[:, 0] >> 6
         self._w1 = (offs[:, 1] + 63) >> 6
         self._rows = torch.arange(self.C, dtype=torch.int64, device=dev).repeat(self.B, 1)
         self._cnt = torch.full((self.B,), self.C, dtype=torch.int32, device=dev)
-        self.op = TopkOp(self.dix, self.B, self.k0,
-                         np.array([[0, self.dix.n_slots]], dtype=np.int64), flags)
+        if path == "masked":
+            self.op = TopkOp(self.dix, self.B, self.k0,
+                             np.array([[0, self.dix.n_slots]], dtype=np.int64), flags)
+            return
+        # the most slots one query can probe: its nprobe largest clusters
+        sizes = np.sort(np.asarray(self.dix.cluster_offsets[:, 1] - self.dix.cluster_offsets[:, 0],
+                                   dtype=np.int64))[::-1]
+        self.cap = int(max(1, sizes[: self.nprobe].sum()))
+        if self.cap >= 1 << 31:
+            raise ValueError("probed slot count exceeds the 32-bit candidate buffer")
+        need_slot = self.dix.slot_of_rank is None or self.k0 > 24576
+        self._cand_key = torch.empty((self.B, self.cap), dtype=torch.int64, device=dev)
+        self._cand_slot = (torch.empty((self.B, self.cap), dtype=torch.int32, device=dev)
+                           if need_slot else None)
+        self._cand_cnt = torch.empty(self.B, dtype=torch.int32, device=dev)
+        self._idx_struct = self.dix.struct()
 
     def probe(self, queries: torch.Tensor) -> torch.Tensor:
         """int64 [B, nprobe] probed cluster ids per query."""
@@ -187,11 +205,35 @@ class IvfSearchOp:
         return torch.where(cover, torch.full_like(cover, -1, dtype=torch.int64),
                            torch.zeros_like(cover, dtype=torch.int64))
 
+    def probe_words(self, clusters: torch.Tensor) -> torch.Tensor:
+        """int64 [B, nprobe, 2] word ranges of the probed clusters."""
+        return torch.stack([self._w0[clusters], self._w1[clusters]], dim=2).contiguous()
+
     def __call__(self, queries: torch.Tensor, filters=None):
         """queries float32 [B, dim] (device) -> TopkOutput; also returns the probed ids."""
         if queries.shape != (self.B, self.dix.dim):
             raise DimMismatch(self.dix.dim, int(queries.shape[-1]))
         clusters = self.probe(queries)
         qq = self.dix.quantize_queries(queries)
-        out = self.op(qq, filters, masks=self.masks(clusters))
+        if self.path == "masked":
+            return self.op(qq, filters, masks=self.masks(clusters)), clusters
+        words = self.probe_words(clusters)
+        dev = qq.device
+        k = max(self.k0, 1)
+        out = TopkOutput(ids=torch.empty((self.B, k), dtype=torch.int64, device=dev),
+                         scores=torch.empty((self.B, k), dtype=torch.int32, device=dev),
+                         count=torch.empty((self.B,), dtype=torch.int32, device=dev),
+                         keys=None, fscores=None)
+        prog = filters.struct() if filters is not None else None
+        qp = self.dix.qp
+        _native.check(_native.lib().fb_ivf_topk(
+            ctypes.byref(self._idx_struct), qq.data_ptr(), self.B,
+            ctypes.byref(prog) if prog is not None else None, words.data_ptr(), self.nprobe,
+            self.k0, self.cap, self._cand_key.data_ptr(),
+            self._cand_slot.data_ptr() if self._cand_slot is not None else None,
+            self._cand_cnt.data_ptr(), out.ids.data_ptr(), out.scores.data_ptr(),
+            out.count.data_ptr(), None, None,
+            float(qp.global_min) if qp else 0.0, float(qp.global_max) if qp else 1.0,
+            _native.stream_ptr()))
+        self._keep = (qq, filters, words)
         return out, clusters

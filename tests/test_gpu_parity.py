@@ -414,9 +414,10 @@ def test_pipelined_topk_matches_batched_op(fb, wl_small):
             assert np.array_equal(sc.numpy(), ref.scores.cpu().numpy())
 
 
+@pytest.mark.parametrize("path", ["probe", "masked"])
 @pytest.mark.parametrize("case,nprobe,filtered", [(0, 3, True), (3, 7, True), (2, 1, False),
                                                 (1, 5, True)])
-def test_ivf_batched_probe_vs_oracle(fb, case, nprobe, filtered):
+def test_ivf_batched_probe_vs_oracle(fb, case, nprobe, filtered, path):
     """Batched IVF-probed co-designed search (IvfSearchOp): per-query centroid probe on the
     GPU (numpy-order float64 dots, ties by cluster id) + per-query probe masks + one
     batched filtered top-k == the oracle's codesigned_search with nprobe, per query."""
@@ -432,7 +433,7 @@ def test_ivf_batched_probe_vs_oracle(fb, case, nprobe, filtered):
                if filtered else None for _ in range(12)]
     batch = FilterBatch.pack(filters, fb.BloomParams()) if filtered else None
     k = 60
-    op = fb.IvfSearchOp(dix, 12, nprobe, k)
+    op = fb.IvfSearchOp(dix, 12, nprobe, k, path=path)
     out, clusters = op(torch.as_tensor(qs, device="cuda"), batch)
     torch.cuda.synchronize()
     lo, hi = (float(x) for x in z[pre + "qp"])
@@ -449,6 +450,49 @@ def test_ivf_batched_probe_vs_oracle(fb, case, nprobe, filtered):
         ids, scores = out.host(t)
         assert np.array_equal(ids, ref.item_ids), t
         assert np.array_equal(scores, ref.scores), t
+
+
+@pytest.mark.parametrize("filtered,k", [(True, 1000), (False, 2000), (True, 30000)])
+def test_ivf_grouped_scan_at_scale_vs_oracle(fb, filtered, k):
+    """The grouped IVF scan (fb_ivf_topk) over a GPU-built IVF index (200k items, 400
+    k-means clusters, 64 queries x 8 probes, the 4-attribute filter) == the oracle's
+    codesigned_search per query; k = 30000 exceeds what one query can probe (all kept) and
+    takes the slot-carrying selection."""
+    from paper_2511_14881_b200 import kmeans, workload
+    from paper_2511_14881_b200.filter_query import FilterBatch
+    n, B, nprobe = 200_000, 64, 8
+    wl = workload.make_workload(20_000, B, dim=128, seed=5)  # for its 4-attribute filters
+    rng = np.random.default_rng(9)
+    centres = rng.standard_normal((500, 128)).astype(np.float32)
+    emb = centres[rng.integers(500, size=n)] + rng.standard_normal((n, 128)).astype(np.float32) * 0.3
+    emb /= np.linalg.norm(emb, axis=1, keepdims=True)
+    ids = rng.permutation(np.arange(1, n + 1, dtype=np.uint64) * 7919)
+    cat = type("Cat", (), {"embeddings": emb, "item_ids": ids, "__len__": lambda self: n})()
+    ivf = kmeans.build_ivf(cat, k=400, seed=1, max_iters=3)
+    feats = [[(1, int(rng.integers(50))), (2, int(rng.integers(50))), (3, int(rng.integers(40))),
+              (4, int(rng.integers(30)))] for _ in range(n)]
+    bloom = fb.build_bloom(ivf.slot_features(feats), fb.BloomParams(), ivf.n_slots)
+    dix = fb.device_index_for(ivf, bloom=bloom)
+    qs = emb[rng.integers(n, size=B)] + rng.standard_normal((B, 128)).astype(np.float32) * 0.05
+    filters = [wl.filters[b] if filtered else None for b in range(B)]
+    batch = FilterBatch.pack(filters, fb.BloomParams()) if filtered else None
+    op = fb.IvfSearchOp(dix, B, nprobe, k)
+    out, clusters = op(torch.as_tensor(qs, device="cuda"), batch)
+    torch.cuda.synchronize()
+    qp = ivf.items_q.params
+    planes = bloom.planes if isinstance(bloom.planes, np.ndarray) else bloom.planes.cpu().numpy()
+    for t in range(0, B, 4):
+        cl = clusters[t].cpu().numpy()
+        prog = None
+        if filters[t] is not None:
+            cf = filters[t]
+            prog = ([(int(o), int(a)) for o, a in cf.ops], [(f, v, b.set_bits) for f, v, b in cf.leaves])
+        ref = orc.codesigned_search(ivf.items_q.data, ivf.valid_mask, ivf.item_ids,
+                                    ivf.cluster_offsets, planes, prog,
+                                    orc.quantize(qs[t], qp.global_min, qp.global_max), cl, k)
+        got_ids, got_scores = out.host(t)
+        assert np.array_equal(got_ids, ref.item_ids), t
+        assert np.array_equal(got_scores, ref.scores), t
 
 
 def test_merge_topk_device(fb, rng):
