@@ -384,10 +384,83 @@ __global__ void __launch_bounds__(256) k_scan_simt(ScanArgs a) {
 // memory and appends its key. The caller sizes cap to the largest possible eligible count,
 // so every eligible pair is kept and the selection is exact without a threshold.
 // ------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(64) k_ivf_scan(IvfScanArgs a) {
+constexpr int kIvfThreads = 64;
+constexpr int kIvfMaxOps = 1024;   // staged ops per query (longer programs: per-word global path)
+constexpr int kIvfMaxPush = 512;
+constexpr int kIvfRing = 4;        // leaves whose plane loads are in flight ahead of the stack
+
+// The query's program, staged per CTA: ops with leaf operands renumbered in push order,
+// and the pushed leaves' plane positions (padded with -1) in the same order.
+struct IvfProg {
+  uint16_t ops[kIvfMaxOps];
+  int16_t pos[kIvfMaxPush * 8];
+  int n_ops, n_push, fast;
+};
+
+// Plane words of leaf li -> ring slot li % kIvfRing of this thread (cp.async: no register
+// holds the pending words, so later loads do not wait on earlier ones); one commit group
+// per leaf, empty groups past the last leaf keep the group count uniform.
+template <int K>
+__device__ __forceinline__ void ivf_issue(const IvfProg& P, int li, const uint64_t* __restrict__ planes,
+                                          int64_t n_words, int64_t w, uint64_t* ring) {
+  if (li < P.n_push) {
+    const int slot = li % kIvfRing;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int p = P.pos[li * 8 + j];
+      uint64_t* dst = ring + (slot * K + j) * kIvfThreads;
+      if (p >= 0) {
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d),
+                     "l"(planes + (int64_t)p * n_words + w) : "memory");
+      } else {
+        *dst = ~0ull;
+      }
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// Filter word of one query on word w: the stack machine of eval_program_word over the staged
+// program, with the plane words of the next kIvfRing leaves in flight ahead of their PUSH.
+template <int K>
+__device__ uint64_t ivf_eval_word(const IvfProg& P, const uint64_t* __restrict__ planes,
+                                  int64_t n_words, int64_t w, uint64_t v, uint64_t* ring) {
+#pragma unroll
+  for (int r = 0; r < kIvfRing; ++r) ivf_issue<K>(P, r, planes, n_words, w, ring);
+  uint64_t stk[FB_MAX_STACK];
+  int sp = 0, li = 0;
+  for (int o = 0; o < P.n_ops; ++o) {
+    const uint32_t op = P.ops[o];
+    const uint32_t code = op >> 14;
+    if (code == FB_OP_PUSH_LEAF) {
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kIvfRing - 1) : "memory");
+      const int slot = li % kIvfRing;
+      uint64_t m = ~0ull;
+#pragma unroll
+      for (int j = 0; j < K; ++j) m &= ring[(slot * K + j) * kIvfThreads];
+      ivf_issue<K>(P, li + kIvfRing, planes, n_words, w, ring);
+      ++li;
+      stk[sp++] = m;
+    } else if (code == FB_OP_NOT) {
+      stk[sp - 1] = ~stk[sp - 1] & v;
+    } else {
+      const uint64_t rhs = stk[--sp];
+      stk[sp - 1] = (code == FB_OP_AND) ? (stk[sp - 1] & rhs) : (stk[sp - 1] | rhs);
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  return stk[0];
+}
+
+template <int K>
+__global__ void __launch_bounds__(kIvfThreads) k_ivf_scan(IvfScanArgs a) {
   __shared__ __align__(16) int8_t s_q[kIvfMaxDimPad];
+  __shared__ IvfProg P;
+  __shared__ uint64_t s_ring[kIvfRing * K * kIvfThreads];
   const int dp = a.idx.dim_pad;
   const int64_t pairs = (int64_t)a.n_queries * a.nprobe;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
     const int q = (int)(pr / a.nprobe);
     const int64_t w0 = a.probe_words[2 * pr], w1 = a.probe_words[2 * pr + 1];
@@ -395,26 +468,78 @@ __global__ void __launch_bounds__(64) k_ivf_scan(IvfScanArgs a) {
     for (int i = threadIdx.x; i < dp / 16; i += blockDim.x)
       reinterpret_cast<int4*>(s_q)[i] =
           __ldg(reinterpret_cast<const int4*>(a.queries + (int64_t)q * dp) + i);
+    if (warp == 0 && a.has_prog) {
+      // stage the program: lanes read 32 ops at a time, PUSH operands renumbered by a
+      // ballot prefix, their positions copied
+      const int o0 = a.prog.op_offset[q], o1 = a.prog.op_offset[q + 1];
+      const int n_ops = o1 - o0;
+      int n_push = 0;
+      bool fast = n_ops <= kIvfMaxOps;
+      for (int b = 0; fast && b < n_ops; b += 32) {
+        const int o = b + lane;
+        const uint32_t op = o < n_ops ? a.prog.ops[o0 + o] : 0u;
+        const bool push = o < n_ops && (op >> 14) == FB_OP_PUSH_LEAF;
+        const uint32_t bal = __ballot_sync(0xffffffffu, push);
+        const int li = n_push + __popc(bal & ((1u << lane) - 1u));
+        if (li + (push ? 1 : 0) > kIvfMaxPush) fast = false;
+        if (o < n_ops && li < kIvfMaxPush) {
+          P.ops[o] = push ? (uint16_t)((FB_OP_PUSH_LEAF << 14) | (li & 0x3FFF)) : (uint16_t)op;
+          if (push) {
+            const int16_t* src = a.prog.leaf_pos + (int64_t)(op & 0x3FFF) * a.prog.k_max;
+            for (int j = 0; j < 8; ++j) P.pos[li * 8 + j] = j < a.prog.k_max && j < K ? src[j] : (int16_t)-1;
+          }
+        }
+        n_push += __popc(bal);
+        fast = __all_sync(0xffffffffu, fast);
+      }
+      if (lane == 0) {
+        P.n_ops = n_ops;
+        P.n_push = n_push;
+        P.fast = fast && a.prog.k_max <= K ? 1 : 0;
+      }
+    }
     __syncthreads();
     for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
       const uint64_t v = a.idx.valid[w];
-      uint64_t m = a.has_prog ? eval_program_word(a.prog, q, a.idx.planes, a.idx.n_words, w, v) & v
-                              : v;
+      if (v == 0) continue;
+      uint64_t m = v;
+      if (a.has_prog) {
+        if (P.n_ops == 0) {
+          m = v;  // unfiltered query inside a filtered batch
+        } else if (P.fast) {
+          m = ivf_eval_word<K>(P, a.idx.planes, a.idx.n_words, w, v, s_ring + threadIdx.x) & v;
+        } else {
+          m = eval_program_word(a.prog, q, a.idx.planes, a.idx.n_words, w, v) & v;
+        }
+      }
+      if (m == 0) continue;
       const int64_t slot0 = w * 64;
-      while (m) {
-        const int i = __ffsll((long long)m) - 1;
+      uint32_t p = atomicAdd(a.out_cnt + q, (uint32_t)__popcll(m));
+      uint64_t* ok = a.out_key + (int64_t)q * a.cap;
+      uint32_t* os = a.out_slot ? a.out_slot + (int64_t)q * a.cap : nullptr;
+      while (m) {  // two rows in flight per step
+        const int i0 = __ffsll((long long)m) - 1;
         m &= m - 1;
-        const int32_t sc = dot_i8(a.idx.items + (slot0 + i) * dp, s_q, dp);
-        const uint32_t p = atomicAdd(a.out_cnt + q, 1u);
+        const int i1 = m ? __ffsll((long long)m) - 1 : -1;
+        if (m) m &= m - 1;
+        const int32_t s0 = dot_i8(a.idx.items + (slot0 + i0) * dp, s_q, dp);
+        const int32_t s1 = i1 >= 0 ? dot_i8(a.idx.items + (slot0 + i1) * dp, s_q, dp) : 0;
         if (p < (uint32_t)a.cap) {
-          a.out_key[(int64_t)q * a.cap + p] = make_key(sc, a.idx.id_rank[slot0 + i]);
-          if (a.out_slot) a.out_slot[(int64_t)q * a.cap + p] = (uint32_t)(slot0 + i);
+          ok[p] = make_key(s0, a.idx.id_rank[slot0 + i0]);
+          if (os) os[p] = (uint32_t)(slot0 + i0);
+        }
+        ++p;
+        if (i1 >= 0) {
+          if (p < (uint32_t)a.cap) {
+            ok[p] = make_key(s1, a.idx.id_rank[slot0 + i1]);
+            if (os) os[p] = (uint32_t)(slot0 + i1);
+          }
+          ++p;
         }
       }
     }
   }
 }
-
 
 // ------------------------------------------------------------------------------------
 // Block-wide bitonic sort (descending by key) over n = power of two elements in smem.
@@ -1317,7 +1442,12 @@ int launch_ivf_scan(const IvfScanArgs& a, cudaStream_t s) {
   const int64_t pairs = (int64_t)a.n_queries * a.nprobe;
   if (pairs <= 0) return FB_OK;
   const int grid = (int)std::min<int64_t>(pairs, 148LL * 64);
-  k_ivf_scan<<<grid, 64, 0, s>>>(a);
+  const int kmax = a.has_prog ? a.prog.k_max : 1;
+  if (kmax <= 5) {
+    k_ivf_scan<5><<<grid, kIvfThreads, 0, s>>>(a);
+  } else {
+    k_ivf_scan<8><<<grid, kIvfThreads, 0, s>>>(a);
+  }
   FB_LAUNCH_CHECK("k_ivf_scan");
   return FB_OK;
 }
