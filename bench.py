@@ -204,6 +204,13 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# one 128x256x32 kind::i8 MMA per 128 cycles per SM (tools/micro/umma_rate.cu on the B200)
+# x 148 SMs x 1965 MHz; MEASURED_PEAKS.json carries no int8 figure
+MEASURED_INT8_TOPS = round(2 * 128 * 256 * 32 / 128 * 148 * 1.965e9 / 1e12, 1)
+MEASURED_INT8_SOURCE = ("measured: tools/micro/umma_rate (128-cycle 128x256x32 kind::i8 MMA per SM) "
+                        "x 148 SMs x 1965 MHz")
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -327,15 +334,23 @@ def run_ours(a):
     peak, peak_kind = measured_peaks()
     traffic = profiled_traffic()
     ops = 2.0 * B * idx.n_slots_pad * idx.dim
+    traffic_b = (traffic.get("dram_bytes_per_launch")
+                 if traffic and traffic.get("config", 2) == a.config else None)
+    tops = ops / (emit_avg / 1e3) / 1e12
     roofline = {"bound": "hbm", "kernel": "fused filter+scan emit pass",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": peak_kind,
-                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "traffic": traffic_b,
                 "algorithmic_bytes_per_launch": alg_bytes, "planes_referenced": planes_used,
                 "emit_ms": round(emit_avg, 4), "select_ms": round(float(np.mean(sel_ms)), 4),
-                "int8_tops_achieved": round(ops / (emit_avg / 1e3) / 1e12, 1),
+                "int8_tops_achieved": round(tops, 1),
                 "int8_tops_nominal": NOMINAL_INT8_TOPS}
-
+    if B >= 512:
+        # past the ridge (~690 int8 ops per HBM byte) the int8 tensor pipe binds
+        roofline.update({"bound": "tensor", "achieved": round(tops, 1), "peak": MEASURED_INT8_TOPS,
+                         "unit": "TOP/s (int8)", "frac": round(tops / MEASURED_INT8_TOPS, 4),
+                         "peak_source": MEASURED_INT8_SOURCE,
+                         "hbm_achieved_gbs": round(achieved, 1), "hbm_peak_gbs": peak})
     # ---- e2e through the public API with host buffers --------------------------------
     # N=1: the serving pipeline (engine.PipelinedTopk): each step copies its queries and
     # filter arrays in from pinned host memory and its ids / scores / counts out, with the
