@@ -241,6 +241,15 @@ class TopkOp:
                 pass
             self._plan = None
 
+    def _unfiltered_batch(self) -> FilterBatch:
+        """A batch of unfiltered queries as a zero-group CNF program (cached): same results
+        as no program, but the scan takes the per-hit CNF kernel instead of the bytecode one."""
+        if getattr(self, "_null_batch", None) is None:
+            from .bloom import BloomParams
+            params = BloomParams(self.index.m_bits, self.index.k_hashes)
+            self._null_batch = FilterBatch.pack([None] * self.n_queries, params).to_device()
+        return self._null_batch
+
     def stats(self) -> _native.FbStats:
         st = _native.FbStats()
         _native.check(_native.load_library().fb_topk_plan_stats(self._plan, ctypes.byref(st)))
@@ -263,7 +272,9 @@ class TopkOp:
             raise ValueError(f"queries_q must be int8 [{self.n_queries}, {self.index.dim_pad}]")
         if out is None:
             out = self.alloc_outputs(keys=keys, fscores=fscores)
-        prog = filters.struct() if filters is not None else None
+        if filters is None:
+            filters = self._unfiltered_batch()
+        prog = filters.struct()
         qp = self.index.qp
         _native.check(_native.lib().fb_topk_execute(
             self._plan, queries_q.data_ptr(), ctypes.byref(prog) if prog is not None else None,

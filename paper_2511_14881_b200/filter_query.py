@@ -551,6 +551,14 @@ class FilterBatch:
         cnf_kw = {}
         if reg and cnf is not None and any(cnf):
             cnf_kw = _pack_cnf(cnf, leaf_fid)
+        elif reg and not leaf_rows:
+            # no query is filtered: the CNF form with zero groups per query (one unused
+            # column) lets the tensor-core scan take its per-hit kernel, where every gated
+            # pair survives
+            cnf_kw = dict(col_leaf=np.zeros(1, dtype=np.int16),
+                          qmask=np.zeros((len(cnf), 1, 1), dtype=np.uint32),
+                          qgroups=np.zeros(len(cnf), dtype=np.int32),
+                          cnf_words=1, cnf_gmax=1, cnf_windowed=1)
         return cls(leaf_pos, np.array(offsets, dtype=np.int32),
                    np.array(ops if ops else [0], dtype=np.uint16), max_stack,
                    np.array(push_bits, dtype=np.int64),
