@@ -52,7 +52,9 @@ NOMINAL_INT8_TOPS = 4500.0
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 100 for our arm: >= ~150 ms timed, so the 20 ms "
+                         "clock sampler sees several samples; 3 for the reference arm)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, choices=[2, 3, 4, 5], default=2)
@@ -66,6 +68,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=0, help="CPU sample size (0: auto)")
     a = ap.parse_args()
+    if a.steps is None:
+        a.steps = 3 if a.impl == "reference" else 100
     items, batch, k = {2: (10_000_000, 256, 10_000), 3: (12_500_000, 1024, 20_000),
                        4: (10_000_000, 256, 10_000), 5: (10_000_000, 64, 5_000)}[a.config]
     a.items = items if a.items is None else a.items
