@@ -258,6 +258,16 @@ int fb_task_dots_f64(const float* cache, int64_t n_rows, int32_t dim, const int6
                      const int32_t* count, int64_t n_cand, const float* users, int32_t n_req,
                      int32_t n_tasks, double* out, void* stream);
 
+/* Device, multi-task union merge (retrieval.merge_candidates with merge="union",
+ * retrieval.py:147-160): keys[(b * n_tasks + t) * k + i], i < counts[b * n_tasks + t], are
+ * fb_topk_execute output keys (they carry the id rank); merged[b * n_tasks * k ..] receives
+ * the distinct ids of request b in ascending id order (padded with all-ones), mcount[b] their
+ * number. bitmap: n_requests * (ceil(n_slots / 64) + 8) u64 of scratch, zero on the first
+ * call; the bitmap part is left zeroed. id_of_rank: fb_index_t.id_of_rank. */
+int fb_merge_union(const uint64_t* keys, const int32_t* counts, int32_t n_requests,
+                   int32_t n_tasks, int32_t k, int64_t n_slots, const uint64_t* id_of_rank,
+                   uint64_t* bitmap, uint64_t* merged, int32_t* mcount, void* stream);
+
 /* Device, IVF-probed batched search (retrieval.codesigned_search with nprobe < n_clusters,
  * retrieval.py:110-144; ivf.search_clusters over the probed clusters, ivf.py:285-334): for
  * query b, probe_words[(b * nprobe + j) * 2 ..] is the 64-slot word range [w0, w1) of its

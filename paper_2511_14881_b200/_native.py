@@ -48,7 +48,7 @@ EXPORTED = (
     "fb_topk_set_timing", "fb_topk_last_timing", "fb_topk_scan_path", "fb_debug_tc_scores",
     "fb_task_dots_f64", "fb_kmeans_min_sqdist", "fb_pairwise_sum_scratch",
     "fb_pairwise_sum_f64", "fb_kmeans_draw", "fb_row_sqnorm_f64", "fb_kmeans_assign",
-    "fb_kmeans_means", "fb_ivf_topk",
+    "fb_kmeans_means", "fb_ivf_topk", "fb_merge_union",
 )
 
 
@@ -148,6 +148,7 @@ def _declare(lib) -> None:
         "fb_ivf_topk": ([ctypes.POINTER(FbIndex), c_vp, i32, ctypes.POINTER(FbFilterProg), c_vp, i32,
                          i32, i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, dbl, dbl, c_vp],
                         i32),
+        "fb_merge_union": ([c_vp, c_vp, i32, i32, i32, i64, c_vp, c_vp, c_vp, c_vp, c_vp], i32),
         "fb_launch_count": ([], ctypes.c_uint64),
         "fb_topk_scan_path": ([c_vp], i32),
         "fb_debug_tc_scores": ([ctypes.POINTER(FbIndex), c_vp, i32, c_vp, c_vp], i32),

@@ -542,6 +542,114 @@ __global__ void __launch_bounds__(kIvfThreads) k_ivf_scan(IvfScanArgs a) {
 }
 
 // ------------------------------------------------------------------------------------
+// Multi-task union merge by id rank (ref retrieval.merge_candidates, retrieval.py:147-160):
+// ranks order ids (id_rank is the rank of the slot's id among the valid ids), so the union
+// of a request's T candidate lists in ascending id order is the set bits of a per-request
+// rank bitmap read in order. k_union_mark sets the bits; k_union_extract (one CTA per
+// request) counts bits per thread-chunk, scans, writes ids in rank order and clears the
+// words it read, leaving the bitmap zeroed for the next call.
+// ------------------------------------------------------------------------------------
+__global__ void k_union_mark(const uint64_t* __restrict__ keys, const int32_t* __restrict__ counts,
+                             int B, int T, int k, int64_t n_words,
+                             unsigned long long* __restrict__ bitmap) {
+  const int64_t total = (int64_t)B * T * k;
+  for (int64_t g = grid_tid(); g < total; g += grid_stride()) {
+    const int64_t bt = g / k;
+    const int i = (int)(g - bt * k);
+    if (i >= counts[bt]) continue;
+    const uint32_t rank = 0xFFFFFFFFu - (uint32_t)keys[g];
+    const int64_t b = bt / T;
+    atomicOr(bitmap + b * n_words + (rank >> 6), 1ull << (rank & 63));
+  }
+}
+
+// Extraction: each request's words split into kUnionSegs segments of one CTA each; pass 1
+// counts set bits per segment, pass 2 places each segment at the prefix of the earlier ones
+// and, inside it, each warp at the prefix of the earlier warps; a warp walks its words 32 at
+// a time (coalesced), lanes placed by a shuffle scan of their popcounts.
+constexpr int kUnionThreads = 256, kUnionSegs = 16;
+
+__device__ __forceinline__ void union_span(int64_t n_words, int seg, int warp, int64_t& w0,
+                                           int64_t& w1) {
+  const int nw = kUnionThreads / 32;
+  const int64_t per_seg = (n_words + kUnionSegs - 1) / kUnionSegs;
+  const int64_t s0 = min(n_words, per_seg * seg), s1 = min(n_words, s0 + per_seg);
+  const int64_t per_warp = ((s1 - s0 + nw - 1) / nw + 31) / 32 * 32;
+  w0 = min(s1, s0 + per_warp * warp);
+  w1 = min(s1, w0 + per_warp);
+}
+
+__device__ __forceinline__ uint32_t union_warp_count(const unsigned long long* bm, int64_t w0,
+                                                     int64_t w1, int lane) {
+  uint32_t c = 0;
+  for (int64_t w = w0 + lane; w < w1; w += 32) c += (uint32_t)__popcll(bm[w]);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+  return c;
+}
+
+__global__ void __launch_bounds__(kUnionThreads) k_union_count(
+    const unsigned long long* __restrict__ bitmap, int64_t n_words, uint32_t* __restrict__ seg_cnt) {
+  __shared__ uint32_t s_c[kUnionThreads / 32];
+  const int b = blockIdx.y, seg = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t w0, w1;
+  union_span(n_words, seg, wid, w0, w1);
+  const uint32_t c = union_warp_count(bitmap + (int64_t)b * n_words, w0, w1, lane);
+  if (lane == 0) s_c[wid] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int i = 0; i < kUnionThreads / 32; ++i) t += s_c[i];
+    seg_cnt[b * kUnionSegs + seg] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kUnionThreads) k_union_extract(
+    unsigned long long* __restrict__ bitmap, int64_t n_words, const uint32_t* __restrict__ seg_cnt,
+    const uint64_t* __restrict__ id_of_rank, int out_len, uint64_t* __restrict__ merged,
+    int32_t* __restrict__ mcount) {
+  __shared__ uint32_t s_c[kUnionThreads / 32];
+  const int b = blockIdx.y, seg = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long* bm = bitmap + (int64_t)b * n_words;
+  int64_t w0, w1;
+  union_span(n_words, seg, wid, w0, w1);
+  const uint32_t c = union_warp_count(bm, w0, w1, lane);
+  if (lane == 0) s_c[wid] = c;
+  __syncthreads();
+  uint32_t pos = 0;
+  for (int i = 0; i < seg; ++i) pos += seg_cnt[b * kUnionSegs + i];
+  for (int i = 0; i < wid; ++i) pos += s_c[i];
+  if (seg == kUnionSegs - 1 && threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int i = 0; i < kUnionSegs; ++i) tot += seg_cnt[b * kUnionSegs + i];
+    mcount[b] = (int32_t)min(tot, (uint32_t)out_len);
+  }
+  uint64_t* out = merged + (int64_t)b * out_len;
+  for (int64_t base = w0; base < w1; base += 32) {
+    const int64_t w = base + lane;
+    unsigned long long m = w < w1 ? bm[w] : 0ull;
+    const uint32_t pc = (uint32_t)__popcll(m);
+    uint32_t incl = pc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    uint32_t p = pos + incl - pc;
+    if (m != 0ull) {
+      bm[w] = 0ull;
+      while (m) {
+        const int i = __ffsll((long long)m) - 1;
+        m &= m - 1;
+        if (p < (uint32_t)out_len) out[p] = id_of_rank[w * 64 + i];
+        ++p;
+      }
+    }
+    pos += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // Block-wide bitonic sort (descending by key) over n = power of two elements in smem.
 // ------------------------------------------------------------------------------------
 template <bool kHasVal>
@@ -1449,6 +1557,30 @@ int launch_ivf_scan(const IvfScanArgs& a, cudaStream_t s) {
     k_ivf_scan<8><<<grid, kIvfThreads, 0, s>>>(a);
   }
   FB_LAUNCH_CHECK("k_ivf_scan");
+  return FB_OK;
+}
+
+int launch_union_merge(const uint64_t* keys, const int32_t* counts, int B, int T, int k,
+                       int64_t n_words, uint64_t* bitmap, const uint64_t* id_of_rank,
+                       uint64_t* merged, int32_t* mcount, cudaStream_t s) {
+  if (B <= 0) return FB_OK;
+  if (B > 65535) return fail(FB_ERR_INVALID, "too many requests");
+  const int out_len = T * k;
+  FB_CUDA(cudaMemsetAsync(merged, 0xFF, sizeof(uint64_t) * (size_t)B * out_len, s));
+  const int64_t total = (int64_t)B * T * k;
+  auto* bm = reinterpret_cast<unsigned long long*>(bitmap);
+  if (total > 0) {
+    k_union_mark<<<grid_for(total, 256), 256, 0, s>>>(keys, counts, B, T, k, n_words, bm);
+    FB_LAUNCH_CHECK("k_union_mark");
+  }
+  // per-segment counts: the caller's scratch past the bitmaps (B * kUnionSegs u32)
+  uint32_t* seg_cnt = reinterpret_cast<uint32_t*>(bitmap + (size_t)B * n_words);
+  const dim3 grid(kUnionSegs, B);
+  k_union_count<<<grid, kUnionThreads, 0, s>>>(bm, n_words, seg_cnt);
+  FB_LAUNCH_CHECK("k_union_count");
+  k_union_extract<<<grid, kUnionThreads, 0, s>>>(bm, n_words, seg_cnt, id_of_rank, out_len, merged,
+                                                 mcount);
+  FB_LAUNCH_CHECK("k_union_extract");
   return FB_OK;
 }
 

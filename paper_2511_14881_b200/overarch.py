@@ -325,6 +325,22 @@ class MultiTaskOp:
             ranges = np.array([[0, index.n_slots]], dtype=np.int64)
         self.op = TopkOp(index, self.B * self.T, self.k0, ranges, flags)
 
+    def _merge_union(self, res):
+        """Union merge through the id-rank bitmap (``fb_merge_union``): same output as
+        ``merge_device(..., "union")``."""
+        B, T, k = self.B, self.T, self.k0
+        dev = res.keys.device
+        if getattr(self, "_bitmap", None) is None:
+            # B rank bitmaps, then 8 u64 of per-request segment counters
+            self._bitmap = torch.zeros(B * (self.index.n_words + 8), dtype=torch.int64, device=dev)
+        merged = torch.empty((B, T * k), dtype=torch.int64, device=dev)
+        mcount = torch.empty(B, dtype=torch.int32, device=dev)
+        _native.check(_native.lib().fb_merge_union(
+            res.keys.data_ptr(), res.count.data_ptr(), B, T, k, self.index.n_slots_pad,
+            self.index.id_of_rank.data_ptr(), self._bitmap.data_ptr(), merged.data_ptr(),
+            mcount.data_ptr(), _native.stream_ptr()))
+        return merged, mcount
+
     def pack_filters(self, filters, params: BloomParams | None = None) -> FilterBatch | None:
         """One compiled filter per request, repeated for each of its tasks."""
         if filters is None or all(f is None for f in filters):
@@ -341,9 +357,13 @@ class MultiTaskOp:
         if queries_q is None:
             queries_q = quantize_device(users.reshape(B * T, -1), self.index.qp,
                                         out_stride=self.index.dim_pad)
-        res = self.op(queries_q, batch)
-        merged, mcount = merge_device(res.ids.view(B, T, self.k0),
-                                      res.count.view(B, T), self.merge)
+        if self.merge == MERGE_UNION and self.index.id_of_rank is not None:
+            res = self.op(queries_q, batch, keys=True)
+            merged, mcount = self._merge_union(res)
+        else:
+            res = self.op(queries_q, batch)
+            merged, mcount = merge_device(res.ids.view(B, T, self.k0),
+                                          res.count.view(B, T), self.merge)
         C = merged.shape[1]
         valid = torch.arange(C, device=merged.device)[None, :] < mcount[:, None]
         rows = self.cache.rows_for(merged, valid)

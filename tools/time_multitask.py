@@ -37,9 +37,9 @@ def main():
         e = [ev() for _ in range(7)]
         e[0].record()
         qq = idx.quantize_queries(users.reshape(R * T, -1))
-        res = op.op(qq, batch)
+        res = op.op(qq, batch, keys=True)
         e[1].record()
-        merged, mcount = merge_device(res.ids.view(R, T, a.k), res.count.view(R, T), "union")
+        merged, mcount = op._merge_union(res)
         e[2].record()
         C = merged.shape[1]
         valid = torch.arange(C, device=merged.device)[None, :] < mcount[:, None]
