@@ -263,10 +263,12 @@ int fb_task_dots_f64(const float* cache, int64_t n_rows, int32_t dim, const int6
  * fb_topk_execute output keys (they carry the id rank); merged[b * n_tasks * k ..] receives
  * the distinct ids of request b in ascending id order (padded with all-ones), mcount[b] their
  * number. bitmap: n_requests * (ceil(n_slots / 64) + 8) u64 of scratch, zero on the first
- * call; the bitmap part is left zeroed. id_of_rank: fb_index_t.id_of_rank. */
+ * call; the bitmap part is left zeroed. id_of_rank: fb_index_t.id_of_rank. merged_ranks
+ * (nullable, same shape as merged, -1 padded) receives the id ranks. */
 int fb_merge_union(const uint64_t* keys, const int32_t* counts, int32_t n_requests,
                    int32_t n_tasks, int32_t k, int64_t n_slots, const uint64_t* id_of_rank,
-                   uint64_t* bitmap, uint64_t* merged, int32_t* mcount, void* stream);
+                   uint64_t* bitmap, uint64_t* merged, int64_t* merged_ranks, int32_t* mcount,
+                   void* stream);
 
 /* Device, IVF-probed batched search (retrieval.codesigned_search with nprobe < n_clusters,
  * retrieval.py:110-144; ivf.search_clusters over the probed clusters, ivf.py:285-334): for

@@ -148,7 +148,8 @@ def _declare(lib) -> None:
         "fb_ivf_topk": ([ctypes.POINTER(FbIndex), c_vp, i32, ctypes.POINTER(FbFilterProg), c_vp, i32,
                          i32, i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, dbl, dbl, c_vp],
                         i32),
-        "fb_merge_union": ([c_vp, c_vp, i32, i32, i32, i64, c_vp, c_vp, c_vp, c_vp, c_vp], i32),
+        "fb_merge_union": ([c_vp, c_vp, i32, i32, i32, i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
+                           i32),
         "fb_launch_count": ([], ctypes.c_uint64),
         "fb_topk_scan_path": ([c_vp], i32),
         "fb_debug_tc_scores": ([ctypes.POINTER(FbIndex), c_vp, i32, c_vp, c_vp], i32),

@@ -534,12 +534,14 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
 
 int fb_merge_union(const uint64_t* keys, const int32_t* counts, int32_t n_requests,
                    int32_t n_tasks, int32_t k, int64_t n_slots, const uint64_t* id_of_rank,
-                   uint64_t* bitmap, uint64_t* merged, int32_t* mcount, void* stream) {
+                   uint64_t* bitmap, uint64_t* merged, int64_t* merged_ranks, int32_t* mcount,
+                   void* stream) {
   if (n_requests < 0 || n_tasks < 0 || k < 0 || n_slots < 0) return fail(FB_ERR_INVALID, "negative size");
   if (id_of_rank == nullptr) return fail(FB_ERR_INVALID, "id_of_rank is required");
   if ((int64_t)n_tasks * k > 0x7fffffffLL) return fail(FB_ERR_INVALID, "merged width overflows");
   return launch_union_merge(keys, counts, n_requests, n_tasks, k, (n_slots + 63) / 64, bitmap,
-                            id_of_rank, merged, mcount, static_cast<cudaStream_t>(stream));
+                            id_of_rank, merged, merged_ranks, mcount,
+                            static_cast<cudaStream_t>(stream));
 }
 
 int fb_ivf_topk(const fb_index_t* idx, const int8_t* queries_q, int32_t n_queries,

@@ -152,7 +152,7 @@ struct IvfScanArgs {
 int launch_ivf_scan(const IvfScanArgs& a, cudaStream_t s);
 int launch_union_merge(const uint64_t* keys, const int32_t* counts, int B, int T, int k,
                        int64_t n_words, uint64_t* bitmap, const uint64_t* id_of_rank,
-                       uint64_t* merged, int32_t* mcount, cudaStream_t s);
+                       uint64_t* merged, int64_t* merged_ranks, int32_t* mcount, cudaStream_t s);
 
 // kernels / launchers implemented in fb_kernels.cu
 int launch_scan_simt(const ScanArgs& a, cudaStream_t s);

@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(kUnionThreads) k_union_count(
 __global__ void __launch_bounds__(kUnionThreads) k_union_extract(
     unsigned long long* __restrict__ bitmap, int64_t n_words, const uint32_t* __restrict__ seg_cnt,
     const uint64_t* __restrict__ id_of_rank, int out_len, uint64_t* __restrict__ merged,
-    int32_t* __restrict__ mcount) {
+    int64_t* __restrict__ merged_ranks, int32_t* __restrict__ mcount) {
   __shared__ uint32_t s_c[kUnionThreads / 32];
   const int b = blockIdx.y, seg = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned long long* bm = bitmap + (int64_t)b * n_words;
@@ -641,7 +641,10 @@ __global__ void __launch_bounds__(kUnionThreads) k_union_extract(
       while (m) {
         const int i = __ffsll((long long)m) - 1;
         m &= m - 1;
-        if (p < (uint32_t)out_len) out[p] = id_of_rank[w * 64 + i];
+        if (p < (uint32_t)out_len) {
+          out[p] = id_of_rank[w * 64 + i];
+          if (merged_ranks) merged_ranks[(int64_t)b * out_len + p] = w * 64 + i;
+        }
         ++p;
       }
     }
@@ -1562,11 +1565,13 @@ int launch_ivf_scan(const IvfScanArgs& a, cudaStream_t s) {
 
 int launch_union_merge(const uint64_t* keys, const int32_t* counts, int B, int T, int k,
                        int64_t n_words, uint64_t* bitmap, const uint64_t* id_of_rank,
-                       uint64_t* merged, int32_t* mcount, cudaStream_t s) {
+                       uint64_t* merged, int64_t* merged_ranks, int32_t* mcount, cudaStream_t s) {
   if (B <= 0) return FB_OK;
   if (B > 65535) return fail(FB_ERR_INVALID, "too many requests");
   const int out_len = T * k;
   FB_CUDA(cudaMemsetAsync(merged, 0xFF, sizeof(uint64_t) * (size_t)B * out_len, s));
+  if (merged_ranks)
+    FB_CUDA(cudaMemsetAsync(merged_ranks, 0xFF, sizeof(int64_t) * (size_t)B * out_len, s));
   const int64_t total = (int64_t)B * T * k;
   auto* bm = reinterpret_cast<unsigned long long*>(bitmap);
   if (total > 0) {
@@ -1579,7 +1584,7 @@ int launch_union_merge(const uint64_t* keys, const int32_t* counts, int B, int T
   k_union_count<<<grid, kUnionThreads, 0, s>>>(bm, n_words, seg_cnt);
   FB_LAUNCH_CHECK("k_union_count");
   k_union_extract<<<grid, kUnionThreads, 0, s>>>(bm, n_words, seg_cnt, id_of_rank, out_len, merged,
-                                                 mcount);
+                                                 merged_ranks, mcount);
   FB_LAUNCH_CHECK("k_union_extract");
   return FB_OK;
 }

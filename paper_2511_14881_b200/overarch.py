@@ -327,19 +327,35 @@ class MultiTaskOp:
 
     def _merge_union(self, res):
         """Union merge through the id-rank bitmap (``fb_merge_union``): same output as
-        ``merge_device(..., "union")``."""
+        ``merge_device(..., "union")``, plus the merged ids' ranks."""
         B, T, k = self.B, self.T, self.k0
         dev = res.keys.device
         if getattr(self, "_bitmap", None) is None:
             # B rank bitmaps, then 8 u64 of per-request segment counters
             self._bitmap = torch.zeros(B * (self.index.n_words + 8), dtype=torch.int64, device=dev)
         merged = torch.empty((B, T * k), dtype=torch.int64, device=dev)
+        ranks = torch.empty((B, T * k), dtype=torch.int64, device=dev)
         mcount = torch.empty(B, dtype=torch.int32, device=dev)
         _native.check(_native.lib().fb_merge_union(
             res.keys.data_ptr(), res.count.data_ptr(), B, T, k, self.index.n_slots_pad,
             self.index.id_of_rank.data_ptr(), self._bitmap.data_ptr(), merged.data_ptr(),
-            mcount.data_ptr(), _native.stream_ptr()))
-        return merged, mcount
+            ranks.data_ptr(), mcount.data_ptr(), _native.stream_ptr()))
+        return merged, ranks, mcount
+
+    def _rows_of_ranks(self, merged, ranks, valid):
+        """Cache rows through a rank -> cache-row table built once per operator (-1 where
+        the cache lacks the id); raises ``MissingItem`` like ``DeviceCache.rows_for``."""
+        if getattr(self, "_row_of_rank", None) is None:
+            key = _u64_order_key(self.index.id_of_rank)
+            sk = self.cache._sorted_key
+            pos = torch.searchsorted(sk, key).clamp_(max=sk.numel() - 1)
+            self._row_of_rank = torch.where(sk[pos] == key, self.cache._row[pos],
+                                            torch.full_like(pos, -1))
+        rows = self._row_of_rank[ranks.clamp(min=0)]
+        bad = valid & (rows < 0)
+        if bool(bad.any()):
+            raise MissingItem(int(merged[bad][0].item()) & 0xFFFFFFFFFFFFFFFF)
+        return torch.where(valid, rows, torch.full_like(rows, -1))
 
     def pack_filters(self, filters, params: BloomParams | None = None) -> FilterBatch | None:
         """One compiled filter per request, repeated for each of its tasks."""
@@ -359,14 +375,15 @@ class MultiTaskOp:
                                         out_stride=self.index.dim_pad)
         if self.merge == MERGE_UNION and self.index.id_of_rank is not None:
             res = self.op(queries_q, batch, keys=True)
-            merged, mcount = self._merge_union(res)
+            merged, ranks, mcount = self._merge_union(res)
+            valid = torch.arange(merged.shape[1], device=merged.device)[None, :] < mcount[:, None]
+            rows = self._rows_of_ranks(merged, ranks, valid)
         else:
             res = self.op(queries_q, batch)
             merged, mcount = merge_device(res.ids.view(B, T, self.k0),
                                           res.count.view(B, T), self.merge)
-        C = merged.shape[1]
-        valid = torch.arange(C, device=merged.device)[None, :] < mcount[:, None]
-        rows = self.cache.rows_for(merged, valid)
+            valid = torch.arange(merged.shape[1], device=merged.device)[None, :] < mcount[:, None]
+            rows = self.cache.rows_for(merged, valid)
         ts = self.scorer.score(self.cache, rows, mcount, users, self.tasks)    # [B, T, C]
         final = value_model_device(self.spec, {t: ts[:, j, :] for j, t in enumerate(self.tasks)},
                                    valid)

@@ -143,3 +143,24 @@ def test_multitask_batched_vs_oracle(cuda):
         assert np.array_equal(ids, want[0]), b
         assert np.array_equal(scores, want[1]), b
         assert np.array_equal(ts, want[2]), b
+
+
+def test_multitask_missing_cache_item_raises(cuda):
+    """A merged candidate absent from the embedding cache raises MissingItem (reference
+    EmbeddingCache.batch, scoring.py:45-52), on the rank-table path."""
+    import paper_2511_14881_b200 as fb
+    from paper_2511_14881_b200 import _device, workload
+    from paper_2511_14881_b200.errors import MissingItem
+    B, T = 2, 4
+    wl = workload.make_workload(20_000, B * T, dim=128, seed=43, filtered=False)
+    idx = wl.index
+    ids = _device.u64_host(idx.item_ids)[: idx.n_slots]
+    vecs = np.random.default_rng(1).standard_normal((idx.n_slots, 128)).astype(np.float32)
+    op = fb.MultiTaskOp(idx, fb.DeviceCache(ids, vecs), B, TASKS, 50, 10)
+    out = op(wl.queries.view(B, T, -1), None)
+    torch.cuda.synchronize()
+    victim = out.host(0)[0][0]
+    keep = ids != victim
+    op2 = fb.MultiTaskOp(idx, fb.DeviceCache(ids[keep], vecs[keep]), B, TASKS, 50, 10)
+    with pytest.raises(MissingItem):
+        op2(wl.queries.view(B, T, -1), None)

@@ -39,11 +39,11 @@ def main():
         qq = idx.quantize_queries(users.reshape(R * T, -1))
         res = op.op(qq, batch, keys=True)
         e[1].record()
-        merged, mcount = op._merge_union(res)
+        merged, ranks, mcount = op._merge_union(res)
         e[2].record()
         C = merged.shape[1]
         valid = torch.arange(C, device=merged.device)[None, :] < mcount[:, None]
-        rows = cache.rows_for(merged, valid)
+        rows = op._rows_of_ranks(merged, ranks, valid)
         e[3].record()
         ts = op.scorer.score(cache, rows, mcount, users, tasks)
         e[4].record()
