@@ -416,7 +416,7 @@ def test_pipelined_topk_matches_batched_op(fb, wl_small):
 
 @pytest.mark.parametrize("path", ["probe", "masked"])
 @pytest.mark.parametrize("case,nprobe,filtered", [(0, 3, True), (3, 7, True), (2, 1, False),
-                                                (1, 5, True)])
+                                                (1, 5, True), (3, 30, True), (0, 20, False)])
 def test_ivf_batched_probe_vs_oracle(fb, case, nprobe, filtered, path):
     """Batched IVF-probed co-designed search (IvfSearchOp): per-query centroid probe on the
     GPU (numpy-order float64 dots, ties by cluster id) + per-query probe masks + one
