@@ -1216,16 +1216,31 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
     dst[atomicAdd(s_bcnt + (int)(c >> bshift), 1u)] = c;
   }
   __syncthreads();
-  for (int i = t; i < kk; i += kRsThreads) {
-    const uint64_t c = dst_smem ? dst[i] : __ldcg(dst + i);
-    const int b = (int)(c >> bshift);
-    const uint32_t lo_b = s_bstart[b], hi_b = s_bcnt[b];
-    uint32_t r = lo_b;
-    if (dst_smem)
+  if (dst_smem) {
+    for (int i = t; i < kk; i += kRsThreads) {
+      const uint64_t c = dst[i];
+      const int b = (int)(c >> bshift);
+      const uint32_t lo_b = s_bstart[b], hi_b = s_bcnt[b];
+      uint32_t r = lo_b;
       for (uint32_t j = lo_b; j < hi_b; ++j) r += dst[j] < c ? 1u : 0u;
-    else
-      for (uint32_t j = lo_b; j < hi_b; ++j) r += __ldcg(dst + j) < c ? 1u : 0u;
-    src[r] = c;
+      src[r] = c;
+    }
+  } else {
+    // the bin-ordered keys come back into shared memory (src is dead after the scatter),
+    // the in-bin ranks are counted there and the sorted keys go out to the global buffer
+    // and back -- two coalesced copies instead of O(bin size) L2 reads per key
+    for (int i = t; i < kk; i += kRsThreads) src[i] = __ldcg(dst + i);
+    __syncthreads();
+    for (int i = t; i < kk; i += kRsThreads) {
+      const uint64_t c = src[i];
+      const int b = (int)(c >> bshift);
+      const uint32_t lo_b = s_bstart[b], hi_b = s_bcnt[b];
+      uint32_t r = lo_b;
+      for (uint32_t j = lo_b; j < hi_b; ++j) r += src[j] < c ? 1u : 0u;
+      dst[r] = c;
+    }
+    __syncthreads();
+    for (int i = t; i < kk; i += kRsThreads) src[i] = __ldcg(dst + i);
   }
   __syncthreads();
 
