@@ -143,12 +143,13 @@ class IvfSearchOp:
     grouped scan ``fb_ivf_topk``: one CTA per (query, probed cluster) evaluates the query's
     filter on that cluster's words only and scores its eligible slots -- work proportional
     to nprobe, not to the index -- followed by the exact top-k selection. ``path="masked"``
-    runs the exhaustive tensor-core scan with per-query probe masks instead (same results).
+    runs the exhaustive tensor-core scan with per-query probe masks instead (same results);
+    ``"auto"`` (default) takes the grouped scan unless its candidate buffer would pass 8 GB.
     """
 
     def __init__(self, index, n_queries: int, nprobe: int, k0: int, flags: int = 0,
-                 path: str = "probe"):
-        if path not in ("probe", "masked"):
+                 path: str = "auto"):
+        if path not in ("probe", "masked", "auto"):
             raise ValueError(f"unknown path {path!r}")
         self.dix = device_index_for(index)
         if self.dix.centroids is None and self.dix.cluster_offsets.shape[0] != 1:
@@ -157,21 +158,25 @@ class IvfSearchOp:
         self.C = int(self.dix.cluster_offsets.shape[0])
         self.nprobe = min(max(int(nprobe), 1), self.C)
         self.k0 = int(k0)
-        self.path = path
         dev = device()
         offs = torch.as_tensor(self.dix.cluster_offsets, dtype=torch.int64, device=dev)
         self._w0 = offs[:, 0] >> 6
         self._w1 = (offs[:, 1] + 63) >> 6
         self._rows = torch.arange(self.C, dtype=torch.int64, device=dev).repeat(self.B, 1)
         self._cnt = torch.full((self.B,), self.C, dtype=torch.int32, device=dev)
-        if path == "masked":
-            self.op = TopkOp(self.dix, self.B, self.k0,
-                             np.array([[0, self.dix.n_slots]], dtype=np.int64), flags)
-            return
         # the most slots one query can probe: its nprobe largest clusters
         sizes = np.sort(np.asarray(self.dix.cluster_offsets[:, 1] - self.dix.cluster_offsets[:, 0],
                                    dtype=np.int64))[::-1]
         self.cap = int(max(1, sizes[: self.nprobe].sum()))
+        if path == "auto":
+            # the grouped scan keeps every probed eligible pair: past ~8 GB of candidate
+            # keys (nprobe close to the cluster count) the exhaustive masked scan is used
+            path = "probe" if self.B * self.cap * 8 <= (8 << 30) else "masked"
+        self.path = path
+        if path == "masked":
+            self.op = TopkOp(self.dix, self.B, self.k0,
+                             np.array([[0, self.dix.n_slots]], dtype=np.int64), flags)
+            return
         if self.cap >= 1 << 31:
             raise ValueError("probed slot count exceeds the 32-bit candidate buffer")
         need_slot = self.dix.slot_of_rank is None or self.k0 > 24576
