@@ -162,8 +162,6 @@ class IvfSearchOp:
         offs = torch.as_tensor(self.dix.cluster_offsets, dtype=torch.int64, device=dev)
         self._w0 = offs[:, 0] >> 6
         self._w1 = (offs[:, 1] + 63) >> 6
-        self._rows = torch.arange(self.C, dtype=torch.int64, device=dev).repeat(self.B, 1)
-        self._cnt = torch.full((self.B,), self.C, dtype=torch.int32, device=dev)
         # the most slots one query can probe: its nprobe largest clusters
         sizes = np.sort(np.asarray(self.dix.cluster_offsets[:, 1] - self.dix.cluster_offsets[:, 0],
                                    dtype=np.int64))[::-1]
@@ -190,13 +188,22 @@ class IvfSearchOp:
         """int64 [B, nprobe] probed cluster ids per query."""
         if self.dix.centroids is None:
             return torch.zeros((self.B, 1), dtype=torch.int64, device=queries.device)
-        dots = torch.empty((self.B, 1, self.C), dtype=torch.float64, device=queries.device)
-        u = queries.to(torch.float32).contiguous()
+        # the batch as groups of 32 "tasks" over one shared row list (every centroid), so a
+        # CTA's staged centroid rows serve 32 queries (fb_task_dots_f64, numpy pairwise order)
+        G = 32
+        ng = (self.B + G - 1) // G
+        u = torch.zeros((ng * G, self.dix.dim), dtype=torch.float32, device=queries.device)
+        u[: self.B] = queries.to(torch.float32)
+        if getattr(self, "_probe_rows", None) is None:
+            self._probe_rows = torch.arange(self.C, dtype=torch.int64,
+                                            device=queries.device).repeat(ng, 1)
+            self._probe_cnt = torch.full((ng,), self.C, dtype=torch.int32, device=queries.device)
+        dots = torch.empty((ng * G, self.C), dtype=torch.float64, device=queries.device)
         _native.check(_native.lib().fb_task_dots_f64(
-            self.dix.centroids.data_ptr(), self.C, self.dix.dim, self._rows.data_ptr(),
-            self._cnt.data_ptr(), self.C, u.data_ptr(), self.B, 1, dots.data_ptr(),
+            self.dix.centroids.data_ptr(), self.C, self.dix.dim, self._probe_rows.data_ptr(),
+            self._probe_cnt.data_ptr(), self.C, u.data_ptr(), ng, G, dots.data_ptr(),
             _native.stream_ptr()))
-        order = torch.sort(dots[:, 0, :], dim=1, descending=True, stable=True).indices
+        order = torch.sort(dots[: self.B], dim=1, descending=True, stable=True).indices
         return order[:, : self.nprobe]
 
     def masks(self, clusters: torch.Tensor) -> torch.Tensor:
