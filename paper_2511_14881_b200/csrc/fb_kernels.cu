@@ -428,8 +428,10 @@ __device__ uint64_t ivf_eval_word(const IvfProg& P, const uint64_t* __restrict__
                                   int64_t n_words, int64_t w, uint64_t v, uint64_t* ring) {
 #pragma unroll
   for (int r = 0; r < kIvfRing; ++r) ivf_issue<K>(P, r, planes, n_words, w, ring);
-  uint64_t stk[FB_MAX_STACK];
-  int sp = 0, li = 0;
+  // stack of depth <= 4 in registers: top cached, the rest shifted on push / pop (no
+  // dynamic indexing, so nothing goes to local memory)
+  uint64_t top = 0ull, s1 = 0ull, s2 = 0ull, s3 = 0ull;
+  int li = 0;
   for (int o = 0; o < P.n_ops; ++o) {
     const uint32_t op = P.ops[o];
     const uint32_t code = op >> 14;
@@ -441,16 +443,20 @@ __device__ uint64_t ivf_eval_word(const IvfProg& P, const uint64_t* __restrict__
       for (int j = 0; j < K; ++j) m &= ring[(slot * K + j) * kIvfThreads];
       ivf_issue<K>(P, li + kIvfRing, planes, n_words, w, ring);
       ++li;
-      stk[sp++] = m;
+      s3 = s2;
+      s2 = s1;
+      s1 = top;
+      top = m;
     } else if (code == FB_OP_NOT) {
-      stk[sp - 1] = ~stk[sp - 1] & v;
+      top = ~top & v;
     } else {
-      const uint64_t rhs = stk[--sp];
-      stk[sp - 1] = (code == FB_OP_AND) ? (stk[sp - 1] & rhs) : (stk[sp - 1] | rhs);
+      top = (code == FB_OP_AND) ? (s1 & top) : (s1 | top);
+      s1 = s2;
+      s2 = s3;
     }
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
-  return stk[0];
+  return top;
 }
 
 template <int K>
@@ -495,7 +501,7 @@ __global__ void __launch_bounds__(kIvfThreads) k_ivf_scan(IvfScanArgs a) {
       if (lane == 0) {
         P.n_ops = n_ops;
         P.n_push = n_push;
-        P.fast = fast && a.prog.k_max <= K ? 1 : 0;
+        P.fast = fast && a.prog.k_max <= K && a.prog.max_stack <= 4 ? 1 : 0;
       }
     }
     __syncthreads();
