@@ -99,6 +99,82 @@ __global__ void k_filter_eval(fb_index_t idx, fb_filter_prog_t prog, int64_t w0,
   }
 }
 
+// Batched evaluation with the batch's leaves shared: a CTA takes kFeWords consecutive words;
+// phase 1 evaluates every distinct leaf of the batch (leaves are de-duplicated across
+// queries) once per word into shared memory, phase 2 runs each query's program over those
+// leaf words (thread = (query, word), a warp = one query's 32 words: coalesced output,
+// uniform program walk). Stack of depth <= 4 in registers.
+constexpr int kFeWords = 32;
+__device__ __forceinline__ uint64_t eval_ops_leafwords(const fb_filter_prog_t& prog, int q,
+                                                       const uint64_t* s_leaf, int j, uint64_t v) {
+  const int32_t o0 = prog.op_offset[q], o1 = prog.op_offset[q + 1];
+  if (o0 == o1) return v;  // unfiltered query
+  if (prog.max_stack <= 4) {
+    uint64_t top = 0ull, s1 = 0ull, s2 = 0ull, s3 = 0ull;
+    for (int o = o0; o < o1; ++o) {
+      const uint32_t op = prog.ops[o];
+      const uint32_t code = op >> 14;
+      if (code == FB_OP_PUSH_LEAF) {
+        s3 = s2;
+        s2 = s1;
+        s1 = top;
+        top = s_leaf[(op & 0x3FFF) * kFeWords + j];
+      } else if (code == FB_OP_NOT) {
+        top = ~top & v;
+      } else {
+        top = (code == FB_OP_AND) ? (s1 & top) : (s1 | top);
+        s1 = s2;
+        s2 = s3;
+      }
+    }
+    return top;
+  }
+  uint64_t stk[FB_MAX_STACK];
+  int sp = 0;
+  for (int o = o0; o < o1; ++o) {
+    const uint32_t op = prog.ops[o];
+    const uint32_t code = op >> 14;
+    if (code == FB_OP_PUSH_LEAF) {
+      stk[sp++] = s_leaf[(op & 0x3FFF) * kFeWords + j];
+    } else if (code == FB_OP_NOT) {
+      stk[sp - 1] = ~stk[sp - 1] & v;
+    } else {
+      const uint64_t rhs = stk[--sp];
+      stk[sp - 1] = (code == FB_OP_AND) ? (stk[sp - 1] & rhs) : (stk[sp - 1] | rhs);
+    }
+  }
+  return stk[0];
+}
+
+__global__ void __launch_bounds__(256) k_filter_eval_shared(fb_index_t idx, fb_filter_prog_t prog,
+                                                            int64_t w0, int64_t w1, int apply_valid,
+                                                            uint64_t* __restrict__ out) {
+  extern __shared__ uint64_t s_leaf[];  // [n_leaves][kFeWords]
+  const int64_t width = w1 - w0;
+  const int nl = prog.n_leaves;
+  for (int64_t c0 = w0 + (int64_t)blockIdx.x * kFeWords; c0 < w1;
+       c0 += (int64_t)gridDim.x * kFeWords) {
+    const int nw = (int)min((int64_t)kFeWords, w1 - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nl * kFeWords; e += blockDim.x) {
+      const int leaf = e / kFeWords, j = e - leaf * kFeWords;
+      s_leaf[e] = j < nw ? leaf_word(prog.leaf_pos + (int64_t)leaf * prog.k_max, prog.k_max,
+                                     idx.planes, idx.n_words, c0 + j)
+                         : 0ull;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < prog.n_queries * kFeWords; e += blockDim.x) {
+      const int q = e / kFeWords, j = e - q * kFeWords;
+      if (j >= nw) continue;
+      const int64_t w = c0 + j;
+      const uint64_t v = idx.valid[w];
+      uint64_t m = eval_ops_leafwords(prog, q, s_leaf, j, v);
+      if (apply_valid) m &= v;
+      out[(int64_t)q * width + (w - w0)] = m;
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------
 // Quantisation: float64 (x - min) * scale, rint (half to even), -128, clip.
 // ------------------------------------------------------------------------------------
@@ -1399,6 +1475,17 @@ int launch_filter_eval(const fb_index_t& idx, const fb_filter_prog_t& prog, int6
                        int apply_valid, uint64_t* out, cudaStream_t s) {
   const int64_t total = (w1 - w0) * prog.n_queries;
   if (total <= 0) return FB_OK;
+  const size_t smem = (size_t)prog.n_leaves * kFeWords * sizeof(uint64_t);
+  if (prog.n_leaves > 0 && smem <= 96 * 1024) {
+    if (smem > 48 * 1024)
+      FB_CUDA(cudaFuncSetAttribute(k_filter_eval_shared, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    const int64_t chunks = (w1 - w0 + kFeWords - 1) / kFeWords;
+    const int grid = (int)std::min<int64_t>(chunks, 148LL * 16);
+    k_filter_eval_shared<<<grid, 256, smem, s>>>(idx, prog, w0, w1, apply_valid, out);
+    FB_LAUNCH_CHECK("k_filter_eval_shared");
+    return FB_OK;
+  }
   k_filter_eval<<<grid_for(total, 256), 256, 0, s>>>(idx, prog, w0, w1, apply_valid, out);
   FB_LAUNCH_CHECK("k_filter_eval");
   return FB_OK;
