@@ -104,48 +104,82 @@ __global__ void k_filter_eval(fb_index_t idx, fb_filter_prog_t prog, int64_t w0,
 // queries) once per word into shared memory, phase 2 runs each query's program over those
 // leaf words (thread = (query, word), a warp = one query's 32 words: coalesced output,
 // uniform program walk). Stack of depth <= 4 in registers.
-constexpr int kFeWords = 32;
-__device__ __forceinline__ uint64_t eval_ops_leafwords(const fb_filter_prog_t& prog, int q,
-                                                       const uint64_t* s_leaf, int j, uint64_t v) {
+constexpr int kFeWords = 64;   // words per CTA chunk
+constexpr int kFeWpt = kFeWords / 32;  // words per thread (one op decode serves them all)
+
+// program of query q over words j + 32 u (u < kFeWpt) of the chunk
+__device__ __forceinline__ void eval_ops_leafwords(const fb_filter_prog_t& prog, int q,
+                                                   const uint64_t* s_leaf, int j,
+                                                   const uint64_t (&v)[kFeWpt],
+                                                   uint64_t (&res)[kFeWpt]) {
   const int32_t o0 = prog.op_offset[q], o1 = prog.op_offset[q + 1];
-  if (o0 == o1) return v;  // unfiltered query
+  if (o0 == o1) {  // unfiltered query
+#pragma unroll
+    for (int u = 0; u < kFeWpt; ++u) res[u] = v[u];
+    return;
+  }
   if (prog.max_stack <= 4) {
-    uint64_t top = 0ull, s1 = 0ull, s2 = 0ull, s3 = 0ull;
+    uint64_t top[kFeWpt], s1[kFeWpt], s2[kFeWpt], s3[kFeWpt];
+#pragma unroll
+    for (int u = 0; u < kFeWpt; ++u) top[u] = s1[u] = s2[u] = s3[u] = 0ull;
+    // ops fetched two ahead of their use (the loads hide behind the current op's work)
+    uint32_t n1 = prog.ops[o0], n2 = o0 + 1 < o1 ? prog.ops[o0 + 1] : 0u;
+    for (int o = o0; o < o1; ++o) {
+      const uint32_t op = n1;
+      n1 = n2;
+      n2 = o + 2 < o1 ? prog.ops[o + 2] : 0u;
+      const uint32_t code = op >> 14;
+      if (code == FB_OP_PUSH_LEAF) {
+        const uint64_t* lw = s_leaf + (op & 0x3FFF) * kFeWords + j;
+#pragma unroll
+        for (int u = 0; u < kFeWpt; ++u) {
+          s3[u] = s2[u];
+          s2[u] = s1[u];
+          s1[u] = top[u];
+          top[u] = lw[32 * u];
+        }
+      } else if (code == FB_OP_NOT) {
+#pragma unroll
+        for (int u = 0; u < kFeWpt; ++u) top[u] = ~top[u] & v[u];
+      } else {
+        const bool is_and = code == FB_OP_AND;
+#pragma unroll
+        for (int u = 0; u < kFeWpt; ++u) {
+          top[u] = is_and ? (s1[u] & top[u]) : (s1[u] | top[u]);
+          s1[u] = s2[u];
+          s2[u] = s3[u];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kFeWpt; ++u) res[u] = top[u];
+    return;
+  }
+#pragma unroll 1
+  for (int u = 0; u < kFeWpt; ++u) {
+    uint64_t stk[FB_MAX_STACK];
+    int sp = 0;
     for (int o = o0; o < o1; ++o) {
       const uint32_t op = prog.ops[o];
       const uint32_t code = op >> 14;
       if (code == FB_OP_PUSH_LEAF) {
-        s3 = s2;
-        s2 = s1;
-        s1 = top;
-        top = s_leaf[(op & 0x3FFF) * kFeWords + j];
+        stk[sp++] = s_leaf[(op & 0x3FFF) * kFeWords + j + 32 * u];
       } else if (code == FB_OP_NOT) {
-        top = ~top & v;
+        stk[sp - 1] = ~stk[sp - 1] & v[u];
       } else {
-        top = (code == FB_OP_AND) ? (s1 & top) : (s1 | top);
-        s1 = s2;
-        s2 = s3;
+        const uint64_t rhs = stk[--sp];
+        stk[sp - 1] = (code == FB_OP_AND) ? (stk[sp - 1] & rhs) : (stk[sp - 1] | rhs);
       }
     }
-    return top;
+    res[u] = stk[0];
   }
-  uint64_t stk[FB_MAX_STACK];
-  int sp = 0;
-  for (int o = o0; o < o1; ++o) {
-    const uint32_t op = prog.ops[o];
-    const uint32_t code = op >> 14;
-    if (code == FB_OP_PUSH_LEAF) {
-      stk[sp++] = s_leaf[(op & 0x3FFF) * kFeWords + j];
-    } else if (code == FB_OP_NOT) {
-      stk[sp - 1] = ~stk[sp - 1] & v;
-    } else {
-      const uint64_t rhs = stk[--sp];
-      stk[sp - 1] = (code == FB_OP_AND) ? (stk[sp - 1] & rhs) : (stk[sp - 1] | rhs);
-    }
-  }
-  return stk[0];
 }
 
+// Batched evaluation with the batch's leaves shared: a CTA takes kFeWords consecutive words;
+// phase 1 evaluates every distinct leaf of the batch (leaves are de-duplicated across
+// queries) once per word into shared memory, phase 2 runs each query's program over those
+// leaf words (a warp = one query; each lane kFeWpt words, so one op decode serves several
+// words; coalesced output). Stack of depth <= 4 in registers.
 __global__ void __launch_bounds__(256) k_filter_eval_shared(fb_index_t idx, fb_filter_prog_t prog,
                                                             int64_t w0, int64_t w1, int apply_valid,
                                                             uint64_t* __restrict__ out) {
@@ -157,20 +191,23 @@ __global__ void __launch_bounds__(256) k_filter_eval_shared(fb_index_t idx, fb_f
     const int nw = (int)min((int64_t)kFeWords, w1 - c0);
     __syncthreads();
     for (int e = threadIdx.x; e < nl * kFeWords; e += blockDim.x) {
-      const int leaf = e / kFeWords, j = e - leaf * kFeWords;
-      s_leaf[e] = j < nw ? leaf_word(prog.leaf_pos + (int64_t)leaf * prog.k_max, prog.k_max,
-                                     idx.planes, idx.n_words, c0 + j)
-                         : 0ull;
+      const int leaf = e / kFeWords, jj = e - leaf * kFeWords;
+      s_leaf[e] = jj < nw ? leaf_word(prog.leaf_pos + (int64_t)leaf * prog.k_max, prog.k_max,
+                                      idx.planes, idx.n_words, c0 + jj)
+                          : 0ull;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < prog.n_queries * kFeWords; e += blockDim.x) {
-      const int q = e / kFeWords, j = e - q * kFeWords;
-      if (j >= nw) continue;
-      const int64_t w = c0 + j;
-      const uint64_t v = idx.valid[w];
-      uint64_t m = eval_ops_leafwords(prog, q, s_leaf, j, v);
-      if (apply_valid) m &= v;
-      out[(int64_t)q * width + (w - w0)] = m;
+    for (int e = threadIdx.x; e < prog.n_queries * 32; e += blockDim.x) {
+      const int q = e >> 5, j = e & 31;
+      uint64_t v[kFeWpt], m[kFeWpt];
+#pragma unroll
+      for (int u = 0; u < kFeWpt; ++u) v[u] = j + 32 * u < nw ? idx.valid[c0 + j + 32 * u] : 0ull;
+      eval_ops_leafwords(prog, q, s_leaf, j, v, m);
+#pragma unroll
+      for (int u = 0; u < kFeWpt; ++u) {
+        const int jj = j + 32 * u;
+        if (jj < nw) out[(int64_t)q * width + (c0 + jj - w0)] = apply_valid ? (m[u] & v[u]) : m[u];
+      }
     }
   }
 }
