@@ -85,6 +85,52 @@ __device__ uint64_t eval_program_word(const fb_filter_prog_t& prog, int q,
   return stk[0];
 }
 
+// eval_program_word over leaf words already in shared memory (s_leaf[leaf]); stack of
+// depth <= 4 in registers
+__device__ uint64_t eval_program_leaves(const fb_filter_prog_t& prog, int q,
+                                        const uint64_t* s_leaf, uint64_t v) {
+  const int32_t o0 = prog.op_offset[q], o1 = prog.op_offset[q + 1];
+  if (o0 == o1) return v;  // unfiltered query
+  if (prog.max_stack <= 4) {
+    uint64_t top = 0ull, s1 = 0ull, s2 = 0ull, s3 = 0ull;
+    uint32_t n1 = prog.ops[o0], n2 = o0 + 1 < o1 ? prog.ops[o0 + 1] : 0u;
+    for (int o = o0; o < o1; ++o) {
+      const uint32_t op = n1;
+      n1 = n2;
+      n2 = o + 2 < o1 ? prog.ops[o + 2] : 0u;
+      const uint32_t code = op >> 14;
+      if (code == FB_OP_PUSH_LEAF) {
+        s3 = s2;
+        s2 = s1;
+        s1 = top;
+        top = s_leaf[op & 0x3FFF];
+      } else if (code == FB_OP_NOT) {
+        top = ~top & v;
+      } else {
+        top = (code == FB_OP_AND) ? (s1 & top) : (s1 | top);
+        s1 = s2;
+        s2 = s3;
+      }
+    }
+    return top;
+  }
+  uint64_t stk[FB_MAX_STACK];
+  int sp = 0;
+  for (int o = o0; o < o1; ++o) {
+    const uint32_t op = prog.ops[o];
+    const uint32_t code = op >> 14;
+    if (code == FB_OP_PUSH_LEAF) {
+      stk[sp++] = s_leaf[op & 0x3FFF];
+    } else if (code == FB_OP_NOT) {
+      stk[sp - 1] = ~stk[sp - 1] & v;
+    } else {
+      const uint64_t rhs = stk[--sp];
+      stk[sp - 1] = (code == FB_OP_AND) ? (stk[sp - 1] & rhs) : (stk[sp - 1] | rhs);
+    }
+  }
+  return stk[0];
+}
+
 __global__ void k_filter_eval(fb_index_t idx, fb_filter_prog_t prog, int64_t w0, int64_t w1,
                               int apply_valid, uint64_t* __restrict__ out) {
   const int64_t width = w1 - w0;
@@ -421,10 +467,23 @@ __device__ __forceinline__ void locate_word(const ScanArgs& a, int64_t g, int64_
   rmask = rem >= 64 ? ~0ull : ((1ull << rem) - 1);
 }
 
+constexpr int kSimtMaxSharedLeaves = 2048;  // 16 KB of leaf words per CTA
+__host__ __device__ __forceinline__ bool simt_shared_leaves(const fb_filter_prog_t& p) {
+  return p.n_leaves > 0 && p.n_leaves <= kSimtMaxSharedLeaves;
+}
+__host__ __device__ __forceinline__ size_t simt_smem(const ScanArgs& a) {
+  return (size_t)64 * a.idx.dim_pad +
+         (a.has_prog && simt_shared_leaves(a.prog) ? (size_t)a.prog.n_leaves * 8 : 0);
+}
+
 template <int MODE>
 __device__ void scan_simt_body(const ScanArgs& a, uint8_t* smem_items) {
   const int dp = a.idx.dim_pad;
   const int64_t n_work = (a.total_words + a.word_stride - 1) / a.word_stride;
+  // the batch's distinct leaves evaluated once per word (behind the staged item rows) when
+  // they fit, instead of once per (query, leaf)
+  const bool shared_leaves = a.has_prog && simt_shared_leaves(a.prog);
+  uint64_t* s_leaf = reinterpret_cast<uint64_t*>(smem_items + (size_t)64 * dp);
   for (int64_t gi = blockIdx.x; gi < n_work; gi += gridDim.x) {
     int64_t w;
     uint64_t rmask;
@@ -436,14 +495,19 @@ __device__ void scan_simt_body(const ScanArgs& a, uint8_t* smem_items) {
       const int4* src = reinterpret_cast<const int4*>(a.idx.items + slot0 * dp);
       int4* dst = reinterpret_cast<int4*>(smem_items);
       for (int i = threadIdx.x; i < 4 * dp; i += blockDim.x) dst[i] = __ldg(src + i);
+      if (shared_leaves)
+        for (int l = threadIdx.x; l < a.prog.n_leaves; l += blockDim.x)
+          s_leaf[l] = leaf_word(a.prog.leaf_pos + (int64_t)l * a.prog.k_max, a.prog.k_max,
+                                a.idx.planes, a.idx.n_words, w);
     }
     __syncthreads();
     if (vword == 0) continue;
     for (int q = threadIdx.x; q < a.n_queries; q += blockDim.x) {
       if (a.fb != nullptr && a.fb[q].state != a.only_state) continue;
-      uint64_t m = a.has_prog
-                       ? eval_program_word(a.prog, q, a.idx.planes, a.idx.n_words, w, vword) & vword
-                       : vword;
+      uint64_t m = !a.has_prog     ? vword
+                   : shared_leaves ? eval_program_leaves(a.prog, q, s_leaf, vword) & vword
+                                   : eval_program_word(a.prog, q, a.idx.planes, a.idx.n_words, w,
+                                                       vword) & vword;
       if (a.masks != nullptr) m &= a.masks[(int64_t)q * a.idx.n_words + w];
       if (m == 0) continue;
       const int8_t* qrow = a.queries + (int64_t)q * dp;
@@ -1598,7 +1662,7 @@ int launch_row_sums(const int8_t* x, int64_t rows, int cols, int stride, int32_t
 int launch_scan_simt(const ScanArgs& a, cudaStream_t s) {
   if (a.total_words <= 0 || a.n_queries <= 0) return FB_OK;
   const int64_t n_work = (a.total_words + a.word_stride - 1) / a.word_stride;
-  const size_t smem = (size_t)64 * a.idx.dim_pad;
+  const size_t smem = simt_smem(a);
   int grid = (int)(n_work < 148 * 8 ? n_work : 148 * 8);
   if (a.mode == SCAN_EMIT) {
     if (smem > 48 * 1024)
@@ -1657,7 +1721,7 @@ int launch_resolve(int32_t n_queries, int32_t k, int32_t cap, Fallback* fb, uint
 
 int launch_fallback(const FallbackArgs& f, cudaStream_t s) {
   if (f.n_queries <= 0) return FB_OK;
-  const size_t smem = (size_t)64 * f.hist.idx.dim_pad;
+  const size_t smem = std::max(simt_smem(f.hist), simt_smem(f.emit));
   if (smem > 48 * 1024)
     FB_CUDA(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
