@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--k", type=int, default=10_000)
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--env", default="", help="VAR=v1,v2,... (one run per value)")
+    ap.add_argument("--replan", action="store_true", help="re-create the plan per --env value")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     wl = workload.make_workload(a.items, a.batch)
@@ -46,6 +47,9 @@ def main():
     for st in settings:
         if st is not None:
             os.environ[st[0]] = st[1]
+            if a.replan:  # plan-time settings: a fresh plan per value
+                op = TopkOp(idx, a.batch, a.k, np.array([[0, idx.n_slots]]))
+                lib.fb_topk_set_timing(op._plan, 1)
         emit, sel, tot = [], [], []
         for i in range(a.iters + 3):
             s0 = torch.cuda.Event(enable_timing=True)
