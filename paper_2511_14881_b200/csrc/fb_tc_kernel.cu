@@ -130,7 +130,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 // Timeline trace (compile with -DFB_TRACE, run with FB_SCAN_DEBUG bit 10): CTA 0 records
 // clock64 at pipeline events of its first 16 tiles and prints them at exit.
 #ifdef FB_TRACE
-__device__ long long g_tr[16][12];
+__device__ long long g_tr[16][16];
 #define FB_TR(a, t, e)                                                          \
   do {                                                                          \
     if (((a).dbg & 1024) && blockIdx.x == 0 && (t) < 16 && (threadIdx.x & 31) == 0) \
@@ -1266,7 +1266,9 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
         iph ^= 1u;
       }
       const int hb = it & 1;
+      if (quad == 0) FB_TR(a, it, 12);
       if (it >= 2) nb_sync(kNbHmEmpty + hb, kNbHmCount);
+      if (quad == 0) FB_TR(a, it, 13);
       const uint32_t hmap = hm_s + (uint32_t)hb * kHmapBytes;
 #pragma unroll 1
       for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
@@ -1276,6 +1278,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
         const int32_t D = gate_digits(qok ? m.sT[q] : ~0ull, all);
         const uint32_t allmask = all ? ~0u : 0u;
         const int ab = acc_it & 1;
+        if (quad == 0 && mb == 0) FB_TR(a, it, 14);
         mbar_wait(acc_full + ab, (uint32_t)(acc_it >> 1) & 1u);
         tc_fence_after();
         if (quad == 0) FB_TR(a, it, 4 + 2 * mb);
@@ -1444,6 +1447,9 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
              t, g_tr[t][0] - t0, g_tr[t][1] - t0, g_tr[t][2] - t0, g_tr[t][3],
              g_tr[t][4] - t0, g_tr[t][5] - t0, g_tr[t][6] - t0, g_tr[t][7] - t0,
              g_tr[t][8] - t0, g_tr[t][11] - t0, g_tr[t][9] - t0, g_tr[t][10] - t0);
+    for (int t = 0; t < 16; ++t)
+      printf("dense %2d: top %6lld afterHmEmpty %6lld beforeAccWait %6lld d0 %6lld\n", t,
+             g_tr[t][12] - t0, g_tr[t][13] - t0, g_tr[t][14] - t0, g_tr[t][4] - t0);
   }
 #endif
   if (warp == 1)
