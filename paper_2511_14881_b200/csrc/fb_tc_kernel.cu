@@ -1253,6 +1253,16 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
     // ================= dense pass (one warp per TMEM lane quadrant) ======================
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
+    // per-row gate constants of both M-blocks, fixed for the whole launch
+    uint32_t allm[2];
+    int32_t Dm[2];
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb) {
+      const int q = mb * kBlockM + row;
+      bool all = false;
+      Dm[mb] = mb < a.n_mblk ? gate_digits(q < a.nq ? m.sT[q] : ~0ull, all) : 0;
+      allm[mb] = all ? ~0u : 0u;
+    }
     int it = 0, acc_it = 0, s = 0;
     uint32_t iph = 0;
     for (int64_t i = blockIdx.x; i < n_sel; i += gridDim.x, ++it) {
@@ -1274,9 +1284,8 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
       for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
         const int q = mb * kBlockM + row;
         const bool qok = q < a.nq;
-        bool all;
-        const int32_t D = gate_digits(qok ? m.sT[q] : ~0ull, all);
-        const uint32_t allmask = all ? ~0u : 0u;
+        const int32_t D = mb == 0 ? Dm[0] : Dm[1];
+        const uint32_t allmask = mb == 0 ? allm[0] : allm[1];
         const int ab = acc_it & 1;
         if (quad == 0 && mb == 0) FB_TR(a, it, 14);
         mbar_wait(acc_full + ab, (uint32_t)(acc_it >> 1) & 1u);
