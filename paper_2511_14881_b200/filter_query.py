@@ -10,6 +10,7 @@ the whole batch, positions hashed in C). ``eval_compiled`` runs ``fb_filter_eval
 from __future__ import annotations
 
 import re
+from collections import OrderedDict
 from dataclasses import dataclass, field
 from enum import IntEnum
 
@@ -225,7 +226,30 @@ class CompiledFilter:
         return peak
 
 
+_COMPILED: "OrderedDict[tuple, CompiledFilter]" = OrderedDict()
+_COMPILED_MAX = 8192
+
+
 def compile_filter(expr: FilterExpr, params: BloomParams) -> CompiledFilter:
+    """``_compile_filter`` behind an LRU cache keyed by the (immutable) expression and the
+    Bloom parameters: serving traffic repeats filters, and a compiled filter is immutable.
+    Unhashable expressions are compiled directly."""
+    try:
+        key = (expr, params)
+        hit = _COMPILED.get(key)
+    except TypeError:
+        return _compile_filter(expr, params)
+    if hit is not None:
+        _COMPILED.move_to_end(key)
+        return hit
+    cf = _compile_filter(expr, params)
+    _COMPILED[key] = cf
+    if len(_COMPILED) > _COMPILED_MAX:
+        _COMPILED.popitem(last=False)
+    return cf
+
+
+def _compile_filter(expr: FilterExpr, params: BloomParams) -> CompiledFilter:
     """Post-order lowering with per-(fid, value) de-duplication (reference
     filter_query.py:280-311); all leaf positions hashed in one ``fb_hash_leaves`` call."""
     leaf_index: dict[tuple[int, int], int] = {}
