@@ -227,3 +227,15 @@ def test_cnf_packing_matches_compiled_programs(n_feat, n_vals, windowed):
             for g in range(int(batch.host_qgroups[q])):
                 w = np.nonzero(nz[q, g])[0]
                 assert len(w) and w.min() // 2 == w.max() // 2
+
+
+def test_compile_filter_cache_returns_identical_program():
+    """Repeated expressions hit the compile cache; the cached program equals a fresh one."""
+    from paper_2511_14881_b200 import filter_query as fq
+    expr = And((Or((Leaf(1, 2), Leaf(1, 3))), Not(Leaf(2, 7))))
+    a = compile_filter(expr, BloomParams())
+    b = compile_filter(And((Or((Leaf(1, 2), Leaf(1, 3))), Not(Leaf(2, 7)))), BloomParams())
+    assert a is b
+    fresh = fq._compile_filter(expr, BloomParams())
+    assert fresh.ops == a.ops and fresh.leaves == a.leaves
+    assert compile_filter(expr, BloomParams(m_bits=512)) is not a   # params are in the key
