@@ -63,8 +63,9 @@ def parse_args():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--dim", type=int, default=128)
     ap.add_argument("--simt", action="store_true", help="force the SIMT scan kernel")
-    ap.add_argument("--exchange", choices=["pruned", "all_gather"], default="pruned",
-                    help="N>1 shard exchange: pruned owner-partitioned all-to-all, or all-gather")
+    ap.add_argument("--exchange", choices=["owner", "pruned", "all_gather"], default="owner",
+                    help="N>1 shard exchange: owner-partitioned all-to-all with static sizes "
+                         "(no host sync), the pruned variant, or all-gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=0, help="CPU sample size (0: auto)")
     a = ap.parse_args()
@@ -87,10 +88,12 @@ def workload_desc(a, n_gpus):
         "filter": "AND of 4 OR-groups, |S|=(17,17,14,11), 59 leaves/query",
         "l2": "inputs 2.6 GB/GPU > 126 MB L2; no flush needed",
         "parallelism": "single GPU" if n_gpus == 1 else
-                       (f"items sharded x{n_gpus}, NCCL all-reduce(max) of local k-th scores + "
-                        "pruned all-to-all to query owners + GPU merge"
-                        if getattr(a, "exchange", "pruned") == "pruned" else
-                        f"items sharded x{n_gpus}, NCCL all-gather + GPU merge"),
+                       {"owner": f"items sharded x{n_gpus}, one NCCL all-to-all of the local "
+                                  "top-k lists to the query owners + GPU merge",
+                        "pruned": f"items sharded x{n_gpus}, NCCL all-reduce(max) of local k-th "
+                                  "scores + pruned all-to-all to query owners + GPU merge",
+                        "all_gather": f"items sharded x{n_gpus}, NCCL all-gather + GPU merge"}
+                       [getattr(a, "exchange", "owner")],
     }
 
 
@@ -113,22 +116,38 @@ def _cpu_query(i):
     prog = d["progs"][i % len(d["progs"])]
     res = orc.codesigned_search(d["items"], d["valid"], d["ids"], d["offs"], d["planes"], prog,
                                 d["qq"][i % len(d["qq"])], [0], d["k"])
-    return len(res.item_ids)
+    return res.item_ids, res.scores
 
 
-def time_cpu_oracle(items, valid, ids, planes, qq, progs, k, n_queries, cores, rounds=1):
+def time_cpu_oracle(items, valid, ids, planes, qq, progs, k, n_queries, cores):
     """Wall time of ``n_queries`` oracle codesigned_search calls over ``cores`` forked
-    workers. Returns (queries/s, seconds, queries)."""
+    workers. Returns (queries/s, seconds, queries, per-query (ids, scores)) -- the answers
+    are kept so the caller can check the GPU's results for the same queries bit for bit."""
     _CPU.update(items=items, valid=valid, ids=ids, offs=np.array([[0, items.shape[0]]]),
                 planes=planes, qq=qq, progs=progs, k=k)
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        pool.map(_cpu_query, range(cores))  # warm the workers (page-in)
+        pool.map(_cpu_query, range(min(cores, n_queries)))  # warm the workers (page-in)
         t0 = time.perf_counter()
-        for _ in range(rounds):
-            pool.map(_cpu_query, range(n_queries), chunksize=1)
+        answers = pool.map(_cpu_query, range(n_queries), chunksize=1)
         dt = time.perf_counter() - t0
-    return n_queries * rounds / dt, dt, n_queries * rounds
+    return n_queries / dt, dt, n_queries, answers
+
+
+def parity_check(out, answers, queries):
+    """Bit-for-bit comparison of the GPU's (ids, int32 scores, count) rows with the oracle's
+    answers for the same queries (ids, order and scores exact)."""
+    from paper_2511_14881_b200._device import u64_host
+    bad = []
+    for q, (ref_ids, ref_scores) in zip(queries, answers):
+        n = int(out.count[q])
+        got_ids = u64_host(out.ids[q, :n])
+        got_scores = out.scores[q, :n].cpu().numpy()
+        if not (np.array_equal(got_ids, ref_ids) and np.array_equal(got_scores, ref_scores)):
+            bad.append(int(q))
+    return {"checked": len(answers), "mismatches": len(bad), "bad_queries": bad[:16],
+            "oracle": "oracle.filtra_oracle.codesigned_search (pinned to reference goldens)",
+            "compared": "item ids, int32 scores, order and count per query"}
 
 
 def progs_of(filters):
@@ -252,20 +271,29 @@ def run_ours(a):
     from paper_2511_14881_b200.bloom import BloomParams
     from paper_2511_14881_b200.filter_query import FilterBatch, compile_filter
     from paper_2511_14881_b200.quantize import quantize_device
-    from paper_2511_14881_b200.serve import exchange_pruned, exchange_topk
+    from paper_2511_14881_b200.serve import exchange_owner, exchange_pruned, exchange_topk
 
     lib = _native.lib()
     B, k = a.batch, a.k
     t_gen = time.perf_counter()
-    wl = workload.make_workload(a.items, B, dim=a.dim, seed=1 + rank)
     if world > 1:
-        # one catalogue: shard r holds global ids [r * n_pad, (r + 1) * n_pad); every rank
-        # answers rank 0's queries with rank 0's quantisation parameters
-        wl.index.item_ids += rank * wl.index.n_slots_pad
-        dist.broadcast(wl.queries, 0)
-        qp_t = torch.tensor([wl.qp.global_min, wl.qp.global_max], dtype=torch.float64,
-                            device="cuda")
-        dist.broadcast(qp_t, 0)
+        # one catalogue of world x items: shard r holds global ids [r * items, (r+1) * items),
+        # quantised with the catalogue's global min/max (all-reduce MIN/MAX before any
+        # quantisation), and every rank answers rank 0's queries
+        def reduce_minmax(lo, hi):
+            t = torch.tensor([-lo, hi], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return -float(t[0]), float(t[1])
+
+        def share_queries(q):
+            dist.broadcast(q, 0)
+            return q
+
+        wl = workload.make_workload(a.items, B, dim=a.dim, seed=1 + rank,
+                                    id_base=rank * a.items, reduce_minmax=reduce_minmax,
+                                    share_queries=share_queries)
+    else:
+        wl = workload.make_workload(a.items, B, dim=a.dim, seed=1)
     gen_s = time.perf_counter() - t_gen
 
     idx = wl.index
@@ -286,7 +314,9 @@ def run_ours(a):
         quantize_device(queries_f32, wl.qp, out_stride=idx.dim_pad, out=qbuf)
         res = op(qbuf, filters, out=outs)
         if world > 1:
-            if a.exchange == "pruned":  # each rank merges its query slice
+            if a.exchange == "owner":  # each rank merges its query slice
+                _, _, s, i, c = exchange_owner(res.scores, res.ids, res.count)
+            elif a.exchange == "pruned":
                 _, _, s, i, c = exchange_pruned(res.scores, res.ids, res.count, k)
             else:
                 s, i, c = exchange_topk(res.scores, res.ids, res.count)
@@ -372,15 +402,16 @@ def run_ours(a):
     if world == 1:
         from paper_2511_14881_b200.engine import PipelinedTopk
         pipe = PipelinedTopk(idx, B, k, flags=flags, filters_template=wl.filters)
-        h_prog = [torch.from_numpy(x).pin_memory() for x in pipe.slots[0]["batch"].host_arrays()]
+        h_batch = FilterBatch.pack(wl.filters, BloomParams()).pin()
+        h_prog = h_batch.pinned_arrays()
         for _ in range(3):
-            pipe.result(pipe.submit(host_q, h_prog))
+            pipe.result(pipe.submit(host_q, h_batch))
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         last = None
         for _ in range(a.steps):
-            last = pipe.submit(host_q, h_prog)
+            last = pipe.submit(host_q, h_batch)
         stream.wait_event(pipe.done_event(last))
         e1.record(stream)
         torch.cuda.synchronize()
@@ -434,6 +465,7 @@ def run_ours(a):
 
     # ---- CPU baseline (rank 0, N=1 only) ---------------------------------------------
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         from paper_2511_14881_b200._device import u64_host
         cores = host_cores()
@@ -444,12 +476,16 @@ def run_ours(a):
         planes = idx.bloom.planes
         qq = wl.queries_q.cpu().numpy()[:, : a.dim]
         progs = progs_of(wl.filters)
-        qps, secs, n = time_cpu_oracle(items, valid, ids, planes, qq[:nq], progs[:nq], k, nq,
-                                       cores)
+        qps, secs, n, answers = time_cpu_oracle(items, valid, ids, planes, qq[:nq], progs[:nq],
+                                                k, nq, cores)
         cpu = {"value": round(qps, 3), "unit": UNIT, "cores": cores, "kind": "port",
                "sample": (f"{n} queries (oracle codesigned_search over the full "
                           f"{a.items / 1e6:g}M-item index, k={k}) in {secs:.1f} s on "
                           f"{cores} forked workers")}
+        # the GPU answered the same queries (the last step left them in ``outs``)
+        step(wl.queries, batch)
+        torch.cuda.synchronize()
+        parity = parity_check(outs, answers, range(nq))
 
     if rank == 0:
         line = {
@@ -463,11 +499,16 @@ def run_ours(a):
             "scan_kernel": "simt" if a.simt else "default",
             "setup_s": round(gen_s, 1),
             "host_compile_pack_ms_per_batch": round(compile_ms, 2),
+            "parity": parity,
         }
         _ = sel
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if parity is not None and parity["mismatches"]:
+        print(f"PARITY FAILURE: {parity['mismatches']} of {parity['checked']} queries differ "
+              f"from the oracle", file=sys.stderr)
+        sys.exit(3)
 
 
 # ------------------------------------------------------------------------------------

@@ -197,3 +197,9 @@ def positions_from_seed(seed: int, params: BloomParams) -> tuple[int, ...]:
         out.add((z ^ (z >> 31)) % params.m_bits)
     return tuple(sorted(out))
 
+
+
+# result / counter types: the reference's classes when it is importable (see _refapi)
+from ._refapi import bind as _bind  # noqa: E402
+
+_bind(globals(), "bloom", ["FilterStats"])

@@ -13,7 +13,9 @@ select -- on the current CUDA stream with no host synchronisation.
 from __future__ import annotations
 
 import ctypes
+import threading
 import weakref
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -288,6 +290,32 @@ class TopkOp:
         return out
 
 
+_PLAN_LOCK = threading.Lock()
+PLAN_CACHE_SIZE = 64
+
+
+def cached_op(index: DeviceIndex, n_queries: int, k: int, ranges, flags: int = 0) -> TopkOp:
+    """A ``TopkOp`` for (B, k, ranges, flags) from a small per-index LRU, so per-call entry
+    points (the B = 1 reference shims, the custom op) do not pay plan creation -- device
+    scratch allocation and uploads -- on every call. Plans are per thread: a plan's
+    scratch is reused call after call on the calling thread's stream, and the reference's
+    ``BatchingServer`` calls concurrently from several threads."""
+    r = np.ascontiguousarray(np.asarray(ranges, dtype=np.int64).reshape(-1, 2))
+    key = (threading.get_ident(), int(n_queries), int(k), r.tobytes(), int(flags))
+    with _PLAN_LOCK:
+        cache = index.__dict__.setdefault("_plans", OrderedDict())
+        op = cache.get(key)
+        if op is not None:
+            cache.move_to_end(key)
+            return op
+    op = TopkOp(index, n_queries, k, r, flags)
+    with _PLAN_LOCK:
+        cache[key] = op
+        while len(cache) > PLAN_CACHE_SIZE:
+            cache.popitem(last=False)
+    return op
+
+
 def filtered_topk(index: DeviceIndex, queries_q: torch.Tensor, k: int,
                   filters: FilterBatch | None = None, ranges=None, flags: int = 0,
                   masks: torch.Tensor | None = None, keys: bool = False,
@@ -359,18 +387,40 @@ class PipelinedTopk:
             })
         self._n = 0
 
-    def submit(self, host_queries: torch.Tensor, host_filter_arrays=None) -> int:
-        """Enqueue one batch (pinned float32 queries [B, dim]; the filter batch's host arrays
-        in ``FilterBatch.host_arrays()`` order, or None to reuse the slot's). Returns a
-        ticket for ``result``."""
+    @staticmethod
+    def _same_shape(batch: FilterBatch, filters: FilterBatch) -> bool:
+        """True when ``filters`` can be copied into ``batch``'s device arrays: the same
+        scalar metadata (program form, leaf/plane/column counts, CNF layout) and the same
+        count, shape and dtype of every array."""
+        if batch is None or batch.meta() != filters.meta():
+            return False
+        dev, host = batch._dev, filters.host_arrays()
+        return len(dev) == len(host) and all(
+            tuple(d.shape) == tuple(h.shape) and d.element_size() == h.itemsize
+            for d, h in zip(dev, host))
+
+    def submit(self, host_queries: torch.Tensor, filters: FilterBatch | None = None) -> int:
+        """Enqueue one batch: float32 queries [B, dim] (pinned for an asynchronous copy) and
+        the batch's packed filters (``FilterBatch.pack``; ``.pin()`` it for asynchronous
+        copies), or None to reuse the slot's filters. A batch with the slot's shape is
+        copied into the slot's device arrays on the copy stream; any other batch replaces
+        the slot's (one upload). Returns a ticket for ``result``."""
+        if tuple(host_queries.shape) != (self.B, self.index.dim):
+            raise ValueError(f"queries must be [{self.B}, {self.index.dim}], got "
+                             f"{tuple(host_queries.shape)}")
+        if filters is not None and filters.n_queries != self.B:
+            raise ValueError(f"filter batch holds {filters.n_queries} programs, expected {self.B}")
         t = self._n
         s = self.slots[t % len(self.slots)]
         self._n += 1
         self.copy_in.wait_event(s["comp"])       # the slot's inputs are no longer read
+        if filters is not None and not self._same_shape(s["batch"], filters):
+            s["batch"] = filters.clone_host().to_device()  # other shape: the slot's own upload
+            filters = None
         with torch.cuda.stream(self.copy_in):
             s["q"].copy_(host_queries, non_blocking=True)
-            if host_filter_arrays is not None and s["batch"] is not None:
-                for d, h in zip(s["batch"]._dev, host_filter_arrays):
+            if filters is not None:
+                for d, h in zip(s["batch"]._dev, filters.pinned_arrays()):
                     d.copy_(h, non_blocking=True)
             s["h2d"].record(self.copy_in)
         self.compute.wait_event(s["h2d"])

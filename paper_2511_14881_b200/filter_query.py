@@ -9,7 +9,9 @@ the whole batch, positions hashed in C). ``eval_compiled`` runs ``fb_filter_eval
 
 from __future__ import annotations
 
+import copy
 import re
+import threading
 from collections import OrderedDict
 from dataclasses import dataclass, field
 from enum import IntEnum
@@ -228,6 +230,7 @@ class CompiledFilter:
 
 _COMPILED: "OrderedDict[tuple, CompiledFilter]" = OrderedDict()
 _COMPILED_MAX = 8192
+_COMPILED_LOCK = threading.Lock()
 
 
 def compile_filter(expr: FilterExpr, params: BloomParams) -> CompiledFilter:
@@ -236,16 +239,19 @@ def compile_filter(expr: FilterExpr, params: BloomParams) -> CompiledFilter:
     Unhashable expressions are compiled directly."""
     try:
         key = (expr, params)
-        hit = _COMPILED.get(key)
+        hash(key)
     except TypeError:
         return _compile_filter(expr, params)
-    if hit is not None:
-        _COMPILED.move_to_end(key)
-        return hit
+    with _COMPILED_LOCK:  # the reference server compiles from several worker threads
+        hit = _COMPILED.get(key)
+        if hit is not None:
+            _COMPILED.move_to_end(key)
+            return hit
     cf = _compile_filter(expr, params)
-    _COMPILED[key] = cf
-    if len(_COMPILED) > _COMPILED_MAX:
-        _COMPILED.popitem(last=False)
+    with _COMPILED_LOCK:
+        _COMPILED[key] = cf
+        while len(_COMPILED) > _COMPILED_MAX:
+            _COMPILED.popitem(last=False)
     return cf
 
 
@@ -490,6 +496,23 @@ class FilterBatch:
                 arrs += [self.host_col_leaf, self.host_qmask.view(np.int32), self.host_qgroups]
         return arrs
 
+    def clone_host(self) -> "FilterBatch":
+        """A copy sharing the (read-only) host arrays, with no device arrays of its own yet."""
+        c = copy.copy(self)
+        c._dev = None
+        return c
+
+    def pin(self) -> "FilterBatch":
+        """Stage the host arrays in pinned memory (asynchronous H2D copies); idempotent."""
+        if getattr(self, "_pinned", None) is None:
+            self._pinned = [torch.from_numpy(a).pin_memory() for a in self.host_arrays()]
+        return self
+
+    def pinned_arrays(self) -> list[torch.Tensor]:
+        """Host arrays as tensors (pinned after ``pin()``; pageable otherwise)."""
+        p = getattr(self, "_pinned", None)
+        return p if p is not None else [torch.from_numpy(a) for a in self.host_arrays()]
+
     def to_device(self) -> "FilterBatch":
         """Upload the bytecode (one H2D copy per array); idempotent."""
         if self._dev is None:
@@ -598,22 +621,46 @@ class FilterBatch:
         cf = CompiledFilter(ops=((OpCode.PUSH_LEAF, 0),), leaves=((0, 0, qb),))
         return cls.pack([cf], params)
 
-    def struct(self) -> _native.FbFilterProg:
-        d = self.to_device()._dev
-        if self.host_rops is not None:
-            extra = (self.n_planes if self.host_plane_list is not None else 0, self.rmax_stack,
-                     int(self.host_rops.size), 0,
-                     d[3].data_ptr(), d[4].data_ptr(), d[5].data_ptr(), d[6].data_ptr())
+    # scalar metadata of the device form, in the order ``struct_from`` reads it
+    META_FIELDS = ("n_queries", "n_leaves", "k_max", "max_stack", "has_rops", "n_planes",
+                   "rmax_stack", "n_rops", "is_cnf", "n_cols", "cnf_words", "cnf_gmax",
+                   "cnf_windowed")
+
+    def meta(self) -> list[int]:
+        has_rops = self.host_rops is not None
+        return [self.n_queries, self.n_leaves, self.k_max, self.max_stack, int(has_rops),
+                self.n_planes if has_rops else 0, self.rmax_stack if has_rops else 0,
+                int(self.host_rops.size) if has_rops else 0, int(self.is_cnf),
+                int(self.host_col_leaf.size) if self.is_cnf else 0, int(self.cnf_words),
+                int(self.cnf_gmax), int(self.cnf_windowed)]
+
+    def device_arrays(self) -> list[torch.Tensor]:
+        return list(self.to_device()._dev)
+
+    @staticmethod
+    def struct_from(d, meta) -> _native.FbFilterProg:
+        """``fb_filter_prog_t`` from device arrays (``host_arrays()`` order) and ``meta()``
+        (the custom-op boundary passes exactly these two)."""
+        (nq, n_leaves, k_max, max_stack, has_rops, n_planes, rmax, n_rops, is_cnf, n_cols,
+         cnf_words, cnf_gmax, cnf_windowed) = (int(x) for x in meta)
+        need = 3 + (4 if has_rops else 0) + (3 if is_cnf else 0)
+        if len(d) != need:
+            raise ValueError(f"filter batch: {len(d)} device arrays, expected {need}")
+        if has_rops:
+            extra = (n_planes, rmax, n_rops, 0, d[3].data_ptr(), d[4].data_ptr(),
+                     d[5].data_ptr(), d[6].data_ptr())
         else:
             extra = (0, 0, 0, 0, None, None, None, None)
-        if self.is_cnf:
-            cnf = (int(self.host_col_leaf.size), self.cnf_words, self.cnf_gmax,
-                   self.cnf_windowed, d[7].data_ptr(), d[8].data_ptr(), d[9].data_ptr())
+        if is_cnf:
+            cnf = (n_cols, cnf_words, cnf_gmax, cnf_windowed, d[7].data_ptr(), d[8].data_ptr(),
+                   d[9].data_ptr())
         else:
             cnf = (0, 0, 0, 0, None, None, None)
-        return _native.FbFilterProg(self.n_queries, self.n_leaves, self.k_max, self.max_stack,
-                                    d[0].data_ptr(), d[1].data_ptr(), d[2].data_ptr(), *extra,
-                                    *cnf)
+        return _native.FbFilterProg(nq, n_leaves, k_max, max_stack, d[0].data_ptr(),
+                                    d[1].data_ptr(), d[2].data_ptr(), *extra, *cnf)
+
+    def struct(self) -> _native.FbFilterProg:
+        return FilterBatch.struct_from(self.to_device()._dev, self.meta())
 
     def evaluate(self, bloom: BloomIndex, valid, w0: int, w1: int,
                  apply_valid: bool = True) -> np.ndarray:

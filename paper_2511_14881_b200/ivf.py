@@ -17,7 +17,7 @@ import torch
 
 from . import _native
 from ._device import device, to_dev, to_dev_u64
-from .engine import DeviceIndex, TopkOp, TopkOutput, device_index_for
+from .engine import DeviceIndex, TopkOp, TopkOutput, cached_op, device_index_for
 from .errors import DimMismatch
 
 TILE_ROWS = 4096  # reference tile contract (ivf.py:24); GPU tiles are 128 rows
@@ -70,7 +70,7 @@ def run_scan(dix: DeviceIndex, query_q: np.ndarray, ranges: np.ndarray, mask, to
     if topk <= 0 or total == 0:
         return _empty(topk)
     k_eff = min(int(topk), total)
-    op = TopkOp(dix, 1, k_eff, ranges, flags)
+    op = cached_op(dix, 1, k_eff, ranges, flags)
     if stats is not None:
         st = op.stats()
         stats.tiles += int(st.tiles)
@@ -121,14 +121,25 @@ def probe_centroids(index, query: np.ndarray, nprobe: int) -> np.ndarray:
     return order[:nprobe].cpu().numpy().astype(np.int64)
 
 
+def quantize_query(dix: DeviceIndex, query) -> torch.Tensor:
+    """The query's int8 codes exactly as reference ``quantize_vector`` (quantize.py:72-76)
+    computes them: from the float64 value of the caller's array (a float32 array widens
+    exactly, so it takes the float32 kernel; anything else is quantised from float64,
+    never rounded through float32 first)."""
+    x = np.asarray(query)
+    if x.dtype != np.float32:
+        x = x.astype(np.float64)
+    dt = torch.float32 if x.dtype == np.float32 else torch.float64
+    return dix.quantize_queries(to_dev(x.reshape(1, -1), dt))
+
+
 def search(index, query: np.ndarray, nprobe: int, topk: int, mask: np.ndarray | None = None,
            stats: ScanStats | None = None) -> TopkResult:
     """Quantise with the index params, probe, fused scan (reference ivf.py:337-343)."""
     dix = device_index_for(index)
-    query = np.asarray(query, dtype=np.float32)
-    if query.shape[0] != dix.dim:
-        raise DimMismatch(dix.dim, query.shape[0])
-    qq = dix.quantize_queries(to_dev(query.reshape(1, -1), torch.float32))
+    if np.asarray(query).shape[0] != dix.dim:
+        raise DimMismatch(dix.dim, np.asarray(query).shape[0])
+    qq = quantize_query(dix, query)
     clusters = probe_centroids(dix, query, nprobe)
     return run_scan(dix, qq, cluster_ranges(dix, clusters), mask, topk, stats=stats)
 
@@ -249,3 +260,9 @@ class IvfSearchOp:
             _native.stream_ptr()))
         self._keep = (qq, filters, words)
         return out, clusters
+
+
+# result / counter types: the reference's classes when it is importable (see _refapi)
+from ._refapi import bind as _bind  # noqa: E402
+
+_bind(globals(), "ivf", ["TopkResult","ScanStats"])

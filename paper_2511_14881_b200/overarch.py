@@ -27,6 +27,7 @@ Here the whole batch of requests runs on the device:
 from __future__ import annotations
 
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -414,7 +415,24 @@ class RetrieveResult:
     filter_stats: FilterStats
 
 
-_CACHE_OBJ: dict = {}
+# device copies of the reference engine's embedding cache / scorer, keyed weakly on the
+# host objects: a snapshot hot swap drops the old engine and with it its HBM copy
+_DEVICE_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_DEVICE_SCORER: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _weak_cached(table, obj, make):
+    try:
+        hit = table.get(obj)
+    except TypeError:  # unhashable / not weak-referenceable: no caching
+        return make(obj)
+    if hit is None:
+        hit = make(obj)
+        try:
+            table[obj] = hit
+        except TypeError:
+            pass
+    return hit
 
 
 def retrieve(engine, req) -> RetrieveResult:
@@ -444,18 +462,13 @@ def retrieve(engine, req) -> RetrieveResult:
     items: list[RetrievedItem] = []
     n = int(mcount[0])
     if n:
-        key = id(engine.cache)
-        cache = _CACHE_OBJ.get(key)
-        if cache is None or cache[0] is not engine.cache:
-            cache = (engine.cache, DeviceCache.from_reference(engine.cache))
-            _CACHE_OBJ[key] = cache
-        dcache = cache[1]
+        dcache = _weak_cached(_DEVICE_CACHE, engine.cache, DeviceCache.from_reference)
         valid = torch.arange(merged.shape[1], device=dev)[None, :] < mcount[:, None]
         rows = dcache.rows_for(merged, valid)
         names = [t.task_name for t in req.tasks]
         users = torch.as_tensor(np.stack([np.asarray(t.user_embedding, dtype=np.float32)
                                           for t in req.tasks]), device=dev)[None]
-        scorer = DeviceScorer.from_reference(engine.scorer)
+        scorer = _weak_cached(_DEVICE_SCORER, engine.scorer, DeviceScorer.from_reference)
         ts = scorer.score(dcache, rows, mcount, users, names)
         vm = req.value_model if req.value_model is not None else engine.default_value_model
         spec = value_model_spec(vm) or mean_of_tasks_spec(names)

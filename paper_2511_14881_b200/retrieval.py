@@ -22,7 +22,8 @@ from .bloom import FilterStats
 from .engine import device_index_for
 from .errors import DimMismatch
 from .filter_query import CompiledFilter, FilterBatch
-from .ivf import ScanStats, TopkResult, cluster_ranges, probe_centroids, run_scan
+from .ivf import (ScanStats, TopkResult, cluster_ranges, probe_centroids, quantize_query,
+                  run_scan)
 
 
 @dataclass
@@ -45,7 +46,8 @@ def codesigned_search(ivf, bloom_index, cf: CompiledFilter | None, query: np.nda
                       timings: StageTimings | None = None) -> TopkResult:
     """Probe, then one fused filter+scan launch sequence over the probed clusters."""
     dix = device_index_for(ivf, bloom=bloom_index if cf is not None else None)
-    query = np.asarray(query, dtype=np.float32)
+    raw_query = query
+    query = np.asarray(query, dtype=np.float32)  # probing is float32 (ref ivf.py:263)
     if query.shape[0] != dix.dim:
         raise DimMismatch(dix.dim, query.shape[0])
     t0 = time.perf_counter()
@@ -64,10 +66,16 @@ def codesigned_search(ivf, bloom_index, cf: CompiledFilter | None, query: np.nda
             words = int(sum(((int(e) + 63) >> 6) - (int(s) >> 6) for s, e in ranges))
             filter_stats.slots_evaluated += words * bitset.WORD_BITS
             filter_stats.words_read += int(filters.push_leaf_bits[0]) * words
-    qq = dix.quantize_queries(to_dev(query.reshape(1, -1), torch.float32))
+    qq = quantize_query(dix, raw_query)  # quantised from float64 (ref quantize.py:73)
     result = run_scan(dix, qq, ranges, None, k0, filters=filters, stats=scan_stats)
     t2 = time.perf_counter()
     if timings is not None:
         timings.probe_us += int((t1 - t0) * 1e6)
         timings.scan_us += int((t2 - t1) * 1e6)
     return result
+
+
+# result / counter types: the reference's classes when it is importable (see _refapi)
+from ._refapi import bind as _bind  # noqa: E402
+
+_bind(globals(), "retrieval", ["StageTimings"])

@@ -4,7 +4,8 @@ The reference fans a request out to in-process shards, concatenates their local
 top-k lists and reduces them with ``_reduce_topk`` (a global
 ``lexsort((ids, -scores))[:k]``, serve.py:98-100). Here one process drives one GPU
 and one shard: every rank runs the fused filtered top-k on its own slot range, the
-per-rank (score, id) lists are exchanged with one NCCL ``all_gather`` over NVLink, and
+per-rank (score, id) lists are exchanged over NVLink (by default one NCCL all-to-all
+to the rank owning each query slice; ``all_gather`` and a pruned variant are kept), and
 ``fb_merge_topk`` merges them on the GPU. Quantisation parameters are global (shared
 by all shards), so the merged answer is bit-identical to the unsharded search.
 """
@@ -26,7 +27,15 @@ def _reduce_topk(ids: np.ndarray, scores: np.ndarray, k: int) -> tuple[np.ndarra
     (each sorted by (score desc, id asc)) is split into its sorted runs and merged on
     the GPU. Any input order is accepted (a run may have length 1)."""
     ids = np.asarray(ids, dtype=np.uint64)
-    scores = np.asarray(scores).astype(np.int64)
+    raw = np.asarray(scores)
+    scores = raw.astype(np.int64)
+    if raw.dtype.kind == "f" and raw.size and not np.array_equal(scores, raw):
+        # the GPU merge ranks exact int32 scores (every shard result of the int8 path);
+        # fractional scores would be truncated and re-ordered, so refuse them loudly
+        raise NotImplementedError("_reduce_topk: the GPU shard merge takes integral int32 "
+                                  "scores; got fractional float scores")
+    if raw.size and (scores.min() < -2**31 or scores.max() >= 2**31):
+        raise NotImplementedError("_reduce_topk: scores outside the int32 range")
     n = len(ids)
     if n == 0 or k <= 0:
         return ids[:0], scores[:0].astype(np.int32)
@@ -75,6 +84,35 @@ def exchange_topk(local_scores: torch.Tensor, local_ids: torch.Tensor, local_cou
 def query_owner_slices(n_queries: int, world: int) -> list[tuple[int, int]]:
     """Contiguous query slice each rank merges in the owner-partitioned exchange."""
     return [(r * n_queries // world, (r + 1) * n_queries // world) for r in range(world)]
+
+
+def exchange_owner(local_scores: torch.Tensor, local_ids: torch.Tensor,
+                   local_count: torch.Tensor, group=None):
+    """Owner-partitioned exchange with static sizes (the default): every rank sends each
+    query's local list to the rank owning the query (``query_owner_slices``) in ONE
+    ``all_to_all_single`` of a packed [B, 3k + 1] int32 payload (ids as two int32 words,
+    scores, count). All split sizes follow from (B, world), so there is no device->host
+    synchronisation and the step can be captured in a CUDA graph. Per rank the traffic is
+    B * k pairs (the all-gather moves (world - 1) * B * k).
+
+    Returns (q0, q1, scores [world, q1-q0, k], ids [...], counts [world, q1-q0])."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    B, k = local_scores.shape
+    payload = torch.cat([local_ids.contiguous().view(torch.int32).view(B, 2 * k),
+                         local_scores.to(torch.int32), local_count.to(torch.int32).view(B, 1)],
+                        dim=1)
+    slices = query_owner_slices(B, world)
+    q0, q1 = slices[rank]
+    nq = q1 - q0
+    recv = torch.empty((world * nq, 3 * k + 1), dtype=torch.int32, device=payload.device)
+    dist.all_to_all_single(recv, payload, output_split_sizes=[nq] * world,
+                           input_split_sizes=[b - a for a, b in slices], group=group)
+    recv = recv.view(world, nq, 3 * k + 1)
+    ids = recv[:, :, : 2 * k].contiguous().view(torch.int64).view(world, nq, k)
+    scores = recv[:, :, 2 * k: 3 * k].contiguous()
+    count = recv[:, :, 3 * k].contiguous()
+    return q0, q1, scores, ids, count
 
 
 def exchange_pruned(local_scores: torch.Tensor, local_ids: torch.Tensor,
@@ -148,14 +186,17 @@ class ShardedSearch:
     op: TopkOp
     group: object = None
     merge: object = None  # injectable merge (tests on CPU/gloo); default: fb_merge_topk
-    exchange: str = "all_gather"  # or "pruned": owner-partitioned, see exchange_pruned
+    exchange: str = "owner"  # "owner" (exchange_owner), "pruned" or "all_gather"
 
     def __call__(self, queries_q: torch.Tensor, filters=None, k: int | None = None) -> TopkOutput:
         """Global top-k: every query on every rank ("all_gather"), or with ``exchange=
-        "pruned"`` the rows of this rank's query slice (``query_owner_slices``)."""
+        "owner"`` / ``"pruned"`` the rows of this rank's query slice (``query_owner_slices``)."""
         local = self.op(queries_q, filters)
         k = self.op.k if k is None else k
         merge = self.merge or merge_topk
+        if self.exchange == "owner":
+            _, _, s, i, c = exchange_owner(local.scores, local.ids, local.count, self.group)
+            return merge(s, i, c, k)
         if self.exchange == "pruned":
             _, _, s, i, c = exchange_pruned(local.scores, local.ids, local.count, k, self.group)
             return merge(s, i, c, k)
@@ -163,5 +204,5 @@ class ShardedSearch:
         return merge(s, i, c, k)
 
 
-__all__ = ["_reduce_topk", "shard_ranges", "exchange_topk", "exchange_pruned",
+__all__ = ["_reduce_topk", "shard_ranges", "exchange_topk", "exchange_owner", "exchange_pruned",
            "query_owner_slices", "ShardedSearch", "DeviceIndex"]

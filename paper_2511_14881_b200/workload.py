@@ -94,10 +94,21 @@ def four_attribute_filter(rng: np.random.Generator, sizes=FOUR_ATTR_SIZES, spec=
 
 def make_workload(n_items: int, n_queries: int, dim: int = 128, seed: int = 1,
                   filter_seed: int = 7, filter_sizes=FOUR_ATTR_SIZES, filtered: bool = True,
-                  params: BloomParams = BloomParams()) -> Workload:
+                  params: BloomParams = BloomParams(), id_base: int = 0,
+                  reduce_minmax=None, share_queries=None) -> Workload:
+    """One shard of the synthetic catalogue.
+
+    Sharded use: ``reduce_minmax(lo, hi) -> (lo, hi)`` turns the
+    shard's min/max into the catalogue's (e.g. an all-reduce MIN/MAX), so every shard
+    quantises with ONE global ``QuantParams``; ``id_base`` offsets this shard's item ids
+    (global ids are fixed before the device index derives its rank tables);
+    ``share_queries(q) -> q`` replaces the float queries (e.g. a broadcast from rank 0)
+    before they are quantised."""
     dev = torch.device("cuda", torch.cuda.current_device())
     emb = make_items(n_items, dim, seed, dev)
     lo, hi = float(emb.min()), float(emb.max())
+    if reduce_minmax is not None:
+        lo, hi = reduce_minmax(lo, hi)
     qp = QuantParams(lo, hi)
     dim_pad = (dim + 31) // 32 * 32
     n_pad = (n_items + 255) // 256 * 256  # whole 256-slot tensor-core tiles
@@ -112,6 +123,8 @@ def make_workload(n_items: int, n_queries: int, dim: int = 128, seed: int = 1,
     rows = torch.randint(0, n_items, (n_queries,), generator=g, device=dev)
     queries = emb[rows] + torch.randn((n_queries, dim), generator=g, device=dev) * 0.05
     queries = queries.float().contiguous()
+    if share_queries is not None:
+        queries = share_queries(queries).float().contiguous()
     del emb
     # validity: all real items; padding cleared
     n_words = n_pad // 64
@@ -120,7 +133,7 @@ def make_workload(n_items: int, n_queries: int, dim: int = 128, seed: int = 1,
     rem = n_items % 64
     if rem:
         valid[n_items // 64] = (1 << rem) - 1
-    ids = torch.arange(n_pad, dtype=torch.int64, device=dev)
+    ids = torch.arange(n_pad, dtype=torch.int64, device=dev) + int(id_base)
     ids[n_items:] = 0
     rank = torch.arange(n_pad, dtype=torch.int32, device=dev)
     fid, val, slot = make_feature_pairs(n_items, seed, dev)

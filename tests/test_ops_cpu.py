@@ -1,0 +1,85 @@
+"""The custom-op boundary and the reference drop-in without a GPU: fake-tensor shapes of
+``torch.ops.filtra_b200.*``, the reference-type binding, and the integration installer."""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+from torch._subclasses.fake_tensor import FakeTensorMode
+
+ROOT = Path(__file__).resolve().parents[1]
+REF = ROOT / "baseline" / "_ref"
+
+
+def test_ops_registered_with_fake_kernels():
+    from paper_2511_14881_b200 import ops  # noqa: F401
+    for name in ("filtered_topk", "merge_topk", "quantize"):
+        assert hasattr(torch.ops.filtra_b200, name)
+    with FakeTensorMode():
+        q = torch.empty((8, 128), dtype=torch.int8, device="cuda")
+        ids, sc, cnt = torch.ops.filtra_b200.filtered_topk(1, q, 100, [], [], [], 0)
+        assert (ids.shape, ids.dtype, sc.dtype, cnt.shape) == ((8, 100), torch.int64,
+                                                               torch.int32, (8,))
+        x = torch.empty((8, 100), dtype=torch.float32, device="cuda")
+        assert torch.ops.filtra_b200.quantize(x, -1.0, 1.0, 128).shape == (8, 128)
+        s = torch.empty((4, 8, 50), dtype=torch.int32, device="cuda")
+        i = torch.empty((4, 8, 50), dtype=torch.int64, device="cuda")
+        c = torch.empty((4, 8), dtype=torch.int32, device="cuda")
+        out = torch.ops.filtra_b200.merge_topk(s, i, c, 70)
+        assert [tuple(t.shape) for t in out] == [(8, 70), (8, 70), (8,)]
+
+
+def test_filter_meta_round_trip():
+    import numpy as np
+    from paper_2511_14881_b200 import BloomParams, FilterBatch, compile_filter, workload
+    rng = np.random.default_rng(7)
+    cfs = [compile_filter(workload.four_attribute_filter(rng), BloomParams()) for _ in range(4)]
+    fb = FilterBatch.pack(cfs, BloomParams())
+    meta = fb.meta()
+    assert len(meta) == len(FilterBatch.META_FIELDS)
+    assert meta[0] == 4 and meta[8] == 1  # four queries, CNF form
+    with pytest.raises(ValueError):
+        FilterBatch.struct_from([torch.zeros(1)], meta)
+
+
+def _run(code: str, **env) -> str:
+    e = dict(os.environ, PYTHONPATH=os.pathsep.join([str(REF), str(ROOT)]), **env)
+    return subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True,
+                          check=True, cwd=ROOT).stdout
+
+
+@pytest.mark.skipif(not (REF / "filtra").is_dir(), reason="baseline/_ref not installed")
+def test_reference_types_bound_when_importable():
+    out = _run("import filtra, paper_2511_14881_b200 as fb;"
+               "print(fb.TopkResult is filtra.ivf.TopkResult,"
+               " fb.errors.DimMismatch is filtra.errors.DimMismatch,"
+               " fb.ScanStats is filtra.ivf.ScanStats, fb.FilterStats is filtra.bloom.FilterStats)")
+    assert out.split() == ["True"] * 4
+    out = _run("import filtra, paper_2511_14881_b200 as fb;"
+               "print(fb.TopkResult is filtra.ivf.TopkResult)", FB_REFERENCE_TYPES="0")
+    assert out.split() == ["False"]
+
+
+@pytest.mark.skipif(not (REF / "filtra").is_dir(), reason="baseline/_ref not installed")
+def test_integration_install_patches_every_binding():
+    out = _run(
+        "import filtra, filtra.ivf, filtra.retrieval, filtra.serve\n"
+        "from paper_2511_14881_b200 import integration, ivf, retrieval, serve\n"
+        "orig = filtra.ivf.search_clusters\n"
+        "rec = integration.install()\n"
+        "assert filtra.ivf.search_clusters is ivf.search_clusters\n"
+        "assert filtra.retrieval.search_clusters is ivf.search_clusters\n"
+        "assert filtra.retrieval.codesigned_search is retrieval.codesigned_search\n"
+        "assert filtra.serve._reduce_topk is serve._reduce_topk\n"
+        "names = {f for _, f, _ in integration.PATCHES}\n"
+        "patched = {a for _, a, _ in rec}\n"
+        "assert names <= patched, names - patched\n"
+        "integration.uninstall(rec)\n"
+        "assert filtra.ivf.search_clusters is orig\n"
+        "print('ok', len(rec))\n")
+    assert out.startswith("ok")
