@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -19,6 +21,19 @@ static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void debug_launch(const char* what) {
+  static const int on = [] {
+    const char* e = getenv("FB_DEBUG_LAUNCH");
+    return e != nullptr && atoi(e) != 0;
+  }();
+  if (!on) return;
+  fprintf(stderr, "[fb] launch %s\n", what);
+  fflush(stderr);
+  cudaError_t e = cudaDeviceSynchronize();
+  fprintf(stderr, "[fb]   done %s: %s\n", what, cudaGetErrorString(e));
+  fflush(stderr);
+}
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int code, const std::string& msg) {
@@ -63,6 +78,7 @@ struct fb_topk_plan {
   Fallback* d_fb = nullptr;
   uint32_t* d_hist = nullptr;
   uint32_t* d_active = nullptr;  // [0] flagged & unresolved, [1] resolved, [2] total flagged
+  uint32_t* d_qrec = nullptr;    // [B, 12] CNF window records (emit kernel scratch)
   int32_t* d_tc_work = nullptr;  // (tile, range) pairs for the tensor-core scan
   int64_t n_tc_work = 0;
   int64_t tc_sample_stride = 0;
@@ -311,6 +327,7 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
   const size_t o_hist = carve(sizeof(uint32_t) * B * kHistBins);
   const size_t o_active = carve(sizeof(uint32_t) * 4);
   const size_t o_tc = carve(sizeof(int32_t) * std::max<size_t>(2, tc_work.size()));
+  const size_t o_qrec = carve(sizeof(uint32_t) * 12 * B);
   cudaError_t e = cudaMalloc(&p->dev, off);
   if (e != cudaSuccess) {
     delete p;
@@ -331,6 +348,7 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
   p->d_hist = reinterpret_cast<uint32_t*>(base + o_hist);
   p->d_active = reinterpret_cast<uint32_t*>(base + o_active);
   p->d_tc_work = reinterpret_cast<int32_t*>(base + o_tc);
+  p->d_qrec = reinterpret_cast<uint32_t*>(base + o_qrec);
   if (p->n_ranges > 0) {
     e = cudaMemcpy(p->d_ranges, p->h_ranges.data(), sizeof(int64_t) * p->h_ranges.size(),
                    cudaMemcpyHostToDevice);
@@ -411,6 +429,7 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
   a.active_count = nullptr;
   a.tc_work = p->d_tc_work;
   a.n_tc_work = p->n_tc_work;
+  a.tc_qrec = p->d_qrec;
   a.mode = SCAN_EMIT;
   const bool use_tc = !(p->flags & FB_PLAN_SIMT) && p->n_tc_work > 0 && scan_tc_supported(a);
   p->last_scan_tc = use_tc ? 1 : 0;

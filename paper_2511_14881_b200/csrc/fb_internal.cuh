@@ -1,6 +1,7 @@
 // Internal declarations shared by the filtra_b200 translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -24,10 +25,13 @@ int cuda_fail(cudaError_t e, const char* what);
   } while (0)
 
 void count_launch();
+// FB_DEBUG_LAUNCH=1: print every launch's name and synchronise after it (hang triage)
+void debug_launch(const char* what);
 
 #define FB_LAUNCH_CHECK(what)                           \
   do {                                                  \
     ::fb::count_launch();                               \
+    ::fb::debug_launch(what);                           \
     cudaError_t e_ = cudaGetLastError();                \
     if (e_ != cudaSuccess) return ::fb::cuda_fail(e_, what); \
   } while (0)
@@ -132,6 +136,7 @@ struct ScanArgs {
   int32_t dense;              // threshold 0 everywhere (sampling): word-level filter is cheaper
   int32_t* dump;              // testing: raw scores [B, dump_ld] (nullable)
   int64_t dump_ld;
+  uint32_t* tc_qrec;          // [B, 12] scratch: CNF window records (fb_emit_kernel.cu)
 };
 
 // IVF-probed scan: per (query, probed cluster) pair, every eligible slot's key
@@ -179,6 +184,9 @@ int launch_row_sums(const int8_t* x, int64_t rows, int cols, int stride, int32_t
 // its envelope (the caller then uses the SIMT kernel)
 int launch_scan_tc(const ScanArgs& a, cudaStream_t s);
 bool scan_tc_supported(const ScanArgs& a);
+// the window-form CNF emit kernel (fb_emit_kernel.cu), dispatched by launch_scan_tc
+bool emit_win_supported(const ScanArgs& a);
+int launch_emit_win(const ScanArgs& a, const CUtensorMap& tmap, int grid, cudaStream_t s);
 
 struct SelectArgs {
   int32_t n_queries;

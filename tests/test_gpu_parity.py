@@ -399,8 +399,8 @@ def test_pipelined_topk_matches_batched_op(fb, wl_small):
     pipe = fb.PipelinedTopk(idx, 24, k, filters_template=wl.filters)
     hq = wl.queries.cpu().pin_memory()
     hq2 = (wl.queries.flip(0)).cpu().pin_memory()
-    h_prog = [torch.from_numpy(x).pin_memory() for x in pipe.slots[0]["batch"].host_arrays()]
-    tickets = [pipe.submit(hq if t % 2 == 0 else hq2, h_prog) for t in range(2)]
+    h_batch = fb.FilterBatch.pack(wl.filters, fb.BloomParams()).pin()
+    tickets = [pipe.submit(hq if t % 2 == 0 else hq2, h_batch) for t in range(2)]
     for t in tickets:
         ids, sc, cnt = pipe.result(t)
         src = hq if t % 2 == 0 else hq2

@@ -3,6 +3,7 @@ instructions / stall samples per CUDA source line (the ncu CUDA view of our capt
 carries no metrics).
 
     python tools/sass_lines.py ncu_sass.csv disasm.sass <mangled-kernel-substring> [--top N]
+                               [--inner] [--src paper_2511_14881_b200/csrc/<file>.cu]
 """
 import csv
 import re
@@ -53,7 +54,9 @@ def main():
         ex[ln] += float(r[iex] or 0)
         sm[ln] += float(r[ism] or 0)
     te, ts = sum(ex.values()), sum(sm.values())
-    src = open("paper_2511_14881_b200/csrc/fb_tc_kernel.cu").read().split("\n")
+    path = (sys.argv[sys.argv.index("--src") + 1] if "--src" in sys.argv
+            else "paper_2511_14881_b200/csrc/fb_tc_kernel.cu")
+    src = open(path).read().split("\n")
     keys = sorted(ex, key=lambda k: -(ex[k] / te + sm[k] / ts))[:top]
     for k in keys:
         n = int(k.split("<")[0]) if k not in ("?", None) else 0
