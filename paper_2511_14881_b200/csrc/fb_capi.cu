@@ -484,6 +484,10 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
     ea.out_slot = select_by_rank(p->cap, k, p->idx.slot_of_rank) ? nullptr : p->d_cand_slot;
     ea.out_cnt = p->d_cnt;
     ea.out_elig = p->d_elig;
+    if (p->sample_stride && use_tc) {
+      ea.sample_cnt = p->d_sample_cnt;
+      ea.sampled_slots = p->tc_sample_fraction * (double)p->total_slots;
+    }
     rc = emit(ea);
     if (rc) return rc;
     if (p->timing) FB_CUDA(cudaEventRecord(p->ev[1], s));

@@ -137,6 +137,10 @@ struct ScanArgs {
   int32_t* dump;              // testing: raw scores [B, dump_ld] (nullable)
   int64_t dump_ld;
   uint32_t* tc_qrec;          // [B, 12] scratch: CNF window records (fb_emit_kernel.cu)
+  // eligible keys per query seen by the sampling pass and the slots it sampled: the emit
+  // pass of a CNF window batch goes filter-first when the batch's sampled eligibility is low
+  const uint32_t* sample_cnt; // [B] (nullable: no sampling pass)
+  double sampled_slots;
 };
 
 // IVF-probed scan: per (query, probed cluster) pair, every eligible slot's key

@@ -85,6 +85,10 @@ struct TcArgs {
   int32_t cnf_words;
   int32_t cnf_gmax;
   int32_t tb_stride;
+  int32_t ffirst;     // CNF window form, filter first: 1 always, 0 never, -1 when the sampled
+                      // eligibility of the batch is below ff_limit (see k_scan_cnf)
+  const uint32_t* sample_cnt;  // [nq] eligible sampled keys per query (nullable)
+  float ff_limit;              // sum of sample_cnt under which the batch goes filter-first
   int32_t dbg;        // timing experiments only (FB_SCAN_DEBUG): bit 0 no plane copies,
                       // bit 1 no hit work, bit 2 no column builds, bit 3 no dense work,
                       // bit 7 no gate arm, bit 8 no TMEM drain,
@@ -435,7 +439,7 @@ constexpr int kNbLeafCount = 32 * (kCnfBuilders + kCnfHitWarps);
 // ================= CNF column builders (nb warps): Bloom test per literal column, then a
 // 32x32 bit transpose so each item row holds its column bits ==========================
 __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m, int lw, int nb,
-                                                 int lane) {
+                                                 int lane, bool ff) {
   uint8_t* sP = m.sP;
   uint8_t* sL = m.sL;
   const int16_t* sLS = m.sLS;
@@ -478,6 +482,16 @@ __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m,
 #pragma unroll
             for (int ib = 0; ib < 8; ++ib) m[ib] = ~m[ib];
           }
+        }
+        if (ff) {  // filter-first: the column's 256 tile bits, column-major
+          const uint32_t cw = su32(TB) + (uint32_t)col * 32u;
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(cw), "r"(m[0]), "r"(m[1]),
+                       "r"(m[2]), "r"(m[3])
+                       : "memory");
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(cw + 16u), "r"(m[4]),
+                       "r"(m[5]), "r"(m[6]), "r"(m[7])
+                       : "memory");
+          continue;
         }
         // eight 32x32 transposes in lockstep (independent shuffles per round)
         const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
@@ -842,9 +856,27 @@ __device__ __forceinline__ void drain_survivors(const TcArgs& a, const Smem& m, 
   }
 }
 
-template <bool kWin>
+// kMode: 0 general CNF form; 1 window form. A window-form launch runs one of two hit passes,
+// chosen per launch from the sampling pass (uniform across CTAs):
+//  * per hit: each gate hit is tested on the item's item-major column bits;
+//  * filter first (low-selectivity batches, where the score gate admits ~k / selectivity hits
+//    per query): the builders leave column-major column words, each hit warp lane builds its
+//    query's eligibility words AND_g OR_{c in S_qg} col_c for the tile's eight chunks and ANDs
+//    them into the hit words, so only eligible hits reach the exact test.
+template <int kMode>
 __global__ void __launch_bounds__(kCnfThreads, 1)
     k_scan_cnf(const __grid_constant__ CUtensorMap tmap_items, const TcArgs a) {
+  constexpr bool kWin = kMode != 0;
+  constexpr bool ff = kMode == 2;
+  if (kWin && a.ffirst < 0) {
+    // both window-form instances are launched; the one the sampled eligibility does not pick
+    // returns at once (uniform across CTAs: every CTA sums the same counts)
+    float sum = 0.f;
+    for (int q = threadIdx.x & 31; q < a.nq; q += 32) sum += (float)a.sample_cnt[q];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+    if ((sum < a.ff_limit) != ff) return;
+  }
   constexpr int NT = kCnfThreads;
   const Smem m = carve(a);
   uint8_t* smem = m.base;
@@ -914,7 +946,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
   } else if (warp == 2) {
     producer_loop(a, &tmap_items, m, lane, false, true);
   } else if (warp < kCnfDense0) {
-    cnf_builder_loop(a, m, warp - 3, kCnfBuilders, lane);
+    cnf_builder_loop(a, m, warp - 3, kCnfBuilders, lane, ff);
   } else if (warp < kCnfHit0) {
     // ================= dense pass (one warp per TMEM lane quadrant) ======================
     const int quad = warp & 3;
@@ -1046,13 +1078,52 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
       const uint32_t hmap = hm_s + (uint32_t)hb * kHmapBytes + 4u * (uint32_t)q;
       // this query's nonzero chunk words
       uint32_t nzm = 0u;
+      uint32_t fw[8];  // filter-first: eligibility words of the tile's eight chunks
+#pragma unroll
+      for (int c = 0; c < 8; ++c) fw[c] = ~0u;
+      if (ff && qok && !nof && !(a.dbg & 2)) {
+        // AND over the query's groups of the OR of its literal columns (window form: group g's
+        // columns are 8 * wo[g] + j, j < 64, flagged in lo / hi)
+        const uint32_t cw0 = tb_s;
+        for (int g = 0; g < ng && g < 4; ++g) {
+          uint32_t acc[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[c] = 0u;
+          const uint32_t glo = g == 0 ? lo[0] : g == 1 ? lo[1] : g == 2 ? lo[2] : lo[3];
+          const uint32_t ghi = g == 0 ? hi[0] : g == 1 ? hi[1] : g == 2 ? hi[2] : hi[3];
+          const uint32_t gwo = g == 0 ? wo[0] : g == 1 ? wo[1] : g == 2 ? wo[2] : wo[3];
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            uint32_t x = half ? ghi : glo;
+            const uint32_t cbase = cw0 + (8u * gwo + 32u * (uint32_t)half) * 32u;
+            while (x != 0u) {
+              const uint32_t j = (uint32_t)(__ffs(x) - 1);
+              x &= x - 1u;
+              const uint4 u0 = lds128(cbase + j * 32u), u1 = lds128(cbase + j * 32u + 16u);
+              acc[0] |= u0.x; acc[1] |= u0.y; acc[2] |= u0.z; acc[3] |= u0.w;
+              acc[4] |= u1.x; acc[5] |= u1.y; acc[6] |= u1.z; acc[7] |= u1.w;
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) fw[c] &= acc[c];
+        }
+      }
+      uint32_t mw[8];
       if (qok && !(a.dbg & 2)) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          nzm |= (lds32(hmap + (uint32_t)c * (kMaxQueries * 4u)) != 0u ? 1u : 0u) << c;
+        for (int c = 0; c < 8; ++c) {
+          mw[c] = lds32(hmap + (uint32_t)c * (kMaxQueries * 4u)) & fw[c];
+          nzm |= (mw[c] != 0u ? 1u : 0u) << c;
+        }
       }
+      auto word_at = [&](int c) -> uint32_t {
+        if (ff)
+          return c < 4 ? (c < 2 ? (c == 0 ? mw[0] : mw[1]) : (c == 2 ? mw[2] : mw[3]))
+                       : (c < 6 ? (c == 4 ? mw[4] : mw[5]) : (c == 6 ? mw[6] : mw[7]));
+        return lds32(hmap + (uint32_t)c * (kMaxQueries * 4u));
+      };
       int cc = nzm ? __ffs(nzm) - 1 : 0;
-      uint32_t cur = nzm ? lds32(hmap + (uint32_t)cc * (kMaxQueries * 4u)) : 0u;
+      uint32_t cur = nzm ? word_at(cc) : 0u;
       uint32_t n_sv = 0;  // warp-uniform survivor count
       int n_rounds = 0;
       while (__any_sync(0xffffffffu, cur != 0u)) {
@@ -1065,7 +1136,9 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
           cur &= cur - 1u;
           item = (uint32_t)(cc * 32 + j);
           const uint32_t tb = tb_s + item * (uint32_t)a.tb_stride * 4u;
-          if (kWin)
+          if (ff)
+            surv = true;  // eligibility already applied
+          else if (kWin)
             surv = nof || cnf_test_win(tb, wo, lo, hi);
           else
             surv = cnf_test_global(tb, qmg, ng, a.cnf_words);
@@ -1073,7 +1146,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
             nzm &= nzm - 1u;
             if (nzm) {
               cc = __ffs(nzm) - 1;
-              cur = lds32(hmap + (uint32_t)cc * (kMaxQueries * 4u));
+              cur = word_at(cc);
             }
           }
         }
@@ -1254,6 +1327,13 @@ int launch_kernel(K kernel, int threads, const CUtensorMap& tmap, const TcArgs& 
   return FB_OK;
 }
 
+// window form, mode chosen on the device from the sampling pass: per-hit and filter-first
+// instances back to back, the one not chosen returns at its first instruction
+int launch_both(const TcArgs& t, const CUtensorMap& tmap, int grid, size_t smem, cudaStream_t s) {
+  const int rc = launch_kernel(k_scan_cnf<1>, kCnfThreads, tmap, t, grid, smem, s);
+  return rc ? rc : launch_kernel(k_scan_cnf<2>, kCnfThreads, tmap, t, grid, smem, s);
+}
+
 }  // namespace
 
 bool scan_tc_supported(const ScanArgs& a) {
@@ -1329,13 +1409,24 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
     t.dump = a.dump ? a.dump + (int64_t)q0 * a.dump_ld : nullptr;
     t.dump_ld = a.dump_ld;
     if (const char* d = getenv("FB_SCAN_DEBUG")) t.dbg = atoi(d);
+    // filter-first below ~3 % sampled eligibility (config-4 sweep: it wins at 1 and 2 %, the
+    // per-hit pass at 5 % and above); FB_CNF_FFIRST = 0 / 1 forces either, _FRAC moves the cut
+    t.ffirst = cnf == 1 ? -1 : 0;
+    if (const char* f = getenv("FB_CNF_FFIRST")) t.ffirst = cnf == 1 ? atoi(f) : 0;
+    double ff_frac = 0.03;
+    if (const char* f = getenv("FB_CNF_FFIRST_FRAC")) ff_frac = atof(f);
+    t.sample_cnt = a.sample_cnt ? a.sample_cnt + q0 : nullptr;
+    t.ff_limit = (float)(ff_frac * a.sampled_slots * (double)nq);
+    if (t.ffirst < 0 && t.sample_cnt == nullptr) t.ffirst = 0;
     size_t smem = 0;
     if (!pick_stages(t, t.n_mblk, t.has_prog ? t.n_planes : 0, t.has_prog ? t.n_leaves : 0,
                      t.has_prog ? t.k_max : 0, t.has_prog ? a.prog.n_rops : 0, cnf, smem))
       return FB_ERR_UNSUPPORTED;
     const int rc =
-        cnf == 1   ? launch_kernel(k_scan_cnf<true>, kCnfThreads, tmap, t, grid, smem, s)
-        : cnf == 2 ? launch_kernel(k_scan_cnf<false>, kCnfThreads, tmap, t, grid, smem, s)
+        cnf == 1 && t.ffirst > 0 ? launch_kernel(k_scan_cnf<2>, kCnfThreads, tmap, t, grid, smem, s)
+        : cnf == 1 && t.ffirst == 0 ? launch_kernel(k_scan_cnf<1>, kCnfThreads, tmap, t, grid, smem, s)
+        : cnf == 1 ? launch_both(t, tmap, grid, smem, s)
+        : cnf == 2 ? launch_kernel(k_scan_cnf<0>, kCnfThreads, tmap, t, grid, smem, s)
                    : launch_kernel(k_scan_tc, kThreads, tmap, t, grid, smem, s);
     if (rc) return rc;
   }

@@ -126,3 +126,39 @@ def test_shuffled_ids_tiebreak(cuda):
                            qp=idx.qp)
     out = run_op(wl, 3000)
     check_rows(out, oracle_answers(wl, 3000, range(0, 32, 3)))
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_filter_first_and_per_hit_modes_agree(cuda, monkeypatch, mode):
+    """The window-form emit pass has two hit passes (per-hit test on item-major column bits,
+    and filter-first eligibility words); the device picks one from the sampled eligibility.
+    Forcing either must give the oracle's rows, at the benchmark's ~10 % selectivity and with
+    explicit masks and ranges."""
+    from paper_2511_14881_b200 import _device, workload
+    from paper_2511_14881_b200.engine import TopkOp
+    monkeypatch.setenv("FB_CNF_FFIRST", mode)
+    wl = workload.make_workload(300_000, 40, seed=6)
+    out = run_op(wl, 2000)
+    check_rows(out, oracle_answers(wl, 2000, range(0, 40, 3)))
+    # ranges + explicit masks through the same kernel
+    idx = wl.index
+    rng = np.random.default_rng(5)
+    ranges = np.array([[0, 64 * 700], [64 * 1500, 64 * 4000]])
+    op = TopkOp(idx, 40, 700, ranges)
+    m = rng.integers(0, 2**63, size=(40, idx.n_words), dtype=np.int64)
+    masks = torch.from_numpy(m).cuda()
+    got = op(wl.queries_q, wl.batch.to_device(), masks=masks)
+    torch.cuda.synchronize()
+    from oracle import filtra_oracle as orc
+    items = idx.items.cpu().numpy()[:, : wl.dim]
+    valid, ids = _device.u64_host(idx.valid), _device.u64_host(idx.item_ids)
+    qq = wl.queries_q.cpu().numpy()[:, : wl.dim]
+    for q in (0, 13, 39):
+        cf = wl.filters[q]
+        prog = ([(int(o), int(a)) for o, a in cf.ops], [(f, v, qb.set_bits) for f, v, qb in cf.leaves])
+        full = orc.eval_compiled(prog[0], prog[1], idx.bloom.planes, valid)
+        keep = full & m[q].view(np.uint64)
+        ref = orc.search_clusters(items, valid, ids, ranges, qq[q], range(len(ranges)), keep, 700)
+        n = int(got.count[q])
+        assert np.array_equal(_device.u64_host(got.ids[q, :n]), ref.item_ids), q
+        assert np.array_equal(got.scores[q, :n].cpu().numpy(), ref.scores), q
