@@ -18,6 +18,9 @@
  *                            filter program this is retrieval.codesigned_search      (ivf.py:272-334, retrieval.py:110-144)
  *   fb_merge_topk         <- serve._reduce_topk over the per-shard results           (serve.py:98-121)
  *   fb_dequant_scores     <- quantize.dequantize applied to both operands of the dot (quantize.py:79-81)
+ *   fb_pack_text /
+ *   fb_pack_postfix       <- filter_query.parse_filter + compile_filter for a whole batch,
+ *                            plus the device-form packing (filter_query.py:82-189, 280-311)
  */
 #ifndef FILTRA_B200_H
 #define FILTRA_B200_H
@@ -29,7 +32,7 @@
 extern "C" {
 #endif
 
-#define FB_ABI_VERSION 3
+#define FB_ABI_VERSION 4
 
 enum fb_status {
   FB_OK = 0,
@@ -39,7 +42,10 @@ enum fb_status {
   FB_ERR_DEGENERATE = 4,       /* errors.DegenerateRange */
   FB_ERR_CUDA = 5,             /* CUDA runtime failure */
   FB_ERR_UNSUPPORTED = 6,      /* outside this build's limits (documented per call) */
-  FB_ERR_NO_DEVICE = 7         /* no sm_100 device */
+  FB_ERR_NO_DEVICE = 7,        /* no sm_100 device */
+  FB_ERR_PARSE = 8             /* filter text not accepted: the caller re-parses it with the
+                                  reference grammar to raise FilterSyntaxError / UnknownFeature /
+                                  UnknownValue with the reference's message */
 };
 
 /* Opcodes of the postfix filter program (filter_query.OpCode, filter_query.py:253-257). */
@@ -84,7 +90,7 @@ typedef struct fb_index {
 /*
  * A batch of compiled filters (filter_query.CompiledFilter, one per query), with the
  * leaves de-duplicated across the batch. All arrays are device pointers.
- *   leaf_pos   i16 [n_leaves * k_max]  plane indices per leaf, ascending, -1 padded
+ *   leaf_pos   i32 [n_leaves * k_max]  plane indices per leaf, ascending, -1 padded
  *   op_offset  i32 [n_queries + 1]     query q's ops are ops[op_offset[q] .. op_offset[q+1])
  *   ops        u16 [...]               (opcode << 14) | leaf index
  * A query with zero ops is unfiltered (mask = validity).
@@ -94,7 +100,7 @@ typedef struct fb_filter_prog {
   int32_t n_leaves;
   int32_t k_max;
   int32_t max_stack;
-  const int16_t* leaf_pos;
+  const int32_t* leaf_pos;
   const int32_t* op_offset;
   const uint16_t* ops;
   /* Register-machine form consumed by the tensor-core scan (all nullable; when absent
@@ -105,7 +111,7 @@ typedef struct fb_filter_prog {
   int32_t rmax_stack;
   int32_t n_rops;              /* total rops (multiple of FB_ROP_ALIGN) */
   int32_t reserved;
-  const int16_t* plane_list;   /* [n_planes] */
+  const int32_t* plane_list;   /* [n_planes] plane ids (any m_bits) */
   const int16_t* leaf_slot;    /* [n_leaves * k_max] */
   const int32_t* rop_offset;   /* [n_queries + 1] */
   const uint16_t* rops;
@@ -324,6 +330,60 @@ int fb_kmeans_assign(const double* data, int64_t n, int32_t dim, const double* c
 int fb_kmeans_means(const double* data, int32_t dim, const int64_t* order,
                     const int64_t* seg_start, const int64_t* seg_count, int32_t k,
                     double* centers, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Host: batch filter compilation + packing (C++, no device work). The output arrays are
+ * exactly the fb_filter_prog_t device form (upload them, then fill the struct from
+ * fb_pack_meta / fb_pack_array) plus per-query push-bit counts (FilterStats.words_read).
+ * Leaf positions are cached per (fid, value, M, K) across calls (bounded, thread-safe).
+ * ------------------------------------------------------------------------------------- */
+typedef struct fb_vocab fb_vocab_t;
+typedef struct fb_pack fb_pack_t;
+
+enum fb_pack_meta_id {
+  FB_PACK_N_QUERIES = 0, FB_PACK_N_LEAVES = 1, FB_PACK_K_MAX = 2, FB_PACK_MAX_STACK = 3,
+  FB_PACK_HAS_ROPS = 4, FB_PACK_N_PLANES = 5, FB_PACK_RMAX_STACK = 6, FB_PACK_N_ROPS = 7,
+  FB_PACK_IS_CNF = 8, FB_PACK_N_COLS = 9, FB_PACK_CNF_WORDS = 10, FB_PACK_CNF_GMAX = 11,
+  FB_PACK_CNF_WINDOWED = 12, FB_PACK_DISTINCT_LEAVES = 13, FB_PACK_DISTINCT_PLANES = 14,
+  FB_PACK_META_N = 16
+};
+enum fb_pack_array_id {
+  FB_PACK_LEAF_POS = 0,    /* i32 [n_leaves * k_max] */
+  FB_PACK_OP_OFFSET = 1,   /* i32 [n_queries + 1] */
+  FB_PACK_OPS = 2,         /* u16 */
+  FB_PACK_PLANE_LIST = 3,  /* i32 [n_planes]            (has_rops) */
+  FB_PACK_LEAF_SLOT = 4,   /* i16 [n_leaves * k_max]    (has_rops) */
+  FB_PACK_ROP_OFFSET = 5,  /* i32 [n_queries + 1]       (has_rops) */
+  FB_PACK_ROPS = 6,        /* u16 [n_rops]              (has_rops) */
+  FB_PACK_COL_LEAF = 7,    /* i16 [n_cols]              (is_cnf) */
+  FB_PACK_QMASK = 8,       /* u32 [n_queries][gmax][words] (is_cnf) */
+  FB_PACK_QGROUPS = 9,     /* i32 [n_queries]           (is_cnf) */
+  FB_PACK_PUSH_BITS = 10,  /* i64 [n_queries] sum of |positions| over the query's pushes */
+  FB_PACK_LEAF_FID = 11,   /* u64 [distinct leaves] */
+  FB_PACK_LEAF_VAL = 12    /* u64 [distinct leaves] */
+};
+
+/* Host: name dictionaries of filter_query.Vocabulary (feature name -> id, value -> id). */
+int fb_vocab_create(int32_t n_feat, const char* const* feat_names, const uint64_t* feat_ids,
+                    int32_t n_vals, const char* const* val_names, const uint64_t* val_ids,
+                    fb_vocab_t** out);
+void fb_vocab_free(fb_vocab_t* vocab);
+
+/* Host: parse + compile + pack one filter text per query (NULL or "" = unfiltered), the
+ * grammar of filter_query.parse_filter (filter_query.py:82-189). FB_ERR_PARSE sets
+ * *bad_query. */
+int fb_pack_text(int32_t n_queries, const char* const* texts, const fb_vocab_t* vocab,
+                 int32_t m_bits, int32_t k_hashes, fb_pack_t** out, int32_t* bad_query);
+
+/* Host: the same from postfix programs (CompiledFilter.ops with the leaves' (fid, value)
+ * inlined): query q's ops are [op_offset[q], op_offset[q+1]) (empty = unfiltered). */
+int fb_pack_postfix(int32_t n_queries, const int64_t* op_offset, const uint8_t* opcode,
+                    const uint64_t* fid, const uint64_t* value, int32_t m_bits,
+                    int32_t k_hashes, fb_pack_t** out);
+
+int fb_pack_meta(const fb_pack_t* pack, int64_t* meta /* [FB_PACK_META_N] */);
+int fb_pack_array(const fb_pack_t* pack, int32_t which, const void** data, int64_t* n_elems);
+void fb_pack_free(fb_pack_t* pack);
 
 #ifdef __cplusplus
 }

@@ -30,6 +30,7 @@ FB_ERR_DEGENERATE = 4
 FB_ERR_CUDA = 5
 FB_ERR_UNSUPPORTED = 6
 FB_ERR_NO_DEVICE = 7
+FB_ERR_PARSE = 8
 
 FB_PLAN_FORCE_FALLBACK = 1
 FB_PLAN_SIMT = 2
@@ -48,11 +49,12 @@ EXPORTED = (
     "fb_topk_set_timing", "fb_topk_last_timing", "fb_topk_scan_path", "fb_debug_tc_scores",
     "fb_task_dots_f64", "fb_kmeans_min_sqdist", "fb_pairwise_sum_scratch",
     "fb_pairwise_sum_f64", "fb_kmeans_draw", "fb_row_sqnorm_f64", "fb_kmeans_assign",
-    "fb_kmeans_means", "fb_ivf_topk", "fb_merge_union",
+    "fb_kmeans_means", "fb_ivf_topk", "fb_merge_union", "fb_vocab_create", "fb_vocab_free",
+    "fb_pack_text", "fb_pack_postfix", "fb_pack_meta", "fb_pack_array", "fb_pack_free",
 )
 
 
-ABI_VERSION = 3  # include/filtra_b200.h FB_ABI_VERSION
+ABI_VERSION = 4  # include/filtra_b200.h FB_ABI_VERSION
 
 
 class FbIndex(ctypes.Structure):
@@ -151,6 +153,13 @@ def _declare(lib) -> None:
         "fb_merge_union": ([c_vp, c_vp, i32, i32, i32, i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
                            i32),
         "fb_launch_count": ([], ctypes.c_uint64),
+        "fb_vocab_create": ([i32, c_vp, c_vp, i32, c_vp, c_vp, c_vp], i32),
+        "fb_vocab_free": ([c_vp], None),
+        "fb_pack_text": ([i32, c_vp, c_vp, i32, i32, c_vp, c_vp], i32),
+        "fb_pack_postfix": ([i32, c_vp, c_vp, c_vp, c_vp, i32, i32, c_vp], i32),
+        "fb_pack_meta": ([c_vp, c_vp], i32),
+        "fb_pack_array": ([c_vp, i32, c_vp, c_vp], i32),
+        "fb_pack_free": ([c_vp], None),
         "fb_topk_scan_path": ([c_vp], i32),
         "fb_debug_tc_scores": ([ctypes.POINTER(FbIndex), c_vp, i32, c_vp, c_vp], i32),
         "fb_topk_set_timing": ([c_vp, i32], i32),
@@ -192,6 +201,8 @@ def check(rc: int) -> None:
         raise errors.DegenerateRange(msg)
     if rc == FB_ERR_UNSUPPORTED:
         raise NotImplementedError(msg)
+    if rc == FB_ERR_PARSE:
+        raise ValueError(msg)
     raise RuntimeError(f"filtra_b200 error {rc}: {msg}")
 
 

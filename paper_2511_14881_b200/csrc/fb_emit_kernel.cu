@@ -90,7 +90,7 @@ struct EmitArgs {
   int32_t n_cols;
   int32_t cnf_words;
   int32_t tb_stride;      // u32 per item row of the column-bit stage
-  const int16_t* plane_list;
+  const int32_t* plane_list;
   const int16_t* leaf_slot;
   const int16_t* col_leaf;
   const uint32_t* qrec;   // [nq][12]: lo[4], hi[4], window byte offsets (packed), unfiltered
@@ -226,7 +226,7 @@ __device__ __forceinline__ void planes_loop(const EmitArgs& a, uint32_t sb, int 
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int e = e0 + 32 * u;
-        pl[u] = e < n2 ? (int)lds16(pl_s + 2u * (uint32_t)(e >> 1)) : 0;
+        pl[u] = e < n2 ? (int)lds32(pl_s + 4u * (uint32_t)(e >> 1)) : 0;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* sT = reinterpret_cast<uint64_t*>(smem + a.off_thr);
     for (int q = threadIdx.x; q < kMaxQ; q += kThreads)
       sT[q] = (a.threshold != nullptr && q < a.nq) ? a.threshold[q] : 0ull;
-    int16_t* pl = reinterpret_cast<int16_t*>(smem + a.off_pl);
+    int32_t* pl = reinterpret_cast<int32_t*>(smem + a.off_pl);
     for (int i = threadIdx.x; i < a.n_planes; i += kThreads) pl[i] = a.plane_list[i];
     // column -> 8 plane-row byte offsets in a plane stage (negated literal: bit 15 of entry
     // 0; missing positions, and the padding column n_cols, point at the all-ones row)
@@ -742,7 +742,7 @@ size_t layout(EmitArgs& t, int plane_stages) {
   t.off_bar = (uint32_t)align_up(off, 16);
   off = t.off_bar + kBarCount * 8;
   t.off_pl = (uint32_t)align_up(off, 16);
-  off = t.off_pl + (size_t)(t.n_planes > 0 ? t.n_planes : 1) * 2;
+  off = t.off_pl + (size_t)(t.n_planes > 0 ? t.n_planes : 1) * 4;
   t.off_gate = (uint32_t)align_up(off, 128);
   off = t.off_gate + kGateBytes + 256;
   t.off_list = (uint32_t)align_up(off, 16);

@@ -50,7 +50,7 @@ __global__ void k_bloom_build(const uint64_t* __restrict__ fid, const uint64_t* 
 // ------------------------------------------------------------------------------------
 // Filter program: postfix stack machine over one 64-slot word.
 // ------------------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t leaf_word(const int16_t* __restrict__ pos, int k_max,
+__device__ __forceinline__ uint64_t leaf_word(const int32_t* __restrict__ pos, int k_max,
                                               const uint64_t* __restrict__ planes, int64_t n_words,
                                               int64_t w) {
   uint64_t m = ~0ull;
@@ -570,7 +570,7 @@ constexpr int kIvfRing = 4;        // leaves whose plane loads are in flight ahe
 // and the pushed leaves' plane positions (padded with -1) in the same order.
 struct IvfProg {
   uint16_t ops[kIvfMaxOps];
-  int16_t pos[kIvfMaxPush * 8];
+  int32_t pos[kIvfMaxPush * 8];
   int n_ops, n_push, fast;
 };
 
@@ -668,8 +668,8 @@ __global__ void __launch_bounds__(kIvfThreads) k_ivf_scan(IvfScanArgs a) {
         if (o < n_ops && li < kIvfMaxPush) {
           P.ops[o] = push ? (uint16_t)((FB_OP_PUSH_LEAF << 14) | (li & 0x3FFF)) : (uint16_t)op;
           if (push) {
-            const int16_t* src = a.prog.leaf_pos + (int64_t)(op & 0x3FFF) * a.prog.k_max;
-            for (int j = 0; j < 8; ++j) P.pos[li * 8 + j] = j < a.prog.k_max && j < K ? src[j] : (int16_t)-1;
+            const int32_t* src = a.prog.leaf_pos + (int64_t)(op & 0x3FFF) * a.prog.k_max;
+            for (int j = 0; j < 8; ++j) P.pos[li * 8 + j] = j < a.prog.k_max && j < K ? src[j] : -1;
           }
         }
         n_push += __popc(bal);

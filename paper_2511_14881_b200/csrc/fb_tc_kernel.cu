@@ -62,7 +62,7 @@ struct TcArgs {
   int32_t n_planes;
   int32_t n_leaves;
   int32_t k_max;
-  const int16_t* plane_list;
+  const int32_t* plane_list;
   const int16_t* leaf_slot;
   const int32_t* rop_offset;
   const uint16_t* rops;
@@ -262,7 +262,7 @@ __device__ __forceinline__ void stage_queries(const TcArgs& a, const Smem& m, in
   }
   for (int q = threadIdx.x; q < kMaxQueries; q += nt)
     m.sT[q] = (a.threshold != nullptr && q < a.nq) ? a.threshold[q] : 0ull;
-  int16_t* pl = reinterpret_cast<int16_t*>(m.base + a.off_pl);
+  int32_t* pl = reinterpret_cast<int32_t*>(m.base + a.off_pl);
   for (int i = threadIdx.x; i < a.n_planes; i += nt) pl[i] = a.plane_list[i];
 }
 
@@ -355,7 +355,7 @@ __device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int e = e0 + 32 * u;
-            pl[u] = e < n2 ? (int)lds16(pl_s + 2u * (uint32_t)(e >> 1)) : 0;
+            pl[u] = e < n2 ? (int)lds32(pl_s + 4u * (uint32_t)(e >> 1)) : 0;
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
@@ -1249,7 +1249,7 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
   t.off_bar = (uint32_t)align_up(off, 16);
   off = t.off_bar + kBarCount * 8;
   t.off_pl = (uint32_t)align_up(off, 16);
-  off = t.off_pl + (size_t)(n_planes > 0 ? n_planes : 1) * 2;
+  off = t.off_pl + (size_t)(n_planes > 0 ? n_planes : 1) * 4;
   if (cnf) {
     t.off_hm = (uint32_t)align_up(off, 128);
     off = t.off_hm + 2ull * kHmapBytes;

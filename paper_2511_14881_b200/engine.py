@@ -415,7 +415,19 @@ class PipelinedTopk:
         self._n += 1
         self.copy_in.wait_event(s["comp"])       # the slot's inputs are no longer read
         if filters is not None and not self._same_shape(s["batch"], filters):
-            s["batch"] = filters.clone_host().to_device()  # other shape: the slot's own upload
+            # another shape (e.g. a fresh batch of request filters): new device arrays for
+            # the slot, allocated and filled on the copy stream from pinned staging so the
+            # host never waits for the scan in flight
+            fresh = filters.clone_host()
+            with torch.cuda.stream(self.copy_in):
+                dev = []
+                for h in filters.pin().pinned_arrays():
+                    d = torch.empty(h.shape, dtype=h.dtype, device=s["q"].device)
+                    d.copy_(h, non_blocking=True)
+                    d.record_stream(self.compute)
+                    dev.append(d)
+            fresh._dev = tuple(dev)
+            s["batch"] = fresh
             filters = None
         with torch.cuda.stream(self.copy_in):
             s["q"].copy_(host_queries, non_blocking=True)

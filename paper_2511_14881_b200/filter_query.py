@@ -4,12 +4,14 @@ Grammar and lowering follow the reference (filter_query.py:1-311): OR binds tigh
 than AND, NOT tightest; AND/OR children are chained pairwise in post-order; leaves
 are de-duplicated per filter. ``FilterBatch`` packs a batch of compiled filters
 into the device bytecode consumed by the fused scan (leaves de-duplicated across
-the whole batch, positions hashed in C). ``eval_compiled`` runs ``fb_filter_eval``.
+the whole batch); the packing -- and, for request texts, parsing and compilation -- runs in
+C++ (csrc/fb_pack.cpp). ``eval_compiled`` runs ``fb_filter_eval``.
 """
 
 from __future__ import annotations
 
 import copy
+import ctypes
 import re
 import threading
 from collections import OrderedDict
@@ -291,146 +293,99 @@ def _compile_filter(expr: FilterExpr, params: BloomParams) -> CompiledFilter:
     return cf
 
 
-# register-machine opcodes (include/filtra_b200.h fb_ropcode)
-ROP_PUSH, ROP_PUSHN, ROP_ANDL, ROP_ORL, ROP_ANDS, ROP_ORS, ROP_NOT, ROP_NOP = range(8)
-ROP_MAX_LEAVES = 1 << 13
-ROP_ALIGN = 8
+# --- batch device form (built by the C++ packer, csrc/fb_pack.cpp) ----------------------
+
+def _flat_program(cf: CompiledFilter):
+    """``cf`` as postfix arrays (opcode u8, leaf fid u64, leaf value u64), cached on the
+    (immutable) compiled filter."""
+    flat = cf.__dict__.get("_flat")
+    if flat is None:
+        codes = np.fromiter((int(o) for o, _ in cf.ops), dtype=np.uint8, count=len(cf.ops))
+        args = np.fromiter((int(a) for _, a in cf.ops), dtype=np.int64, count=len(cf.ops))
+        lf = np.array([int(l[0]) for l in cf.leaves] or [0], dtype=np.uint64)
+        lv = np.array([int(l[1]) for l in cf.leaves] or [0], dtype=np.uint64)
+        push = codes == OpCode.PUSH_LEAF
+        a = np.where(push, args, 0)
+        flat = (codes, np.where(push, lf[a], 0).astype(np.uint64),
+                np.where(push, lv[a], 0).astype(np.uint64))
+        object.__setattr__(cf, "_flat", flat)
+    return flat
 
 
-def lower_to_register_ops(ops: list[tuple[int, int]]) -> tuple[list[int], int]:
-    """Peephole-lower postfix ``(opcode, global_leaf)`` ops to the register machine the
-    tensor-core epilogue runs: ``PUSH l; AND`` -> ``ANDL l``, ``PUSH l; OR`` -> ``ORL l``,
-    ``PUSH l; NOT`` -> ``PUSHN l``. Returns (encoded u16 ops, max stack depth)."""
-    out: list[tuple[int, int]] = []
-    for op, leaf in ops:
-        if op == OpCode.PUSH_LEAF:
-            out.append((ROP_PUSH, leaf))
-        elif op == OpCode.NOT:
-            if out and out[-1][0] == ROP_PUSH:
-                out[-1] = (ROP_PUSHN, out[-1][1])
-            else:
-                out.append((ROP_NOT, 0))
-        else:
-            combine_leaf = ROP_ANDL if op == OpCode.AND else ROP_ORL
-            if out and out[-1][0] == ROP_PUSH and len(out) >= 2:
-                out[-1] = (combine_leaf, out[-1][1])
-            else:
-                out.append((ROP_ANDS if op == OpCode.AND else ROP_ORS, 0))
-    depth = peak = 0
-    for code, _ in out:
-        if code in (ROP_PUSH, ROP_PUSHN):
-            depth += 1
-        elif code in (ROP_ANDS, ROP_ORS):
-            depth -= 1
-        peak = max(peak, depth)
-    return [(c << 13) | l for c, l in out], peak
+_PACK_ARRAYS = ("leaf_pos", "op_offset", "ops", "plane_list", "leaf_slot", "rop_offset", "rops",
+                "col_leaf", "qmask", "qgroups", "push_leaf_bits")
+_PACK_DTYPES = (np.int32, np.int32, np.uint16, np.int32, np.int16, np.int32, np.uint16, np.int16,
+                np.uint32, np.int32, np.int64)
 
 
-CNF_MAX_WORDS = 8    # leaf columns per batch <= 256
-CNF_MAX_GROUPS = 8
+def _take_pack(handle) -> dict:
+    """FilterBatch kwargs from a ``fb_pack_t`` (arrays copied out, handle freed)."""
+    lib = _native.load_library()
+    try:
+        meta = (ctypes.c_int64 * 16)()
+        _native.check(lib.fb_pack_meta(handle, meta))
+        meta = list(meta)
+        arrs = {}
+        for which, (name, dt) in enumerate(zip(_PACK_ARRAYS, _PACK_DTYPES)):
+            data, n = ctypes.c_void_p(), ctypes.c_int64()
+            _native.check(lib.fb_pack_array(handle, which, ctypes.byref(data), ctypes.byref(n)))
+            if n.value == 0 or not data.value:
+                arrs[name] = np.zeros(0, dtype=dt)
+                continue
+            buf = (ctypes.c_char * (n.value * np.dtype(dt).itemsize)).from_address(data.value)
+            arrs[name] = np.frombuffer(buf, dtype=dt).copy()
+    finally:
+        lib.fb_pack_free(handle)
+    nq, rows, k_max, max_stack, has_rops = meta[0:5]
+    rmax, is_cnf, words, gmax, windowed = meta[6], meta[8], meta[10], meta[11], meta[12]
+    kw = dict(leaf_pos=arrs["leaf_pos"].reshape(rows, k_max), op_offset=arrs["op_offset"],
+              ops=arrs["ops"], max_stack=max_stack, push_leaf_bits=arrs["push_leaf_bits"])
+    if has_rops:
+        kw.update(plane_list=arrs["plane_list"], leaf_slot=arrs["leaf_slot"].reshape(rows, k_max),
+                  rop_offset=arrs["rop_offset"], rops=arrs["rops"], rmax_stack=rmax)
+    if is_cnf:
+        kw.update(col_leaf=arrs["col_leaf"], qmask=arrs["qmask"].reshape(nq, gmax, words),
+                  qgroups=arrs["qgroups"], cnf_words=words, cnf_gmax=gmax,
+                  cnf_windowed=windowed)
+    return kw
 
 
-def cnf_groups(ops: list[tuple[int, int]]):
-    """Conjunctive normal form of a postfix program over (global) leaves, or None.
+_VOCAB_LOCK = threading.Lock()
 
-    NOTs are pushed down to literals (De Morgan; exact for bitwise masks because the
-    result is ANDed with validity at the end), same-operator nodes are flattened, and the
-    result must be an AND of ORs of literals. Returns a list of groups, each a list of
-    ``(leaf, negated)`` literals."""
-    stack: list = []
-    for op, leaf in ops:
-        if op == OpCode.PUSH_LEAF:
-            stack.append(("lit", leaf, False))
-        elif op == OpCode.NOT:
-            stack.append(("not", stack.pop()))
-        else:
-            rhs = stack.pop()
-            lhs = stack.pop()
-            stack.append(("and" if op == OpCode.AND else "or", [lhs, rhs]))
-    if len(stack) != 1:
+
+class _NativeVocab:
+    def __init__(self, vocab):
+        lib = _native.load_library()
+        feats = [(k, v) for k, v in vocab.feature_ids.items() if 0 <= int(v) < 1 << 64]
+        vals = [(k, v) for k, v in vocab.values.items() if 0 <= int(v) < 1 << 64]
+        fn = (ctypes.c_char_p * max(1, len(feats)))(*[k.encode() for k, _ in feats])
+        fi = np.array([int(v) for _, v in feats] or [0], dtype=np.uint64)
+        vn = (ctypes.c_char_p * max(1, len(vals)))(*[k.encode() for k, _ in vals])
+        vi = np.array([int(v) for _, v in vals] or [0], dtype=np.uint64)
+        h = ctypes.c_void_p()
+        _native.check(lib.fb_vocab_create(len(feats), fn, fi.ctypes.data, len(vals), vn,
+                                          vi.ctypes.data, ctypes.byref(h)))
+        self.handle = h
+        self.sizes = (len(vocab.feature_ids), len(vocab.values))
+
+    def __del__(self):
+        try:
+            _native.load_library().fb_vocab_free(self.handle)
+        except Exception:
+            pass
+
+
+def _native_vocab(vocab):
+    if vocab is None:
         return None
+    # cached on the (frozen, unhashable) vocabulary object itself; rebuilt if its dicts grew
+    with _VOCAB_LOCK:
+        nv = vocab.__dict__.get("_fb_native")
+        if nv is None or nv.sizes != (len(vocab.feature_ids), len(vocab.values)):
+            nv = _NativeVocab(vocab)
+            object.__setattr__(vocab, "_fb_native", nv)
+        return nv
 
-    def nnf(node, neg):
-        kind = node[0]
-        if kind == "lit":
-            return ("lit", node[1], node[2] != neg)
-        if kind == "not":
-            return nnf(node[1], not neg)
-        flip = {"and": "or", "or": "and"}
-        k = flip[kind] if neg else kind
-        kids = []
-        for child in node[1]:
-            c = nnf(child, neg)
-            kids.extend(c[1] if c[0] == k else [c])
-        return (k, kids)
-
-    root = nnf(stack[0], False)
-
-    def clause(node):
-        if node[0] == "lit":
-            return [(node[1], node[2])]
-        if node[0] == "or" and all(c[0] == "lit" for c in node[1]):
-            return [(c[1], c[2]) for c in node[1]]
-        return None
-
-    if root[0] == "and":
-        groups = [clause(c) for c in root[1]]
-        return None if any(g is None for g in groups) else groups
-    g = clause(root)
-    return None if g is None else [g]
-
-
-def _pack_cnf(cnf, leaf_fid):
-    """CNF column layout of a batch. Literals (leaf, negated) become columns; columns are
-    grouped by feature id and the features bin-packed (first fit, decreasing) into 64-column
-    windows, so a group whose literals share a feature -- the usual ``f in S`` group --
-    tests one aligned u32 pair of the item's column bits. Falls back to first-seen order when
-    the windows would need more than CNF_MAX_WORDS words. Returns the FilterBatch kwargs, or
-    {} when the batch does not fit the CNF limits."""
-    lits: dict[tuple[int, bool], int] = {}
-    for groups in cnf:
-        for g in groups:
-            for lit in g:
-                lits.setdefault(lit, len(lits))
-    gmax = max(len(groups) for groups in cnf)
-    if gmax > CNF_MAX_GROUPS:
-        return {}
-    by_fid: dict[int, list] = {}
-    for lit in lits:
-        by_fid.setdefault(leaf_fid[lit[0]], []).append(lit)
-    bins: list[list] = []
-    if all(len(v) <= 64 for v in by_fid.values()):
-        for fid in sorted(by_fid, key=lambda f: (-len(by_fid[f]), f)):
-            for b in bins:
-                if len(b) + len(by_fid[fid]) <= 64:
-                    b.extend(by_fid[fid])
-                    break
-            else:
-                bins.append(list(by_fid[fid]))
-    if bins and 2 * len(bins) <= CNF_MAX_WORDS:
-        cols = {lit: 64 * bi + i for bi, b in enumerate(bins) for i, lit in enumerate(b)}
-        n_cols = 64 * (len(bins) - 1) + len(bins[-1])
-    else:
-        cols, n_cols = dict(lits), len(lits)
-    words = (n_cols + 31) // 32
-    if words > CNF_MAX_WORDS:
-        return {}
-    qmask = np.zeros((len(cnf), gmax, words), dtype=np.uint32)
-    for q, groups in enumerate(cnf):
-        for gi, g in enumerate(groups):
-            for lit in g:
-                c = cols[lit]
-                qmask[q, gi, c >> 5] |= np.uint32(1 << (c & 31))
-    col_leaf = np.zeros(n_cols, dtype=np.int16)  # padding columns: leaf 0, never referenced
-    for (leaf, neg), c in cols.items():
-        col_leaf[c] = ~leaf if neg else leaf
-    nz = qmask != 0
-    first = np.where(nz.any(axis=2), nz.argmax(axis=2), 0)
-    last = np.where(nz.any(axis=2), words - 1 - nz[:, :, ::-1].argmax(axis=2), 0)
-    windowed = int(gmax <= 4 and bool(np.all((first >> 1) == (last >> 1))))
-    return dict(col_leaf=col_leaf, qmask=qmask,
-                qgroups=np.array([len(g) for g in cnf], dtype=np.int32),
-                cnf_words=words, cnf_gmax=gmax, cnf_windowed=windowed)
 
 
 class FilterBatch:
@@ -444,7 +399,7 @@ class FilterBatch:
       that list, and peephole-lowered ``rops``.
     """
 
-    def __init__(self, leaf_pos, op_offset, ops, max_stack, push_leaf_bits, *,
+    def __init__(self, leaf_pos, op_offset, ops, max_stack, push_leaf_bits=None, *,
                  plane_list=None, leaf_slot=None, rop_offset=None, rops=None, rmax_stack=0,
                  col_leaf=None, qmask=None, qgroups=None, cnf_words=0, cnf_gmax=0,
                  cnf_windowed=0):
@@ -452,10 +407,10 @@ class FilterBatch:
         self.n_leaves = leaf_pos.shape[0]
         self.k_max = leaf_pos.shape[1]
         self.max_stack = max_stack
-        self.host_leaf_pos = np.ascontiguousarray(leaf_pos, dtype=np.int16)
+        self.host_leaf_pos = np.ascontiguousarray(leaf_pos, dtype=np.int32)
         self.host_op_offset = np.ascontiguousarray(op_offset, dtype=np.int32)
         self.host_ops = np.ascontiguousarray(ops, dtype=np.uint16)
-        self.host_plane_list = (np.ascontiguousarray(plane_list, dtype=np.int16)
+        self.host_plane_list = (np.ascontiguousarray(plane_list, dtype=np.int32)
                                 if plane_list is not None else None)
         self.host_leaf_slot = (np.ascontiguousarray(leaf_slot, dtype=np.int16)
                                if leaf_slot is not None else None)
@@ -534,87 +489,48 @@ class FilterBatch:
 
     @classmethod
     def pack(cls, filters, params: BloomParams) -> "FilterBatch":
-        if params.m_bits > 32767:
-            raise NotImplementedError("device filter evaluation supports m_bits <= 32767")
-        glob: dict[tuple[int, int], int] = {}
-        leaf_rows: list[tuple[int, ...]] = []
-        leaf_fid: list[int] = []
-        ops: list[int] = []
-        offsets = [0]
-        rops: list[int] = []
-        rop_offsets = [0]
-        push_bits = []
-        max_stack = 1
-        rmax = 0
-        cnf: list | None = []
-        for cf in filters:
-            nbits = 0
-            if cf is not None:
-                local = []
-                for fid, val, qb in cf.leaves:
-                    key = (int(fid), int(val))
-                    g = glob.get(key)
-                    if g is None:
-                        g = glob[key] = len(leaf_rows)
-                        leaf_rows.append(tuple(qb.set_bits))
-                        leaf_fid.append(int(fid))
-                    local.append(g)
-                gops = []
-                for op, arg in cf.ops:
-                    if op == OpCode.PUSH_LEAF:
-                        ops.append(local[arg])
-                        gops.append((int(op), local[arg]))
-                        nbits += len(cf.leaves[arg][2].set_bits)
-                    else:
-                        ops.append(int(op) << 14)
-                        gops.append((int(op), 0))
-                max_stack = max(max_stack, cf.max_stack_depth())
-                enc, depth = lower_to_register_ops(gops)
-                enc += [ROP_NOP << 13] * (-len(enc) % ROP_ALIGN)
-                rops.extend(enc)
-                rmax = max(rmax, depth)
-                if cnf is not None:
-                    groups = cnf_groups(gops)
-                    cnf = None if groups is None else cnf + [groups]
-            elif cnf is not None:
-                cnf.append([])
-            offsets.append(len(ops))
-            rop_offsets.append(len(rops))
-            push_bits.append(nbits)
-        if len(leaf_rows) > _native.FB_MAX_LEAVES:
-            raise NotImplementedError(f"more than {_native.FB_MAX_LEAVES} distinct leaves in a batch")
-        if max_stack > _native.FB_MAX_STACK:
-            raise NotImplementedError(f"filter stack depth {max_stack} > {_native.FB_MAX_STACK}")
-        k_max = max([1] + [len(r) for r in leaf_rows])
-        leaf_pos = np.full((max(1, len(leaf_rows)), k_max), -1, dtype=np.int16)
-        for i, r in enumerate(leaf_rows):
-            leaf_pos[i, : len(r)] = r
-        planes = np.unique(leaf_pos[leaf_pos >= 0]).astype(np.int16)
-        slot_of = {int(p): i for i, p in enumerate(planes)}
-        leaf_slot = np.full_like(leaf_pos, -1)
-        for i, r in enumerate(leaf_rows):
-            leaf_slot[i, : len(r)] = [slot_of[p] for p in r]
-        reg = len(leaf_rows) <= ROP_MAX_LEAVES
-        cnf_kw = {}
-        if reg and cnf is not None and any(cnf):
-            cnf_kw = _pack_cnf(cnf, leaf_fid)
-        elif reg and not leaf_rows:
-            # no query is filtered: the CNF form with zero groups per query (one unused
-            # column) lets the tensor-core scan take its per-hit kernel, where every gated
-            # pair survives
-            cnf_kw = dict(col_leaf=np.zeros(1, dtype=np.int16),
-                          qmask=np.zeros((len(cnf), 1, 1), dtype=np.uint32),
-                          qgroups=np.zeros(len(cnf), dtype=np.int32),
-                          cnf_words=1, cnf_gmax=1, cnf_windowed=1)
-        return cls(leaf_pos, np.array(offsets, dtype=np.int32),
-                   np.array(ops if ops else [0], dtype=np.uint16), max_stack,
-                   np.array(push_bits, dtype=np.int64),
-                   plane_list=planes if (reg and planes.size) else (np.zeros(1, np.int16) if reg else None),
-                   leaf_slot=leaf_slot if reg else None,
-                   rop_offset=np.array(rop_offsets, dtype=np.int32) if reg else None,
-                   rops=(np.array(rops if rops else [ROP_NOP << 13] * ROP_ALIGN, dtype=np.uint16)
-                         if reg else None),
-                   rmax_stack=rmax, **cnf_kw)
+        """Batch device form of compiled filters (``None`` = unfiltered), packed in C++
+        (``fb_pack_postfix``): leaves de-duplicated across the batch, postfix and register
+        ops, the CNF column windows."""
+        flats = [None if cf is None else _flat_program(cf) for cf in filters]
+        nq = len(flats)
+        off = np.zeros(nq + 1, dtype=np.int64)
+        for q, f in enumerate(flats):
+            off[q + 1] = off[q] + (0 if f is None else len(f[0]))
+        live = [f for f in flats if f is not None]
+        codes = np.concatenate([f[0] for f in live]) if live else np.zeros(1, np.uint8)
+        fid = np.concatenate([f[1] for f in live]) if live else np.zeros(1, np.uint64)
+        val = np.concatenate([f[2] for f in live]) if live else np.zeros(1, np.uint64)
+        h = ctypes.c_void_p()
+        _native.check(_native.load_library().fb_pack_postfix(
+            nq, off.ctypes.data, codes.ctypes.data, fid.ctypes.data, val.ctypes.data,
+            params.m_bits, params.k_hashes, ctypes.byref(h)))
+        return cls(**_take_pack(h))
+
+    @classmethod
+    def from_text(cls, texts, vocab: Vocabulary | None, params: BloomParams) -> "FilterBatch":
+        """Parse + compile + pack one filter text per query (``None`` / ``""`` = unfiltered)
+        in C++ (``fb_pack_text``): the serving path for request filters (reference
+        serve.py:204-205 -> parse_filter -> compile_filter, for a whole batch). A text the
+        native parser does not accept is re-parsed by ``parse_filter`` (the reference
+        grammar), which raises the reference's exception; text that only the Unicode-aware
+        Python tokenizer accepts is compiled in Python and packed through the same C++
+        packer."""
+        texts = list(texts)
+        enc = [t.encode("utf-8") if t else None for t in texts]
+        arr = (ctypes.c_char_p * max(1, len(enc)))(*enc)
+        nv = _native_vocab(vocab)
+        h, bad = ctypes.c_void_p(), ctypes.c_int32(-1)
+        lib = _native.load_library()
+        rc = lib.fb_pack_text(len(enc), arr, nv.handle if nv is not None else None,
+                              params.m_bits, params.k_hashes, ctypes.byref(h), ctypes.byref(bad))
+        if rc == _native.FB_ERR_PARSE:
+            parse_filter(texts[bad.value], vocab)  # raises the reference's exception
+            exprs = [parse_filter(t, vocab) if t else None for t in texts]
+            return cls.pack([compile_filter(e, params) if e is not None else None for e in exprs],
+                            params)
+        _native.check(rc)
+        return cls(**_take_pack(h))
 
     @classmethod
     def from_leaf(cls, qb: QueryBloom, params: BloomParams) -> "FilterBatch":

@@ -16,6 +16,8 @@ def pytest_configure(config):
     _RECORD.extend(integration.install())
     patched = sorted({f"{m.__name__}.{a}" for m, a, _ in _RECORD})
     config._fb_patched = patched
+    # also on stdout: ``-q`` runs (tests/test_reference_suite.py) suppress report headers
+    print("B200 drop-in patched: " + ", ".join(patched), flush=True)
 
 
 def pytest_report_header(config):

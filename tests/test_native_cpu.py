@@ -21,7 +21,7 @@ from paper_2511_14881_b200.filter_query import (And, FilterBatch, Leaf, Not, OpC
 
 def header_symbols() -> set[str]:
     text = (ROOT / "include" / "filtra_b200.h").read_text()
-    return set(re.findall(r"^\s*(?:int|int64_t|const char\*|uint64_t)\s+(fb_\w+)\(", text, flags=re.M))
+    return set(re.findall(r"^\s*(?:int|int64_t|const char\*|uint64_t|void)\s+(fb_\w+)\(", text, flags=re.M))
 
 
 def test_library_exports_every_header_symbol():
@@ -31,7 +31,7 @@ def test_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.fb_abi_version() == _native.ABI_VERSION == 3
+    assert lib.fb_abi_version() == _native.ABI_VERSION == 4
 
 
 def test_library_is_sm100a_only():
