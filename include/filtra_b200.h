@@ -375,11 +375,14 @@ void fb_vocab_free(fb_vocab_t* vocab);
 int fb_pack_text(int32_t n_queries, const char* const* texts, const fb_vocab_t* vocab,
                  int32_t m_bits, int32_t k_hashes, fb_pack_t** out, int32_t* bad_query);
 
-/* Host: the same from postfix programs (CompiledFilter.ops with the leaves' (fid, value)
- * inlined): query q's ops are [op_offset[q], op_offset[q+1]) (empty = unfiltered). */
+/* Host: the same from postfix programs (CompiledFilter.ops with the leaves inlined): query
+ * q's ops are [op_offset[q], op_offset[q+1]) (empty = unfiltered); a PUSH_LEAF op i carries
+ * its leaf's (fid, value) and, when pos_offset is not NULL, the leaf's positions
+ * pos[pos_offset[i] .. pos_offset[i+1]) (QueryBloom.set_bits; otherwise they are hashed).
+ * Leaves are de-duplicated by (fid, value), first push wins. */
 int fb_pack_postfix(int32_t n_queries, const int64_t* op_offset, const uint8_t* opcode,
-                    const uint64_t* fid, const uint64_t* value, int32_t m_bits,
-                    int32_t k_hashes, fb_pack_t** out);
+                    const uint64_t* fid, const uint64_t* value, const int64_t* pos_offset,
+                    const int32_t* pos, int32_t m_bits, int32_t k_hashes, fb_pack_t** out);
 
 int fb_pack_meta(const fb_pack_t* pack, int64_t* meta /* [FB_PACK_META_N] */);
 int fb_pack_array(const fb_pack_t* pack, int32_t which, const void** data, int64_t* n_elems);

@@ -156,7 +156,7 @@ def _declare(lib) -> None:
         "fb_vocab_create": ([i32, c_vp, c_vp, i32, c_vp, c_vp, c_vp], i32),
         "fb_vocab_free": ([c_vp], None),
         "fb_pack_text": ([i32, c_vp, c_vp, i32, i32, c_vp, c_vp], i32),
-        "fb_pack_postfix": ([i32, c_vp, c_vp, c_vp, c_vp, i32, i32, c_vp], i32),
+        "fb_pack_postfix": ([i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, i32, i32, c_vp], i32),
         "fb_pack_meta": ([c_vp, c_vp], i32),
         "fb_pack_array": ([c_vp, i32, c_vp, c_vp], i32),
         "fb_pack_free": ([c_vp], None),

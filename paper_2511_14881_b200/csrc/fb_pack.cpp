@@ -85,8 +85,10 @@ void lookup_positions(const uint64_t* fid, const uint64_t* val, size_t n, int m,
 
 // ---- one query's postfix program ---------------------------------------------------------
 struct Op {
-  uint8_t code;    // FB_OP_*
+  uint8_t code;       // FB_OP_*
   uint64_t fid, val;  // PUSH_LEAF operand
+  const int32_t* xpos = nullptr;  // explicit positions (CompiledFilter leaves); null: hash
+  int32_t nxpos = 0;
 };
 
 // ---- text grammar (reference filter_query.py:82-189) --------------------------------------
@@ -479,6 +481,7 @@ int pack_programs(const std::vector<std::vector<Op>>& progs, const std::vector<c
   memset(P.meta, 0, sizeof(P.meta));
   P.meta[FB_PACK_N_QUERIES] = nq;
   // global leaves in order of first push across the batch
+  std::vector<std::pair<const int32_t*, int32_t>> leaf_x;  // first push's explicit positions
   // open-addressing (fid, value) -> global leaf table, grown at half load
   std::vector<int32_t> tab(1024, -1);
   size_t tmask = tab.size() - 1;
@@ -504,6 +507,7 @@ int pack_programs(const std::vector<std::vector<Op>>& progs, const std::vector<c
             g = e = (int32_t)P.leaf_fid.size();
             P.leaf_fid.push_back(o.fid);
             P.leaf_val.push_back(o.val);
+            leaf_x.push_back({o.xpos, o.nxpos});
             if (2 * P.leaf_fid.size() > tab.size()) {  // rehash
               tab.assign(tab.size() * 2, -1);
               tmask = tab.size() - 1;
@@ -537,8 +541,25 @@ int pack_programs(const std::vector<std::vector<Op>>& progs, const std::vector<c
   if (max_stack > FB_MAX_STACK)
     return fail(FB_ERR_UNSUPPORTED, "filter stack depth " + std::to_string(max_stack) + " > " +
                                         std::to_string(FB_MAX_STACK));
-  std::vector<Positions> pos;
-  lookup_positions(P.leaf_fid.data(), P.leaf_val.data(), (size_t)n_leaves, m_bits, k_hashes, pos);
+  // each leaf's positions, flat: the compiled filter's own (QueryBloom.set_bits) when given,
+  // else hashed (cached per (fid, value, M, K))
+  std::vector<Positions> hashed;
+  lookup_positions(P.leaf_fid.data(), P.leaf_val.data(), (size_t)n_leaves, m_bits, k_hashes, hashed);
+  std::vector<int32_t> lp_off(n_leaves + 1, 0), lp;
+  lp.reserve((size_t)n_leaves * k_hashes);
+  for (int i = 0; i < n_leaves; ++i) {
+    if (leaf_x[i].first != nullptr) {
+      for (int j = 0; j < leaf_x[i].second; ++j) {
+        const int32_t v = leaf_x[i].first[j];
+        if (v < 0 || v >= m_bits) return fail(FB_ERR_INVALID, "leaf position outside [0, m_bits)");
+        lp.push_back(v);
+      }
+    } else {
+      lp.insert(lp.end(), hashed[i].p, hashed[i].p + hashed[i].n);
+    }
+    lp_off[i + 1] = (int32_t)lp.size();
+  }
+  auto npos = [&](int i) { return lp_off[i + 1] - lp_off[i]; };
   // postfix ops, register ops, push bits, CNF
   const bool reg = n_leaves <= kRopMaxLeaves;
   int rmax = 0;
@@ -558,7 +579,7 @@ int pack_programs(const std::vector<std::vector<Op>>& progs, const std::vector<c
       for (const auto& o : gops[q]) {
         if (o.first == FB_OP_PUSH_LEAF) {
           P.ops.push_back((uint16_t)o.second);
-          bits += pos[o.second].n;
+          bits += npos(o.second);
         } else {
           P.ops.push_back((uint16_t)(o.first << 14));
         }
@@ -575,23 +596,23 @@ int pack_programs(const std::vector<std::vector<Op>>& progs, const std::vector<c
     P.rop_offset.push_back((int32_t)P.rops.size());
   }
   int k_max = 1;
-  for (int i = 0; i < n_leaves; ++i) k_max = std::max(k_max, (int)pos[i].n);
+  for (int i = 0; i < n_leaves; ++i) k_max = std::max(k_max, npos(i));
   const int rows = std::max(1, n_leaves);
   P.leaf_pos.assign((size_t)rows * k_max, -1);
   std::vector<int32_t> planes;
   for (int i = 0; i < n_leaves; ++i)
-    for (int j = 0; j < pos[i].n; ++j) {
-      P.leaf_pos[(size_t)i * k_max + j] = pos[i].p[j];
-      planes.push_back(pos[i].p[j]);
+    for (int j = 0; j < npos(i); ++j) {
+      P.leaf_pos[(size_t)i * k_max + j] = lp[lp_off[i] + j];
+      planes.push_back(lp[lp_off[i] + j]);
     }
   std::sort(planes.begin(), planes.end());
   planes.erase(std::unique(planes.begin(), planes.end()), planes.end());
   if (reg) {
     P.leaf_slot.assign((size_t)rows * k_max, -1);
     for (int i = 0; i < n_leaves; ++i)
-      for (int j = 0; j < pos[i].n; ++j)
+      for (int j = 0; j < npos(i); ++j)
         P.leaf_slot[(size_t)i * k_max + j] = (int16_t)(
-            std::lower_bound(planes.begin(), planes.end(), pos[i].p[j]) - planes.begin());
+            std::lower_bound(planes.begin(), planes.end(), lp[lp_off[i] + j]) - planes.begin());
     P.plane_list = planes.empty() ? std::vector<int32_t>(1, 0) : planes;
     if (P.rops.empty())
       for (int i = 0; i < FB_ROP_ALIGN; ++i) P.rops.push_back((uint16_t)(FB_ROP_NOP << 13));
@@ -669,8 +690,8 @@ int fb_pack_text(int32_t n_queries, const char* const* texts, const fb_vocab_t* 
 }
 
 int fb_pack_postfix(int32_t n_queries, const int64_t* op_offset, const uint8_t* opcode,
-                    const uint64_t* fid, const uint64_t* value, int32_t m_bits,
-                    int32_t k_hashes, fb_pack_t** out) {
+                    const uint64_t* fid, const uint64_t* value, const int64_t* pos_offset,
+                    const int32_t* pos, int32_t m_bits, int32_t k_hashes, fb_pack_t** out) {
   if (out == nullptr || n_queries < 0 || op_offset == nullptr)
     return fb::fail(FB_ERR_INVALID, "bad arguments");
   if (m_bits < 1 || k_hashes < 1) return fb::fail(FB_ERR_INVALID, "m_bits and k_hashes must be >= 1");
@@ -684,7 +705,14 @@ int fb_pack_postfix(int32_t n_queries, const int64_t* op_offset, const uint8_t* 
     if (b == a) continue;  // unfiltered
     filtered[q] = 1;
     progs[q].reserve((size_t)(b - a));
-    for (int64_t i = a; i < b; ++i) progs[q].push_back({opcode[i], fid[i], value[i]});
+    for (int64_t i = a; i < b; ++i) {
+      fb::Op o{opcode[i], fid[i], value[i]};
+      if (pos_offset != nullptr && opcode[i] == FB_OP_PUSH_LEAF) {
+        o.xpos = pos + pos_offset[i];
+        o.nxpos = (int32_t)(pos_offset[i + 1] - pos_offset[i]);
+      }
+      progs[q].push_back(o);
+    }
   }
   auto P = std::make_unique<fb_pack>();
   const int rc = fb::pack_programs(progs, filtered, m_bits, k_hashes, *P);

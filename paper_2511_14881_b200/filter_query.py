@@ -296,18 +296,27 @@ def _compile_filter(expr: FilterExpr, params: BloomParams) -> CompiledFilter:
 # --- batch device form (built by the C++ packer, csrc/fb_pack.cpp) ----------------------
 
 def _flat_program(cf: CompiledFilter):
-    """``cf`` as postfix arrays (opcode u8, leaf fid u64, leaf value u64), cached on the
-    (immutable) compiled filter."""
+    """``cf`` as postfix arrays: opcode u8, leaf fid / value u64 per op, and the pushed
+    leaf's positions (its QueryBloom.set_bits, so a compiled filter carrying its own
+    positions -- e.g. ``bloom_eval_leaf``'s single leaf -- keeps them) as per-op counts +
+    a flat int32 array; cached on the (immutable) compiled filter."""
     flat = cf.__dict__.get("_flat")
     if flat is None:
-        codes = np.fromiter((int(o) for o, _ in cf.ops), dtype=np.uint8, count=len(cf.ops))
-        args = np.fromiter((int(a) for _, a in cf.ops), dtype=np.int64, count=len(cf.ops))
+        n = len(cf.ops)
+        codes = np.fromiter((int(o) for o, _ in cf.ops), dtype=np.uint8, count=n)
+        args = np.fromiter((int(a) for _, a in cf.ops), dtype=np.int64, count=n)
         lf = np.array([int(l[0]) for l in cf.leaves] or [0], dtype=np.uint64)
         lv = np.array([int(l[1]) for l in cf.leaves] or [0], dtype=np.uint64)
+        lpos = [np.asarray(l[2].set_bits, dtype=np.int64) for l in cf.leaves]
         push = codes == OpCode.PUSH_LEAF
         a = np.where(push, args, 0)
+        cnt = np.array([len(lpos[int(x)]) if p else 0 for x, p in zip(a, push)], dtype=np.int64)
+        pos = (np.concatenate([lpos[int(x)] for x, p in zip(a, push) if p])
+               if cnt.sum() else np.zeros(0, np.int64))
+        if pos.size and (pos.min() < 0 or pos.max() >= 1 << 31):
+            raise ValueError("leaf position outside the int32 range")
         flat = (codes, np.where(push, lf[a], 0).astype(np.uint64),
-                np.where(push, lv[a], 0).astype(np.uint64))
+                np.where(push, lv[a], 0).astype(np.uint64), cnt, pos.astype(np.int32))
         object.__setattr__(cf, "_flat", flat)
     return flat
 
@@ -501,10 +510,15 @@ class FilterBatch:
         codes = np.concatenate([f[0] for f in live]) if live else np.zeros(1, np.uint8)
         fid = np.concatenate([f[1] for f in live]) if live else np.zeros(1, np.uint64)
         val = np.concatenate([f[2] for f in live]) if live else np.zeros(1, np.uint64)
+        cnt = np.concatenate([f[3] for f in live]) if live else np.zeros(1, np.int64)
+        pos_off = np.zeros(cnt.size + 1, dtype=np.int64)
+        np.cumsum(cnt, out=pos_off[1:])
+        pos = np.concatenate([f[4] for f in live] + [np.zeros(1, np.int32)])
         h = ctypes.c_void_p()
         _native.check(_native.load_library().fb_pack_postfix(
             nq, off.ctypes.data, codes.ctypes.data, fid.ctypes.data, val.ctypes.data,
-            params.m_bits, params.k_hashes, ctypes.byref(h)))
+            pos_off.ctypes.data, pos.ctypes.data, params.m_bits, params.k_hashes,
+            ctypes.byref(h)))
         return cls(**_take_pack(h))
 
     @classmethod

@@ -167,3 +167,17 @@ def test_cold_text_pack_time():
     dt = (time.perf_counter() - t0) * 1e3
     print(f"cold text parse+compile+pack, 256 four-attribute filters: {dt:.2f} ms")
     assert b.is_cnf and dt < 200
+
+
+def test_explicit_leaf_positions_are_kept():
+    """A compiled filter's own leaf positions (bloom_eval_leaf's QueryBloom) win over
+    hashing its (fid, value) placeholder."""
+    from paper_2511_14881_b200.bloom import QueryBloom
+    from paper_2511_14881_b200.filter_query import CompiledFilter, OpCode
+    qb = QueryBloom((3, 700, 1023))
+    b = FilterBatch.from_leaf(qb, BloomParams())
+    assert b.host_leaf_pos[0].tolist() == [3, 700, 1023]
+    cf = CompiledFilter(ops=((OpCode.PUSH_LEAF, 0),), leaves=((0, 0, qb),))
+    assert_same(b, FilterBatch(**pack_py([cf], BloomParams())))
+    with pytest.raises(ValueError):
+        FilterBatch.from_leaf(QueryBloom((5, 2048)), BloomParams())
