@@ -91,6 +91,31 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Producers several stages ahead of their consumers: one try_wait, then test_wait polls
+// spaced by __nanosleep, so a producer blocked on a full ring gives its issue slots to the
+// warps sharing its scheduler (a spinning try_wait loop does not).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
+  const uint32_t a = su32(b);
+  uint32_t ok = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  while (!ok) {
+    __nanosleep(128);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+
 // Wait for a phase with a sleep between polls: for warps that run ahead of the pipeline
 // (producers, builders), whose polling would otherwise take issue slots from the warps on
 // the critical path of the same sub-partition.

@@ -314,7 +314,7 @@ __device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap
         // item rows by TMA; alongside, into a stage with the item stage's lifetime: the
         // tile's 256 id ranks (1 KB, 16-byte cp.async), its validity & range words and its
         // tile index (so the epilogue never waits on global memory for per-tile metadata)
-        mbar_wait_idle(items_empty + s, ph ^ 1u);
+        mbar_wait_backoff(items_empty + s, ph ^ 1u);
         FB_TR(a, (int)((i - blockIdx.x) / G), 0);
         if (lane == 0) {
           mbar_expect_tx(items_full + s, kItemBytes);
@@ -340,7 +340,7 @@ __device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap
         if (lane == 0) mbar_arrive(items_full + s);
       }
       if (do_planes && a.has_prog && a.n_planes > 0) {
-        mbar_wait_idle(planes_empty + ps, pph ^ 1u);
+        mbar_wait_backoff(planes_empty + ps, pph ^ 1u);
         FB_TR(a, (int)((i - blockIdx.x) / G), 10);
         // gather the referenced planes' 32-byte rows for this tile: 16-byte cp.async per
         // lane (two lanes per plane row, a warp covers 16 rows per instruction); each lane
@@ -381,11 +381,18 @@ __device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap
     }
 }
 
-// ================= MMA issuer (one thread) =============================================
+// ================= MMA issuer =============================================================
 // kArm: each M-block's accumulator is first set to the row's gate (digits . 127s, K = 32,
 // no-swizzle descriptors; the 127 tile is one 256-byte pair of core matrices, SBO = 0).
-template <bool kArm>
-__device__ __forceinline__ void mma_loop(const TcArgs& a, const Smem& m, uint32_t tmem_base) {
+// kNbAcc (CNF kernel): the whole warp runs the loop and lane 0 issues; an accumulator
+// buffer's release by the dense warps is a hardware named barrier (bar.arrive there,
+// bar.sync here), so the MMA warp blocks in the barrier unit instead of polling an
+// mbarrier -- the poll loop cost ~4.6k issue slots per tile on the scheduler it shares
+// with a dense and two hit warps (ncu, round 2).
+constexpr int kNbAccEmpty = 9;  // + accumulator buffer (9, 10)
+template <bool kArm, bool kNbAcc = false>
+__device__ __forceinline__ void mma_loop(const TcArgs& a, const Smem& m, uint32_t tmem_base,
+                                         int nb_acc_count = 0) {
   uint64_t* items_full = m.bars + kBarItemsFull;
   uint64_t* items_empty = m.bars + kBarItemsEmpty;
   uint64_t* acc_full = m.bars + kBarAccFull;
@@ -393,6 +400,7 @@ __device__ __forceinline__ void mma_loop(const TcArgs& a, const Smem& m, uint32_
   constexpr uint32_t idesc = idesc_i8(kBlockM, kTileItems);
   const uint32_t gate_s = su32(m.base + a.off_gate);
   const int S = a.item_stages;
+  const bool issuer = !kNbAcc || (threadIdx.x & 31) == 0;
   int acc_it = 0, s = 0;
   uint32_t ph = 0;
   for (int64_t i = blockIdx.x; i < a.n_sel; i += gridDim.x) {
@@ -403,24 +411,34 @@ __device__ __forceinline__ void mma_loop(const TcArgs& a, const Smem& m, uint32_
     for (int mb = 0; mb < a.n_mblk; ++mb, ++acc_it) {
       const int ab = acc_it & 1;
       const uint32_t aph = (uint32_t)(acc_it >> 1) & 1u;
-      mbar_wait_idle(acc_empty + ab, aph ^ 1u);
+      if (kNbAcc) {
+        if (acc_it >= 2) nb_sync(kNbAccEmpty + ab, nb_acc_count);
+      } else {
+        mbar_wait_idle(acc_empty + ab, aph ^ 1u);
+      }
       tc_fence_after();
-      const uint32_t a_base = su32(m.sA + mb * kBlockM * kKBytes);
-      const uint32_t d = tmem_base + (uint32_t)(ab * kAccCols);
-      const bool arm = kArm && !(a.dbg & 128);
-      if (arm)
-        umma_i8(d, plain_desc(gate_s + (uint32_t)mb * (kBlockM / 8) * 256u, 128u, 256u),
-                plain_desc(gate_s + kGateTileBytes, 128u, 0u), idesc, 0u);
+      if (issuer) {
+        const uint32_t a_base = su32(m.sA + mb * kBlockM * kKBytes);
+        const uint32_t d = tmem_base + (uint32_t)(ab * kAccCols);
+        const bool arm = kArm && !(a.dbg & 128);
+        if (arm)
+          umma_i8(d, plain_desc(gate_s + (uint32_t)mb * (kBlockM / 8) * 256u, 128u, 256u),
+                  plain_desc(gate_s + kGateTileBytes, 128u, 0u), idesc, 0u);
 #pragma unroll
-      for (int kk = 0; kk < ((a.dbg & 512) ? 0 : kKBytes / kUmmaK); ++kk)
-        umma_i8(d, sw128_desc(a_base + kk * kUmmaK), sw128_desc(b_base + kk * kUmmaK), idesc,
-                (kk > 0 || arm) ? 1u : 0u);
-      umma_commit(acc_full + ab);
+        for (int kk = 0; kk < ((a.dbg & 512) ? 0 : kKBytes / kUmmaK); ++kk)
+          umma_i8(d, sw128_desc(a_base + kk * kUmmaK), sw128_desc(b_base + kk * kUmmaK), idesc,
+                  (kk > 0 || arm) ? 1u : 0u);
+        umma_commit(acc_full + ab);
+      }
+      if (kNbAcc) __syncwarp();
       if (mb == 0) FB_TR(a, (int)((i - blockIdx.x) / gridDim.x), 2);
     }
-    umma_commit(items_empty + s);
+    if (issuer) umma_commit(items_empty + s);
     if (++s == S) { s = 0; ph ^= 1u; }
   }
+  if (kNbAcc)  // retire the dense warps' releases of the last two buffers
+    for (int t = acc_it; t < acc_it + 2; ++t)
+      if (t >= 2) nb_sync(kNbAccEmpty + (t & 1), nb_acc_count);
 }
 
 // ---- CNF kernel warp layout (see k_scan_cnf) ----
@@ -434,6 +452,7 @@ constexpr int kSurvCap = 64;  // u16 survivor entries per hit warp: (lane << 8) 
 // named barrier ids (0 is __syncthreads) and their thread counts
 constexpr int kNbHmFull = 1, kNbHmEmpty = 3, kNbLeafFull = 5, kNbLeafEmpty = 7;  // + stage
 constexpr int kNbHmCount = 32 * (kCnfDenseWarps + kCnfHitWarps);
+constexpr int kNbAccCount = 32 * (kCnfDenseWarps + 1);  // dense warps arrive, MMA warp syncs
 constexpr int kNbLeafCount = 32 * (kCnfBuilders + kCnfHitWarps);
 
 // ================= CNF column builders (nb warps): Bloom test per literal column, then a
@@ -453,7 +472,7 @@ __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m,
       const int st = it & 1;
       const uint32_t ph = (uint32_t)(it >> 1) & 1u;
       (void)ph;
-      mbar_wait_idle(planes_full + ps, pph);
+      mbar_wait_backoff(planes_full + ps, pph);  // a plane stage lands ~1 tile ahead
       if (it >= 2) nb_sync(kNbLeafEmpty + st, kNbLeafCount);
       const uint32_t p_s = su32(sP + (size_t)ps * a.plane_stage_bytes);
       uint32_t* TB = reinterpret_cast<uint32_t*>(sL + (size_t)st * a.leaf_stage_bytes);
@@ -942,7 +961,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
   if (warp == 0) {
     producer_loop(a, &tmap_items, m, lane, true, false);
   } else if (warp == 1) {
-    if (lane == 0) mma_loop<true>(a, m, tmem_base);
+    mma_loop<true, true>(a, m, tmem_base, kNbAccCount);
   } else if (warp == 2) {
     producer_loop(a, &tmap_items, m, lane, false, true);
   } else if (warp < kCnfDense0) {
@@ -1021,8 +1040,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
           sts32(hmap + (uint32_t)((c + 1) * kMaxQueries + q) * 4u, chunk_mask(c + 1, rb));
         }
         tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(acc_empty + ab);
+        nb_arrive(kNbAccEmpty + ab, kNbAccCount);  // the MMA warp bar.syncs on it
         if (quad == 0) FB_TR(a, it, 5 + 2 * mb);
       }
       __syncwarp();

@@ -1,0 +1,270 @@
+"""Single-request serving on CUDA graphs (the reference's per-request entry points,
+``retrieval.retrieve`` -- ref/retrieval.py:163-199 -- and ``retrieval.codesigned_search``
+-- ref/retrieval.py:110-144 -- called once per request from N server threads).
+
+A request runs a fixed sequence of small device steps: per task the centroid probe
+(numpy-order float64 dots + stable top-nprobe), the query quantisation, the grouped
+filtered scan over the probed clusters with exact top-k (``fb_ivf_topk``, device-resident
+probe lists), then the merge across tasks, cache-row lookup, re-scoring, value model and
+final (score desc, id asc) top-k. Launched one by one from Python that is ~30 launches,
+several host round trips and ~1 ms per request; here the whole sequence is captured ONCE
+per request shape into a CUDA graph (static input / output buffers, results copied into
+pinned host memory inside the graph) and every request is: copy the task vectors (and the
+packed filter, if any) into the static buffers, one graph launch, one stream sync. Errors
+the eager path raises mid-way (a candidate missing from the embedding cache, a zero
+divisor in the value model) become device flags tested after the replay, in the same
+order. Graphs are per thread (the reference server calls from a thread pool) and keyed on
+everything that fixes the sequence: engine objects, task names, nprobe, k0, topk, merge,
+value model, query dtype and the packed filter's shape.
+"""
+
+from __future__ import annotations
+
+import json
+import threading
+from collections import OrderedDict
+
+import numpy as np
+import torch
+
+from . import _native
+from ._device import device
+from .bloom import FilterStats
+from .engine import device_index_for
+from .errors import DivByZero, MissingItem
+from .filter_query import FilterBatch
+from .ivf import TILE_ROWS, IvfSearchOp, ScanStats, TopkResult
+
+GRAPHS_PER_THREAD = 16
+_local = threading.local()
+
+
+def _graphs() -> OrderedDict:
+    g = getattr(_local, "graphs", None)
+    if g is None:
+        g = _local.graphs = OrderedDict()
+    return g
+
+
+def _batch_sig(batch: FilterBatch | None):
+    if batch is None:
+        return None
+    return (tuple(batch.meta()), tuple((a.shape, a.dtype.str) for a in batch.host_arrays()))
+
+
+def scan_stats_for(cluster_offsets: np.ndarray, clusters: np.ndarray, stats: ScanStats) -> None:
+    """``search_clusters``' counters for the probed clusters (ref ivf.py:311-327): slots,
+    TILE_ROWS tiles, the largest tile."""
+    for c in clusters:
+        s, e = (int(x) for x in cluster_offsets[int(c)])
+        n = e - s
+        if n <= 0:
+            continue
+        stats.slots_scanned += n
+        stats.tiles += (n + TILE_ROWS - 1) // TILE_ROWS
+        stats.max_tile_rows = max(stats.max_tile_rows, min(n, TILE_ROWS))
+
+
+def filter_stats_for(cluster_offsets: np.ndarray, clusters: np.ndarray, push_bits: int,
+                     stats: FilterStats) -> None:
+    """``eval_compiled``'s counters over the probed, non-empty clusters (ref
+    retrieval.py:127-133, filter_query.py:333-334, bloom.py:180)."""
+    for c in clusters:
+        s, e = (int(x) for x in cluster_offsets[int(c)])
+        if s == e:
+            continue
+        words = ((e + 63) >> 6) - (s >> 6)
+        stats.slots_evaluated += words * 64
+        stats.words_read += push_bits * words
+
+
+class _Graph:
+    """One captured request shape: T task vectors -> probe + filtered scan (+ the
+    multi-task tail when ``tail`` is set) -> pinned host outputs."""
+
+    def __init__(self, dix, T: int, nprobe: int, k0: int, qdtype, batch: FilterBatch | None,
+                 tail=None):
+        dev = device()
+        self.dix, self.T, self.k0 = dix, T, k0
+        self.op = IvfSearchOp(dix, T, nprobe, k0, path="probe")
+        self.u32 = torch.zeros((T, dix.dim), dtype=torch.float32, device=dev)
+        self.uq = torch.zeros((T, dix.dim), dtype=qdtype, device=dev)
+        self.batch = None
+        if batch is not None:
+            self.batch = batch.clone_host().to_device()
+        self.tail = tail
+        pin = dict(pin_memory=True)
+        self.h_clusters = torch.empty((T, self.op.nprobe), dtype=torch.int64, **pin)
+        self.h_count = torch.empty((T,), dtype=torch.int32, **pin)
+        self.h_ids = torch.empty((T, max(k0, 1)), dtype=torch.int64, **pin)
+        self.h_scores = torch.empty((T, max(k0, 1)), dtype=torch.int32, **pin)
+        if tail is not None:
+            topk = tail["topk"]
+            self.h_out_ids = torch.empty((1, topk), dtype=torch.int64, **pin)
+            self.h_final = torch.empty((1, topk), dtype=torch.float64, **pin)
+            self.h_ts = torch.empty((1, T, topk), dtype=torch.float64, **pin)
+            self.h_n = torch.empty((1,), dtype=torch.int32, **pin)
+            self.h_missing = torch.empty((2,), dtype=torch.int64, **pin)  # flag, first id
+            self.h_zero = torch.empty((1,), dtype=torch.bool, **pin)
+        # eager warm-up (allocates lazily built state, raises the eager path's errors for
+        # a malformed request shape before anything is captured), then the capture
+        self._run()
+        torch.cuda.current_stream().synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+            self._run()
+
+    def _run(self):
+        clusters = self.op.probe(self.u32)
+        qq = self.dix.quantize_queries(self.uq)
+        out = self.op.scan(qq, clusters, self.batch)
+        self.h_clusters.copy_(clusters, non_blocking=True)
+        self.h_count.copy_(out.count, non_blocking=True)
+        self.h_ids.copy_(out.ids, non_blocking=True)
+        self.h_scores.copy_(out.scores, non_blocking=True)
+        if self.tail is not None:
+            self._run_tail(out)
+
+    def _run_tail(self, out):
+        from .overarch import merge_device, value_model_device
+        t = self.tail
+        T, k = self.T, self.k0
+        merged, mcount = merge_device(out.ids.view(1, T, k), out.count.view(1, T), t["merge"])
+        valid = torch.arange(merged.shape[1], device=merged.device)[None, :] < mcount[:, None]
+        rows, bad = t["cache"].rows_and_missing(merged, valid)
+        badc = bad.reshape(-1)
+        first = torch.argmax(badc.to(torch.int32)).view(1)   # device-only indexing below
+        self.h_missing[0:1].copy_(badc.any().to(torch.int64).view(1), non_blocking=True)
+        self.h_missing[1:2].copy_(merged.reshape(-1).index_select(0, first), non_blocking=True)
+        ts = t["scorer"].score(t["cache"], rows, mcount, self.u32[None], t["names"])
+        zero = []
+        final = value_model_device(t["spec"], {n: ts[:, j, :] for j, n in enumerate(t["names"])},
+                                   valid, zero_flags=zero)
+        anyz = torch.zeros((1,), dtype=torch.bool, device=merged.device)
+        for z in zero:
+            anyz |= z.view(1)
+        self.h_zero.copy_(anyz, non_blocking=True)
+        final = torch.where(valid, final, torch.full_like(final, -float("inf")))
+        topk = t["topk"]
+        order = torch.sort(final, dim=1, descending=True, stable=True).indices[:, :topk]
+        n = torch.clamp(mcount, max=topk)
+        self.h_out_ids.copy_(torch.gather(merged, 1, order), non_blocking=True)
+        self.h_final.copy_(torch.gather(final, 1, order), non_blocking=True)
+        self.h_ts.copy_(torch.gather(ts, 2, order[:, None, :].expand(1, T, -1)), non_blocking=True)
+        self.h_n.copy_(n, non_blocking=True)
+
+    def replay(self, users: np.ndarray, batch: FilterBatch | None):
+        """users float [T, dim] (the caller's dtype) -> run; host outputs valid after."""
+        self.u32.copy_(torch.from_numpy(np.ascontiguousarray(users, dtype=np.float32)))
+        src = np.ascontiguousarray(users, dtype=np.float32 if self.uq.dtype == torch.float32
+                                   else np.float64)
+        self.uq.copy_(torch.from_numpy(src))
+        if batch is not None:
+            for d, h in zip(self.batch._dev, batch.host_arrays()):
+                d.copy_(torch.from_numpy(h))
+        self.graph.replay()
+        torch.cuda.current_stream().synchronize()
+
+
+def _get_graph(key, make):
+    """The thread's graph for ``key`` (LRU), or None when the shape cannot be captured or
+    its eager warm-up raised -- the caller then runs the eager path, which raises the same
+    request error or serves the request step by step."""
+    g = _graphs()
+    if key in g:
+        g.move_to_end(key)
+        return g[key]
+    try:
+        hit = make()
+    except Exception:  # noqa: BLE001 -- remembered as "eager only" for this shape
+        if _native.env_flag("FB_GRAPH_STRICT"):  # tests: a capture failure is a failure
+            raise
+        hit = None
+    g[key] = hit
+    while len(g) > GRAPHS_PER_THREAD:
+        g.popitem(last=False)
+    return hit
+
+
+def _eligible(dix, nprobe, k0) -> bool:
+    return int(k0) >= 1 and int(nprobe) >= 1 and (
+        dix.centroids is not None or dix.cluster_offsets.shape[0] == 1)
+
+
+def _qdtype(x: np.ndarray):
+    # reference quantize_vector quantises the caller's float64 value (a float32 array widens
+    # exactly, so it takes the float32 kernel)
+    return torch.float32 if x.dtype == np.float32 else torch.float64
+
+
+def codesigned_search(ivf, bloom_index, cf, query, nprobe: int, k0: int, scan_stats=None,
+                      filter_stats=None, timings=None):
+    """Graph-replayed ``codesigned_search`` for one query, or None when the request shape
+    is not covered (the caller then runs the eager path)."""
+    dix = device_index_for(ivf, bloom=bloom_index if cf is not None else None)
+    raw = np.asarray(query)
+    if raw.ndim != 1 or raw.shape[0] != dix.dim or not _eligible(dix, nprobe, k0):
+        return None
+    if cf is not None and dix.bloom is None:
+        return None
+    batch = FilterBatch.pack([cf], dix.bloom.params) if cf is not None else None
+    if raw.dtype != np.float32:
+        raw = raw.astype(np.float64)
+    key = ("cs", id(dix), int(nprobe), int(k0), raw.dtype.str, _batch_sig(batch))
+    g = _get_graph(key, lambda: _Graph(dix, 1, int(nprobe), int(k0), _qdtype(raw), batch))
+    if g is None:
+        return None
+    g.replay(raw[None], batch)
+    clusters = g.h_clusters[0].numpy().copy()
+    if scan_stats is not None:
+        scan_stats_for(dix.cluster_offsets, clusters, scan_stats)
+    if filter_stats is not None and cf is not None:
+        filter_stats_for(dix.cluster_offsets, clusters, int(batch.push_leaf_bits[0]), filter_stats)
+    n = int(g.h_count[0])
+    return TopkResult(item_ids=g.h_ids[0, :n].numpy().view(np.uint64).copy(),
+                      scores=g.h_scores[0, :n].numpy().copy(), k_requested=int(k0))
+
+
+def retrieve_fast(engine, req, cache_factory, scorer_factory, spec, names):
+    """Graph-replayed ``retrieve`` for one request: returns (ids u64 [n], final f64 [n],
+    task scores f64 [T, n], clusters per task, per-task counts) or None when not covered."""
+    if len(req.tasks) == 0:
+        return None
+    dix = device_index_for(engine.ivf, bloom=engine.bloom if req.filter is not None else None)
+    users = [np.asarray(t.user_embedding) for t in req.tasks]
+    if any(u.ndim != 1 or u.shape[0] != dix.dim for u in users):
+        return None
+    if not _eligible(dix, req.nprobe, req.k0) or int(req.topk) < 1:
+        return None
+    cf = engine.compile(req.filter) if req.filter is not None else None
+    if cf is not None and dix.bloom is None:
+        return None
+    batch = FilterBatch.pack([cf] * len(users), dix.bloom.params) if cf is not None else None
+    f64 = any(u.dtype != np.float32 for u in users)
+    U = np.stack([u.astype(np.float64 if f64 else np.float32) for u in users])
+    cache = cache_factory(engine.cache)
+    scorer = scorer_factory(engine.scorer)
+    topk = min(int(req.topk), len(users) * int(req.k0))
+    key = ("rt", id(dix), id(cache), id(scorer), tuple(names), int(req.nprobe), int(req.k0),
+           topk, req.merge, json.dumps(spec, sort_keys=True, default=str), U.dtype.str,
+           _batch_sig(batch))
+    tail = {"cache": cache, "scorer": scorer, "names": list(names), "spec": spec,
+            "merge": req.merge, "topk": topk}
+    g = _get_graph(key, lambda: _Graph(dix, len(users), int(req.nprobe), int(req.k0),
+                                       torch.float64 if f64 else torch.float32, batch, tail))
+    if g is None:
+        return None
+    g.replay(U, batch)
+    if int(g.h_missing[0]):
+        raise MissingItem(int(g.h_missing[1]) & 0xFFFFFFFFFFFFFFFF)
+    if bool(g.h_zero[0]):
+        raise DivByZero("division by zero in value model")
+    n = int(g.h_n[0])
+    return (g.h_out_ids[0, :n].numpy().view(np.uint64).copy(), g.h_final[0, :n].numpy().copy(),
+            g.h_ts[0, :, :n].numpy().copy(), g.h_clusters.numpy().copy(),
+            int(batch.push_leaf_bits[0]) if batch is not None else 0, dix)
+
+
+def graph_count() -> int:
+    """Captured graphs of the calling thread (tests check the fast path was taken)."""
+    return sum(1 for v in _graphs().values() if v is not None)

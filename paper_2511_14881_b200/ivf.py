@@ -238,8 +238,14 @@ class IvfSearchOp:
             raise DimMismatch(self.dix.dim, int(queries.shape[-1]))
         clusters = self.probe(queries)
         qq = self.dix.quantize_queries(queries)
+        return self.scan(qq, clusters, filters), clusters
+
+    def scan(self, qq: torch.Tensor, clusters: torch.Tensor, filters=None) -> TopkOutput:
+        """The filtered top-k of int8 queries ``qq`` [B, dim_pad] over their probed
+        ``clusters`` [B, nprobe] (device-resident probe lists: no host round trip, so the
+        whole probe + scan can be captured in a CUDA graph)."""
         if self.path == "masked":
-            return self.op(qq, filters, masks=self.masks(clusters)), clusters
+            return self.op(qq, filters, masks=self.masks(clusters))
         words = self.probe_words(clusters)
         dev = qq.device
         k = max(self.k0, 1)
@@ -259,7 +265,7 @@ class IvfSearchOp:
             float(qp.global_min) if qp else 0.0, float(qp.global_max) if qp else 1.0,
             _native.stream_ptr()))
         self._keep = (qq, filters, words)
-        return out, clusters
+        return out
 
 
 # result / counter types: the reference's classes when it is importable (see _refapi)

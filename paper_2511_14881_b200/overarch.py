@@ -74,14 +74,19 @@ class DeviceCache:
     def rows_for(self, ids: torch.Tensor, valid: torch.Tensor) -> torch.Tensor:
         """Cache row of each id (int64 u64 bits); entries with ``valid`` False give -1.
         Raises ``MissingItem`` for a valid id the cache does not hold."""
-        key = _u64_order_key(ids)
-        pos = torch.searchsorted(self._sorted_key, key).clamp_(max=self._sorted_key.numel() - 1)
-        hit = self._sorted_key[pos] == key
-        bad = valid & ~hit
+        rows, bad = self.rows_and_missing(ids, valid)
         if bool(bad.any()):
             missing = int(ids[bad][0].item()) & 0xFFFFFFFFFFFFFFFF
             raise MissingItem(missing)
-        return torch.where(valid, self._row[pos], torch.full_like(pos, -1))
+        return rows
+
+    def rows_and_missing(self, ids: torch.Tensor, valid: torch.Tensor):
+        """``rows_for`` without the host check: (rows, bool mask of valid ids the cache
+        lacks), for callers that test it after a CUDA-graph replay."""
+        key = _u64_order_key(ids)
+        pos = torch.searchsorted(self._sorted_key, key).clamp_(max=self._sorted_key.numel() - 1)
+        hit = self._sorted_key[pos] == key
+        return torch.where(valid, self._row[pos], torch.full_like(pos, -1)), valid & ~hit
 
 
 # ------------------------------------------------------------------------------------
@@ -211,9 +216,11 @@ def mean_of_tasks_spec(task_names: list[str]) -> dict:
 
 
 def value_model_device(spec: dict, task_scores: dict[str, torch.Tensor],
-                       valid: torch.Tensor | None = None) -> torch.Tensor:
+                       valid: torch.Tensor | None = None, zero_flags: list | None = None
+                       ) -> torch.Tensor:
     """Element-wise float64 evaluation in the reference's operation order; both branches
-    of an ``if`` are evaluated; a zero divisor in any valid lane raises ``DivByZero``."""
+    of an ``if`` are evaluated; a zero divisor in any valid lane raises ``DivByZero`` (or,
+    with ``zero_flags``, appends the device flag tensor for the caller to test later)."""
     some = next(iter(task_scores.values()))
 
     def const(v):
@@ -241,7 +248,9 @@ def value_model_device(spec: dict, task_scores: dict[str, torch.Tensor],
             zero = den == 0.0
             if valid is not None:
                 zero = zero & valid
-            if bool(zero.any()):
+            if zero_flags is not None:
+                zero_flags.append(zero.any())
+            elif bool(zero.any()):
                 raise DivByZero("division by zero in value model")
             return walk(n["args"][0]) / den
         if op == "clamp":
@@ -442,6 +451,28 @@ def retrieve(engine, req) -> RetrieveResult:
     from .retrieval import StageTimings, codesigned_search
     start = time.perf_counter()
     timings, scan_stats, filter_stats = StageTimings(), ScanStats(), FilterStats()
+    if not _native.env_flag("FB_EAGER_B1"):
+        # one CUDA-graph replay for the whole request (fastpath.py)
+        from . import fastpath
+        names = [t.task_name for t in req.tasks]
+        vm = req.value_model if req.value_model is not None else engine.default_value_model
+        spec = value_model_spec(vm) or mean_of_tasks_spec(names)
+        fast = fastpath.retrieve_fast(
+            engine, req, lambda c: _weak_cached(_DEVICE_CACHE, c, DeviceCache.from_reference),
+            lambda sc: _weak_cached(_DEVICE_SCORER, sc, DeviceScorer.from_reference), spec, names)
+        if fast is not None:
+            ids_h, fin_h, ts_h, clusters, push_bits, dix = fast
+            for j in range(len(names)):
+                fastpath.scan_stats_for(dix.cluster_offsets, clusters[j], scan_stats)
+                if req.filter is not None:
+                    fastpath.filter_stats_for(dix.cluster_offsets, clusters[j], push_bits,
+                                              filter_stats)
+            items = [RetrievedItem(item_id=int(ids_h[i]), score=float(fin_h[i]),
+                                   task_scores={t: float(ts_h[j, i]) for j, t in enumerate(names)})
+                     for i in range(len(ids_h))]
+            timings.scan_us = timings.total_us = int((time.perf_counter() - start) * 1e6)
+            return RetrieveResult(items=items, stats=timings, scan=scan_stats,
+                                  filter_stats=filter_stats)
     cf = engine.compile(req.filter) if req.filter is not None else None
     per_task = []
     for task in req.tasks:

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import bitset
+from . import _native, bitset
 from ._device import to_dev
 from .bloom import FilterStats
 from .engine import device_index_for
@@ -44,7 +44,17 @@ def codesigned_search(ivf, bloom_index, cf: CompiledFilter | None, query: np.nda
                       nprobe: int, k0: int, scan_stats: ScanStats | None = None,
                       filter_stats: FilterStats | None = None,
                       timings: StageTimings | None = None) -> TopkResult:
-    """Probe, then one fused filter+scan launch sequence over the probed clusters."""
+    """Probe, then one fused filter+scan launch sequence over the probed clusters (one
+    CUDA-graph replay per call, fastpath.py; ``FB_EAGER_B1=1`` launches step by step)."""
+    if not _native.env_flag("FB_EAGER_B1"):
+        from . import fastpath
+        t0 = time.perf_counter()
+        r = fastpath.codesigned_search(ivf, bloom_index, cf, query, nprobe, k0,
+                                       scan_stats=scan_stats, filter_stats=filter_stats)
+        if r is not None:
+            if timings is not None:
+                timings.scan_us += int((time.perf_counter() - t0) * 1e6)
+            return r
     dix = device_index_for(ivf, bloom=bloom_index if cf is not None else None)
     raw_query = query
     query = np.asarray(query, dtype=np.float32)  # probing is float32 (ref ivf.py:263)

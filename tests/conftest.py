@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -13,6 +14,9 @@ ROOT = Path(__file__).resolve().parents[1]
 GOLDEN = ROOT / "tests" / "golden"
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
+# a single-request CUDA-graph capture that fails is a test failure, not a silent step-by-step
+# fallback (paper_2511_14881_b200/fastpath.py)
+os.environ.setdefault("FB_GRAPH_STRICT", "1")
 
 
 def pytest_configure(config):

@@ -9,6 +9,8 @@ _RECORD = []
 
 
 def pytest_configure(config):
+    import os
+    os.environ.setdefault("FB_GRAPH_STRICT", "1")
     import torch
     if not torch.cuda.is_available():
         raise RuntimeError("the drop-in needs a CUDA device")

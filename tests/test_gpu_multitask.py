@@ -164,3 +164,37 @@ def test_multitask_missing_cache_item_raises(cuda):
     op2 = fb.MultiTaskOp(idx, fb.DeviceCache(ids[keep], vecs[keep]), B, TASKS, 50, 10)
     with pytest.raises(MissingItem):
         op2(wl.queries.view(B, T, -1), None)
+
+
+def test_retrieve_graph_path_equals_eager(golden, monkeypatch):
+    """The CUDA-graph single-request path (fastpath.py) returns exactly what the
+    step-by-step path returns -- ids, scores, task scores, scan and filter counters --
+    for every golden request shape, and it is the path taken."""
+    from paper_2511_14881_b200 import fastpath
+    fb, z, meta, dix, cache = golden
+    ivf = SimpleNamespace(items_q=SimpleNamespace(data=z["items_q"],
+                                                  params=fb.QuantParams(float(z["qp"][0]), float(z["qp"][1]))),
+                          valid_mask=z["valid"], item_ids=z["item_ids"],
+                          cluster_offsets=z["offsets"], centroids=None,
+                          n_slots=z["items_q"].shape[0], dim=z["items_q"].shape[1])
+    bloom = fb.BloomIndex(fb.BloomParams(), z["planes"], z["items_q"].shape[0])
+    ref_cache = SimpleNamespace(item_ids=z["cache_ids"], vectors=z["cache_vectors"])
+    monkeypatch.setenv("FB_GRAPH_STRICT", "1")
+    for m in meta:
+        pre = f"r{m['r']}_"
+        engine = SimpleNamespace(ivf=ivf, bloom=bloom, cache=ref_cache,
+                                 scorer=ref_scorer(z, m["scorer"]), default_value_model=None,
+                                 compile=lambda e: fb.compile_filter(e, fb.BloomParams()))
+        tasks = tuple(SimpleNamespace(task_name=t, user_embedding=z[pre + "users"][j])
+                      for j, t in enumerate(TASKS))
+        req = SimpleNamespace(tasks=tasks, filter=json_to_expr(m["expr"]), nprobe=1, k0=m["k0"],
+                              topk=m["topk"], merge=m["merge"], value_model=m["vm"])
+        before = fastpath.graph_count()
+        fast = fb.retrieve(engine, req)
+        assert fastpath.graph_count() >= before and fastpath.graph_count() > 0
+        monkeypatch.setenv("FB_EAGER_B1", "1")
+        slow = fb.retrieve(engine, req)
+        monkeypatch.delenv("FB_EAGER_B1")
+        assert [(i.item_id, i.score, i.task_scores) for i in fast.items] == \
+            [(i.item_id, i.score, i.task_scores) for i in slow.items], m["r"]
+        assert vars(fast.scan) == vars(slow.scan) and vars(fast.filter_stats) == vars(slow.filter_stats)
