@@ -33,10 +33,13 @@ from .bloom import FilterStats
 from .engine import device_index_for
 from .errors import DivByZero, MissingItem
 from .filter_query import FilterBatch
-from .ivf import TILE_ROWS, IvfSearchOp, ScanStats, TopkResult
+from .ivf import IvfSearchOp, ScanStats, TopkResult, count_scan
 
 GRAPHS_PER_THREAD = 16
 _local = threading.local()
+# one capture or replay at a time: a capture forbids any other thread's legacy-stream work,
+# and replays share the device anyway (the host side of a request stays concurrent)
+_GPU_LOCK = threading.RLock()
 
 
 def _graphs() -> OrderedDict:
@@ -53,16 +56,8 @@ def _batch_sig(batch: FilterBatch | None):
 
 
 def scan_stats_for(cluster_offsets: np.ndarray, clusters: np.ndarray, stats: ScanStats) -> None:
-    """``search_clusters``' counters for the probed clusters (ref ivf.py:311-327): slots,
-    TILE_ROWS tiles, the largest tile."""
-    for c in clusters:
-        s, e = (int(x) for x in cluster_offsets[int(c)])
-        n = e - s
-        if n <= 0:
-            continue
-        stats.slots_scanned += n
-        stats.tiles += (n + TILE_ROWS - 1) // TILE_ROWS
-        stats.max_tile_rows = max(stats.max_tile_rows, min(n, TILE_ROWS))
+    """``search_clusters``' counters for the probed clusters (ivf.count_scan)."""
+    count_scan([cluster_offsets[int(c)] for c in clusters], stats)
 
 
 def filter_stats_for(cluster_offsets: np.ndarray, clusters: np.ndarray, push_bits: int,
@@ -93,19 +88,31 @@ class _Graph:
         if batch is not None:
             self.batch = batch.clone_host().to_device()
         self.tail = tail
-        pin = dict(pin_memory=True)
-        self.h_clusters = torch.empty((T, self.op.nprobe), dtype=torch.int64, **pin)
-        self.h_count = torch.empty((T,), dtype=torch.int32, **pin)
-        self.h_ids = torch.empty((T, max(k0, 1)), dtype=torch.int64, **pin)
-        self.h_scores = torch.empty((T, max(k0, 1)), dtype=torch.int32, **pin)
+        # every output lives in one flat device buffer written inside the graph and copied
+        # to pinned host memory by ONE copy after the replay (no pinned-memory copies inside
+        # the capture: torch's host allocator polls events, which a capture forbids)
+        P = self.op.nprobe
+        K = max(k0, 1)
+        spec = [("clusters", (T, P), torch.int64), ("count", (T,), torch.int32),
+                ("ids", (T, K), torch.int64), ("scores", (T, K), torch.int32)]
         if tail is not None:
             topk = tail["topk"]
-            self.h_out_ids = torch.empty((1, topk), dtype=torch.int64, **pin)
-            self.h_final = torch.empty((1, topk), dtype=torch.float64, **pin)
-            self.h_ts = torch.empty((1, T, topk), dtype=torch.float64, **pin)
-            self.h_n = torch.empty((1,), dtype=torch.int32, **pin)
-            self.h_missing = torch.empty((2,), dtype=torch.int64, **pin)  # flag, first id
-            self.h_zero = torch.empty((1,), dtype=torch.bool, **pin)
+            spec += [("out_ids", (1, topk), torch.int64), ("final", (1, topk), torch.float64),
+                     ("ts", (1, T, topk), torch.float64), ("n", (1,), torch.int32),
+                     ("missing", (2,), torch.int64), ("zero", (1,), torch.int32)]
+        offs, off = {}, 0
+        for name, shape, dt in spec:
+            nbytes = int(np.prod(shape)) * torch.empty((), dtype=dt).element_size()
+            offs[name] = (off, shape, dt)
+            off += (nbytes + 15) // 16 * 16
+        self.d_out = torch.zeros(max(off, 16), dtype=torch.uint8, device=dev)
+        self.h_out = torch.zeros(max(off, 16), dtype=torch.uint8, pin_memory=True)
+
+        def views(buf):
+            return {n: buf[o: o + int(np.prod(sh)) * torch.empty((), dtype=dt).element_size()]
+                    .view(dt).view(sh) for n, (o, sh, dt) in offs.items()}
+        self.d = views(self.d_out)
+        self.h = views(self.h_out)
         # eager warm-up (allocates lazily built state, raises the eager path's errors for
         # a malformed request shape before anything is captured), then the capture
         self._run()
@@ -118,10 +125,11 @@ class _Graph:
         clusters = self.op.probe(self.u32)
         qq = self.dix.quantize_queries(self.uq)
         out = self.op.scan(qq, clusters, self.batch)
-        self.h_clusters.copy_(clusters, non_blocking=True)
-        self.h_count.copy_(out.count, non_blocking=True)
-        self.h_ids.copy_(out.ids, non_blocking=True)
-        self.h_scores.copy_(out.scores, non_blocking=True)
+        d = self.d
+        d["clusters"].copy_(clusters)
+        d["count"].copy_(out.count)
+        d["ids"].copy_(out.ids)
+        d["scores"].copy_(out.scores)
         if self.tail is not None:
             self._run_tail(out)
 
@@ -134,8 +142,9 @@ class _Graph:
         rows, bad = t["cache"].rows_and_missing(merged, valid)
         badc = bad.reshape(-1)
         first = torch.argmax(badc.to(torch.int32)).view(1)   # device-only indexing below
-        self.h_missing[0:1].copy_(badc.any().to(torch.int64).view(1), non_blocking=True)
-        self.h_missing[1:2].copy_(merged.reshape(-1).index_select(0, first), non_blocking=True)
+        d = self.d
+        d["missing"][0:1].copy_(badc.any().to(torch.int64).view(1))
+        d["missing"][1:2].copy_(merged.reshape(-1).index_select(0, first))
         ts = t["scorer"].score(t["cache"], rows, mcount, self.u32[None], t["names"])
         zero = []
         final = value_model_device(t["spec"], {n: ts[:, j, :] for j, n in enumerate(t["names"])},
@@ -143,27 +152,30 @@ class _Graph:
         anyz = torch.zeros((1,), dtype=torch.bool, device=merged.device)
         for z in zero:
             anyz |= z.view(1)
-        self.h_zero.copy_(anyz, non_blocking=True)
+        d["zero"].copy_(anyz.to(torch.int32))
         final = torch.where(valid, final, torch.full_like(final, -float("inf")))
         topk = t["topk"]
         order = torch.sort(final, dim=1, descending=True, stable=True).indices[:, :topk]
         n = torch.clamp(mcount, max=topk)
-        self.h_out_ids.copy_(torch.gather(merged, 1, order), non_blocking=True)
-        self.h_final.copy_(torch.gather(final, 1, order), non_blocking=True)
-        self.h_ts.copy_(torch.gather(ts, 2, order[:, None, :].expand(1, T, -1)), non_blocking=True)
-        self.h_n.copy_(n, non_blocking=True)
+        d["out_ids"].copy_(torch.gather(merged, 1, order))
+        d["final"].copy_(torch.gather(final, 1, order))
+        d["ts"].copy_(torch.gather(ts, 2, order[:, None, :].expand(1, T, -1)))
+        d["n"].copy_(n.to(torch.int32))
 
     def replay(self, users: np.ndarray, batch: FilterBatch | None):
         """users float [T, dim] (the caller's dtype) -> run; host outputs valid after."""
-        self.u32.copy_(torch.from_numpy(np.ascontiguousarray(users, dtype=np.float32)))
-        src = np.ascontiguousarray(users, dtype=np.float32 if self.uq.dtype == torch.float32
-                                   else np.float64)
-        self.uq.copy_(torch.from_numpy(src))
-        if batch is not None:
-            for d, h in zip(self.batch._dev, batch.host_arrays()):
-                d.copy_(torch.from_numpy(h))
-        self.graph.replay()
-        torch.cuda.current_stream().synchronize()
+        u32 = torch.from_numpy(np.ascontiguousarray(users, dtype=np.float32))
+        src = torch.from_numpy(np.ascontiguousarray(
+            users, dtype=np.float32 if self.uq.dtype == torch.float32 else np.float64))
+        with _GPU_LOCK:
+            self.u32.copy_(u32)
+            self.uq.copy_(src)
+            if batch is not None:
+                for d, h in zip(self.batch._dev, batch.host_arrays()):
+                    d.copy_(torch.from_numpy(h))
+            self.graph.replay()
+            self.h_out.copy_(self.d_out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
 
 
 def _get_graph(key, make):
@@ -175,7 +187,8 @@ def _get_graph(key, make):
         g.move_to_end(key)
         return g[key]
     try:
-        hit = make()
+        with _GPU_LOCK:
+            hit = make()
     except Exception:  # noqa: BLE001 -- remembered as "eager only" for this shape
         if _native.env_flag("FB_GRAPH_STRICT"):  # tests: a capture failure is a failure
             raise
@@ -215,14 +228,15 @@ def codesigned_search(ivf, bloom_index, cf, query, nprobe: int, k0: int, scan_st
     if g is None:
         return None
     g.replay(raw[None], batch)
-    clusters = g.h_clusters[0].numpy().copy()
+    h = g.h
+    clusters = h["clusters"][0].numpy().copy()
     if scan_stats is not None:
         scan_stats_for(dix.cluster_offsets, clusters, scan_stats)
     if filter_stats is not None and cf is not None:
         filter_stats_for(dix.cluster_offsets, clusters, int(batch.push_leaf_bits[0]), filter_stats)
-    n = int(g.h_count[0])
-    return TopkResult(item_ids=g.h_ids[0, :n].numpy().view(np.uint64).copy(),
-                      scores=g.h_scores[0, :n].numpy().copy(), k_requested=int(k0))
+    n = int(h["count"][0])
+    return TopkResult(item_ids=h["ids"][0, :n].numpy().view(np.uint64).copy(),
+                      scores=h["scores"][0, :n].numpy().copy(), k_requested=int(k0))
 
 
 def retrieve_fast(engine, req, cache_factory, scorer_factory, spec, names):
@@ -255,13 +269,14 @@ def retrieve_fast(engine, req, cache_factory, scorer_factory, spec, names):
     if g is None:
         return None
     g.replay(U, batch)
-    if int(g.h_missing[0]):
-        raise MissingItem(int(g.h_missing[1]) & 0xFFFFFFFFFFFFFFFF)
-    if bool(g.h_zero[0]):
+    h = g.h
+    if int(h["missing"][0]):
+        raise MissingItem(int(h["missing"][1]) & 0xFFFFFFFFFFFFFFFF)
+    if int(h["zero"][0]):
         raise DivByZero("division by zero in value model")
-    n = int(g.h_n[0])
-    return (g.h_out_ids[0, :n].numpy().view(np.uint64).copy(), g.h_final[0, :n].numpy().copy(),
-            g.h_ts[0, :, :n].numpy().copy(), g.h_clusters.numpy().copy(),
+    n = int(h["n"][0])
+    return (h["out_ids"][0, :n].numpy().view(np.uint64).copy(), h["final"][0, :n].numpy().copy(),
+            h["ts"][0, :, :n].numpy().copy(), h["clusters"].numpy().copy(),
             int(batch.push_leaf_bits[0]) if batch is not None else 0, dix)
 
 

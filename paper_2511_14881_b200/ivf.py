@@ -61,20 +61,28 @@ def cluster_ranges(dix: DeviceIndex, clusters) -> np.ndarray:
     return np.ascontiguousarray(offs[cl].astype(np.int64))
 
 
+def count_scan(ranges, stats: ScanStats) -> None:
+    """``search_clusters``' counters for slot ranges, in the reference's tile contract (ref
+    ivf.py:311-327: slots per range, ``TILE_ROWS``-row tiles, the largest tile) -- the
+    GPU's own 256-item tiles are an implementation detail the counters do not expose."""
+    for s, e in ranges:
+        n = int(e) - int(s)
+        stats.slots_scanned += n
+        if n > 0:
+            stats.tiles += (n + TILE_ROWS - 1) // TILE_ROWS
+            stats.max_tile_rows = max(stats.max_tile_rows, min(n, TILE_ROWS))
+
+
 def run_scan(dix: DeviceIndex, query_q: np.ndarray, ranges: np.ndarray, mask, topk: int,
              filters=None, stats: ScanStats | None = None, flags: int = 0) -> TopkResult:
     """B = 1 view of the batched operator."""
     total = int(sum(int(e) - int(s) for s, e in ranges))
     if stats is not None:
-        stats.slots_scanned += total
+        count_scan(ranges, stats)
     if topk <= 0 or total == 0:
         return _empty(topk)
     k_eff = min(int(topk), total)
     op = cached_op(dix, 1, k_eff, ranges, flags)
-    if stats is not None:
-        st = op.stats()
-        stats.tiles += int(st.tiles)
-        stats.max_tile_rows = max(stats.max_tile_rows, int(st.max_tile_rows))
     q = dix.pad_queries(query_q)
     masks = None
     if mask is not None:

@@ -208,7 +208,9 @@ def test_scan_stats_and_codesign_accounting(fb):
     probed = fb.probe_centroids(ivf, qf, 3)
     expected = sum(int(e - s) for s, e in (z["s2_offsets"][int(c)] for c in probed))
     assert scan.slots_scanned == expected and filt.slots_evaluated == expected
-    assert 0 < scan.max_tile_rows <= 4096 and scan.tiles >= 1
+    sizes = [int(e - s) for s, e in (z["s2_offsets"][int(c)] for c in probed)]
+    assert scan.tiles == sum((n + 4095) // 4096 for n in sizes if n > 0)  # ref ivf.py:311-327
+    assert scan.max_tile_rows == max([min(n, 4096) for n in sizes if n > 0] or [0])
     assert filt.words_read == sum(len(qb.set_bits) for _, _, qb in cf.leaves) * expected // 64
 
 
