@@ -42,3 +42,65 @@ def pad_rows_i8(items: torch.Tensor, dim_pad: int, n_rows: int) -> torch.Tensor:
 
 def round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
+
+
+class IdentityCache:
+    """Values keyed on an object's IDENTITY, dropped when the object is collected.
+
+    The reference's engine parts (``IvfIndex``, ``BloomIndex``, ``EmbeddingCache``, the
+    scorers) are ``@dataclass`` instances: ``eq=True`` makes them unhashable, so a
+    ``WeakKeyDictionary`` cannot hold them and every request would re-upload them. Entries
+    here hold a weak reference (the value dies with its host object, so a snapshot hot swap
+    frees the old device copy); objects that cannot be weakly referenced are held strongly,
+    at most ``max_strong`` of them (LRU)."""
+
+    def __init__(self, max_strong: int = 8):
+        import threading
+        from collections import OrderedDict
+        self._d: dict = {}
+        self._strong: "OrderedDict" = OrderedDict()
+        self._max_strong = max_strong
+        self._lock = threading.Lock()
+
+    def get(self, obj):
+        with self._lock:
+            e = self._d.get(id(obj))
+            if e is None:
+                return None
+            ref, val = e
+            if ref is None:  # strongly held
+                if self._strong.get(id(obj)) is not obj:
+                    return None
+                self._strong.move_to_end(id(obj))
+                return val
+            return val if ref() is obj else None
+
+    def put(self, obj, val) -> None:
+        import weakref
+        k = id(obj)
+
+        def drop(r, k=k):
+            with self._lock:
+                e = self._d.get(k)
+                if e is not None and e[0] is r:
+                    del self._d[k]
+
+        try:
+            ref = weakref.ref(obj, drop)
+        except TypeError:
+            ref = None
+        with self._lock:
+            self._d[k] = (ref, val)
+            if ref is None:
+                self._strong[k] = obj
+                self._strong.move_to_end(k)
+                while len(self._strong) > self._max_strong:
+                    old, _ = self._strong.popitem(last=False)
+                    self._d.pop(old, None)
+
+    def get_or_make(self, obj, make):
+        hit = self.get(obj)
+        if hit is None:
+            hit = make(obj)
+            self.put(obj, hit)
+        return hit

@@ -14,7 +14,6 @@ from __future__ import annotations
 
 import ctypes
 import threading
-import weakref
 from collections import OrderedDict
 from dataclasses import dataclass
 
@@ -22,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _native
-from ._device import device, round_up, to_dev, to_dev_u64, u64_host
+from ._device import IdentityCache, device, round_up, to_dev, to_dev_u64, u64_host
 from .bloom import BloomIndex, BloomParams
 from .filter_query import FilterBatch
 from .quantize import QuantParams, quantize_device
@@ -182,7 +181,7 @@ class DeviceIndex:
         return out
 
 
-_REF_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_REF_CACHE = IdentityCache()
 
 
 def device_index_for(index, bloom=None) -> DeviceIndex:
@@ -191,12 +190,7 @@ def device_index_for(index, bloom=None) -> DeviceIndex:
     uploaded once and cached on the object."""
     if isinstance(index, DeviceIndex):
         return index
-    key = index
-    cached = None
-    try:
-        cached = _REF_CACHE.get(key)
-    except TypeError:
-        key = None
+    cached = _REF_CACHE.get(index)
     if cached is not None and (bloom is None or cached.bloom is not None):
         return cached
     if bloom is not None and not isinstance(bloom, BloomIndex):
@@ -208,12 +202,43 @@ def device_index_for(index, bloom=None) -> DeviceIndex:
         qp=QuantParams(float(qp.global_min), float(qp.global_max)),
         cluster_offsets=np.asarray(index.cluster_offsets, dtype=np.int64),
         centroids=getattr(getattr(index, "centroids", None), "vectors", None))
-    if key is not None:
-        try:
-            _REF_CACHE[key] = dix
-        except TypeError:
-            pass
+    _REF_CACHE.put(index, dix)
     return dix
+
+
+# Plans whose owner was collected while this thread was capturing a CUDA graph: a plan
+# destroy is a cudaFree, which would invalidate the capture, so it waits for the next plan
+# create (fastpath.py captures single-request graphs; the GC can run a finalizer anywhere).
+_DEFERRED_PLANS: list = []
+_DEFERRED_LOCK = threading.Lock()
+
+
+def _capturing() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_current_stream_capturing()
+    except Exception:  # noqa: BLE001 -- interpreter shutdown
+        return False
+
+
+def _destroy_plan(plan) -> None:
+    if _capturing():
+        with _DEFERRED_LOCK:
+            _DEFERRED_PLANS.append(plan)
+        return
+    try:
+        _native.load_library().fb_topk_plan_destroy(plan)
+    except Exception:  # noqa: BLE001 -- interpreter shutdown
+        pass
+
+
+def _drain_deferred_plans() -> None:
+    if not _DEFERRED_PLANS or _capturing():
+        return
+    with _DEFERRED_LOCK:
+        plans, _DEFERRED_PLANS[:] = list(_DEFERRED_PLANS), []
+    for p in plans:
+        _destroy_plan(p)
 
 
 class TopkOp:
@@ -228,6 +253,7 @@ class TopkOp:
         r = np.ascontiguousarray(np.asarray(ranges, dtype=np.int64).reshape(-1, 2))
         self.ranges = r
         self._idx_struct = index.struct()
+        _drain_deferred_plans()
         plan = ctypes.c_void_p()
         _native.check(_native.lib().fb_topk_plan_create(
             ctypes.byref(self._idx_struct), self.n_queries, self.k, r.ctypes.data, r.shape[0],
@@ -237,10 +263,7 @@ class TopkOp:
     def __del__(self):
         plan = getattr(self, "_plan", None)
         if plan is not None and plan.value:
-            try:
-                _native.load_library().fb_topk_plan_destroy(plan)
-            except Exception:  # interpreter shutdown
-                pass
+            _destroy_plan(plan)
             self._plan = None
 
     def _unfiltered_batch(self) -> FilterBatch:

@@ -20,6 +20,7 @@ value model, query dtype and the packed filter's shape.
 
 from __future__ import annotations
 
+import gc
 import json
 import threading
 from collections import OrderedDict
@@ -37,9 +38,71 @@ from .ivf import IvfSearchOp, ScanStats, TopkResult, count_scan
 
 GRAPHS_PER_THREAD = 16
 _local = threading.local()
-# one capture or replay at a time: a capture forbids any other thread's legacy-stream work,
-# and replays share the device anyway (the host side of a request stays concurrent)
-_GPU_LOCK = threading.RLock()
+
+
+class _CaptureLock:
+    """Captures run alone (exclusive); replays run concurrently (shared), each thread on
+    its own stream, so the small single-request graphs of N server threads overlap on the
+    device instead of queueing behind one lock and one stream."""
+
+    def __init__(self):
+        self._cv = threading.Condition()
+        self._readers = 0
+        self._writer = False
+
+    def shared(self):
+        lock = self
+
+        class _S:
+            def __enter__(self):
+                with lock._cv:
+                    while lock._writer:
+                        lock._cv.wait()
+                    lock._readers += 1
+
+            def __exit__(self, *exc):
+                with lock._cv:
+                    lock._readers -= 1
+                    if lock._readers == 0:
+                        lock._cv.notify_all()
+        return _S()
+
+    def exclusive(self):
+        lock = self
+
+        class _X:
+            def __enter__(self):
+                with lock._cv:
+                    while lock._writer or lock._readers:
+                        lock._cv.wait()
+                    lock._writer = True
+
+            def __exit__(self, *exc):
+                with lock._cv:
+                    lock._writer = False
+                    lock._cv.notify_all()
+        return _X()
+
+
+_GPU_LOCK = _CaptureLock()
+
+
+def _stream() -> torch.cuda.Stream:
+    """The calling thread's stream for captures and replays."""
+    s = getattr(_local, "stream", None)
+    if s is None:
+        s = _local.stream = torch.cuda.Stream()
+    return s
+
+
+def _ck(tag: str) -> None:
+    """FB_CAPTURE_TRACE=1: print the current stream's capture status after a step (finds
+    the step that invalidates a capture)."""
+    if not _native.env_flag("FB_CAPTURE_TRACE"):
+        return
+    from cuda.bindings import runtime as rt
+    err, st = rt.cudaStreamIsCapturing(torch.cuda.current_stream().cuda_stream)
+    print(f"[capture] {tag}: {st}", flush=True)
 
 
 def _graphs() -> OrderedDict:
@@ -82,11 +145,22 @@ class _Graph:
         dev = device()
         self.dix, self.T, self.k0 = dix, T, k0
         self.op = IvfSearchOp(dix, T, nprobe, k0, path="probe")
-        self.u32 = torch.zeros((T, dix.dim), dtype=torch.float32, device=dev)
-        self.uq = torch.zeros((T, dix.dim), dtype=qdtype, device=dev)
+        # inputs: the task vectors as float32 (probe) and in the caller's dtype (quantise),
+        # staged in one pinned buffer and sent by ONE copy per request
+        nq = T * dix.dim * torch.empty((), dtype=qdtype).element_size()
+        n32 = T * dix.dim * 4
+        self.h_in = torch.zeros(n32 + nq, dtype=torch.uint8, pin_memory=True)
+        self.d_in = torch.zeros(n32 + nq, dtype=torch.uint8, device=dev)
+        self.u32 = self.d_in[:n32].view(torch.float32).view(T, dix.dim)
+        self.uq = self.d_in[n32:].view(qdtype).view(T, dix.dim)
+        self.h_u32 = self.h_in[:n32].view(torch.float32).view(T, dix.dim).numpy()
+        self.h_uq = self.h_in[n32:].view(qdtype).view(T, dix.dim).numpy()
         self.batch = None
+        self.h_batch = []
         if batch is not None:
             self.batch = batch.clone_host().to_device()
+            self.h_batch = [torch.zeros(d.shape, dtype=d.dtype, pin_memory=True)
+                            for d in self.batch._dev]
         self.tail = tail
         # every output lives in one flat device buffer written inside the graph and copied
         # to pinned host memory by ONE copy after the replay (no pinned-memory copies inside
@@ -118,13 +192,25 @@ class _Graph:
         self._run()
         torch.cuda.current_stream().synchronize()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
-            self._run()
+        # no collector pass inside the capture: a finalizer that frees device memory (a
+        # collected TopkOp's plan) would invalidate it (engine._destroy_plan defers those too)
+        gc.collect()
+        gc_was = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.graph(self.graph, capture_error_mode="thread_local"):
+                self._run()
+        finally:
+            if gc_was:
+                gc.enable()
 
     def _run(self):
         clusters = self.op.probe(self.u32)
+        _ck("probe")
         qq = self.dix.quantize_queries(self.uq)
+        _ck("quantize")
         out = self.op.scan(qq, clusters, self.batch)
+        _ck("scan")
         d = self.d
         d["clusters"].copy_(clusters)
         d["count"].copy_(out.count)
@@ -138,6 +224,7 @@ class _Graph:
         t = self.tail
         T, k = self.T, self.k0
         merged, mcount = merge_device(out.ids.view(1, T, k), out.count.view(1, T), t["merge"])
+        _ck("merge")
         valid = torch.arange(merged.shape[1], device=merged.device)[None, :] < mcount[:, None]
         rows, bad = t["cache"].rows_and_missing(merged, valid)
         badc = bad.reshape(-1)
@@ -145,10 +232,13 @@ class _Graph:
         d = self.d
         d["missing"][0:1].copy_(badc.any().to(torch.int64).view(1))
         d["missing"][1:2].copy_(merged.reshape(-1).index_select(0, first))
+        _ck("rows")
         ts = t["scorer"].score(t["cache"], rows, mcount, self.u32[None], t["names"])
+        _ck("score")
         zero = []
         final = value_model_device(t["spec"], {n: ts[:, j, :] for j, n in enumerate(t["names"])},
                                    valid, zero_flags=zero)
+        _ck("value_model")
         anyz = torch.zeros((1,), dtype=torch.bool, device=merged.device)
         for z in zero:
             anyz |= z.view(1)
@@ -164,18 +254,20 @@ class _Graph:
 
     def replay(self, users: np.ndarray, batch: FilterBatch | None):
         """users float [T, dim] (the caller's dtype) -> run; host outputs valid after."""
-        u32 = torch.from_numpy(np.ascontiguousarray(users, dtype=np.float32))
-        src = torch.from_numpy(np.ascontiguousarray(
-            users, dtype=np.float32 if self.uq.dtype == torch.float32 else np.float64))
-        with _GPU_LOCK:
-            self.u32.copy_(u32)
-            self.uq.copy_(src)
+        # the previous replay on this thread's stream ended with a synchronize, so the
+        # pinned staging buffers are free to overwrite
+        np.copyto(self.h_u32, users, casting="unsafe")
+        np.copyto(self.h_uq, users, casting="unsafe")
+        st = _stream()
+        with _GPU_LOCK.shared(), torch.cuda.stream(st):
+            self.d_in.copy_(self.h_in, non_blocking=True)
             if batch is not None:
-                for d, h in zip(self.batch._dev, batch.host_arrays()):
-                    d.copy_(torch.from_numpy(h))
+                for d, hp, h in zip(self.batch._dev, self.h_batch, batch.host_arrays()):
+                    hp.numpy()[...] = h
+                    d.copy_(hp, non_blocking=True)
             self.graph.replay()
             self.h_out.copy_(self.d_out, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            st.synchronize()
 
 
 def _get_graph(key, make):
@@ -187,8 +279,9 @@ def _get_graph(key, make):
         g.move_to_end(key)
         return g[key]
     try:
-        with _GPU_LOCK:
+        with _GPU_LOCK.exclusive(), torch.cuda.stream(_stream()):
             hit = make()
+            torch.cuda.current_stream().synchronize()
     except Exception:  # noqa: BLE001 -- remembered as "eager only" for this shape
         if _native.env_flag("FB_GRAPH_STRICT"):  # tests: a capture failure is a failure
             raise

@@ -27,14 +27,13 @@ Here the whole batch of requests runs on the device:
 from __future__ import annotations
 
 import time
-import weakref
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _native
-from ._device import device, to_dev, to_dev_u64, u64_host
+from ._device import IdentityCache, device, to_dev, to_dev_u64, u64_host
 from .bloom import BloomParams, FilterStats
 from .engine import DeviceIndex, TopkOp, _u64_order_key
 from .errors import DivByZero, FiltraError, MissingItem, UnknownTask
@@ -426,22 +425,12 @@ class RetrieveResult:
 
 # device copies of the reference engine's embedding cache / scorer, keyed weakly on the
 # host objects: a snapshot hot swap drops the old engine and with it its HBM copy
-_DEVICE_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
-_DEVICE_SCORER: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_DEVICE_CACHE = IdentityCache()
+_DEVICE_SCORER = IdentityCache()
 
 
-def _weak_cached(table, obj, make):
-    try:
-        hit = table.get(obj)
-    except TypeError:  # unhashable / not weak-referenceable: no caching
-        return make(obj)
-    if hit is None:
-        hit = make(obj)
-        try:
-            table[obj] = hit
-        except TypeError:
-            pass
-    return hit
+def _weak_cached(table: IdentityCache, obj, make):
+    return table.get_or_make(obj, make)
 
 
 def retrieve(engine, req) -> RetrieveResult:

@@ -83,3 +83,35 @@ def test_integration_install_patches_every_binding():
         "assert filtra.ivf.search_clusters is orig\n"
         "print('ok', len(rec))\n")
     assert out.startswith("ok")
+
+
+def test_identity_cache_unhashable_dataclass():
+    """Reference engine parts are eq-dataclasses (unhashable): the device-copy caches key
+    them by identity and drop the entry when the host object is collected."""
+    import gc
+    from dataclasses import dataclass
+
+    import numpy as np
+
+    from paper_2511_14881_b200._device import IdentityCache
+
+    @dataclass
+    class Part:
+        data: np.ndarray
+
+    c = IdentityCache()
+    a, b = Part(np.zeros(3)), Part(np.zeros(3))
+    made = []
+    assert c.get_or_make(a, lambda o: made.append(1) or "A") == "A"
+    assert c.get_or_make(a, lambda o: made.append(1) or "A2") == "A"
+    assert c.get_or_make(b, lambda o: made.append(1) or "B") == "B"
+    assert len(made) == 2
+    del a
+    gc.collect()
+    assert len(c._d) == 1
+    # objects without weakref support are held strongly, LRU-bounded
+    s = IdentityCache(max_strong=2)
+    objs = [(i,) for i in range(3)]
+    for o in objs:
+        s.put(o, o[0])
+    assert s.get(objs[0]) is None and s.get(objs[2]) == 2
