@@ -103,13 +103,17 @@ def load_library() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not _LIB_PATH.exists():
+    path = _LIB_PATH
+    variant = os.environ.get("FB_LIB_VARIANT", "")  # A/B builds of the same sources (tools/)
+    if variant:
+        path = _LIB_PATH.with_name(f"libfiltra_b200_{variant}.so")
+    if not path.exists():
         raise NativeUnavailable(
-            f"{_LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
-    lib = ctypes.CDLL(str(_LIB_PATH))
+            f"{path} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(str(path))
     _declare(lib)
     if lib.fb_abi_version() != ABI_VERSION:
-        raise NativeUnavailable(f"{_LIB_PATH} has ABI {lib.fb_abi_version()}, expected "
+        raise NativeUnavailable(f"{path} has ABI {lib.fb_abi_version()}, expected "
                                 f"{ABI_VERSION}: rebuild the library")
     _lib = lib
     return lib

@@ -94,7 +94,14 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
 // Producers several stages ahead of their consumers: one try_wait, then test_wait polls
 // spaced by __nanosleep, so a producer blocked on a full ring gives its issue slots to the
 // warps sharing its scheduler (a spinning try_wait loop does not).
+#ifndef FB_BACKOFF
+#define FB_BACKOFF 0
+#endif
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
+#if FB_BACKOFF == 1
+  mbar_wait(b, parity);
+  return;
+#endif
   const uint32_t a = su32(b);
   uint32_t ok = 0;
   asm volatile(
@@ -105,7 +112,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) 
       : "r"(a), "r"(parity)
       : "memory");
   while (!ok) {
-    __nanosleep(128);
+    __nanosleep(FB_BACKOFF == 2 ? 1000 : 128);
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"

@@ -23,6 +23,7 @@
 #include "fb_ptx.cuh"
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstdio>
 
@@ -266,6 +267,16 @@ __device__ __forceinline__ void stage_queries(const TcArgs& a, const Smem& m, in
   for (int i = threadIdx.x; i < a.n_planes; i += nt) pl[i] = a.plane_list[i];
 }
 
+// Plane stage layout in the CNF kernels: plane slot p's 32-byte tile row as two 16-byte
+// halves, swapped when bit 2 of p is set, so the builders' 16-byte loads of 32 random slots
+// spread over all eight 16-byte bank groups (not just the even ones)
+#ifndef FB_PLANE_SWZ
+#define FB_PLANE_SWZ 1
+#endif
+__device__ __forceinline__ uint32_t plane_half_off(uint32_t slot, uint32_t half) {
+  return (2u * slot + (half ^ (FB_PLANE_SWZ ? ((slot >> 2) & 1u) : 0u))) * 16u;
+}
+
 // ================= producer (one warp): TMA item tile + Bloom plane words ==============
 // The per-tile global reads (work item, then its validity & range words) are issued one
 // tile ahead, so their latency never sits on the producer's critical path.
@@ -273,7 +284,7 @@ __device__ __forceinline__ void stage_queries(const TcArgs& a, const Smem& m, in
 // do both, or two warps split them so the gather never queues behind an item stage).
 __device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap* tmap,
                                               const Smem& m, int lane, bool do_items,
-                                              bool do_planes) {
+                                              bool do_planes, bool swz = false) {
   uint8_t* smem = m.base;
   uint8_t* sB = m.sB;
   uint8_t* sP = m.sP;
@@ -362,8 +373,9 @@ __device__ __forceinline__ void producer_loop(const TcArgs& a, const CUtensorMap
             const int e = e0 + 32 * u;
             if (e < n2) {
               const uint64_t* src = a.planes + (int64_t)pl[u] * a.n_words + col0 + 2 * (e & 1);
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                               dst + (uint32_t)e * 16u),
+              const uint32_t doff = swz ? plane_half_off((uint32_t)(e >> 1), (uint32_t)(e & 1))
+                                        : (uint32_t)e * 16u;
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + doff),
                            "l"(src)
                            : "memory");
             }
@@ -448,7 +460,7 @@ constexpr int kCnfDense0 = 8;
 constexpr int kCnfDenseWarps = 4;
 constexpr int kCnfHit0 = 12;
 constexpr int kCnfHitWarps = 8;
-constexpr int kSurvCap = 64;  // u16 survivor entries per hit warp: (lane << 8) | item
+constexpr int kSurvCap = 128;  // u16 survivor entries per hit warp: (lane << 8) | item
 // named barrier ids (0 is __syncthreads) and their thread counts
 constexpr int kNbHmFull = 1, kNbHmEmpty = 3, kNbLeafFull = 5, kNbLeafEmpty = 7;  // + stage
 constexpr int kNbHmCount = 32 * (kCnfDenseWarps + kCnfHitWarps);
@@ -457,8 +469,17 @@ constexpr int kNbLeafCount = 32 * (kCnfBuilders + kCnfHitWarps);
 
 // ================= CNF column builders (nb warps): Bloom test per literal column, then a
 // 32x32 bit transpose so each item row holds its column bits ==========================
+
+struct NoTail {
+  __device__ void operator()(int) const {}
+};
+// tail(it) runs after the builders have published tile it + 1's column bits (and once more
+// after the last tile): mode 3 drains tile it's survivors there
+template <typename Tail = NoTail>
 __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m, int lw, int nb,
-                                                 int lane, bool ff) {
+                                                 int lane, bool ff, int leaf_count = kNbLeafCount,
+                                                 Tail tail = Tail()) {
+  constexpr bool kDrain = !std::is_same<Tail, NoTail>::value;
   uint8_t* sP = m.sP;
   uint8_t* sL = m.sL;
   const int16_t* sLS = m.sLS;
@@ -473,9 +494,11 @@ __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m,
       const uint32_t ph = (uint32_t)(it >> 1) & 1u;
       (void)ph;
       mbar_wait_backoff(planes_full + ps, pph);  // a plane stage lands ~1 tile ahead
-      if (it >= 2) nb_sync(kNbLeafEmpty + st, kNbLeafCount);
+      if (it >= 2) nb_sync(kNbLeafEmpty + st, leaf_count);
+      if (kDrain && lw == 0) FB_TR(a, it, 12);
       const uint32_t p_s = su32(sP + (size_t)ps * a.plane_stage_bytes);
       uint32_t* TB = reinterpret_cast<uint32_t*>(sL + (size_t)st * a.leaf_stage_bytes);
+      const uint32_t sls_s = su32(sLS);
       for (int cb = lw; cb < ((a.dbg & 4) ? 0 : a.cnf_words); cb += nb) {  // 32-column block
         const int col = cb * 32 + lane;
         // the column's 256 tile bits: AND of its planes' 32-byte rows (8 x u32, one per
@@ -486,14 +509,14 @@ __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m,
         if (col < a.n_cols) {
           bool neg = false;
           for (int j = 0; j < a.k_max; ++j) {
-            int sl = sLS[col * a.k_max + j];
+            int sl = (int)(int16_t)lds16(sls_s + 2u * (uint32_t)(col * a.k_max + j));
             if (j == 0) {
               neg = (sl & 0x4000) != 0;
               sl &= ~0x4000;
             }
             if (sl < 0) break;
-            const uint4 lo = lds128(p_s + (uint32_t)sl * 32u);
-            const uint4 hi = lds128(p_s + (uint32_t)sl * 32u + 16u);
+            const uint4 lo = lds128(p_s + plane_half_off((uint32_t)sl, 0u));
+            const uint4 hi = lds128(p_s + plane_half_off((uint32_t)sl, 1u));
             m[0] &= lo.x; m[1] &= lo.y; m[2] &= lo.z; m[3] &= lo.w;
             m[4] &= hi.x; m[5] &= hi.y; m[6] &= hi.z; m[7] &= hi.w;
           }
@@ -512,32 +535,43 @@ __device__ __forceinline__ void cnf_builder_loop(const TcArgs& a, const Smem& m,
                        : "memory");
           continue;
         }
-        // eight 32x32 transposes in lockstep (independent shuffles per round)
+        // eight 32x32 transposes in lockstep (independent shuffles per round). Per word and
+        // round: the partner's word rotated by s (left in the lower lane of a pair, right in
+        // the upper) lands its exchanged bit blocks in place, so one SHFL + one rotate + one
+        // LOP3 (keep = the lane's own blocks) does the round
         const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
           const int sft = 16 >> k;
-          const uint32_t mk = masks[k];
           const bool upper = (lane & sft) != 0;
-          uint32_t y[8];
+          const uint32_t keep = upper ? ~masks[k] : masks[k];
+          const uint32_t amt = upper ? (uint32_t)(32 - sft) : (uint32_t)sft;
 #pragma unroll
-          for (int ib = 0; ib < 8; ++ib) y[ib] = __shfl_xor_sync(0xffffffffu, m[ib], sft);
-#pragma unroll
-          for (int ib = 0; ib < 8; ++ib)
-            m[ib] = upper ? ((m[ib] & ~mk) | ((y[ib] & ~mk) >> sft))
-                          : ((m[ib] & mk) | ((y[ib] & mk) << sft));
+          for (int ib = 0; ib < 8; ++ib) {
+            const uint32_t y = __shfl_xor_sync(0xffffffffu, m[ib], sft);
+            const uint32_t rot = __funnelshift_l(y, y, amt);
+            m[ib] = (m[ib] & keep) | (rot & ~keep);
+          }
         }
 #pragma unroll
         for (int ib = 0; ib < 8; ++ib) TB[(ib * 32 + lane) * a.tb_stride + cb] = m[ib];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(planes_empty + ps);  // one arrival per builder warp
-      nb_arrive(kNbLeafFull + st, kNbLeafCount);
+      nb_arrive(kNbLeafFull + st, leaf_count);
       if (++ps == PS) { ps = 0; pph ^= 1u; }
+      if constexpr (kDrain) {
+        if (lw == 0) FB_TR(a, it, 13);
+        if (it >= 1) tail(it - 1);
+        if (lw == 0 && it >= 1) FB_TR(a, it - 1, 14);
+      }
+    }
+    if constexpr (kDrain) {
+      if (it >= 1) tail(it - 1);
     }
     // retire the hit pass's releases of the last two stages (every barrier phase completes)
     for (int t = it; t < it + 2; ++t)
-      if (t >= 2) nb_sync(kNbLeafEmpty + (t & 1), kNbLeafCount);
+      if (t >= 2) nb_sync(kNbLeafEmpty + (t & 1), leaf_count);
 }
 
 // ---- tensor memory -----------------------------------------------------------------------
@@ -864,6 +898,7 @@ __device__ __forceinline__ void drain_survivors(const TcArgs& a, const Smem& m, 
                                                 uint32_t sv_s, uint32_t n, int qbase,
                                                 uint32_t b_s, uint32_t mst, int64_t tile,
                                                 int lane) {
+  if (a.dbg & 4096) return;  // timing only: survivors dropped
   for (uint32_t i = (uint32_t)lane; i < n; i += 32u) {
     const uint32_t ent = lds16(sv_s + 2u * i);
     const int q = qbase + (int)(ent >> 8);
@@ -871,7 +906,130 @@ __device__ __forceinline__ void drain_survivors(const TcArgs& a, const Smem& m, 
     const int32_t score = smem_dot(su32(m.sA) + (uint32_t)q * kKBytes, (uint32_t)q & 7u,
                                    b_s + item * kKBytes, item & 7u);
     const uint64_t key = make_key(score, lds32(mst + 4u * item));
-    if (key >= m.sT[q]) emit_one(a, e, q, key, (uint32_t)(tile * kTileItems) + item);
+    if (key >= m.sT[q] && !(a.dbg & 8192)) emit_one(a, e, q, key, (uint32_t)(tile * kTileItems) + item);
+  }
+}
+
+// ---- mode 3 (window form, two M-blocks): 24 warps -------------------------------------
+// Eight dense warps instead of four: warp (mb, quad) drains accumulator buffer mb (M-block mb
+// of every tile) in TMEM lane quadrant quad, so two warps per scheduler overlap their
+// tcgen05.ld round trips and each warp's per-tile chain is half as long (ncu, round 2: the
+// four-warp dense pass was the critical path -- ~760 dependent instructions per warp per
+// tile). The other roles are mode 1's. 768 threads = six warps per scheduler, so 80
+// registers each (16K per scheduler): the dense warps load one 32-column chunk at a time
+// (FB_C3_DBUF=1 builds the double-buffered variant).
+// Survivors (gate hit + filter pass) of a tile are handed to the column builders, which
+// are idle most of each period: the hit warps queue them per tile (double-buffered lists),
+// the builders compute the exact scores and emit them after building the next tile.
+#ifndef FB_C3_HANDOFF
+#define FB_C3_HANDOFF 1
+#endif
+constexpr int kNbSvFull = 11, kNbSvEmpty = 13;  // + tile parity
+constexpr int kNbSvCount = 32 * (kCnfBuilders + kCnfHitWarps);
+constexpr uint32_t kSvListBytes = kSurvCap * 2u;  // per hit warp and parity
+constexpr uint32_t kSvBytes = 2u * kCnfHitWarps * kSvListBytes + 2u * kCnfHitWarps * 4u;
+constexpr int kCnf3Threads = 768;
+constexpr int kC3DenseWarps = 8;
+constexpr int kC3Builders = 5;
+#ifndef FB_C3_DBUF
+#define FB_C3_DBUF 0
+#endif
+
+__device__ __forceinline__ void cnf3_dense_loop(const TcArgs& a, const Smem& m, uint32_t tmem_base,
+                                                uint32_t hm_s, int warp, int lane, int hm_count) {
+  uint64_t* items_full = m.bars + kBarItemsFull;
+  uint64_t* acc_full = m.bars + kBarAccFull;
+  const int quad = warp & 3;
+  const int mb = (warp - kCnfDense0) >> 2;  // dense warps 8..15
+  const int row = quad * 32 + lane;
+  const int q = mb * kBlockM + row;
+  const bool qok = q < a.nq;
+  bool all = false;
+  (void)gate_digits(qok ? m.sT[q] : ~0ull, all);
+  const uint32_t allmask = all ? ~0u : 0u;
+  int it = 0, s = 0;
+  uint32_t iph = 0;
+  for (int64_t i = blockIdx.x; i < a.n_sel; i += gridDim.x, ++it) {
+    mbar_wait(items_full + s, iph);
+    const uint32_t mst = su32(m.base + a.off_id) + (uint32_t)s * kStageMeta;
+    const int64_t tile = (int64_t)lds32(mst + kMetaTile);
+    const uint32_t vchunk = lane < 8 ? lds32(mst + kMetaValid + 4u * lane) : 0u;
+    if (++s == a.item_stages) {
+      s = 0;
+      iph ^= 1u;
+    }
+    const int hb = it & 1;
+    if (it >= 2) nb_sync(kNbHmEmpty + hb, hm_count);
+    const uint32_t hmap = hm_s + (uint32_t)hb * kHmapBytes + 4u * (uint32_t)q;
+    mbar_wait(acc_full + mb, (uint32_t)it & 1u);
+    tc_fence_after();
+    if (quad == 0) FB_TR(a, it, mb ? 6 : 4);
+    const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(mb * kAccCols);
+    auto chunk_mask = [&](int c, const int32_t (&r)[32]) -> uint32_t {
+      uint32_t em = __shfl_sync(0xffffffffu, vchunk, c);
+      if (!qok) em = 0u;
+      if (a.masks != nullptr && em != 0u)
+        em &= (uint32_t)(__ldg(a.masks + (int64_t)q * a.n_words + tile * kTileWords + (c >> 1)) >>
+                         (32 * (c & 1)));
+      return (a.dbg & 8) ? 0u : (nonneg_mask32(r) | allmask) & em;
+    };
+#if FB_C3_DBUF
+    int32_t ra[32], rb[32];
+    tmem_ld32_async(taddr, ra);
+#pragma unroll 1
+    for (int c = 0; c < 8; c += 2) {
+      tmem_wait32(ra);
+      tmem_ld32_async(taddr + (uint32_t)((c + 1) * 32), rb);
+      sts32(hmap + (uint32_t)c * (kMaxQueries * 4u), chunk_mask(c, ra));
+      tmem_wait32(rb);
+      if (c + 2 < 8) tmem_ld32_async(taddr + (uint32_t)((c + 2) * 32), ra);
+      sts32(hmap + (uint32_t)(c + 1) * (kMaxQueries * 4u), chunk_mask(c + 1, rb));
+    }
+#else
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      int32_t r[32];
+      tmem_ld32_async(taddr + (uint32_t)(c * 32), r);
+      tmem_wait32(r);
+      sts32(hmap + (uint32_t)c * (kMaxQueries * 4u), chunk_mask(c, r));
+    }
+#endif
+    tc_fence_before();
+    nb_arrive(kNbAccEmpty + mb, kNbAccCount);  // the MMA warp bar.syncs on it
+    if (quad == 0) FB_TR(a, it, mb ? 7 : 5);
+    __syncwarp();
+    nb_arrive(kNbHmFull + hb, hm_count);
+  }
+  for (int t = it; t < it + 2; ++t)
+    if (t >= 2) nb_sync(kNbHmEmpty + (t & 1), hm_count);
+}
+
+// Builders' share of a mode-3 tile: the survivors the hit warps queued for tile `it`
+// (item stage s). Builder warp w takes hit lists w and w + 5 (< 8) as one index space.
+__device__ __forceinline__ void cnf3_builder_drain(const TcArgs& a, const Smem& m, EmitState& e,
+                                                   int it, int lw, int lane) {
+  const int par = it & 1;
+  const int s = it % a.item_stages;
+  const uint32_t sv0 = su32(m.base + a.off_sv);
+  const uint32_t cnt_s = sv0 + 2u * kCnfHitWarps * kSvListBytes + (uint32_t)par * kCnfHitWarps * 4u;
+  const int la = lw, lb = lw + kCnfBuilders;
+  const uint32_t na = lds32(cnt_s + 4u * (uint32_t)la);
+  const uint32_t nb = lb < kCnfHitWarps ? lds32(cnt_s + 4u * (uint32_t)lb) : 0u;
+  const uint32_t mst = su32(m.base + a.off_id) + (uint32_t)s * kStageMeta;
+  const int64_t tile = (int64_t)lds32(mst + kMetaTile);
+  const uint32_t b_s = su32(m.sB + (size_t)s * kItemBytes);
+  if (a.dbg & 4096) return;
+  for (uint32_t i = (uint32_t)lane; i < na + nb; i += 32u) {
+    const bool in_a = i < na;
+    const int l = in_a ? la : lb;
+    const uint32_t ent =
+        lds16(sv0 + ((uint32_t)par * kCnfHitWarps + (uint32_t)l) * kSvListBytes + 2u * (in_a ? i : i - na));
+    const int q = l * 32 + (int)(ent >> 8);
+    const uint32_t item = ent & 255u;
+    const int32_t score = smem_dot(su32(m.sA) + (uint32_t)q * kKBytes, (uint32_t)q & 7u,
+                                   b_s + item * kKBytes, item & 7u);
+    const uint64_t key = make_key(score, lds32(mst + 4u * item));
+    if (key >= m.sT[q] && !(a.dbg & 8192)) emit_one(a, e, q, key, (uint32_t)(tile * kTileItems) + item);
   }
 }
 
@@ -883,8 +1041,8 @@ __device__ __forceinline__ void drain_survivors(const TcArgs& a, const Smem& m, 
 //    query's eligibility words AND_g OR_{c in S_qg} col_c for the tile's eight chunks and ANDs
 //    them into the hit words, so only eligible hits reach the exact test.
 template <int kMode>
-__global__ void __launch_bounds__(kCnfThreads, 1)
-    k_scan_cnf(const __grid_constant__ CUtensorMap tmap_items, const TcArgs a) {
+__global__ void __launch_bounds__(kMode == 3 ? kCnf3Threads : kCnfThreads)
+    __maxnreg__(kMode == 3 ? 80 : 96) k_scan_cnf(const __grid_constant__ CUtensorMap tmap_items, const TcArgs a) {
   constexpr bool kWin = kMode != 0;
   constexpr bool ff = kMode == 2;
   if (kWin && a.ffirst < 0) {
@@ -896,7 +1054,15 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
     for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
     if ((sum < a.ff_limit) != ff) return;
   }
-  constexpr int NT = kCnfThreads;
+  constexpr int NT = kMode == 3 ? kCnf3Threads : kCnfThreads;
+  constexpr int kDenseN = kMode == 3 ? kC3DenseWarps : kCnfDenseWarps;
+  constexpr int kBuildN = kMode == 3 ? kC3Builders : kCnfBuilders;
+  constexpr int kDense0 = 3 + kBuildN;
+  constexpr int kHit0 = kDense0 + kDenseN;
+  constexpr int kHmCount = 32 * (kDenseN + kCnfHitWarps);
+  constexpr int kLeafCount = 32 * (kBuildN + kCnfHitWarps);
+  constexpr bool kHand = kMode == 3 && FB_C3_HANDOFF;  // survivors drained by the builders
+  static_assert(32 * (kHit0 + kCnfHitWarps) == NT, "warp layout");
   const Smem m = carve(a);
   uint8_t* smem = m.base;
   uint64_t* bars = m.bars;
@@ -941,11 +1107,12 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < 4; ++s) {
       mbar_init(items_full + s, 1 + 32 + 1);          // TMA expect-tx, id ranks, meta
-      mbar_init(items_empty + s, 1 + kCnfHitWarps);  // MMA commit + hit warps (B tile, ids)
+      // MMA commit + hit warps (B tile, ids) [+ builders: mode 3 drains survivors there]
+      mbar_init(items_empty + s, 1 + kCnfHitWarps + (kHand ? kCnfBuilders : 0));
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(planes_full + s, 32);
-      mbar_init(planes_empty + s, kCnfBuilders);
+      mbar_init(planes_empty + s, kBuildN);
       mbar_init(acc_full + s, 1);
       mbar_init(acc_empty + s, kCnfDenseWarps);
     }
@@ -963,10 +1130,33 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
   } else if (warp == 1) {
     mma_loop<true, true>(a, m, tmem_base, kNbAccCount);
   } else if (warp == 2) {
-    producer_loop(a, &tmap_items, m, lane, false, true);
-  } else if (warp < kCnfDense0) {
-    cnf_builder_loop(a, m, warp - 3, kCnfBuilders, lane, ff);
-  } else if (warp < kCnfHit0) {
+    producer_loop(a, &tmap_items, m, lane, false, true, true);
+  } else if (warp < kDense0) {
+    if constexpr (kHand) {
+      EmitState be;
+      be.pa.q = be.pb.q = -1;
+      be.pa.p = be.pb.p = 0u;
+      be.pa.key = be.pb.key = 0ull;
+      be.pa.slot = be.pb.slot = 0u;
+      be.par = false;
+      const int lw = warp - 3;
+      auto tail = [&](int t) {
+        const int par = t & 1;
+        nb_sync(kNbSvFull + par, kNbSvCount);
+        cnf3_builder_drain(a, m, be, t, lw, lane);
+        __syncwarp();
+        nb_arrive(kNbSvEmpty + par, kNbSvCount);
+        if (lane == 0) mbar_arrive(items_empty + (t % a.item_stages));
+      };
+      cnf_builder_loop(a, m, lw, kBuildN, lane, ff, kLeafCount, tail);
+      flush_pending(a, be.pa);
+      flush_pending(a, be.pb);
+    } else {
+      cnf_builder_loop(a, m, warp - 3, kBuildN, lane, ff, kLeafCount);
+    }
+  } else if (kMode == 3 && warp < kHit0) {
+    cnf3_dense_loop(a, m, tmem_base, hm_s, warp, lane, kHmCount);
+  } else if (warp < kHit0) {
     // ================= dense pass (one warp per TMEM lane quadrant) ======================
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
@@ -994,7 +1184,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
       }
       const int hb = it & 1;
       if (quad == 0) FB_TR(a, it, 12);
-      if (it >= 2) nb_sync(kNbHmEmpty + hb, kNbHmCount);
+      if (it >= 2) nb_sync(kNbHmEmpty + hb, kHmCount);
       if (quad == 0) FB_TR(a, it, 13);
       const uint32_t hmap = hm_s + (uint32_t)hb * kHmapBytes;
 #pragma unroll 1
@@ -1044,13 +1234,13 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
         if (quad == 0) FB_TR(a, it, 5 + 2 * mb);
       }
       __syncwarp();
-      nb_arrive(kNbHmFull + hb, kNbHmCount);
+      nb_arrive(kNbHmFull + hb, kHmCount);
     }
     for (int t = it; t < it + 2; ++t)
-      if (t >= 2) nb_sync(kNbHmEmpty + (t & 1), kNbHmCount);
+      if (t >= 2) nb_sync(kNbHmEmpty + (t & 1), kHmCount);
   } else {
     // ================= hit pass (lane = query) =========================================
-    const int qbase = (warp - kCnfHit0) * 32;
+    const int qbase = (warp - kHit0) * 32;
     const int q = qbase + lane;
     const bool qok = q < a.nq;
     const uint64_t T = qok ? m.sT[q] : ~0ull;
@@ -1073,7 +1263,7 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
         hi[g] = w0 + 1 < a.cnf_words ? mg[w0 + 1] : 0u;
       }
     }
-    const uint32_t sv_s = su32(smem + a.off_sv) + (uint32_t)(warp - kCnfHit0) * (kSurvCap * 2u);
+    const uint32_t sv_base = su32(smem + a.off_sv) + (uint32_t)(warp - kHit0) * kSvListBytes;
     EmitState e;
     e.pa.q = e.pb.q = -1;
     e.pa.p = e.pb.p = 0u;
@@ -1088,11 +1278,14 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
       const int64_t tile = (int64_t)lds32(mst + kMetaTile);
       const uint32_t b_s = su32(m.sB + (size_t)s * kItemBytes);
       const int st = it & 1;
-      nb_sync(kNbLeafFull + st, kNbLeafCount);
+      nb_sync(kNbLeafFull + st, kLeafCount);
       const uint32_t tb_s = su32(m.sL + (size_t)st * a.leaf_stage_bytes);
       const int hb = it & 1;
-      nb_sync(kNbHmFull + hb, kNbHmCount);
-      if (warp == kCnfHit0) FB_TR(a, it, 8);
+      nb_sync(kNbHmFull + hb, kHmCount);
+      if (warp == kHit0) FB_TR(a, it, 8);
+      // mode 3: this tile's survivor list (the builders drain it after building the next tile)
+      const uint32_t sv_s = sv_base + (kHand ? (uint32_t)(it & 1) * kCnfHitWarps * kSvListBytes : 0u);
+      if (kHand && it >= 2) nb_sync(kNbSvEmpty + (it & 1), kNbSvCount);
       const uint32_t hmap = hm_s + (uint32_t)hb * kHmapBytes + 4u * (uint32_t)q;
       // this query's nonzero chunk words
       uint32_t nzm = 0u;
@@ -1140,11 +1333,65 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
                        : (c < 6 ? (c == 4 ? mw[4] : mw[5]) : (c == 6 ? mw[6] : mw[7]));
         return lds32(hmap + (uint32_t)c * (kMaxQueries * 4u));
       };
-      int cc = nzm ? __ffs(nzm) - 1 : 0;
-      uint32_t cur = nzm ? word_at(cc) : 0u;
       uint32_t n_sv = 0;  // warp-uniform survivor count
       int n_rounds = 0;
-      while (__any_sync(0xffffffffu, cur != 0u)) {
+      if constexpr (kMode == 3) {
+        // two cursors per lane (chunks 0-3 and 4-7): two independent filter tests per round,
+        // their eight row loads issued together, about half the rounds of one cursor
+        uint32_t nzA = nzm & 0xFu, nzB = nzm & 0xF0u;
+        int ca = nzA ? __ffs(nzA) - 1 : 0, cb = nzB ? __ffs(nzB) - 1 : 4;
+        uint32_t curA = nzA ? word_at(ca) : 0u, curB = nzB ? word_at(cb) : 0u;
+        const uint32_t lt = lanemask_lt();
+        const uint32_t rstride = (uint32_t)a.tb_stride * 4u;
+        while (__any_sync(0xffffffffu, (curA | curB) != 0u)) {
+          ++n_rounds;
+          const bool hasA = curA != 0u, hasB = curB != 0u;
+          const uint32_t ia = hasA ? (uint32_t)(ca * 32 + __ffs(curA) - 1) : 0u;
+          const uint32_t ib = hasB ? (uint32_t)(cb * 32 + __ffs(curB) - 1) : 0u;
+          curA &= curA - 1u;
+          curB &= curB - 1u;
+          const uint32_t rowA = tb_s + ia * rstride, rowB = tb_s + ib * rstride;
+          uint32_t xa[4], xb[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint2 ta = lds64v(rowA + wo[g]);
+            const uint2 tb = lds64v(rowB + wo[g]);
+            xa[g] = (ta.x & lo[g]) | (ta.y & hi[g]);
+            xb[g] = (tb.x & lo[g]) | (tb.y & hi[g]);
+          }
+          const bool sa = hasA && (nof || min(min(xa[0], xa[1]), min(xa[2], xa[3])) != 0u);
+          const bool sb2 = hasB && (nof || min(min(xb[0], xb[1]), min(xb[2], xb[3])) != 0u);
+          if (hasA && curA == 0u) {
+            nzA &= nzA - 1u;
+            if (nzA) {
+              ca = __ffs(nzA) - 1;
+              curA = word_at(ca);
+            }
+          }
+          if (hasB && curB == 0u) {
+            nzB &= nzB - 1u;
+            if (nzB) {
+              cb = __ffs(nzB) - 1;
+              curB = word_at(cb);
+            }
+          }
+          const uint32_t bA = __ballot_sync(0xffffffffu, sa);
+          const uint32_t bB = __ballot_sync(0xffffffffu, sb2);
+          if (sa) sts16(sv_s + 2u * (n_sv + (uint32_t)__popc(bA & lt)), ((uint32_t)lane << 8) | ia);
+          n_sv += (uint32_t)__popc(bA);
+          if (sb2) sts16(sv_s + 2u * (n_sv + (uint32_t)__popc(bB & lt)), ((uint32_t)lane << 8) | ib);
+          n_sv += (uint32_t)__popc(bB);
+          if (n_sv > (uint32_t)(kSurvCap - 64)) {
+            __syncwarp();
+            drain_survivors(a, m, e, sv_s, n_sv, qbase, b_s, mst, tile, lane);
+            __syncwarp();
+            n_sv = 0;
+          }
+        }
+      }
+      int cc = nzm ? __ffs(nzm) - 1 : 0;
+      uint32_t cur = (kMode != 3 && nzm) ? word_at(cc) : 0u;
+      while (kMode != 3 && __any_sync(0xffffffffu, cur != 0u)) {
         ++n_rounds;
         (void)n_rounds;
         bool surv = false;
@@ -1181,21 +1428,34 @@ __global__ void __launch_bounds__(kCnfThreads, 1)
         }
       }
       __syncwarp();
-      nb_arrive(kNbHmEmpty + hb, kNbHmCount);
-      if (warp == kCnfHit0) FB_TR(a, it, 11);
+      nb_arrive(kNbHmEmpty + hb, kHmCount);
+      if (warp == kHit0) FB_TR(a, it, 11);
 #ifdef FB_TRACE
-      if ((a.dbg & 1024) && blockIdx.x == 0 && warp == kCnfHit0 && lane == 0 && it < 16)
+      if ((a.dbg & 1024) && blockIdx.x == 0 && warp == kHit0 && lane == 0 && it < 16)
         g_tr[it][3] = (long long)n_rounds * 1000 + n_sv;
 #endif
-      if (n_sv) drain_survivors(a, m, e, sv_s, n_sv, qbase, b_s, mst, tile, lane);
+      if constexpr (kHand) {
+        if (lane == 0)
+          sts32(su32(smem + a.off_sv) + 2u * kCnfHitWarps * kSvListBytes +
+                    ((uint32_t)(it & 1) * kCnfHitWarps + (uint32_t)(warp - kHit0)) * 4u,
+                n_sv);
+        __syncwarp();
+        nb_arrive(kNbSvFull + (it & 1), kNbSvCount);
+      } else if (n_sv) {
+        drain_survivors(a, m, e, sv_s, n_sv, qbase, b_s, mst, tile, lane);
+      }
       __syncwarp();
-      nb_arrive(kNbLeafEmpty + st, kNbLeafCount);
+      nb_arrive(kNbLeafEmpty + st, kLeafCount);
       if (lane == 0) mbar_arrive(items_empty + s);
       if (++s == a.item_stages) {
         s = 0;
         iph ^= 1u;
       }
-      if (warp == kCnfHit0) FB_TR(a, it, 9);
+      if (warp == kHit0) FB_TR(a, it, 9);
+    }
+    if constexpr (kHand) {  // retire the builders' releases of the last two lists
+      for (int t = it; t < it + 2; ++t)
+        if (t >= 2) nb_sync(kNbSvEmpty + (t & 1), kNbSvCount);
     }
     flush_pending(a, e.pa);
     flush_pending(a, e.pb);
@@ -1274,7 +1534,7 @@ size_t layout(TcArgs& t, int n_mblk, int n_planes, int n_leaves, int k_max, int 
     t.off_gate = (uint32_t)align_up(off, 128);
     off = t.off_gate + kGateTileBytes + 256;
     t.off_sv = (uint32_t)align_up(off, 16);
-    off = t.off_sv + (size_t)kCnfHitWarps * kSurvCap * 2;
+    off = t.off_sv + (size_t)kSvBytes;  // mode 3's double-buffered lists (mode 1 uses half)
   }
   t.off_id = (uint32_t)align_up(off, 16);
   off = t.off_id + (size_t)stages * kStageMeta;
@@ -1347,8 +1607,18 @@ int launch_kernel(K kernel, int threads, const CUtensorMap& tmap, const TcArgs& 
 
 // window form, mode chosen on the device from the sampling pass: per-hit and filter-first
 // instances back to back, the one not chosen returns at its first instruction
+bool use_mode3(const TcArgs& t) {
+  const char* v1 = getenv("FB_CNF_V1");  // A/B: the 20-warp organisation
+  return t.n_mblk == 2 && !(v1 != nullptr && atoi(v1) != 0);
+}
+
+int launch_win(const TcArgs& t, const CUtensorMap& tmap, int grid, size_t smem, cudaStream_t s) {
+  return use_mode3(t) ? launch_kernel(k_scan_cnf<3>, kCnf3Threads, tmap, t, grid, smem, s)
+                      : launch_kernel(k_scan_cnf<1>, kCnfThreads, tmap, t, grid, smem, s);
+}
+
 int launch_both(const TcArgs& t, const CUtensorMap& tmap, int grid, size_t smem, cudaStream_t s) {
-  const int rc = launch_kernel(k_scan_cnf<1>, kCnfThreads, tmap, t, grid, smem, s);
+  const int rc = launch_win(t, tmap, grid, smem, s);
   return rc ? rc : launch_kernel(k_scan_cnf<2>, kCnfThreads, tmap, t, grid, smem, s);
 }
 
@@ -1442,7 +1712,7 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
       return FB_ERR_UNSUPPORTED;
     const int rc =
         cnf == 1 && t.ffirst > 0 ? launch_kernel(k_scan_cnf<2>, kCnfThreads, tmap, t, grid, smem, s)
-        : cnf == 1 && t.ffirst == 0 ? launch_kernel(k_scan_cnf<1>, kCnfThreads, tmap, t, grid, smem, s)
+        : cnf == 1 && t.ffirst == 0 ? launch_win(t, tmap, grid, smem, s)
         : cnf == 1 ? launch_both(t, tmap, grid, smem, s)
         : cnf == 2 ? launch_kernel(k_scan_cnf<0>, kCnfThreads, tmap, t, grid, smem, s)
                    : launch_kernel(k_scan_tc, kThreads, tmap, t, grid, smem, s);

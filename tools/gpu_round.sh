@@ -10,8 +10,8 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'^k_' --csv \
   --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
   > gpurun_out/b_ncu_${TAG}.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_scan_(tc|cnf)' \
-  --launch-skip 3 --launch-count 1 -o gpurun_out/emit_${TAG} -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_scan_cnf' \
+  --launch-skip 2 --launch-count 1 -o gpurun_out/emit_${TAG} -f \
   python tools/profile_scan.py --iters 3 > gpurun_out/prof_${TAG}.log 2>&1
 tail -n 2 gpurun_out/pytest_gpu_${TAG}.log gpurun_out/smoke_${TAG}.log
 cat gpurun_out/bench_${TAG}.json gpurun_out/bench_ref_${TAG}.json

@@ -50,7 +50,8 @@ def main():
     h = rows[1]
     ia, iex = h.index("Address"), h.index("Instructions Executed")
     stall_cols = [i for i, n in enumerate(h) if n.startswith("stall_") and "Not Issued" not in n]
-    lm = line_map(sass, kre.split("|")[0])
+    import os
+    lm = line_map(sass, os.environ.get("SASS_KERNEL", kre.split("|")[0]))
     ex, st = defaultdict(float), defaultdict(lambda: defaultdict(float))
     base = None
     for r in rows[2:]:
