@@ -227,11 +227,13 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# one 128x256x32 kind::i8 MMA per 128 cycles per SM (tools/micro/umma_rate.cu on the B200)
-# x 148 SMs x 1965 MHz; MEASURED_PEAKS.json carries no int8 figure
-MEASURED_INT8_TOPS = round(2 * 128 * 256 * 32 / 128 * 148 * 1.965e9 / 1e12, 1)
-MEASURED_INT8_SOURCE = ("measured: tools/micro/umma_rate (128-cycle 128x256x32 kind::i8 MMA per SM) "
-                        "x 148 SMs x 1965 MHz")
+# dense int8 tensor peak MEASURED on a B200 of this pool (tools/micro/i8_peak.cu: 148
+# persistent CTAs issuing tcgen05.mma.kind::i8 M128 N256 K32 back to back, CUDA events,
+# profiles/r2/i8_peak_*.log); MEASURED_PEAKS.json carries no int8 figure. The umma_rate
+# derivation (one MMA per 128 cycles per SM x 148 SMs x 1965 MHz) gives 4764.8.
+MEASURED_INT8_TOPS = 4598.5
+MEASURED_INT8_SOURCE = ("measured: tools/micro/i8_peak (148 CTAs, back-to-back kind::i8 "
+                        "128x256x32 MMAs, median of 3 x 0.27 s; profiles/r2/i8_peak_burst.log)")
 
 
 def measured_peaks():
