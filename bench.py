@@ -67,6 +67,8 @@ def parse_args():
                     help="N>1 shard exchange: owner-partitioned all-to-all with static sizes "
                          "(no host sync), the pruned variant, or all-gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--selectivities", default=None,
+                    help="config 4: comma-separated target pass fractions (default: the sweep)")
     ap.add_argument("--cpu-queries", type=int, default=0, help="CPU sample size (0: auto)")
     a = ap.parse_args()
     if a.steps is None:
@@ -700,7 +702,7 @@ def run_sweep(a):
     op = TopkOp(idx, B, k, np.array([[0, idx.n_slots]]))
     outs = op.alloc_outputs()
     stream = torch.cuda.current_stream()
-    for p in SWEEP:
+    for p in (tuple(float(x) for x in a.selectivities.split(",")) if a.selectivities else SWEEP):
         if p >= 1.0:
             batch, sizes, sel = None, None, 1.0
         else:

@@ -1041,10 +1041,11 @@ __device__ __forceinline__ void cnf3_builder_drain(const TcArgs& a, const Smem& 
 //    query's eligibility words AND_g OR_{c in S_qg} col_c for the tile's eight chunks and ANDs
 //    them into the hit words, so only eligible hits reach the exact test.
 template <int kMode>
-__global__ void __launch_bounds__(kMode == 3 ? kCnf3Threads : kCnfThreads)
-    __maxnreg__(kMode == 3 ? 80 : 96) k_scan_cnf(const __grid_constant__ CUtensorMap tmap_items, const TcArgs a) {
+__global__ void __launch_bounds__(kMode >= 3 ? kCnf3Threads : kCnfThreads)
+    __maxnreg__(kMode >= 3 ? 80 : 96) k_scan_cnf(const __grid_constant__ CUtensorMap tmap_items, const TcArgs a) {
   constexpr bool kWin = kMode != 0;
-  constexpr bool ff = kMode == 2;
+  constexpr bool ff = kMode == 2 || kMode == 4;
+  constexpr bool kL3 = kMode >= 3;  // 24-warp layout (mode 3 per-hit, mode 4 filter-first)
   if (kWin && a.ffirst < 0) {
     // both window-form instances are launched; the one the sampled eligibility does not pick
     // returns at once (uniform across CTAs: every CTA sums the same counts)
@@ -1054,14 +1055,14 @@ __global__ void __launch_bounds__(kMode == 3 ? kCnf3Threads : kCnfThreads)
     for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
     if ((sum < a.ff_limit) != ff) return;
   }
-  constexpr int NT = kMode == 3 ? kCnf3Threads : kCnfThreads;
-  constexpr int kDenseN = kMode == 3 ? kC3DenseWarps : kCnfDenseWarps;
-  constexpr int kBuildN = kMode == 3 ? kC3Builders : kCnfBuilders;
+  constexpr int NT = kL3 ? kCnf3Threads : kCnfThreads;
+  constexpr int kDenseN = kL3 ? kC3DenseWarps : kCnfDenseWarps;
+  constexpr int kBuildN = kL3 ? kC3Builders : kCnfBuilders;
   constexpr int kDense0 = 3 + kBuildN;
   constexpr int kHit0 = kDense0 + kDenseN;
   constexpr int kHmCount = 32 * (kDenseN + kCnfHitWarps);
   constexpr int kLeafCount = 32 * (kBuildN + kCnfHitWarps);
-  constexpr bool kHand = kMode == 3 && FB_C3_HANDOFF;  // survivors drained by the builders
+  constexpr bool kHand = kL3 && FB_C3_HANDOFF;  // survivors drained by the builders
   static_assert(32 * (kHit0 + kCnfHitWarps) == NT, "warp layout");
   const Smem m = carve(a);
   uint8_t* smem = m.base;
@@ -1154,7 +1155,7 @@ __global__ void __launch_bounds__(kMode == 3 ? kCnf3Threads : kCnfThreads)
     } else {
       cnf_builder_loop(a, m, warp - 3, kBuildN, lane, ff, kLeafCount);
     }
-  } else if (kMode == 3 && warp < kHit0) {
+  } else if (kL3 && warp < kHit0) {
     cnf3_dense_loop(a, m, tmem_base, hm_s, warp, lane, kHmCount);
   } else if (warp < kHit0) {
     // ================= dense pass (one warp per TMEM lane quadrant) ======================
@@ -1607,7 +1608,7 @@ int launch_kernel(K kernel, int threads, const CUtensorMap& tmap, const TcArgs& 
 
 // window form, mode chosen on the device from the sampling pass: per-hit and filter-first
 // instances back to back, the one not chosen returns at its first instruction
-bool use_mode3(const TcArgs& t) {
+bool use_mode3(const TcArgs& t) {  // (and mode 4, its filter-first twin)
   const char* v1 = getenv("FB_CNF_V1");  // A/B: the 20-warp organisation
   return t.n_mblk == 2 && !(v1 != nullptr && atoi(v1) != 0);
 }
@@ -1617,9 +1618,14 @@ int launch_win(const TcArgs& t, const CUtensorMap& tmap, int grid, size_t smem, 
                       : launch_kernel(k_scan_cnf<1>, kCnfThreads, tmap, t, grid, smem, s);
 }
 
+int launch_ff(const TcArgs& t, const CUtensorMap& tmap, int grid, size_t smem, cudaStream_t s) {
+  return use_mode3(t) ? launch_kernel(k_scan_cnf<4>, kCnf3Threads, tmap, t, grid, smem, s)
+                      : launch_kernel(k_scan_cnf<2>, kCnfThreads, tmap, t, grid, smem, s);
+}
+
 int launch_both(const TcArgs& t, const CUtensorMap& tmap, int grid, size_t smem, cudaStream_t s) {
   const int rc = launch_win(t, tmap, grid, smem, s);
-  return rc ? rc : launch_kernel(k_scan_cnf<2>, kCnfThreads, tmap, t, grid, smem, s);
+  return rc ? rc : launch_ff(t, tmap, grid, smem, s);
 }
 
 }  // namespace
@@ -1711,7 +1717,7 @@ int launch_scan_tc(const ScanArgs& a, cudaStream_t s) {
                      t.has_prog ? t.k_max : 0, t.has_prog ? a.prog.n_rops : 0, cnf, smem))
       return FB_ERR_UNSUPPORTED;
     const int rc =
-        cnf == 1 && t.ffirst > 0 ? launch_kernel(k_scan_cnf<2>, kCnfThreads, tmap, t, grid, smem, s)
+        cnf == 1 && t.ffirst > 0 ? launch_ff(t, tmap, grid, smem, s)
         : cnf == 1 && t.ffirst == 0 ? launch_win(t, tmap, grid, smem, s)
         : cnf == 1 ? launch_both(t, tmap, grid, smem, s)
         : cnf == 2 ? launch_kernel(k_scan_cnf<0>, kCnfThreads, tmap, t, grid, smem, s)
