@@ -398,8 +398,11 @@ def run_ours(a):
     peak, peak_kind = measured_peaks()
     traffic = profiled_traffic()
     ops = 2.0 * B * idx.n_slots_pad * idx.dim
-    traffic_b = (traffic.get("dram_bytes_per_launch")
-                 if traffic and traffic.get("config", 2) == a.config else None)
+    # ncu DRAM bytes of the emit kernel (profiles/roofline_traffic.json, one full capture
+    # per config) x its launches per emit pass
+    t_cfg = (traffic or {}).get("configs", {}).get(str(a.config))
+    traffic_b = (int(t_cfg["dram_bytes_per_launch"] * t_cfg.get("launches_per_emit", 1))
+                 if t_cfg else None)
     tops = ops / (emit_avg / 1e3) / 1e12
     roofline = {"bound": "hbm", "kernel": "fused filter+scan emit pass",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
