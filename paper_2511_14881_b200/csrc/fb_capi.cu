@@ -270,10 +270,13 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
   // The sampled threshold lands ~jd / f above the k-th key (jd = mu + 5 sqrt(mu) + 8,
   // mu = k f, f ~ 1/128) with a spread of ~sqrt(jd) / f; room for 5.5 sigma of it.
   int64_t want = std::max<int64_t>(2LL * k + 2048, 8192);
+  // sampled share of the tiles is 1 / sdiv (FB_SAMPLE_DIV: A/B experiments only)
+  const char* sdiv_env = getenv("FB_SAMPLE_DIV");
+  const double sdiv = sdiv_env ? std::max(1.0, atof(sdiv_env)) : 128.0;
   {
-    const double mu = (double)k / 128.0;
+    const double mu = (double)k / sdiv;
     const double jd = mu + 5.0 * std::sqrt(mu) + 8.0;
-    const int64_t noise = (int64_t)std::ceil(128.0 * (jd + 5.5 * std::sqrt(jd)));
+    const int64_t noise = (int64_t)std::ceil(sdiv * (jd + 5.5 * std::sqrt(jd)));
     // k <= 10240: stay within the selection's shared-memory staging when that is close
     want = std::max<int64_t>(want, k <= 10240 ? std::min<int64_t>(kSelectMaxCand, noise) : noise);
   }
@@ -290,7 +293,7 @@ int fb_topk_plan_create(const fb_index_t* idx, int32_t n_queries, int32_t k, con
       // the tiles (>= 256 tiles, ~65k slots) -- enough for the rank estimate
       // (rounded to whole waves of one tile per SM so no CTA runs a tile more than others)
       const int64_t target_tiles = std::max<int64_t>(std::min<int64_t>(p->n_tc_work, 256),
-                                                     p->n_tc_work / 128);
+                                                     (int64_t)((double)p->n_tc_work / sdiv));
       int n_sm = 148;
       cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
       const int64_t waves = std::max<int64_t>(1, (target_tiles + n_sm / 2) / n_sm);
