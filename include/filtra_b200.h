@@ -276,6 +276,16 @@ int fb_merge_union(const uint64_t* keys, const int32_t* counts, int32_t n_reques
                    uint64_t* bitmap, uint64_t* merged, int64_t* merged_ranks, int32_t* mcount,
                    void* stream);
 
+/* Device, final ranking of multi-task retrieval (retrieval.retrieve, retrieval.py:190:
+ * np.lexsort((merged, -final))[:topk]): for request b, the first count[b] values of
+ * final_scores[b * ld ..] (merged candidates in ascending id order) ordered by (value desc,
+ * position asc) with NumPy's float order (NaN last, -0.0 == +0.0); order[b * topk + r] is
+ * the position of rank r (0 past out_count[b] = min(topk, count[b])). ld <= 24576,
+ * topk <= 8192 (FB_ERR_UNSUPPORTED otherwise). */
+int fb_final_topk(const double* final_scores, int64_t ld, const int32_t* count,
+                  int32_t n_requests, int32_t topk, int64_t* order, int32_t* out_count,
+                  void* stream);
+
 /* Device, IVF-probed batched search (retrieval.codesigned_search with nprobe < n_clusters,
  * retrieval.py:110-144; ivf.search_clusters over the probed clusters, ivf.py:285-334): for
  * query b, probe_words[(b * nprobe + j) * 2 ..] is the 64-slot word range [w0, w1) of its

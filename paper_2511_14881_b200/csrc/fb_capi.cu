@@ -570,6 +570,17 @@ int fb_merge_union(const uint64_t* keys, const int32_t* counts, int32_t n_reques
                             static_cast<cudaStream_t>(stream));
 }
 
+int fb_final_topk(const double* final_scores, int64_t ld, const int32_t* count,
+                  int32_t n_requests, int32_t topk, int64_t* order, int32_t* out_count,
+                  void* stream) {
+  if (n_requests < 0 || topk < 0 || ld < 0) return fail(FB_ERR_INVALID, "negative size");
+  if (n_requests > 0 && topk > 0 && (final_scores == nullptr || count == nullptr || order == nullptr ||
+                                     out_count == nullptr))
+    return fail(FB_ERR_INVALID, "null buffer");
+  return launch_final_topk(final_scores, ld, count, n_requests, topk, order, out_count,
+                           static_cast<cudaStream_t>(stream));
+}
+
 int fb_ivf_topk(const fb_index_t* idx, const int8_t* queries_q, int32_t n_queries,
                 const fb_filter_prog_t* prog, const int64_t* probe_words, int32_t nprobe, int32_t k,
                 int32_t cap, uint64_t* cand_key, uint32_t* cand_slot, uint32_t* cand_cnt,

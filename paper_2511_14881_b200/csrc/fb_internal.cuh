@@ -159,6 +159,8 @@ struct IvfScanArgs {
   int32_t cap;
 };
 int launch_ivf_scan(const IvfScanArgs& a, cudaStream_t s);
+int launch_final_topk(const double* final_, int64_t ld, const int32_t* count, int n_requests,
+                      int topk, int64_t* order, int32_t* out_count, cudaStream_t s);
 int launch_union_merge(const uint64_t* keys, const int32_t* counts, int B, int T, int k,
                        int64_t n_words, uint64_t* bitmap, const uint64_t* id_of_rank,
                        uint64_t* merged, int64_t* merged_ranks, int32_t* mcount, cudaStream_t s);

@@ -1820,4 +1820,167 @@ int launch_dequant(const int32_t* scores, const int32_t* item_row_sum, const int
   return FB_OK;
 }
 
+// ------------------------------------------------------------------------------------
+// Final ranking of multi-task retrieval (ref retrieval.retrieve, retrieval.py:190:
+// order = np.lexsort((merged, -final))[:topk]): per request CTA, the first n = count[b]
+// entries of final[b, :] (merged candidates in ascending id order, so position breaks ties
+// as the id does) ordered by (final desc, position asc) with NumPy's float order: NaN after
+// every number, -0.0 == +0.0. Keys u = orderable(-final) ascending:
+//   1. keys staged in smem; an MSD radix select finds the boundary prefix of the kk-th key;
+//   2. keys below the boundary are kept, keys on it in position order until kk are kept;
+//   3. a bitonic sort of the kk (key, position) pairs; order[b, r] = position.
+// ------------------------------------------------------------------------------------
+constexpr int kFtThreads = 1024;
+constexpr int kFtMaxN = 24576;   // staged keys per request
+constexpr int kFtMaxK = 8192;    // sorted selection (power of two)
+constexpr size_t kFtSmem = (size_t)kFtMaxN * 8 + (size_t)kFtMaxK * 4 + 256 * 4 + 64 * 4;
+
+__device__ __forceinline__ uint64_t ft_key(double v) {
+  const double u = -v;
+  if (u != u) return ~0ull;  // NaN: after every number
+  uint64_t b = (uint64_t)__double_as_longlong(u == 0.0 ? 0.0 : u);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void __launch_bounds__(kFtThreads, 1)
+    k_final_topk(const double* __restrict__ final_, int64_t ld, const int32_t* __restrict__ count,
+                 int32_t topk, int64_t* __restrict__ order, int32_t* __restrict__ out_count) {
+  extern __shared__ __align__(16) uint8_t ft_smem[];
+  uint64_t* s_key = reinterpret_cast<uint64_t*>(ft_smem);               // [kFtMaxN]
+  uint32_t* s_pos = reinterpret_cast<uint32_t*>(s_key + kFtMaxN);       // [kFtMaxK]
+  uint32_t* s_hist = s_pos + kFtMaxK;                                   // [256]
+  uint32_t* s_misc = s_hist + 256;                                      // [64]
+  const int b = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int n = min(count[b], kFtMaxN);
+  const int kk = min(topk, n);
+  const double* f = final_ + (int64_t)b * ld;
+  for (int i = t; i < n; i += kFtThreads) s_key[i] = ft_key(f[i]);
+  // 1. radix select: prefix / mask of the kk-th smallest key, r = its rank inside the bin
+  uint64_t prefix = 0ull, mask = 0ull;
+  int r = kk;
+  __syncthreads();
+  for (int shift = 56; shift >= 0 && kk > 0; shift -= 8) {
+    for (int i = t; i < 256; i += kFtThreads) s_hist[i] = 0u;
+    __syncthreads();
+    for (int i = t; i < n; i += kFtThreads) {
+      const uint64_t u = s_key[i];
+      if ((u & mask) == prefix) atomicAdd(s_hist + (int)((u >> shift) & 0xFF), 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {  // the digit whose cumulative count reaches r
+      uint32_t c[8], sum = 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = s_hist[lane * 8 + j];
+        sum += c[j];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
+      }
+      uint32_t run = incl - sum;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (run < (uint32_t)r && run + c[j] >= (uint32_t)r) {
+          s_misc[0] = (uint32_t)(lane * 8 + j);
+          s_misc[1] = run;
+          s_misc[2] = c[j];
+        }
+        run += c[j];
+      }
+    }
+    __syncthreads();
+    const uint32_t d = s_misc[0];
+    r -= (int)s_misc[1];
+    const uint32_t bin = s_misc[2];
+    prefix |= (uint64_t)d << shift;
+    mask |= 0xFFull << shift;
+    __syncthreads();
+    if ((int)bin == r) break;  // the whole bin completes the count
+  }
+  // 2. selection: keys below the boundary (any order), then r keys on it in position order
+  if (t == 0) s_misc[3] = 0u;
+  __syncthreads();
+  for (int i = t; i < n; i += kFtThreads) {
+    const uint64_t u = s_key[i];
+    if ((u & mask) < prefix) s_pos[atomicAdd(s_misc + 3, 1u)] = (uint32_t)i;
+  }
+  __syncthreads();
+  const uint32_t n_lt = s_misc[3];
+  uint32_t taken = 0u;
+  for (int base = 0; base < n && (int)taken < r; base += kFtThreads) {
+    const int i = base + t;
+    const bool e = i < n && (s_key[i] & mask) == prefix;
+    const uint32_t bal = __ballot_sync(0xffffffffu, e);
+    if (lane == 0) s_misc[32 + warp] = (uint32_t)__popc(bal);
+    __syncthreads();
+    uint32_t before = 0u, total = 0u;
+    for (int w = 0; w < kFtThreads / 32; ++w) {
+      const uint32_t c = s_misc[32 + w];
+      before += w < warp ? c : 0u;
+      total += c;
+    }
+    const uint32_t pos = taken + before + (uint32_t)__popc(bal & ((1u << lane) - 1u));
+    if (e && (int)pos < r) s_pos[n_lt + pos] = (uint32_t)i;
+    taken += total;
+    __syncthreads();
+  }
+  __syncthreads();
+  // 3. bitonic sort of (key, position) over the next power of two >= kk; padding last
+  int P = 1;
+  while (P < kk) P <<= 1;
+  // keys of the selected positions into registers, then over the (now free) key buffer
+  constexpr int kPer = kFtMaxK / kFtThreads;
+  uint64_t kv[kPer];
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int i = t + j * kFtThreads;
+    kv[j] = i < kk ? s_key[s_pos[i]] : ~0ull;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int i = t + j * kFtThreads;
+    if (i < P) {
+      s_key[i] = kv[j];
+      if (i >= kk) s_pos[i] = 0xFFFFFFFFu;
+    }
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int x = t; x < P / 2; x += kFtThreads) {
+        const int lo = 2 * x - (x & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t ka = s_key[lo], kb = s_key[hi];
+        const uint32_t pa = s_pos[lo], pb = s_pos[hi];
+        const bool gt = ka > kb || (ka == kb && pa > pb);
+        if (gt == up) {
+          s_key[lo] = kb; s_key[hi] = ka;
+          s_pos[lo] = pb; s_pos[hi] = pa;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  int64_t* o = order + (int64_t)b * topk;
+  for (int i = t; i < topk; i += kFtThreads) o[i] = i < kk ? (int64_t)s_pos[i] : 0;
+  if (t == 0) out_count[b] = kk;
+}
+
+int launch_final_topk(const double* final_, int64_t ld, const int32_t* count, int n_requests,
+                      int topk, int64_t* order, int32_t* out_count, cudaStream_t s) {
+  if (n_requests <= 0 || topk <= 0) return FB_OK;
+  if (topk > kFtMaxK) return fail(FB_ERR_UNSUPPORTED, "final top-k above 8192");
+  if (ld > kFtMaxN) return fail(FB_ERR_UNSUPPORTED, "more than 24576 merged candidates");
+  FB_CUDA(cudaFuncSetAttribute(k_final_topk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kFtSmem));
+  k_final_topk<<<n_requests, kFtThreads, kFtSmem, s>>>(final_, ld, count, topk, order, out_count);
+  FB_LAUNCH_CHECK("k_final_topk");
+  return FB_OK;
+}
+
 }  // namespace fb

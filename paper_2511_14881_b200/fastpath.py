@@ -220,7 +220,7 @@ class _Graph:
             self._run_tail(out)
 
     def _run_tail(self, out):
-        from .overarch import merge_device, value_model_device
+        from .overarch import final_topk_device, merge_device, value_model_device
         t = self.tail
         T, k = self.T, self.k0
         merged, mcount = merge_device(out.ids.view(1, T, k), out.count.view(1, T), t["merge"])
@@ -243,10 +243,8 @@ class _Graph:
         for z in zero:
             anyz |= z.view(1)
         d["zero"].copy_(anyz.to(torch.int32))
-        final = torch.where(valid, final, torch.full_like(final, -float("inf")))
         topk = t["topk"]
-        order = torch.sort(final, dim=1, descending=True, stable=True).indices[:, :topk]
-        n = torch.clamp(mcount, max=topk)
+        order, n = final_topk_device(final, mcount, topk)
         d["out_ids"].copy_(torch.gather(merged, 1, order))
         d["final"].copy_(torch.gather(final, 1, order))
         d["ts"].copy_(torch.gather(ts, 2, order[:, None, :].expand(1, T, -1)))

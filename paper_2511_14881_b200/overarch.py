@@ -266,6 +266,37 @@ def value_model_device(spec: dict, task_scores: dict[str, torch.Tensor],
 
 
 # ------------------------------------------------------------------------------------
+# final ranking
+# ------------------------------------------------------------------------------------
+FINAL_TOPK_MAX_CAND = 24576  # fb_final_topk's staging limit (merged candidates per request)
+FINAL_TOPK_MAX_K = 8192
+
+
+def final_topk_device(final: torch.Tensor, mcount: torch.Tensor, topk: int):
+    """``np.lexsort((merged, -final))[:topk]`` per request (ref retrieval.py:190) on the
+    device: final float64 [B, C] over merged candidates in ascending id order, mcount int32
+    [B] valid entries -> (order int64 [B, topk], n int32 [B] = min(topk, mcount)).
+    NumPy's float order (NaN last, -0.0 == +0.0) through ``fb_final_topk``; shapes past its
+    limits take a stable device sort instead."""
+    B, C = final.shape
+    topk = int(topk)
+    if C > FINAL_TOPK_MAX_CAND or topk > FINAL_TOPK_MAX_K:
+        valid = torch.arange(C, device=final.device)[None, :] < mcount[:, None]
+        f = torch.where(valid, final, torch.full_like(final, -float("inf")))
+        order = torch.sort(f, dim=1, descending=True, stable=True).indices[:, :topk]
+        n = torch.clamp(mcount, max=topk).to(torch.int32)
+        return order, n
+    f = final.contiguous()
+    cnt = mcount.to(torch.int32).contiguous()
+    order = torch.empty((B, topk), dtype=torch.int64, device=final.device)
+    n = torch.empty(B, dtype=torch.int32, device=final.device)
+    _native.check(_native.lib().fb_final_topk(f.data_ptr(), C, cnt.data_ptr(), B, topk,
+                                              order.data_ptr(), n.data_ptr(),
+                                              _native.stream_ptr()))
+    return order, n
+
+
+# ------------------------------------------------------------------------------------
 # merge
 # ------------------------------------------------------------------------------------
 def merge_device(ids: torch.Tensor, counts: torch.Tensor, merge: str):
@@ -396,9 +427,7 @@ class MultiTaskOp:
         ts = self.scorer.score(self.cache, rows, mcount, users, self.tasks)    # [B, T, C]
         final = value_model_device(self.spec, {t: ts[:, j, :] for j, t in enumerate(self.tasks)},
                                    valid)
-        final = torch.where(valid, final, torch.full_like(final, -float("inf")))
-        order = torch.sort(final, dim=1, descending=True, stable=True).indices[:, : self.topk]
-        n = torch.minimum(mcount, torch.tensor(self.topk, dtype=torch.int32, device=mcount.device))
+        order, n = final_topk_device(final, mcount, self.topk)
         return MultiTaskOutput(ids=torch.gather(merged, 1, order),
                                scores=torch.gather(final, 1, order),
                                task_scores=torch.gather(ts, 2, order[:, None, :].expand(B, T, -1)),
@@ -493,8 +522,7 @@ def retrieve(engine, req) -> RetrieveResult:
         vm = req.value_model if req.value_model is not None else engine.default_value_model
         spec = value_model_spec(vm) or mean_of_tasks_spec(names)
         final = value_model_device(spec, {t: ts[:, j, :] for j, t in enumerate(names)}, valid)
-        final = torch.where(valid, final, torch.full_like(final, -float("inf")))
-        order = torch.sort(final, dim=1, descending=True, stable=True).indices[0, : min(req.topk, n)]
+        order = final_topk_device(final, mcount, min(req.topk, n))[0][0]
         ids_h = u64_host(merged[0, order].contiguous())
         fin_h = final[0, order].cpu().numpy()
         ts_h = ts[0][:, order].cpu().numpy()

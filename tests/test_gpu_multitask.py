@@ -198,3 +198,29 @@ def test_retrieve_graph_path_equals_eager(golden, monkeypatch):
         assert [(i.item_id, i.score, i.task_scores) for i in fast.items] == \
             [(i.item_id, i.score, i.task_scores) for i in slow.items], m["r"]
         assert vars(fast.scan) == vars(slow.scan) and vars(fast.filter_stats) == vars(slow.filter_stats)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("C,topk", [(20000, 5000), (37, 5), (1000, 1000), (24576, 8192)])
+def test_final_topk_kernel_numpy_order(C, topk):
+    """fb_final_topk == np.lexsort((positions, -final))[:topk] per request (ref
+    retrieval.py:190) on values with heavy ties, NaN, +-0.0, +-inf and short counts."""
+    import numpy as np
+    import torch
+
+    from paper_2511_14881_b200.overarch import final_topk_device
+    rng = np.random.default_rng(C + topk)
+    B = 6
+    vals = rng.integers(-50, 50, size=(B, C)).astype(np.float64) / 8.0
+    specials = np.array([np.nan, 0.0, -0.0, np.inf, -np.inf])
+    hit = rng.random((B, C)) < 0.02
+    vals[hit] = specials[rng.integers(0, len(specials), size=int(hit.sum()))]
+    counts = np.array([C, C - 1, topk // 2, 0, 1, max(1, C // 3)], dtype=np.int32)
+    order, n = final_topk_device(torch.as_tensor(vals, device="cuda"),
+                                 torch.as_tensor(counts, device="cuda"), topk)
+    order, n = order.cpu().numpy(), n.cpu().numpy()
+    for b in range(B):
+        m = int(counts[b])
+        want = np.lexsort((np.arange(m), -vals[b, :m]))[:topk]
+        assert n[b] == len(want)
+        assert np.array_equal(order[b, : n[b]], want), f"request {b}"
