@@ -128,24 +128,27 @@ def test_shuffled_ids_tiebreak(cuda):
     check_rows(out, oracle_answers(wl, 3000, range(0, 32, 3)))
 
 
-@pytest.mark.parametrize("mode", ["0", "1"])
-def test_filter_first_and_per_hit_modes_agree(cuda, monkeypatch, mode):
+@pytest.mark.parametrize("mode,B,v1", [("0", 40, "0"), ("1", 40, "0"), ("0", 200, "0"),
+                                        ("1", 200, "0"), ("0", 200, "1"), ("1", 200, "1")])
+def test_filter_first_and_per_hit_modes_agree(cuda, monkeypatch, mode, B, v1):
     """The window-form emit pass has two hit passes (per-hit test on item-major column bits,
     and filter-first eligibility words); the device picks one from the sampled eligibility.
     Forcing either must give the oracle's rows, at the benchmark's ~10 % selectivity and with
-    explicit masks and ranges."""
+    explicit masks and ranges -- in the 20-warp layout (B <= 128, or FB_CNF_V1=1) and in the
+    24-warp layout of two M-blocks (modes 3 and 4)."""
     from paper_2511_14881_b200 import _device, workload
     from paper_2511_14881_b200.engine import TopkOp
     monkeypatch.setenv("FB_CNF_FFIRST", mode)
-    wl = workload.make_workload(300_000, 40, seed=6)
+    monkeypatch.setenv("FB_CNF_V1", v1)
+    wl = workload.make_workload(300_000, B, seed=6)
     out = run_op(wl, 2000)
-    check_rows(out, oracle_answers(wl, 2000, range(0, 40, 3)))
+    check_rows(out, oracle_answers(wl, 2000, range(0, B, 7 if B > 64 else 3)))
     # ranges + explicit masks through the same kernel
     idx = wl.index
     rng = np.random.default_rng(5)
     ranges = np.array([[0, 64 * 700], [64 * 1500, 64 * 4000]])
-    op = TopkOp(idx, 40, 700, ranges)
-    m = rng.integers(0, 2**63, size=(40, idx.n_words), dtype=np.int64)
+    op = TopkOp(idx, B, 700, ranges)
+    m = rng.integers(0, 2**63, size=(B, idx.n_words), dtype=np.int64)
     masks = torch.from_numpy(m).cuda()
     got = op(wl.queries_q, wl.batch.to_device(), masks=masks)
     torch.cuda.synchronize()
@@ -153,7 +156,7 @@ def test_filter_first_and_per_hit_modes_agree(cuda, monkeypatch, mode):
     items = idx.items.cpu().numpy()[:, : wl.dim]
     valid, ids = _device.u64_host(idx.valid), _device.u64_host(idx.item_ids)
     qq = wl.queries_q.cpu().numpy()[:, : wl.dim]
-    for q in (0, 13, 39):
+    for q in (0, 13, 39, B - 1):
         cf = wl.filters[q]
         prog = ([(int(o), int(a)) for o, a in cf.ops], [(f, v, qb.set_bits) for f, v, qb in cf.leaves])
         full = orc.eval_compiled(prog[0], prog[1], idx.bloom.planes, valid)
