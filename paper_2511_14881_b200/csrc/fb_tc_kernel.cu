@@ -1144,6 +1144,7 @@ __global__ void __launch_bounds__(kMode >= 3 ? kCnf3Threads : kCnfThreads)
       auto tail = [&](int t) {
         const int par = t & 1;
         nb_sync(kNbSvFull + par, kNbSvCount);
+        if (lw == 0) FB_TR(a, t, 15);
         cnf3_builder_drain(a, m, be, t, lw, lane);
         __syncwarp();
         nb_arrive(kNbSvEmpty + par, kNbSvCount);
@@ -1341,7 +1342,15 @@ __global__ void __launch_bounds__(kMode >= 3 ? kCnf3Threads : kCnfThreads)
         // their eight row loads issued together, about half the rounds of one cursor
         uint32_t nzA = nzm & 0xFu, nzB = nzm & 0xF0u;
         int ca = nzA ? __ffs(nzA) - 1 : 0, cb = nzB ? __ffs(nzB) - 1 : 4;
-        uint32_t curA = nzA ? word_at(ca) : 0u, curB = nzB ? word_at(cb) : 0u;
+        // the tile's hit words stay in registers (mw): advancing a cursor selects the next
+        // word instead of re-reading it from the hit map
+        auto wordA = [&](int c) -> uint32_t {
+          return c < 2 ? (c == 0 ? mw[0] : mw[1]) : (c == 2 ? mw[2] : mw[3]);
+        };
+        auto wordB = [&](int c) -> uint32_t {
+          return c < 6 ? (c == 4 ? mw[4] : mw[5]) : (c == 6 ? mw[6] : mw[7]);
+        };
+        uint32_t curA = nzA ? wordA(ca) : 0u, curB = nzB ? wordB(cb) : 0u;
         const uint32_t lt = lanemask_lt();
         const uint32_t rstride = (uint32_t)a.tb_stride * 4u;
         while (__any_sync(0xffffffffu, (curA | curB) != 0u)) {
@@ -1366,14 +1375,14 @@ __global__ void __launch_bounds__(kMode >= 3 ? kCnf3Threads : kCnfThreads)
             nzA &= nzA - 1u;
             if (nzA) {
               ca = __ffs(nzA) - 1;
-              curA = word_at(ca);
+              curA = wordA(ca);
             }
           }
           if (hasB && curB == 0u) {
             nzB &= nzB - 1u;
             if (nzB) {
               cb = __ffs(nzB) - 1;
-              curB = word_at(cb);
+              curB = wordB(cb);
             }
           }
           const uint32_t bA = __ballot_sync(0xffffffffu, sa);
@@ -1475,8 +1484,9 @@ __global__ void __launch_bounds__(kMode >= 3 ? kCnf3Threads : kCnfThreads)
              g_tr[t][4] - t0, g_tr[t][5] - t0, g_tr[t][6] - t0, g_tr[t][7] - t0,
              g_tr[t][8] - t0, g_tr[t][11] - t0, g_tr[t][9] - t0, g_tr[t][10] - t0);
     for (int t = 0; t < 16; ++t)
-      printf("dense %2d: top %6lld afterHmEmpty %6lld beforeAccWait %6lld d0 %6lld\n", t,
-             g_tr[t][12] - t0, g_tr[t][13] - t0, g_tr[t][14] - t0, g_tr[t][4] - t0);
+      printf("dense %2d: top %6lld afterHmEmpty %6lld beforeAccWait %6lld d0 %6lld | ev15 %6lld\n", t,
+             g_tr[t][12] - t0, g_tr[t][13] - t0, g_tr[t][14] - t0, g_tr[t][4] - t0,
+             g_tr[t][15] - t0);
   }
 #endif
   if (warp == 1)
