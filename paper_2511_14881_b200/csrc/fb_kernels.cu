@@ -562,8 +562,8 @@ __global__ void __launch_bounds__(256) k_scan_simt(ScanArgs a) {
 // so every eligible pair is kept and the selection is exact without a threshold.
 // ------------------------------------------------------------------------------------
 constexpr int kIvfThreads = 64;
-constexpr int kIvfMaxOps = 1024;   // staged ops per query (longer programs: per-word global path)
-constexpr int kIvfMaxPush = 512;
+constexpr int kIvfMaxOps = 512;    // staged ops per query (longer programs: per-word global path)
+constexpr int kIvfMaxPush = 128;  // (smem per CTA bounds the resident CTAs: 17 KB -> 13 per SM)
 constexpr int kIvfRing = 4;        // leaves whose plane loads are in flight ahead of the stack
 
 // The query's program, staged per CTA: ops with leaf operands renumbered in push order,
