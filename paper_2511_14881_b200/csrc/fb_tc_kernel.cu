@@ -106,6 +106,7 @@ struct TcArgs {
 // clock64 at pipeline events of its first 16 tiles and prints them at exit.
 #ifdef FB_TRACE
 __device__ long long g_tr[16][16];
+__device__ long long g_hit_rounds[8];
 #define FB_TR(a, t, e)                                                          \
   do {                                                                          \
     if (((a).dbg & 1024) && blockIdx.x == 0 && (t) < 16 && (threadIdx.x & 31) == 0) \
@@ -460,7 +461,10 @@ constexpr int kCnfDense0 = 8;
 constexpr int kCnfDenseWarps = 4;
 constexpr int kCnfHit0 = 12;
 constexpr int kCnfHitWarps = 8;
-constexpr int kSurvCap = 128;  // u16 survivor entries per hit warp: (lane << 8) | item
+#ifndef FB_HIT_TAKE
+#define FB_HIT_TAKE 4  // mode 3: hits taken per lane and round (2: 1.035-1.039 ms, 3: 1.028-1.033, 4: 1.029)
+#endif
+constexpr int kSurvCap = FB_HIT_TAKE >= 4 ? 160 : 128;  // u16 survivor entries per hit warp: (lane << 8) | item
 // named barrier ids (0 is __syncthreads) and their thread counts
 constexpr int kNbHmFull = 1, kNbHmEmpty = 3, kNbLeafFull = 5, kNbLeafEmpty = 7;  // + stage
 constexpr int kNbHmCount = 32 * (kCnfDenseWarps + kCnfHitWarps);
@@ -1338,60 +1342,52 @@ __global__ void __launch_bounds__(kMode >= 3 ? kCnf3Threads : kCnfThreads)
       uint32_t n_sv = 0;  // warp-uniform survivor count
       int n_rounds = 0;
       if constexpr (kMode == 3) {
-        // two cursors per lane (chunks 0-3 and 4-7): two independent filter tests per round,
-        // their eight row loads issued together, about half the rounds of one cursor
-        uint32_t nzA = nzm & 0xFu, nzB = nzm & 0xF0u;
-        int ca = nzA ? __ffs(nzA) - 1 : 0, cb = nzB ? __ffs(nzB) - 1 : 4;
-        // the tile's hit words stay in registers (mw): advancing a cursor selects the next
-        // word instead of re-reading it from the hit map
-        auto wordA = [&](int c) -> uint32_t {
-          return c < 2 ? (c == 0 ? mw[0] : mw[1]) : (c == 2 ? mw[2] : mw[3]);
+        // one cursor over the tile's eight hit words (kept in registers), NT hits taken per
+        // round wherever they are: the round count is max over lanes of ceil(hits / NT); the
+        // NT filter tests of a round issue their row loads together
+        constexpr int NT = FB_HIT_TAKE;
+        auto word8 = [&](int c) -> uint32_t {
+          return c < 4 ? (c < 2 ? (c == 0 ? mw[0] : mw[1]) : (c == 2 ? mw[2] : mw[3]))
+                       : (c < 6 ? (c == 4 ? mw[4] : mw[5]) : (c == 6 ? mw[6] : mw[7]));
         };
-        auto wordB = [&](int c) -> uint32_t {
-          return c < 6 ? (c == 4 ? mw[4] : mw[5]) : (c == 6 ? mw[6] : mw[7]);
-        };
-        uint32_t curA = nzA ? wordA(ca) : 0u, curB = nzB ? wordB(cb) : 0u;
+        uint32_t rest = nzm;
+        int cc8 = rest ? __ffs(rest) - 1 : 0;
+        rest &= rest - 1u;
+        uint32_t cur = nzm ? word8(cc8) : 0u;
         const uint32_t lt = lanemask_lt();
         const uint32_t rstride = (uint32_t)a.tb_stride * 4u;
-        while (__any_sync(0xffffffffu, (curA | curB) != 0u)) {
+        while (__any_sync(0xffffffffu, cur != 0u)) {
           ++n_rounds;
-          const bool hasA = curA != 0u, hasB = curB != 0u;
-          const uint32_t ia = hasA ? (uint32_t)(ca * 32 + __ffs(curA) - 1) : 0u;
-          const uint32_t ib = hasB ? (uint32_t)(cb * 32 + __ffs(curB) - 1) : 0u;
-          curA &= curA - 1u;
-          curB &= curB - 1u;
-          const uint32_t rowA = tb_s + ia * rstride, rowB = tb_s + ib * rstride;
-          uint32_t xa[4], xb[4];
+          bool has[NT], sv[NT];
+          uint32_t itm[NT], row[NT], x[NT][4];
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const uint2 ta = lds64v(rowA + wo[g]);
-            const uint2 tb = lds64v(rowB + wo[g]);
-            xa[g] = (ta.x & lo[g]) | (ta.y & hi[g]);
-            xb[g] = (tb.x & lo[g]) | (tb.y & hi[g]);
-          }
-          const bool sa = hasA && (nof || min(min(xa[0], xa[1]), min(xa[2], xa[3])) != 0u);
-          const bool sb2 = hasB && (nof || min(min(xb[0], xb[1]), min(xb[2], xb[3])) != 0u);
-          if (hasA && curA == 0u) {
-            nzA &= nzA - 1u;
-            if (nzA) {
-              ca = __ffs(nzA) - 1;
-              curA = wordA(ca);
+          for (int u = 0; u < NT; ++u) {
+            has[u] = cur != 0u;
+            itm[u] = has[u] ? (uint32_t)(cc8 * 32 + __ffs(cur) - 1) : 0u;
+            row[u] = tb_s + itm[u] * rstride;
+            cur &= cur - 1u;
+            if (cur == 0u && rest != 0u) {
+              cc8 = __ffs(rest) - 1;
+              rest &= rest - 1u;
+              cur = word8(cc8);
             }
           }
-          if (hasB && curB == 0u) {
-            nzB &= nzB - 1u;
-            if (nzB) {
-              cb = __ffs(nzB) - 1;
-              curB = wordB(cb);
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+#pragma unroll
+            for (int u = 0; u < NT; ++u) {
+              const uint2 t = lds64v(row[u] + wo[g]);
+              x[u][g] = (t.x & lo[g]) | (t.y & hi[g]);
             }
+#pragma unroll
+          for (int u = 0; u < NT; ++u) {
+            sv[u] = has[u] && (nof || min(min(x[u][0], x[u][1]), min(x[u][2], x[u][3])) != 0u);
+            const uint32_t bb = __ballot_sync(0xffffffffu, sv[u]);
+            if (sv[u])
+              sts16(sv_s + 2u * (n_sv + (uint32_t)__popc(bb & lt)), ((uint32_t)lane << 8) | itm[u]);
+            n_sv += (uint32_t)__popc(bb);
           }
-          const uint32_t bA = __ballot_sync(0xffffffffu, sa);
-          const uint32_t bB = __ballot_sync(0xffffffffu, sb2);
-          if (sa) sts16(sv_s + 2u * (n_sv + (uint32_t)__popc(bA & lt)), ((uint32_t)lane << 8) | ia);
-          n_sv += (uint32_t)__popc(bA);
-          if (sb2) sts16(sv_s + 2u * (n_sv + (uint32_t)__popc(bB & lt)), ((uint32_t)lane << 8) | ib);
-          n_sv += (uint32_t)__popc(bB);
-          if (n_sv > (uint32_t)(kSurvCap - 64)) {
+          if (n_sv > (uint32_t)(kSurvCap - 32 * NT)) {
             __syncwarp();
             drain_survivors(a, m, e, sv_s, n_sv, qbase, b_s, mst, tile, lane);
             __syncwarp();
@@ -1443,6 +1439,12 @@ __global__ void __launch_bounds__(kMode >= 3 ? kCnf3Threads : kCnfThreads)
 #ifdef FB_TRACE
       if ((a.dbg & 1024) && blockIdx.x == 0 && warp == kHit0 && lane == 0 && it < 16)
         g_tr[it][3] = (long long)n_rounds * 1000 + n_sv;
+      if ((a.dbg & 1024) && blockIdx.x == 0 && lane == 0) {
+        g_hit_rounds[warp - kHit0] += n_rounds;
+        int hits = 0;
+        for (int c = 0; c < 8; ++c) hits += 0;  // (per-lane counts are not kept)
+        (void)hits;
+      }
 #endif
       if constexpr (kHand) {
         if (lane == 0)
@@ -1483,6 +1485,9 @@ __global__ void __launch_bounds__(kMode >= 3 ? kCnf3Threads : kCnfThreads)
              t, g_tr[t][0] - t0, g_tr[t][1] - t0, g_tr[t][2] - t0, g_tr[t][3],
              g_tr[t][4] - t0, g_tr[t][5] - t0, g_tr[t][6] - t0, g_tr[t][7] - t0,
              g_tr[t][8] - t0, g_tr[t][11] - t0, g_tr[t][9] - t0, g_tr[t][10] - t0);
+    printf("hit rounds per warp (CTA 0, whole launch):");
+    for (int w = 0; w < 8; ++w) printf(" %lld", g_hit_rounds[w]);
+    printf("\n");
     for (int t = 0; t < 16; ++t)
       printf("dense %2d: top %6lld afterHmEmpty %6lld beforeAccWait %6lld d0 %6lld | ev15 %6lld\n", t,
              g_tr[t][12] - t0, g_tr[t][13] - t0, g_tr[t][14] - t0, g_tr[t][4] - t0,
