@@ -276,6 +276,16 @@ int fb_merge_union(const uint64_t* keys, const int32_t* counts, int32_t n_reques
                    uint64_t* bitmap, uint64_t* merged, int64_t* merged_ranks, int32_t* mcount,
                    void* stream);
 
+/* Device, OverArch value model (value_model.py:31-91 as retrieval.retrieve applies it,
+ * retrieval.py:186-189): out[b * ld + i] = formula(task_scores[(b * n_tasks + t) * ld + i])
+ * for every request b and candidate i < ld, in float64 with NumPy's rounding. code: postfix
+ * u16 words (op | arg << 8): CONST c, TASK t, ADD, SUB, MUL, DIV, MIN, MAX, CLAMP c (consts
+ * c, c + 1), IF_{LT,LE,GT,GE,EQ} (left right then else); consts: float64. A zero divisor for
+ * a candidate i < count[b] sets *zero_flag to 1 (the reference raises DivByZero). */
+int fb_value_model(const uint16_t* code, int32_t n_code, const double* consts,
+                   const double* task_scores, int32_t n_requests, int32_t n_tasks, int64_t ld,
+                   const int32_t* count, double* out, int32_t* zero_flag, void* stream);
+
 /* Device, final ranking of multi-task retrieval (retrieval.retrieve, retrieval.py:190:
  * np.lexsort((merged, -final))[:topk]): for request b, the first count[b] values of
  * final_scores[b * ld ..] (merged candidates in ascending id order) ordered by (value desc,

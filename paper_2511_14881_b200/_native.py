@@ -49,7 +49,7 @@ EXPORTED = (
     "fb_topk_set_timing", "fb_topk_last_timing", "fb_topk_scan_path", "fb_debug_tc_scores",
     "fb_task_dots_f64", "fb_kmeans_min_sqdist", "fb_pairwise_sum_scratch",
     "fb_pairwise_sum_f64", "fb_kmeans_draw", "fb_row_sqnorm_f64", "fb_kmeans_assign",
-    "fb_kmeans_means", "fb_ivf_topk", "fb_merge_union", "fb_final_topk", "fb_vocab_create", "fb_vocab_free",
+    "fb_kmeans_means", "fb_ivf_topk", "fb_merge_union", "fb_final_topk", "fb_value_model", "fb_vocab_create", "fb_vocab_free",
     "fb_pack_text", "fb_pack_postfix", "fb_pack_meta", "fb_pack_array", "fb_pack_free",
 )
 
@@ -154,6 +154,7 @@ def _declare(lib) -> None:
         "fb_ivf_topk": ([ctypes.POINTER(FbIndex), c_vp, i32, ctypes.POINTER(FbFilterProg), c_vp, i32,
                          i32, i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, dbl, dbl, c_vp],
                         i32),
+        "fb_value_model": ([c_vp, i32, c_vp, c_vp, i32, i32, i64, c_vp, c_vp, c_vp, c_vp], i32),
         "fb_final_topk": ([c_vp, i64, c_vp, i32, i32, c_vp, c_vp, c_vp], i32),
         "fb_merge_union": ([c_vp, c_vp, i32, i32, i32, i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
                            i32),

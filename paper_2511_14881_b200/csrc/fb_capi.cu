@@ -570,6 +570,15 @@ int fb_merge_union(const uint64_t* keys, const int32_t* counts, int32_t n_reques
                             static_cast<cudaStream_t>(stream));
 }
 
+int fb_value_model(const uint16_t* code, int32_t n_code, const double* consts,
+                   const double* task_scores, int32_t n_requests, int32_t n_tasks, int64_t ld,
+                   const int32_t* count, double* out, int32_t* zero_flag, void* stream) {
+  if (n_code <= 0 || n_requests < 0 || n_tasks < 0 || ld < 0)
+    return fail(FB_ERR_INVALID, "bad value-model size");
+  return launch_value_model(code, n_code, consts, task_scores, n_requests, n_tasks, ld, count, out,
+                            zero_flag, static_cast<cudaStream_t>(stream));
+}
+
 int fb_final_topk(const double* final_scores, int64_t ld, const int32_t* count,
                   int32_t n_requests, int32_t topk, int64_t* order, int32_t* out_count,
                   void* stream) {

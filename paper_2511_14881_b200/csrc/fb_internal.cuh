@@ -159,6 +159,9 @@ struct IvfScanArgs {
   int32_t cap;
 };
 int launch_ivf_scan(const IvfScanArgs& a, cudaStream_t s);
+int launch_value_model(const uint16_t* code, int n_code, const double* consts, const double* ts,
+                       int B, int T, int64_t C, const int32_t* count, double* out,
+                       int32_t* zero_flag, cudaStream_t s);
 int launch_final_topk(const double* final_, int64_t ld, const int32_t* count, int n_requests,
                       int topk, int64_t* order, int32_t* out_count, cudaStream_t s);
 int launch_union_merge(const uint64_t* keys, const int32_t* counts, int B, int T, int k,

@@ -1854,17 +1854,47 @@ __global__ void __launch_bounds__(kFtThreads, 1)
   const int n = min(count[b], kFtMaxN);
   const int kk = min(topk, n);
   const double* f = final_ + (int64_t)b * ld;
-  for (int i = t; i < n; i += kFtThreads) s_key[i] = ft_key(f[i]);
-  // 1. radix select: prefix / mask of the kk-th smallest key, r = its rank inside the bin
-  uint64_t prefix = 0ull, mask = 0ull;
+  uint64_t kor = 0ull, kand = ~0ull;  // bits that differ among the keys
+  for (int i = t; i < n; i += kFtThreads) {
+    const uint64_t u = ft_key(f[i]);
+    s_key[i] = u;
+    kor |= u;
+    kand &= u;
+  }
+  // 1. radix select: prefix / mask of the kk-th smallest key, r = its rank inside the bin;
+  //    it starts at the highest byte where the keys differ (the leading ones are common)
+  uint64_t* s_red = reinterpret_cast<uint64_t*>(s_misc + 32);  // [2] (s_misc[32..35])
+  if (t == 0) {
+    s_red[0] = 0ull;
+    s_red[1] = ~0ull;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    kor |= __shfl_xor_sync(0xffffffffu, kor, d);
+    kand &= __shfl_xor_sync(0xffffffffu, kand, d);
+  }
+  if (lane == 0) {
+    atomicOr(reinterpret_cast<unsigned long long*>(s_red), kor);
+    atomicAnd(reinterpret_cast<unsigned long long*>(s_red + 1), kand);
+  }
+  __syncthreads();
+  const uint64_t diff = s_red[0] & ~s_red[1];
+  const int top = diff == 0ull ? 0 : (63 - __clzll((long long)diff)) / 8 * 8;
+  uint64_t mask = top >= 56 ? 0ull : ~0ull << (top + 8);
+  uint64_t prefix = s_red[0] & mask;  // the common leading bytes
   int r = kk;
   __syncthreads();
-  for (int shift = 56; shift >= 0 && kk > 0; shift -= 8) {
+  for (int shift = top; shift >= 0 && kk > 0; shift -= 8) {
     for (int i = t; i < 256; i += kFtThreads) s_hist[i] = 0u;
     __syncthreads();
     for (int i = t; i < n; i += kFtThreads) {
       const uint64_t u = s_key[i];
-      if ((u & mask) == prefix) atomicAdd(s_hist + (int)((u >> shift) & 0xFF), 1u);
+      const bool in = (u & mask) == prefix;
+      const uint32_t dg = in ? (uint32_t)((u >> shift) & 0xFF) : 256u;
+      // one atomic per distinct digit per warp (the keys crowd into few bins)
+      const uint32_t peers = __match_any_sync(__activemask(), dg);
+      if (in && lane == __ffs(peers) - 1) atomicAdd(s_hist + dg, (uint32_t)__popc(peers));
     }
     __syncthreads();
     if (warp == 0) {  // the digit whose cumulative count reaches r
@@ -1980,6 +2010,82 @@ int launch_final_topk(const double* final_, int64_t ld, const int32_t* count, in
                                (int)kFtSmem));
   k_final_topk<<<n_requests, kFtThreads, kFtSmem, s>>>(final_, ld, count, topk, order, out_count);
   FB_LAUNCH_CHECK("k_final_topk");
+  return FB_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// OverArch value model (ref value_model.py:31-91, evaluated by retrieval.retrieve): a
+// formula over the task scores compiled on the host to postfix bytecode (overarch.py
+// value_model_code) and run element-wise in float64, one thread per (request, candidate),
+// with a register stack. Every operation rounds as NumPy does (no FMA contraction: the
+// intrinsics pin each add / mul / div); min / max propagate NaN; clamp keeps NaN; `if`
+// evaluates both branches. A zero divisor on a valid candidate (index < count[b]) sets
+// *zero_flag (the caller raises DivByZero).
+// ------------------------------------------------------------------------------------
+enum : uint8_t {
+  VM_CONST = 0, VM_TASK = 1, VM_ADD = 2, VM_SUB = 3, VM_MUL = 4, VM_DIV = 5, VM_MIN = 6,
+  VM_MAX = 7, VM_CLAMP = 8, VM_IF_LT = 9, VM_IF_LE = 10, VM_IF_GT = 11, VM_IF_GE = 12,
+  VM_IF_EQ = 13
+};
+constexpr int kVmStack = 16;
+
+__global__ void k_value_model(const uint16_t* __restrict__ code, int n_code,
+                              const double* __restrict__ consts, const double* __restrict__ ts,
+                              int B, int T, int64_t C, const int32_t* __restrict__ count,
+                              double* __restrict__ out, int32_t* __restrict__ zero_flag) {
+  const int64_t total = (int64_t)B * C;
+  for (int64_t g = grid_tid(); g < total; g += grid_stride()) {
+    const int64_t b = g / C, i = g - b * C;
+    const bool valid = i < (int64_t)count[b];
+    double st[kVmStack];
+    int sp = 0;
+    for (int pc = 0; pc < n_code; ++pc) {
+      const uint32_t w = code[pc];
+      const uint32_t op = w & 0xFF, arg = w >> 8;
+      if (op == VM_CONST) {
+        st[sp++] = consts[arg];
+      } else if (op == VM_TASK) {
+        st[sp++] = ts[(b * T + arg) * C + i];
+      } else if (op == VM_CLAMP) {  // np.clip: minimum(maximum(x, lo), hi)
+        const double x = st[sp - 1], lo = consts[arg], hi = consts[arg + 1];
+        const double t = (x != x || lo != lo) ? (x + lo) : (lo > x ? lo : x);
+        st[sp - 1] = (t != t || hi != hi) ? (t + hi) : (hi < t ? hi : t);
+      } else if (op >= VM_IF_LT) {  // left right then else -> cond ? then : else
+        const double e = st[sp - 1], t = st[sp - 2], r = st[sp - 3], l = st[sp - 4];
+        const bool c = op == VM_IF_LT ? l < r : op == VM_IF_LE ? l <= r : op == VM_IF_GT ? l > r
+                       : op == VM_IF_GE ? l >= r : l == r;
+        sp -= 3;
+        st[sp - 1] = c ? t : e;
+      } else {
+        const double y = st[sp - 1], x = st[sp - 2];
+        double z;
+        switch (op) {
+          case VM_ADD: z = __dadd_rn(x, y); break;
+          case VM_SUB: z = __dsub_rn(x, y); break;
+          case VM_MUL: z = __dmul_rn(x, y); break;
+          case VM_DIV:
+            if (y == 0.0 && valid) atomicOr(zero_flag, 1);
+            z = __ddiv_rn(x, y);
+            break;
+          case VM_MIN: z = (x != x || y != y) ? (x + y) : (y < x ? y : x); break;
+          default: z = (x != x || y != y) ? (x + y) : (y > x ? y : x); break;
+        }
+        sp -= 1;
+        st[sp - 1] = z;
+      }
+    }
+    out[g] = st[0];
+  }
+}
+
+int launch_value_model(const uint16_t* code, int n_code, const double* consts, const double* ts,
+                       int B, int T, int64_t C, const int32_t* count, double* out,
+                       int32_t* zero_flag, cudaStream_t s) {
+  const int64_t total = (int64_t)B * C;
+  if (total <= 0) return FB_OK;
+  k_value_model<<<grid_for(total, 256), 256, 0, s>>>(code, n_code, consts, ts, B, T, C, count,
+                                                     out, zero_flag);
+  FB_LAUNCH_CHECK("k_value_model");
   return FB_OK;
 }
 

@@ -220,7 +220,8 @@ class _Graph:
             self._run_tail(out)
 
     def _run_tail(self, out):
-        from .overarch import final_topk_device, merge_device, value_model_device
+        from .overarch import (final_topk_device, merge_device, value_model_device,
+                               value_model_kernel)
         t = self.tail
         T, k = self.T, self.k0
         merged, mcount = merge_device(out.ids.view(1, T, k), out.count.view(1, T), t["merge"])
@@ -236,8 +237,15 @@ class _Graph:
         ts = t["scorer"].score(t["cache"], rows, mcount, self.u32[None], t["names"])
         _ck("score")
         zero = []
-        final = value_model_device(t["spec"], {n: ts[:, j, :] for j, n in enumerate(t["names"])},
-                                   valid, zero_flags=zero)
+        if getattr(self, "_vm_zero", None) is None:
+            self._vm_zero = torch.zeros(1, dtype=torch.int32, device=ts.device)
+        vm = value_model_kernel(t["spec"], t["names"], ts, mcount, zero=self._vm_zero)
+        if vm is None:
+            final = value_model_device(t["spec"], {n: ts[:, j, :] for j, n in enumerate(t["names"])},
+                                       valid, zero_flags=zero)
+        else:
+            final, zf = vm
+            zero.append(zf != 0)
         _ck("value_model")
         anyz = torch.zeros((1,), dtype=torch.bool, device=merged.device)
         for z in zero:

@@ -26,6 +26,7 @@ Here the whole batch of requests runs on the device:
 
 from __future__ import annotations
 
+import json
 import time
 from dataclasses import dataclass
 
@@ -265,6 +266,101 @@ def value_model_device(spec: dict, task_scores: dict[str, torch.Tensor],
     return walk(spec)
 
 
+_VM_OPS = {"add": 2, "sub": 3, "mul": 4, "div": 5, "min": 6, "max": 7}
+_VM_IF = {"<": 9, "<=": 10, ">": 11, ">=": 12, "==": 13}
+_VM_STACK = 16
+_VM_CODE: dict = {}
+
+
+def value_model_code(spec: dict, names: list[str]):
+    """Postfix bytecode of a value-model formula for ``fb_value_model`` (u16 words
+    op | arg << 8, float64 constants), in the reference's evaluation order
+    (ref value_model.py:75-124: n-ary ops fold left). Returns None when the formula is
+    deeper than the kernel's stack."""
+    code: list[int] = []
+    consts: list[float] = []
+    depth = [0, 0]  # current, max
+
+    def push():
+        depth[0] += 1
+        depth[1] = max(depth[1], depth[0])
+
+    def walk(n):
+        op = n["op"]
+        if op == "const":
+            code.append(0 | (len(consts) << 8))
+            consts.append(float(n["value"]))
+            push()
+        elif op == "task":
+            if n["task"] not in names:
+                raise UnknownTask(n["task"])
+            code.append(1 | (names.index(n["task"]) << 8))
+            push()
+        elif op in ("add", "mul", "min", "max"):
+            walk(n["args"][0])
+            for a in n["args"][1:]:
+                walk(a)
+                code.append(_VM_OPS[op])
+                depth[0] -= 1
+        elif op in ("sub", "div"):
+            walk(n["args"][0])
+            walk(n["args"][1])
+            code.append(_VM_OPS[op])
+            depth[0] -= 1
+        elif op == "clamp":
+            walk(n["args"][0])
+            code.append(8 | (len(consts) << 8))
+            consts.extend([float(n["lo"]), float(n["hi"])])
+        elif op == "if":
+            c = n["cond"]
+            walk(c["left"])
+            walk(c["right"])
+            walk(n["then"])
+            walk(n["else"])
+            code.append(_VM_IF[c["cmp"]])
+            depth[0] -= 3
+        else:
+            raise ValueError(f"unknown formula op {op!r}")
+
+    walk(spec)
+    if depth[1] > _VM_STACK or len(consts) >= 256 or len(names) >= 256:
+        return None
+    return code, consts
+
+
+def value_model_kernel(spec: dict, names: list[str], ts: torch.Tensor, mcount: torch.Tensor,
+                       zero: torch.Tensor | None = None):
+    """The value model on ``fb_value_model``: ts float64 [B, T, C] task scores (task order
+    = ``names``), mcount [B] valid candidates -> (final float64 [B, C], zero int32 [1] set
+    to 1 when a valid candidate divides by zero). None when the formula does not compile
+    (deeper than the kernel's stack)."""
+    key = (json.dumps(spec, sort_keys=True, default=str), tuple(names), ts.device.index)
+    hit = _VM_CODE.get(key)
+    if hit is None:
+        cc = value_model_code(spec, names)
+        if cc is None:
+            return None
+        code, consts = cc
+        dev = ts.device
+        hit = (torch.from_numpy(np.asarray(code, dtype=np.uint16).view(np.int16)).to(dev),
+               torch.tensor(consts or [0.0], dtype=torch.float64, device=dev), len(code))
+        _VM_CODE[key] = hit
+    code_t, consts_t, n_code = hit
+    B, T, C = ts.shape
+    t = ts.contiguous()
+    cnt = mcount.to(torch.int32).contiguous()
+    out = torch.empty((B, C), dtype=torch.float64, device=ts.device)
+    if zero is None:
+        zero = torch.zeros(1, dtype=torch.int32, device=ts.device)
+    else:
+        zero.zero_()
+    _native.check(_native.lib().fb_value_model(code_t.data_ptr(), n_code, consts_t.data_ptr(),
+                                               t.data_ptr(), B, T, C, cnt.data_ptr(),
+                                               out.data_ptr(), zero.data_ptr(),
+                                               _native.stream_ptr()))
+    return out, zero
+
+
 # ------------------------------------------------------------------------------------
 # final ranking
 # ------------------------------------------------------------------------------------
@@ -425,8 +521,14 @@ class MultiTaskOp:
             valid = torch.arange(merged.shape[1], device=merged.device)[None, :] < mcount[:, None]
             rows = self.cache.rows_for(merged, valid)
         ts = self.scorer.score(self.cache, rows, mcount, users, self.tasks)    # [B, T, C]
-        final = value_model_device(self.spec, {t: ts[:, j, :] for j, t in enumerate(self.tasks)},
-                                   valid)
+        vm = value_model_kernel(self.spec, self.tasks, ts, mcount)
+        if vm is None:
+            final = value_model_device(self.spec, {t: ts[:, j, :] for j, t in enumerate(self.tasks)},
+                                       valid)
+        else:
+            final, zero = vm
+            if bool(zero.item()):
+                raise DivByZero("division by zero in value model")
         order, n = final_topk_device(final, mcount, self.topk)
         return MultiTaskOutput(ids=torch.gather(merged, 1, order),
                                scores=torch.gather(final, 1, order),
@@ -521,7 +623,13 @@ def retrieve(engine, req) -> RetrieveResult:
         ts = scorer.score(dcache, rows, mcount, users, names)
         vm = req.value_model if req.value_model is not None else engine.default_value_model
         spec = value_model_spec(vm) or mean_of_tasks_spec(names)
-        final = value_model_device(spec, {t: ts[:, j, :] for j, t in enumerate(names)}, valid)
+        vmk = value_model_kernel(spec, names, ts, mcount)
+        if vmk is None:
+            final = value_model_device(spec, {t: ts[:, j, :] for j, t in enumerate(names)}, valid)
+        else:
+            final, zero = vmk
+            if bool(zero.item()):
+                raise DivByZero("division by zero in value model")
         order = final_topk_device(final, mcount, min(req.topk, n))[0][0]
         ids_h = u64_host(merged[0, order].contiguous())
         fin_h = final[0, order].cpu().numpy()

@@ -224,3 +224,82 @@ def test_final_topk_kernel_numpy_order(C, topk):
         want = np.lexsort((np.arange(m), -vals[b, :m]))[:topk]
         assert n[b] == len(want)
         assert np.array_equal(order[b, : n[b]], want), f"request {b}"
+
+
+@pytest.mark.gpu
+def test_value_model_kernel_matches_numpy():
+    """fb_value_model == the reference's NumPy evaluation (ref value_model.py:75-124)
+    bit for bit: n-ary folds, sub/div, min/max with NaN, clip, if with both branches,
+    and the zero-divisor flag only for valid candidates."""
+    import numpy as np
+    import torch
+
+    from paper_2511_14881_b200.overarch import value_model_kernel
+    rng = np.random.default_rng(11)
+    B, T, C = 3, 3, 1000
+    ts = rng.standard_normal((B, T, C))
+    ts[rng.random((B, T, C)) < 0.01] = np.nan
+    ts[rng.random((B, T, C)) < 0.01] = 0.0
+    names = ["a", "b", "c"]
+    t = {"op": "task"}
+    A, Bt, Ct = ({**t, "task": n} for n in names)
+    specs = [
+        {"op": "mul", "args": [{"op": "const", "value": 1 / 3}, {"op": "add", "args": [A, Bt, Ct]}]},
+        {"op": "sub", "args": [{"op": "max", "args": [A, Bt, {"op": "const", "value": 0.25}]},
+                               {"op": "min", "args": [Ct, A]}]},
+        {"op": "clamp", "args": [{"op": "add", "args": [A, Ct]}], "lo": -0.5, "hi": 0.75},
+        {"op": "if", "cond": {"left": A, "cmp": ">=", "right": Bt},
+         "then": {"op": "mul", "args": [A, {"op": "const", "value": 3.0}]}, "else": Ct},
+        {"op": "div", "args": [A, {"op": "add", "args": [Bt, {"op": "const", "value": 10.0}]}]},
+    ]
+
+    def ref(spec, s):
+        op = spec["op"]
+        if op == "const":
+            return spec["value"]
+        if op == "task":
+            return s[names.index(spec["task"])]
+        if op in ("add", "mul", "min", "max"):
+            acc = ref(spec["args"][0], s)
+            f = {"add": np.add, "mul": np.multiply, "min": np.minimum, "max": np.maximum}[op]
+            for x in spec["args"][1:]:
+                acc = f(acc, ref(x, s))
+            return acc
+        if op == "sub":
+            return ref(spec["args"][0], s) - ref(spec["args"][1], s)
+        if op == "div":
+            return ref(spec["args"][0], s) / ref(spec["args"][1], s)
+        if op == "clamp":
+            return np.clip(ref(spec["args"][0], s), spec["lo"], spec["hi"])
+        c = spec["cond"]
+        cmp = {"<": np.less, "<=": np.less_equal, ">": np.greater, ">=": np.greater_equal,
+               "==": np.equal}[c["cmp"]]
+        return np.where(cmp(ref(c["left"], s), ref(c["right"], s)), ref(spec["then"], s),
+                        ref(spec["else"], s))
+
+    counts = np.array([C, 600, 0], dtype=np.int32)
+    for spec in specs:
+        out, zero = value_model_kernel(spec, names, torch.as_tensor(ts, device="cuda"),
+                                       torch.as_tensor(counts, device="cuda"))
+        got = out.cpu().numpy()
+        for b in range(B):
+            m = int(counts[b])
+            with np.errstate(all="ignore"):
+                want = np.broadcast_to(ref(spec, ts[b]), (C,))
+            assert np.array_equal(got[b, :m], want[:m], equal_nan=True), (spec["op"], b)
+        assert int(zero.item()) == 0
+    # a zero divisor inside a valid candidate sets the flag; past the count it does not
+    z = ts.copy()
+    z[1, 1, 700] = 0.0
+    z[1, 1, 10] = 1.0
+    div = {"op": "div", "args": [A, Bt]}
+    zt = np.where(np.isnan(z), 1.0, z)
+    zt[:, 1, :] = np.where(zt[:, 1, :] == 0.0, 2.0, zt[:, 1, :])
+    zt[1, 1, 700] = 0.0
+    _, zero = value_model_kernel(div, names, torch.as_tensor(zt, device="cuda"),
+                                 torch.as_tensor(np.array([C, 600, 0], dtype=np.int32), device="cuda"))
+    assert int(zero.item()) == 0
+    zt[1, 1, 10] = 0.0
+    _, zero = value_model_kernel(div, names, torch.as_tensor(zt, device="cuda"),
+                                 torch.as_tensor(np.array([C, 600, 0], dtype=np.int32), device="cuda"))
+    assert int(zero.item()) == 1

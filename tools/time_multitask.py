@@ -13,7 +13,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 from paper_2511_14881_b200 import _device, workload  # noqa: E402
 from paper_2511_14881_b200.overarch import (DeviceCache, MultiTaskOp, merge_device,  # noqa: E402
-                                            value_model_device, final_topk_device)
+                                            value_model_device, final_topk_device,
+                                            value_model_kernel)
 
 
 def main():
@@ -47,7 +48,7 @@ def main():
         e[3].record()
         ts = op.scorer.score(cache, rows, mcount, users, tasks)
         e[4].record()
-        final = value_model_device(op.spec, {t: ts[:, j, :] for j, t in enumerate(tasks)}, valid)
+        final, _ = value_model_kernel(op.spec, tasks, ts, mcount)
         e[5].record()
         order, _ = final_topk_device(final, mcount, a.k)
         torch.gather(merged, 1, order)
