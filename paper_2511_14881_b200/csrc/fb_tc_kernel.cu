@@ -786,14 +786,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t* osp = a.out_slot ? a.out_slot + (int64_t)q * a.cap : nullptr;
                 const uint32_t ids = id_s + (uint32_t)(c * 32) * 4u;
                 const uint32_t cap = (uint32_t)a.cap;
+                if (osp == nullptr && p + 32u <= cap) {
+                  // the sampling pass (no slots, room for the whole word): keys only
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                  const bool on = ((cm >> j) & 1u) != 0u;
-                  if (on && p < cap) {
-                    okp[p] = make_key(r[j], lds32(ids + 4u * j));
-                    if (osp != nullptr) osp[p] = slot0 + (uint32_t)j;
+                  for (int j = 0; j < 32; ++j) {
+                    const bool on = ((cm >> j) & 1u) != 0u;
+                    if (on) okp[p] = make_key(r[j], lds32(ids + 4u * j));
+                    p += on ? 1u : 0u;
                   }
-                  p += on ? 1u : 0u;
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 32; ++j) {
+                    const bool on = ((cm >> j) & 1u) != 0u;
+                    if (on && p < cap) {
+                      okp[p] = make_key(r[j], lds32(ids + 4u * j));
+                      if (osp != nullptr) osp[p] = slot0 + (uint32_t)j;
+                    }
+                    p += on ? 1u : 0u;
+                  }
                 }
               } else if (cm != 0u) {
                 const int64_t slot0 = tile * kTileItems + half * 128 + c * 32;
