@@ -1854,47 +1854,17 @@ __global__ void __launch_bounds__(kFtThreads, 1)
   const int n = min(count[b], kFtMaxN);
   const int kk = min(topk, n);
   const double* f = final_ + (int64_t)b * ld;
-  uint64_t kor = 0ull, kand = ~0ull;  // bits that differ among the keys
-  for (int i = t; i < n; i += kFtThreads) {
-    const uint64_t u = ft_key(f[i]);
-    s_key[i] = u;
-    kor |= u;
-    kand &= u;
-  }
-  // 1. radix select: prefix / mask of the kk-th smallest key, r = its rank inside the bin;
-  //    it starts at the highest byte where the keys differ (the leading ones are common)
-  uint64_t* s_red = reinterpret_cast<uint64_t*>(s_misc + 32);  // [2] (s_misc[32..35])
-  if (t == 0) {
-    s_red[0] = 0ull;
-    s_red[1] = ~0ull;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    kor |= __shfl_xor_sync(0xffffffffu, kor, d);
-    kand &= __shfl_xor_sync(0xffffffffu, kand, d);
-  }
-  if (lane == 0) {
-    atomicOr(reinterpret_cast<unsigned long long*>(s_red), kor);
-    atomicAnd(reinterpret_cast<unsigned long long*>(s_red + 1), kand);
-  }
-  __syncthreads();
-  const uint64_t diff = s_red[0] & ~s_red[1];
-  const int top = diff == 0ull ? 0 : (63 - __clzll((long long)diff)) / 8 * 8;
-  uint64_t mask = top >= 56 ? 0ull : ~0ull << (top + 8);
-  uint64_t prefix = s_red[0] & mask;  // the common leading bytes
+  for (int i = t; i < n; i += kFtThreads) s_key[i] = ft_key(f[i]);
+  // 1. radix select: prefix / mask of the kk-th smallest key, r = its rank inside the bin
+  uint64_t prefix = 0ull, mask = 0ull;
   int r = kk;
   __syncthreads();
-  for (int shift = top; shift >= 0 && kk > 0; shift -= 8) {
+  for (int shift = 56; shift >= 0 && kk > 0; shift -= 8) {
     for (int i = t; i < 256; i += kFtThreads) s_hist[i] = 0u;
     __syncthreads();
     for (int i = t; i < n; i += kFtThreads) {
       const uint64_t u = s_key[i];
-      const bool in = (u & mask) == prefix;
-      const uint32_t dg = in ? (uint32_t)((u >> shift) & 0xFF) : 256u;
-      // one atomic per distinct digit per warp (the keys crowd into few bins)
-      const uint32_t peers = __match_any_sync(__activemask(), dg);
-      if (in && lane == __ffs(peers) - 1) atomicAdd(s_hist + dg, (uint32_t)__popc(peers));
+      if ((u & mask) == prefix) atomicAdd(s_hist + (int)((u >> shift) & 0xFF), 1u);
     }
     __syncthreads();
     if (warp == 0) {  // the digit whose cumulative count reaches r
