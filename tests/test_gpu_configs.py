@@ -129,7 +129,8 @@ def test_shuffled_ids_tiebreak(cuda):
 
 
 @pytest.mark.parametrize("mode,B,v1", [("0", 40, "0"), ("1", 40, "0"), ("0", 200, "0"),
-                                        ("1", 200, "0"), ("0", 200, "1"), ("1", 200, "1")])
+                                        ("1", 200, "0"), ("0", 200, "1"), ("1", 200, "1"),
+                                        ("0", 129, "0"), ("1", 256, "0")])
 def test_filter_first_and_per_hit_modes_agree(cuda, monkeypatch, mode, B, v1):
     """The window-form emit pass has two hit passes (per-hit test on item-major column bits,
     and filter-first eligibility words); the device picks one from the sampled eligibility.
