@@ -116,3 +116,64 @@ def test_sharded_real_kernels_equal_unsharded(cuda, n_items, B, k, exchange):
             assert np.array_equal(gs, ref.scores), (exchange, qi)
             seen.add(qi)
     assert seen == set(range(B))
+
+
+def _graph_worker(port, exchange, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        from paper_2511_14881_b200 import _device, workload
+        from paper_2511_14881_b200.engine import TopkOp
+        from paper_2511_14881_b200.serve import ShardedSearch
+        wl = workload.make_workload(40_000, 16, seed=5)
+        idx = wl.index
+        op = TopkOp(idx, 16, 500, np.array([[0, idx.n_slots]]))
+        ss = ShardedSearch(op, exchange=exchange)
+        batch = wl.batch.to_device()
+        want = ss(wl.queries_q, batch)  # eager (also the warm-up)
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            ss(wl.queries_q, batch)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            got = ss(wl.queries_q, batch)
+        g.replay()
+        torch.cuda.synchronize()
+        ok = True
+        for q in range(16):
+            n = int(want.count[q])
+            ok &= int(got.count[q]) == n
+            ok &= np.array_equal(_device.u64_host(got.ids[q, :n]), _device.u64_host(want.ids[q, :n]))
+            ok &= np.array_equal(got.scores[q, :n].cpu().numpy(), want.scores[q, :n].cpu().numpy())
+        result_q.put(("ok" if ok else "mismatch", None))
+    except Exception as e:  # noqa: BLE001
+        result_q.put(("error", f"{type(e).__name__}: {e}"))
+    # no NCCL teardown: the process ends here (a communicator destroy can block at exit)
+    result_q.close()
+    result_q.join_thread()
+    os._exit(0)
+
+
+@pytest.mark.parametrize("exchange", ["owner", "all_gather"])
+def test_sharded_step_captures_in_cuda_graph(cuda, exchange):
+    """The sharded step (local filtered top-k -> NCCL exchange -> GPU merge) has no
+    device->host synchronisation, so it captures in one CUDA graph; the replay returns the
+    eager step's rows (world size 1 on the one GPU: the collectives are real NCCL calls)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_graph_worker, args=(_free_port(), exchange, q))
+    p.start()
+    try:
+        status, msg = q.get(timeout=600)
+    finally:
+        p.join(timeout=60)
+        if p.is_alive():
+            p.kill()
+            p.join(timeout=30)
+    assert status == "ok", msg
