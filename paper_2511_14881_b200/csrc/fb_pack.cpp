@@ -12,13 +12,20 @@
 // integers beyond u64) is reported as FB_ERR_PARSE with the query index; the Python
 // wrapper re-runs the reference-grammar parser on that one text to raise the reference's
 // exception (FilterSyntaxError / UnknownFeature / UnknownValue) with its exact message.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <stdint.h>
 #include <string.h>
 
 #include <algorithm>
 #include <array>
 #include <memory>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -41,6 +48,83 @@ struct fb_pack {
 
 namespace fb {
 namespace {
+
+// A small persistent worker pool for the per-query host work (parsing a batch of filter
+// texts): threads are started once, a call splits [0, n) into one contiguous chunk per
+// thread and the caller works on chunk 0. FB_PACK_THREADS caps the count (1 = serial).
+class Pool {
+ public:
+  static Pool& get() {
+    static Pool p;
+    return p;
+  }
+  int size() const { return (int)workers_.size() + 1; }
+  void run(int n, const std::function<void(int, int)>& fn) {
+    const int T = std::min(size(), std::max(1, n / 16));
+    if (T <= 1) {
+      fn(0, n);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(call_mu_);  // one parallel call at a time
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      fn_ = &fn;
+      n_ = n;
+      chunks_ = T;
+      pending_ = T - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0, n / T);
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  Pool() {
+    int t = (int)std::thread::hardware_concurrency();
+    if (const char* e = getenv("FB_PACK_THREADS")) t = atoi(e);
+    t = std::max(1, std::min(t, 16));
+    for (int i = 1; i < t; ++i) workers_.emplace_back([this, i] { loop(i); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  void loop(int id) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int, int)>* fn;
+      int n, chunks;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        fn = fn_;
+        n = n_;
+        chunks = chunks_;
+      }
+      if (id < chunks) {
+        (*fn)((int)((int64_t)n * id / chunks), (int)((int64_t)n * (id + 1) / chunks));
+        std::lock_guard<std::mutex> g(mu_);
+        if (--pending_ == 0) done_cv_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int, int)>* fn_ = nullptr;
+  int n_ = 0, chunks_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
 
 // ---- per-(fid, value, M, K) leaf position cache ------------------------------------------
 struct PosKey {
@@ -673,17 +757,32 @@ int fb_pack_text(int32_t n_queries, const char* const* texts, const fb_vocab_t* 
   *out = nullptr;
   std::vector<std::vector<fb::Op>> progs(n_queries);
   std::vector<char> filtered(n_queries, 0);
-  for (int q = 0; q < n_queries; ++q) {
-    const char* t = texts[q];
-    if (t == nullptr || t[0] == '\0') continue;
-    if (!fb::parse_text(t, vocab, progs[q])) {
+  auto T0 = std::chrono::steady_clock::now();
+  // texts parse independently: split over the pool; the first bad query is reported
+  std::vector<char> bad(n_queries, 0);
+  fb::Pool::get().run(n_queries, [&](int q0, int q1) {
+    for (int q = q0; q < q1; ++q) {
+      const char* t = texts[q];
+      if (t == nullptr || t[0] == '\0') continue;
+      if (!fb::parse_text(t, vocab, progs[q]))
+        bad[q] = 1;
+      else
+        filtered[q] = 1;
+    }
+  });
+  for (int q = 0; q < n_queries; ++q)
+    if (bad[q]) {
       if (bad_query) *bad_query = q;
       return fb::fail(FB_ERR_PARSE, "filter text not accepted (query " + std::to_string(q) + ")");
     }
-    filtered[q] = 1;
-  }
+  auto T1 = std::chrono::steady_clock::now();
   auto P = std::make_unique<fb_pack>();
   const int rc = fb::pack_programs(progs, filtered, m_bits, k_hashes, *P);
+  auto T2 = std::chrono::steady_clock::now();
+  if (getenv("FB_PACK_TIMING"))
+    fprintf(stderr, "parse %.3f ms pack %.3f ms\n",
+            std::chrono::duration<double, std::milli>(T1 - T0).count(),
+            std::chrono::duration<double, std::milli>(T2 - T1).count());
   if (rc) return rc;
   *out = P.release();
   return FB_OK;
@@ -699,6 +798,7 @@ int fb_pack_postfix(int32_t n_queries, const int64_t* op_offset, const uint8_t* 
   *out = nullptr;
   std::vector<std::vector<fb::Op>> progs(n_queries);
   std::vector<char> filtered(n_queries, 0);
+  auto T0 = std::chrono::steady_clock::now();
   for (int q = 0; q < n_queries; ++q) {
     const int64_t a = op_offset[q], b = op_offset[q + 1];
     if (b < a) return fb::fail(FB_ERR_INVALID, "op_offset not ascending");
