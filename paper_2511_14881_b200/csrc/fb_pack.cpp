@@ -26,6 +26,8 @@
 #include <functional>
 #include <mutex>
 #include <thread>
+
+#include <pthread.h>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -55,10 +57,15 @@ namespace {
 class Pool {
  public:
   static Pool& get() {
-    static Pool p;
-    return p;
+    // never destroyed (no joins at process exit); a forked child has no workers, so it
+    // runs every call serially
+    static Pool* p = [] {
+      pthread_atfork(nullptr, nullptr, [] { forked_child() = true; });
+      return new Pool;
+    }();
+    return *p;
   }
-  int size() const { return (int)workers_.size() + 1; }
+  int size() const { return forked_child() ? 1 : (int)workers_.size() + 1; }
   void run(int n, const std::function<void(int, int)>& fn) {
     const int T = std::min(size(), std::max(1, n / 16));
     if (T <= 1) {
@@ -88,13 +95,9 @@ class Pool {
     t = std::max(1, std::min(t, 16));
     for (int i = 1; i < t; ++i) workers_.emplace_back([this, i] { loop(i); });
   }
-  ~Pool() {
-    {
-      std::lock_guard<std::mutex> g(mu_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto& w : workers_) w.join();
+  static bool& forked_child() {
+    static bool f = false;
+    return f;
   }
   void loop(int id) {
     uint64_t seen = 0;
