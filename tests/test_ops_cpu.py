@@ -115,3 +115,29 @@ def test_identity_cache_unhashable_dataclass():
     for o in objs:
         s.put(o, o[0])
     assert s.get(objs[0]) is None and s.get(objs[2]) == 2
+
+
+def test_value_model_code_postfix():
+    """The value-model compiler (fb_value_model's bytecode) folds n-ary ops left to right as
+    the reference evaluates them (ref value_model.py:75-124) and rejects unknown tasks."""
+    import pytest
+
+    from paper_2511_14881_b200.errors import UnknownTask
+    from paper_2511_14881_b200.overarch import mean_of_tasks_spec, value_model_code
+    code, consts = value_model_code(mean_of_tasks_spec(["a", "b", "c"]), ["a", "b", "c"])
+    # CONST(1/3) TASK a TASK b ADD TASK c ADD MUL
+    assert code == [0, 1, 1 | (1 << 8), 2, 1 | (2 << 8), 2, 4] and consts == [1 / 3]
+    spec = {"op": "if", "cond": {"left": {"op": "task", "task": "b"}, "cmp": ">=",
+                                 "right": {"op": "const", "value": 2.0}},
+            "then": {"op": "clamp", "args": [{"op": "task", "task": "a"}], "lo": -1, "hi": 1},
+            "else": {"op": "div", "args": [{"op": "task", "task": "a"},
+                                           {"op": "task", "task": "b"}]}}
+    code, consts = value_model_code(spec, ["a", "b"])
+    assert code == [1 | (1 << 8), 0, 1, 8 | (1 << 8), 1, 1 | (1 << 8), 5, 12]
+    assert consts == [2.0, -1.0, 1.0]
+    with pytest.raises(UnknownTask):
+        value_model_code({"op": "task", "task": "z"}, ["a"])
+    deep = {"op": "task", "task": "a"}
+    for _ in range(20):  # right-nested: the stack grows by one per level
+        deep = {"op": "add", "args": [{"op": "task", "task": "a"}, deep]}
+    assert value_model_code(deep, ["a"]) is None  # deeper than the kernel's stack
