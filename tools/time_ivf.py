@@ -149,9 +149,10 @@ def main():
                                     orc.quantize(qf[t], qp.global_min, qp.global_max), cl, a.k)
         got = res["probe"][0][t, : int(res["probe"][2][t])].cpu().numpy().view(np.uint64)
         assert np.array_equal(got, ref.item_ids), t
-    per = (time.perf_counter() - t0) / a.cpu_queries
-    out["cpu_oracle_ms_per_query"] = round(1e3 * per, 1)
-    out["cpu_oracle_qps_1core"] = round(1.0 / per, 2)
+    if a.cpu_queries > 0:
+        per = (time.perf_counter() - t0) / a.cpu_queries
+        out["cpu_oracle_ms_per_query"] = round(1e3 * per, 1)
+        out["cpu_oracle_qps_1core"] = round(1.0 / per, 2)
     out["oracle_checked_queries"] = a.cpu_queries
     print(json.dumps(out))
 
