@@ -461,6 +461,9 @@ constexpr int kCnfDense0 = 8;
 constexpr int kCnfDenseWarps = 4;
 constexpr int kCnfHit0 = 12;
 constexpr int kCnfHitWarps = 8;
+#ifndef FB_HM_EARLY
+#define FB_HM_EARLY 1  // modes 3 / 4: release the hit map right after the words are read
+#endif
 #ifndef FB_HIT_TAKE
 #define FB_HIT_TAKE 4  // mode 3: hits taken per lane and round (2: 1.035-1.039 ms, 3: 1.028-1.033, 4: 1.029)
 #endif
@@ -1343,6 +1346,14 @@ __global__ void __launch_bounds__(kMode >= 3 ? kCnf3Threads : kCnfThreads)
           nzm |= (mw[c] != 0u ? 1u : 0u) << c;
         }
       }
+#if FB_HM_EARLY
+      if constexpr (kMode >= 3) {
+        // the walk reads the hit words from registers only: the hit map goes back to the
+        // dense warps now, so their next drain (and the MMA after it) need not wait for it
+        __syncwarp();
+        nb_arrive(kNbHmEmpty + hb, kHmCount);
+      }
+#endif
       auto word_at = [&](int c) -> uint32_t {
         if (ff)
           return c < 4 ? (c < 2 ? (c == 0 ? mw[0] : mw[1]) : (c == 2 ? mw[2] : mw[3]))
@@ -1444,7 +1455,7 @@ __global__ void __launch_bounds__(kMode >= 3 ? kCnf3Threads : kCnfThreads)
         }
       }
       __syncwarp();
-      nb_arrive(kNbHmEmpty + hb, kHmCount);
+      if (!(FB_HM_EARLY && kMode >= 3)) nb_arrive(kNbHmEmpty + hb, kHmCount);
       if (warp == kHit0) FB_TR(a, it, 11);
 #ifdef FB_TRACE
       if ((a.dbg & 1024) && blockIdx.x == 0 && warp == kHit0 && lane == 0 && it < 16)
