@@ -90,7 +90,10 @@ class Pool {
 
  private:
   Pool() {
-    int t = (int)std::thread::hardware_concurrency();
+    // four threads by default: the serving loop's other host threads (the Python driver,
+    // the copy stream's callbacks) share the cores, and waking more workers per batch cost
+    // more than it saved (fresh-filter e2e on the GPU box: 4 threads 179-190k q/s, 16: 170-173k)
+    int t = std::min(4, (int)std::thread::hardware_concurrency());
     if (const char* e = getenv("FB_PACK_THREADS")) t = atoi(e);
     t = std::max(1, std::min(t, 16));
     for (int i = 1; i < t; ++i) workers_.emplace_back([this, i] { loop(i); });
@@ -564,6 +567,7 @@ int lower_rops(const std::vector<std::pair<uint8_t, int32_t>>& ops, std::vector<
 // The batch form of programs[q] (empty = unfiltered).
 int pack_programs(const std::vector<std::vector<Op>>& progs, const std::vector<char>& filtered,
                   int32_t m_bits, int32_t k_hashes, fb_pack& P) {
+  auto TT0 = std::chrono::steady_clock::now();
   const int nq = (int)progs.size();
   memset(P.meta, 0, sizeof(P.meta));
   P.meta[FB_PACK_N_QUERIES] = nq;
@@ -621,6 +625,7 @@ int pack_programs(const std::vector<std::vector<Op>>& progs, const std::vector<c
       max_stack = std::max(max_stack, peak);
     }
   }
+  auto TT1 = std::chrono::steady_clock::now();
   const int n_leaves = (int)P.leaf_fid.size();
   if (n_leaves > FB_MAX_LEAVES)
     return fail(FB_ERR_UNSUPPORTED,
@@ -647,6 +652,7 @@ int pack_programs(const std::vector<std::vector<Op>>& progs, const std::vector<c
     lp_off[i + 1] = (int32_t)lp.size();
   }
   auto npos = [&](int i) { return lp_off[i + 1] - lp_off[i]; };
+  auto TT2 = std::chrono::steady_clock::now();
   // postfix ops, register ops, push bits, CNF
   const bool reg = n_leaves <= kRopMaxLeaves;
   int rmax = 0;
@@ -660,20 +666,54 @@ int pack_programs(const std::vector<std::vector<Op>>& progs, const std::vector<c
   for (int q = 0; q < nq; ++q) total_ops += gops[q].size();
   P.ops.reserve(total_ops + 1);
   P.rops.reserve(total_ops + 8 * (size_t)nq);
-  for (int q = 0; q < nq; ++q) {
-    if (filtered[q]) {
-      int64_t bits = 0;
-      for (const auto& o : gops[q]) {
-        if (o.first == FB_OP_PUSH_LEAF) {
-          P.ops.push_back((uint16_t)o.second);
-          bits += npos(o.second);
+  // per query (in parallel on the pool): postfix ops, register ops, push bits, CNF groups;
+  // then concatenated in query order (each query's register ops are padded to
+  // FB_ROP_ALIGN on their own, as the serial lowering pads them in place)
+  struct QOut {
+    std::vector<uint16_t> ops, rops;
+    int64_t bits = 0;
+    int rpeak = 0;
+    bool cnf_ok = false;
+    Cnf cnf;
+  };
+  std::vector<QOut> qo(nq);
+  Pool::get().run(nq, [&](int q0, int q1) {
+    CnfScratch sc;
+    std::vector<std::pair<int, int32_t>> rs;
+    for (int q = q0; q < q1; ++q) {
+      if (!filtered[q]) continue;
+      QOut& o = qo[q];
+      o.ops.reserve(gops[q].size());
+      for (const auto& x : gops[q]) {
+        if (x.first == FB_OP_PUSH_LEAF) {
+          o.ops.push_back((uint16_t)x.second);
+          o.bits += npos(x.second);
         } else {
-          P.ops.push_back((uint16_t)(o.first << 14));
+          o.ops.push_back((uint16_t)(x.first << 14));
         }
       }
-      P.push_bits[q] = bits;
-      rmax = std::max(rmax, lower_rops(gops[q], P.rops, rscratch));
-      if (all_cnf) all_cnf = cnf_groups(gops[q], cnf, scratch);
+      o.rpeak = lower_rops(gops[q], o.rops, rs);
+      o.cnf_ok = cnf_groups(gops[q], o.cnf, sc);
+    }
+  });
+  (void)scratch;
+  (void)rscratch;
+  for (int q = 0; q < nq; ++q) {
+    if (filtered[q]) {
+      const QOut& o = qo[q];
+      P.ops.insert(P.ops.end(), o.ops.begin(), o.ops.end());
+      P.push_bits[q] = o.bits;
+      rmax = std::max(rmax, o.rpeak);
+      P.rops.insert(P.rops.end(), o.rops.begin(), o.rops.end());
+      if (all_cnf) {
+        if (!o.cnf_ok) {
+          all_cnf = false;
+        } else {
+          const int32_t base = (int32_t)cnf.lits.size();
+          for (const int32_t g : o.cnf.gstart) cnf.gstart.push_back(g + base);
+          cnf.lits.insert(cnf.lits.end(), o.cnf.lits.begin(), o.cnf.lits.end());
+        }
+      }
     }
     if (all_cnf) {
       cnf.qstart.push_back((int32_t)cnf.gstart.size());
@@ -682,6 +722,12 @@ int pack_programs(const std::vector<std::vector<Op>>& progs, const std::vector<c
     P.op_offset.push_back((int32_t)P.ops.size());
     P.rop_offset.push_back((int32_t)P.rops.size());
   }
+  auto TT3 = std::chrono::steady_clock::now();
+  if (getenv("FB_PACK_TIMING"))
+    fprintf(stderr, "  leaves %.3f positions %.3f lowering+cnf %.3f ms\n",
+            std::chrono::duration<double, std::milli>(TT1 - TT0).count(),
+            std::chrono::duration<double, std::milli>(TT2 - TT1).count(),
+            std::chrono::duration<double, std::milli>(TT3 - TT2).count());
   int k_max = 1;
   for (int i = 0; i < n_leaves; ++i) k_max = std::max(k_max, npos(i));
   const int rows = std::max(1, n_leaves);
