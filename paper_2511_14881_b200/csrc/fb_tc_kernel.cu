@@ -1346,6 +1346,7 @@ __global__ void __launch_bounds__(kMode >= 3 ? kCnf3Threads : kCnfThreads)
           nzm |= (mw[c] != 0u ? 1u : 0u) << c;
         }
       }
+      if (a.dbg & 16384) nzm &= 0x0Fu;  // timing only: walk half the chunks (wrong results)
 #if FB_HM_EARLY
       if constexpr (kMode >= 3) {
         // the walk reads the hit words from registers only: the hit map goes back to the
