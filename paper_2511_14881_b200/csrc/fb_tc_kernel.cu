@@ -465,9 +465,9 @@ constexpr int kCnfHitWarps = 8;
 #define FB_HM_EARLY 1  // modes 3 / 4: release the hit map right after the words are read
 #endif
 #ifndef FB_HIT_TAKE
-#define FB_HIT_TAKE 4  // mode 3: hits taken per lane and round (2: 1.035-1.039 ms, 3: 1.028-1.033, 4: 1.029)
+#define FB_HIT_TAKE 3  // mode 3: hits taken per lane and round (with the early hit-map release: 3: 1.004 ms, 4: 1.022, 5: 1.019)
 #endif
-constexpr int kSurvCap = FB_HIT_TAKE >= 4 ? 160 : 128;  // u16 survivor entries per hit warp: (lane << 8) | item
+constexpr int kSurvCap = FB_HIT_TAKE >= 5 ? 192 : FB_HIT_TAKE >= 4 ? 160 : 128;  // u16 survivor entries per hit warp: (lane << 8) | item
 // named barrier ids (0 is __syncthreads) and their thread counts
 constexpr int kNbHmFull = 1, kNbHmEmpty = 3, kNbLeafFull = 5, kNbLeafEmpty = 7;  // + stage
 constexpr int kNbHmCount = 32 * (kCnfDenseWarps + kCnfHitWarps);
