@@ -1236,11 +1236,23 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
   //    max / min
   const bool staged = n <= kRsMaxK;
   uint64_t mx = 0ull, mn = ~0ull;
-  for (int i = t; i < n; i += kRsThreads) {
-    const uint64_t k = gk[i];
-    if (staged) s_key[i] = k;
-    mx = k > mx ? k : mx;
-    mn = k < mn ? k : mn;
+  constexpr int kLdU = 8;  // candidate loads in flight per thread
+  for (int i0 = 0; i0 < n; i0 += kRsThreads * kLdU) {
+    uint64_t kv[kLdU];
+#pragma unroll
+    for (int u = 0; u < kLdU; ++u) {
+      const int i = i0 + u * kRsThreads + t;
+      kv[u] = i < n ? gk[i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kLdU; ++u) {
+      const int i = i0 + u * kRsThreads + t;
+      if (i < n) {
+        if (staged) s_key[i] = kv[u];
+        mx = kv[u] > mx ? kv[u] : mx;
+        mn = kv[u] < mn ? kv[u] : mn;
+      }
+    }
   }
   mx = warp_max_u64(mx);
   mn = warp_min_u64(mn);
@@ -1326,17 +1338,31 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
   const int id_bits = a.n_slots <= 1 ? 0 : 64 - __clzll((long long)(a.n_slots - 1));
   if (t == 0) s_pos = 0u;
   __syncthreads();
-  for (int i0 = 0; i0 < n; i0 += kRsThreads) {
-    const int i = i0 + t;
-    const uint64_t k = i < n ? gk[i] : 0ull;
-    const bool keep = i < n && k >= lo;
-    const uint32_t b = __ballot_sync(0xffffffffu, keep);
-    uint32_t base = 0u;
-    if (lane == 0 && b != 0u) base = atomicAdd(&s_pos, (uint32_t)__popc(b));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (keep)
-      s_key[base + __popc(b & ((1u << lane) - 1u))] =
-          ((uint64_t)((uint32_t)(k >> 32) - sb_lo) << id_bits) | (uint64_t)((uint32_t)k - id_base);
+  // Staged candidates are compacted in place: all keys of a chunk are read before any
+  // kept key of it is written (one barrier per chunk), and writes stay below the chunk's
+  // end (kept <= read). Otherwise the keys are re-read from L2.
+  constexpr int kCmU = 4;
+  for (int i0 = 0; i0 < n; i0 += kRsThreads * kCmU) {
+    uint64_t kv[kCmU];
+#pragma unroll
+    for (int u = 0; u < kCmU; ++u) {
+      const int i = i0 + u * kRsThreads + t;
+      kv[u] = i < n ? (staged ? s_key[i] : __ldcg(gk + i)) : 0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kCmU; ++u) {
+      const int i = i0 + u * kRsThreads + t;
+      const bool keep = i < n && kv[u] >= lo;
+      const uint32_t b = __ballot_sync(0xffffffffu, keep);
+      uint32_t base = 0u;
+      if (lane == 0 && b != 0u) base = atomicAdd(&s_pos, (uint32_t)__popc(b));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep)
+        s_key[base + __popc(b & ((1u << lane) - 1u))] =
+            ((uint64_t)((uint32_t)(kv[u] >> 32) - sb_lo) << id_bits) |
+            (uint64_t)((uint32_t)kv[u] - id_base);
+    }
   }
   __syncthreads();
 
@@ -1434,6 +1460,39 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
   const uint64_t id_mask = id_bits >= 64 ? ~0ull : ((1ull << id_bits) - 1ull);
   // ids straight from the rank (one gather) unless the dequantised scores need the slot
   const bool by_id = a.id_of_rank != nullptr && a.out_fscores == nullptr;
+  if (by_id) {
+    // ids only: kIdU id gathers in flight per thread (one round at k = 10000); the keys
+    // are re-read from shared memory. The random gathers are the kernel's largest cost
+    // (~45 % at config 2, FB timing ablation in DESIGN §4.2).
+    constexpr int kIdU = 12;
+    for (int r0 = 0; r0 < kk; r0 += kRsThreads * kIdU) {
+      uint64_t iid[kIdU];
+#pragma unroll
+      for (int u = 0; u < kIdU; ++u) {
+        const int r = r0 + u * kRsThreads + t;
+        iid[u] = 0ull;
+        if (r < kk) {
+          const uint32_t low = (uint32_t)(src[kk - 1 - r] & id_mask) + id_base;
+          iid[u] = __ldg(a.id_of_rank + (0xFFFFFFFFu - low));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kIdU; ++u) {
+        const int r = r0 + u * kRsThreads + t;
+        if (r < kk) {
+          const uint64_t c = src[kk - 1 - r];
+          const uint32_t sb = (uint32_t)(c >> id_bits) + sb_lo;
+          const uint32_t low = (uint32_t)(c & id_mask) + id_base;
+          const uint64_t key = ((uint64_t)sb << 32) | low;
+          const int64_t o = (int64_t)q * a.k + r;
+          a.out_ids[o] = iid[u];
+          a.out_scores[o] = key_score(key);
+          if (a.out_keys) a.out_keys[o] = key;
+        }
+      }
+    }
+    return;
+  }
   for (int r0 = 0; r0 < kk; r0 += kRsThreads * kOutU) {
     uint64_t key[kOutU];
     uint32_t slot[kOutU];
