@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define FB_ABI_VERSION 4
+#define FB_ABI_VERSION 5
 
 enum fb_status {
   FB_OK = 0,
@@ -85,6 +85,12 @@ typedef struct fb_index {
   /* Nullable: item id of each rank (item_ids[slot_of_rank[r]]), so the selection gathers
    * an output id with one load instead of two dependent ones. */
   const uint64_t* id_of_rank;
+  /* Dense ids: non-zero when id_of_rank[r] == id_base + r (mod 2^64) for the rank r of
+   * every valid slot (a shard whose valid ids are one contiguous run, e.g. 0..n-1). The
+   * selection then computes each output id from its rank instead of gathering it from
+   * id_of_rank (2.56M random 8-byte reads per batch at config 2). Zero: use the table. */
+  int32_t id_dense;
+  uint64_t id_base;
 } fb_index_t;
 
 /*

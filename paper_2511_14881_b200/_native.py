@@ -54,7 +54,7 @@ EXPORTED = (
 )
 
 
-ABI_VERSION = 4  # include/filtra_b200.h FB_ABI_VERSION
+ABI_VERSION = 5  # include/filtra_b200.h FB_ABI_VERSION
 
 
 class FbIndex(ctypes.Structure):
@@ -65,6 +65,7 @@ class FbIndex(ctypes.Structure):
         ("dim", ctypes.c_int32), ("dim_pad", ctypes.c_int32),
         ("m_bits", ctypes.c_int32), ("k_hashes", ctypes.c_int32),
         ("slot_of_rank", c_vp), ("id_of_rank", c_vp),
+        ("id_dense", ctypes.c_int32), ("id_base", ctypes.c_uint64),
     ]
 
 

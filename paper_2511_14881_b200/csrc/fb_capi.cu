@@ -533,6 +533,8 @@ int fb_topk_execute(fb_topk_plan_t* p, const int8_t* queries_q, const fb_filter_
   sel.cand_slot = p->d_cand_slot;
   sel.slot_of_rank = p->idx.slot_of_rank;
   sel.id_of_rank = p->idx.id_of_rank;
+  sel.id_dense = p->idx.id_dense;
+  sel.dense_id_base = p->idx.id_base;
   sel.n_slots = p->idx.n_slots;
   sel.cnt = p->d_cnt;
   sel.item_ids = p->idx.item_ids;
@@ -636,6 +638,8 @@ int fb_ivf_topk(const fb_index_t* idx, const int8_t* queries_q, int32_t n_querie
   sel.cand_slot = cand_slot;
   sel.slot_of_rank = idx->slot_of_rank;
   sel.id_of_rank = idx->id_of_rank;
+  sel.id_dense = idx->id_dense;
+  sel.dense_id_base = idx->id_base;
   sel.n_slots = idx->n_slots;
   sel.cnt = cand_cnt;
   sel.item_ids = idx->item_ids;

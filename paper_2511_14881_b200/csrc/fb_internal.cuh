@@ -220,6 +220,8 @@ struct SelectArgs {
   uint32_t* scratch_slot;     // [B, cap]
   const uint32_t* slot_of_rank;  // [n_slots] nullable (fb_index_t.slot_of_rank)
   const uint64_t* id_of_rank;    // [n_slots] nullable (fb_index_t.id_of_rank)
+  int32_t id_dense;              // fb_index_t.id_dense: id = dense_id_base + rank, no gather
+  uint64_t dense_id_base;        // fb_index_t.id_base
   int64_t n_slots;               // ranks are a permutation of [0, n_slots)
 };
 int launch_select(const SelectArgs& a, cudaStream_t s);

@@ -1460,6 +1460,20 @@ __global__ void __launch_bounds__(kRsThreads, 1) k_select_radix(SelectArgs a) {
   const uint64_t id_mask = id_bits >= 64 ? ~0ull : ((1ull << id_bits) - 1ull);
   // ids straight from the rank (one gather) unless the dequantised scores need the slot
   const bool by_id = a.id_of_rank != nullptr && a.out_fscores == nullptr;
+  if (by_id && a.id_dense) {
+    // dense ids (fb_index_t.id_dense): id = base + rank, computed, no gather
+    for (int r = t; r < kk; r += kRsThreads) {
+      const uint64_t c = src[kk - 1 - r];
+      const uint32_t sb = (uint32_t)(c >> id_bits) + sb_lo;
+      const uint32_t low = (uint32_t)(c & id_mask) + id_base;
+      const uint64_t key = ((uint64_t)sb << 32) | low;
+      const int64_t o = (int64_t)q * a.k + r;
+      a.out_ids[o] = a.dense_id_base + (uint64_t)(0xFFFFFFFFu - low);
+      a.out_scores[o] = key_score(key);
+      if (a.out_keys) a.out_keys[o] = key;
+    }
+    return;
+  }
   if (by_id) {
     // ids only: kIdU id gathers in flight per thread (one round at k = 10000); the keys
     // are re-read from shared memory. The random gathers are the kernel's largest cost

@@ -73,6 +73,7 @@ class DeviceIndex:
         self.slot_of_rank = self._inverse_ranks(id_rank)  # int32 [n_slots_pad] or None
         self.id_of_rank = (self.item_ids[self.slot_of_rank.long()]  # int64 (u64 bits) or None
                            if self.slot_of_rank is not None else None)
+        self.id_dense, self.id_base = self._dense_ids()
         if row_sum is None:
             row_sum = torch.empty(items.shape[0], dtype=torch.int32, device=items.device)
             _native.check(_native.lib().fb_row_sums(items.data_ptr(), items.shape[0], self.dim,
@@ -101,12 +102,31 @@ class DeviceIndex:
     def n_slots_pad(self) -> int:
         return int(self.items.shape[0])
 
+    def _valid_slots(self) -> torch.Tensor:
+        """bool [n_slots_pad]: the validity bitmap unpacked."""
+        bits = torch.arange(64, device=self.items.device, dtype=torch.int64)
+        words = self.valid.view(-1, 1)
+        return ((words >> bits) & 1).view(-1)[: self.n_slots_pad].bool()
+
+    def _dense_ids(self) -> tuple[int, int]:
+        """(1, base) when every valid slot's id is base + its rank (mod 2^64), i.e. the
+        valid ids are one contiguous run in rank order; (0, 0) otherwise. With it the
+        selection computes output ids instead of gathering them (fb_index_t.id_dense)."""
+        if self.id_of_rank is None:
+            return 0, 0
+        ranks = self.id_rank[self._valid_slots()].to(torch.int64)
+        if ranks.numel() == 0:
+            return 0, 0
+        base = self.id_of_rank[ranks] - ranks  # int64 arithmetic wraps like u64
+        b0 = base[:1]
+        if not bool((base == b0).all()):
+            return 0, 0
+        return 1, int(b0.item()) & 0xFFFFFFFFFFFFFFFF
+
     def _ranks_from_ids(self) -> torch.Tensor:
         """Rank of each valid slot's id among the valid ids (ascending u64)."""
         n = self.n_slots_pad
-        bits = torch.arange(64, device=self.items.device, dtype=torch.int64)
-        words = self.valid.view(-1, 1)
-        vbool = ((words >> bits) & 1).view(-1)[:n].bool()
+        vbool = self._valid_slots()
         key = _u64_order_key(self.item_ids)
         key = torch.where(vbool, key, torch.full_like(key, (1 << 63) - 1))
         order = torch.argsort(key, stable=True)
@@ -163,7 +183,7 @@ class DeviceIndex:
                                self.slot_of_rank.data_ptr() if self.slot_of_rank is not None
                                else None,
                                self.id_of_rank.data_ptr() if self.id_of_rank is not None
-                               else None)
+                               else None, self.id_dense, self.id_base)
 
     def quantize_queries(self, queries: torch.Tensor) -> torch.Tensor:
         if self.qp is None:

@@ -694,3 +694,42 @@ def test_select_heavy_ties(fb, rng):
             gi, gs = out.host(b)
             assert np.array_equal(gi, ref.item_ids), (k, b)
             assert np.array_equal(gs, ref.scores), (k, b)
+
+
+def test_select_dense_ids(fb, rng):
+    """Shards whose valid ids are one contiguous run (in rank order) take the computed-id
+    selection (fb_index_t.id_dense: id = base + rank, no id_of_rank gather); any other id
+    set keeps the table. Both agree with brute force, and forcing the table on a dense
+    shard gives identical outputs. Invalid slots hold ids outside the run; the base sits
+    above 2^63 so the u64 arithmetic is exercised."""
+    from paper_2511_14881_b200 import _device, _native
+    n = 40_000
+    items = rng.integers(-3, 4, size=(n, 128)).astype(np.int8)
+    valid = rng.random(n) < 0.85
+    base = np.uint64((1 << 63) + 12345)
+    ids = np.full(n, np.uint64(7), dtype=np.uint64)
+    order = rng.permutation(int(valid.sum()))
+    ids[valid] = base + order.astype(np.uint64)
+    q = rng.integers(-3, 4, size=(4, 128)).astype(np.int8)
+    broken = ids.copy()
+    broken[np.flatnonzero(valid)[0]] = base + np.uint64(n * 2)  # a gap: not dense
+    for id_set, dense in ((ids, 1), (broken, 0)):
+        dix = fb.DeviceIndex.from_arrays(items, orc.from_bool(valid), id_set)
+        assert dix.id_dense == dense
+        if dense:
+            assert dix.id_base == int(base)
+        for k in (100, 10_000):
+            outs = []
+            for force_table in ((False, True) if dense else (False,)):
+                if force_table:
+                    dix.id_dense = 0
+                op = fb.TopkOp(dix, 4, k, np.array([[0, n]]), _native.FB_PLAN_NO_SAMPLE)
+                out = op(_device.to_dev(q, torch.int8), None)
+                torch.cuda.synchronize()
+                outs.append([out.host(b) for b in range(4)])
+                dix.id_dense = dense
+            for b in range(4):
+                ref = orc.brute_force_int8(items, id_set, q[b], k, keep=valid)
+                for o in outs:
+                    assert np.array_equal(o[b][0], ref.item_ids), (dense, k, b)
+                    assert np.array_equal(o[b][1], ref.scores), (dense, k, b)

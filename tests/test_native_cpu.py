@@ -31,7 +31,7 @@ def test_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.fb_abi_version() == _native.ABI_VERSION == 4
+    assert lib.fb_abi_version() == _native.ABI_VERSION == 5
 
 
 def test_library_is_sm100a_only():
