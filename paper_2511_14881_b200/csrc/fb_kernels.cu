@@ -876,8 +876,11 @@ __device__ __forceinline__ int pow2_ceil(int n) {
 // of the true top-k and fits the buffer with overwhelming probability at any selectivity
 // (the check/fallback keeps the answer exact regardless). Samples that fit are staged in
 // shared memory; larger ones are re-read from global memory (L2) per digit pass.
-constexpr int kThrSmemKeys = 26624;  // 208 KB
-__global__ void __launch_bounds__(kSelectThreads) k_threshold(ThresholdArgs a) {
+// 104 KB: two 1024-thread CTAs per SM (32 registers), so a 256-query batch runs in one
+// wave on 148 SMs (a filtered config-2 query keeps ~8.7k sampled keys; at 208 KB the
+// 256 CTAs took two waves)
+constexpr int kThrSmemKeys = 13312;
+__global__ void __launch_bounds__(kSelectThreads, 2) k_threshold(ThresholdArgs a) {
   extern __shared__ __align__(16) uint64_t s_key[];
   const int q = blockIdx.x;
   if (threadIdx.x == 0) {
