@@ -402,15 +402,22 @@ class PipelinedTopk:
     compute stream while batch i+1's queries and filter arrays are copied in on one copy
     stream and batch i-1's ids / scores are copied out on another (``depth`` slots of
     device and pinned host buffers, ordered by CUDA events; separate streams so a copy-out
-    waiting for its scan never holds up the next copy-in)."""
+    waiting for its scan never holds up the next copy-in).
+
+    With ``overlap`` (default) every slot also has its own plan and compute stream, so batch
+    i+1's sampling pass and threshold (about 0.1 ms, two partial waves) fill the SMs that
+    batch i's selection leaves idle in its second wave, instead of waiting behind it."""
 
     def __init__(self, index: DeviceIndex, n_queries: int, k: int, ranges=None,
-                 flags: int = 0, depth: int = 2, filters_template=None):
+                 flags: int = 0, depth: int = 2, filters_template=None, overlap: bool = True):
         if ranges is None:
             ranges = np.array([[0, index.n_slots]], dtype=np.int64)
         self.index, self.B, self.k = index, int(n_queries), max(int(k), 1)
-        self.op = TopkOp(index, n_queries, k, ranges, flags)
+        n_ops = depth if overlap else 1
+        self.ops = [TopkOp(index, n_queries, k, ranges, flags) for _ in range(n_ops)]
+        self.op = self.ops[0]
         self.compute = torch.cuda.current_stream()
+        self.streams = [self.compute] + [torch.cuda.Stream() for _ in range(n_ops - 1)]
         self.copy_in = torch.cuda.Stream()
         self.copy_out = torch.cuda.Stream()
         dev = index.items.device
@@ -419,6 +426,8 @@ class PipelinedTopk:
             batch = None
             if filters_template is not None:
                 batch = FilterBatch.pack(filters_template, index.bloom.params).to_device()
+                for d in batch._dev:  # read on the slot's compute stream
+                    d.record_stream(self.streams[len(self.slots) % len(self.streams)])
             self.slots.append({
                 "q": torch.empty((self.B, index.dim), dtype=torch.float32, device=dev),
                 "qq": torch.empty((self.B, index.dim_pad), dtype=torch.int8, device=dev),
@@ -455,6 +464,7 @@ class PipelinedTopk:
             raise ValueError(f"filter batch holds {filters.n_queries} programs, expected {self.B}")
         t = self._n
         s = self.slots[t % len(self.slots)]
+        op, cs = self.ops[t % len(self.ops)], self.streams[t % len(self.streams)]
         self._n += 1
         self.copy_in.wait_event(s["comp"])       # the slot's inputs are no longer read
         if filters is not None and not self._same_shape(s["batch"], filters):
@@ -467,7 +477,7 @@ class PipelinedTopk:
                 for h in filters.pin().pinned_arrays():
                     d = torch.empty(h.shape, dtype=h.dtype, device=s["q"].device)
                     d.copy_(h, non_blocking=True)
-                    d.record_stream(self.compute)
+                    d.record_stream(cs)
                     dev.append(d)
             fresh._dev = tuple(dev)
             s["batch"] = fresh
@@ -478,11 +488,12 @@ class PipelinedTopk:
                 for d, h in zip(s["batch"]._dev, filters.pinned_arrays()):
                     d.copy_(h, non_blocking=True)
             s["h2d"].record(self.copy_in)
-        self.compute.wait_event(s["h2d"])
-        self.compute.wait_event(s["d2h"])        # the slot's outputs were copied out
-        quantize_device(s["q"], self.index.qp, out_stride=self.index.dim_pad, out=s["qq"])
-        res = self.op(s["qq"], s["batch"], out=s["out"])
-        s["comp"].record(self.compute)
+        cs.wait_event(s["h2d"])
+        cs.wait_event(s["d2h"])                  # the slot's outputs were copied out
+        with torch.cuda.stream(cs):
+            quantize_device(s["q"], self.index.qp, out_stride=self.index.dim_pad, out=s["qq"])
+            res = op(s["qq"], s["batch"], out=s["out"])
+        s["comp"].record(cs)
         self.copy_out.wait_event(s["comp"])
         with torch.cuda.stream(self.copy_out):
             s["ids"].copy_(res.ids, non_blocking=True)

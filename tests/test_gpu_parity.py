@@ -733,3 +733,35 @@ def test_select_dense_ids(fb, rng):
                 for o in outs:
                     assert np.array_equal(o[b][0], ref.item_ids), (dense, k, b)
                     assert np.array_equal(o[b][1], ref.scores), (dense, k, b)
+
+
+@pytest.mark.parametrize("depth", [2, 3])
+def test_pipelined_topk_overlapped_plans(fb, wl_small, depth):
+    """Per-slot plans on per-slot compute streams (overlap=True: batch i+1's sample pass
+    and threshold run beside batch i's selection) return, for a stream of alternating
+    batches kept ``depth`` deep in flight, exactly the single-plan results."""
+    wl = wl_small
+    idx = wl.index
+    k = 400
+    op = fb.TopkOp(idx, 24, k, np.array([[0, idx.n_slots]]))
+    srcs = [wl.queries, wl.queries.flip(0), wl.queries.roll(5, 0)]
+    want = []
+    for q in srcs:
+        r = op(idx.quantize_queries(q), wl.batch)
+        want.append((r.ids.cpu().numpy().copy(), r.scores.cpu().numpy().copy(),
+                     r.count.cpu().numpy().copy()))
+    hq = [q.cpu().pin_memory() for q in srcs]
+    h_batch = fb.FilterBatch.pack(wl.filters, fb.BloomParams()).pin()
+    pipe = fb.PipelinedTopk(idx, 24, k, depth=depth, filters_template=wl.filters)
+    assert len(pipe.ops) == depth and len(set(id(s) for s in pipe.streams)) == depth
+    n = 9
+    for t in range(n + depth - 1):
+        if t < n:
+            pipe.submit(hq[t % 3], h_batch)
+        c = t - depth + 1
+        if c >= 0:
+            ids, sc, cnt = pipe.result(c)
+            w = want[c % 3]
+            assert np.array_equal(ids.numpy(), w[0]), (depth, c)
+            assert np.array_equal(sc.numpy(), w[1]), (depth, c)
+            assert np.array_equal(cnt.numpy(), w[2]), (depth, c)
