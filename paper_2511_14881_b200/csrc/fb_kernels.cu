@@ -911,10 +911,15 @@ __global__ void __launch_bounds__(kSelectThreads, 2) k_threshold(ThresholdArgs a
   if (staged)
     for (int i = threadIdx.x; i < nk; i += blockDim.x) s_key[i] = gkey[i];
   // radix select (8-bit digits, most significant first) of the key with exactly `jd`
-  // larger keys: one histogram pass over the kept sample per digit
+  // larger keys: one histogram pass over the kept sample per digit. The rank half (low 32
+  // bits) is resolved only when the jd-th key's score is shared by more than two smaller
+  // sampled keys: otherwise T keeps that score with the rank half zeroed, T <= the jd-th
+  // key, admitting only the few candidates tied on its score (exactness needs T <= the
+  // true k-th key, never an exact T) -- four passes instead of eight
   __shared__ uint32_t hist[256];
   __shared__ uint64_t s_prefix;
   __shared__ uint32_t s_need;
+  __shared__ uint32_t s_binc;  // sampled keys in the chosen digit's bin
   if (threadIdx.x == 0) {
     s_prefix = 0ull;
     s_need = (uint32_t)jd + 1u;
@@ -951,6 +956,7 @@ __global__ void __launch_bounds__(kSelectThreads, 2) k_threshold(ThresholdArgs a
           if (cum + c[j] >= need) {
             s_prefix = prefix | ((uint64_t)(255 - 8 * threadIdx.x - j) << shift);
             s_need = need - cum;
+            s_binc = c[j];
             break;
           }
           cum += c[j];
@@ -958,6 +964,7 @@ __global__ void __launch_bounds__(kSelectThreads, 2) k_threshold(ThresholdArgs a
       }
     }
     __syncthreads();
+    if (shift == 32 && s_binc - s_need <= 2u) break;  // uniform: shared values
   }
   if (threadIdx.x == 0) a.threshold[q] = s_prefix;
 }
